@@ -1,0 +1,27 @@
+# libballcorr: hand-written sm_100a CUDA behind a C ABI (include/ballcorr.h)
+NVCC ?= nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -Xptxas -v
+SRC := $(wildcard paper_1711_05075_b200/csrc/*.cu)
+HDR := $(wildcard paper_1711_05075_b200/csrc/*.cuh) include/ballcorr.h
+LIB := paper_1711_05075_b200/lib/libballcorr.so
+OBJDIR := build/obj
+OBJ := $(patsubst paper_1711_05075_b200/csrc/%.cu,$(OBJDIR)/%.o,$(SRC))
+
+all: $(LIB) oracle/liboracle.so
+
+$(OBJDIR)/%.o: paper_1711_05075_b200/csrc/%.cu $(HDR)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $@.ptxas.log || (cat $@.ptxas.log; false)
+
+$(LIB): $(OBJ)
+	@mkdir -p $(dir $(LIB))
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJ)
+
+oracle/liboracle.so: oracle/lens_oracle.c
+	gcc -O2 -fopenmp -shared -fPIC -std=c99 -o $@ $< -lm
+
+clean:
+	rm -rf build $(LIB) oracle/liboracle.so
+
+.PHONY: all clean

@@ -1,0 +1,167 @@
+/*
+ * ballcorr.h -- C ABI of the B200 ball-set correlator (libballcorr.so).
+ *
+ * Operation (eq_relg_0 / eq_relg):
+ *
+ *     f_R(t) = < f_A , f_{RB} o T^{-1} > = integral rho_A(x) rho_{RB}(x - t) dx
+ *
+ * for two solids given as weighted sums of ball indicators (eq_un;
+ * sharp alpha -> infinity limit of eq_psi)
+ *
+ *     rho_A(x) = sum_i w_i 1{|x - a_i| <= r_i},   rho_B(x) = sum_j v_j 1{|x - b_j| <= s_j},
+ *
+ * rotated about B's frame origin (x -> R x, eq_Mink0, Appendix B)
+ * and evaluated on the translation grid t_m = t0 + m h, m in [0, N)^3.  Up to
+ * rounding and the band limit below, f_R(t) = sum_ij w_i v_j V(r_i, s_j,
+ * |a_i - R b_j - t|) with V the two-ball lens volume (eq_ORP / eq_convgP,
+ * L343-L360).
+ *
+ * Two modes compute it:
+ *   BC_MODE_SPECTRAL  the paper's Fourier route (L398-L419 eq_ccghat,
+ *                     L276-L294 eq_fballhat / eq_rhoPhat): knot spectra with
+ *                     the exact ball transform, the conjugate spectral
+ *                     product, one inverse FFT per rotation.  Result = the
+ *                     Fourier partial sum over the band |k_i| <= K (k/P,
+ *                     P = Np h) of the P-periodised f (fp32).
+ *   BC_MODE_EXACT     the paper's combinatorial route (obstacle knots
+ *                     a_i - R b_j with primitive kernel f_{B1} * f_{B2} = V,
+ *                     L347-L360): direct pair-lens spreading (fp32 or fp64).
+ *
+ * Conventions
+ *   * Arrays are C order.  A full output f[n_rot][N][N][N] is indexed
+ *     f[r][mx][my][mz] (z fastest); the linear index reported by the
+ *     reductions is (mx*N + my)*N + mz.  Ties resolve to the lowest index.
+ *   * Complex weights (BC_WEIGHTS_COMPLEX) are interleaved (re, im) doubles.
+ *     f is defined WITHOUT conjugating weights (reading C-3): the
+ *     pair weight is w_i * v_j.
+ *   * Pointers documented "host or device" are classified with
+ *     cudaPointerGetAttributes; host buffers are staged by the library.
+ *   * `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *
+ * Ownership and threading: the caller owns every buffer it passes; the
+ * library copies inputs it keeps (shapes, R) and owns all device scratch,
+ * freed by bc_destroy.  A context is bound to one device and is NOT
+ * thread-safe: one host thread per context.
+ *
+ * Errors: every call returns bc_status; bc_last_error(ctx) gives a message.
+ * Asynchronous CUDA faults surface at the next synchronising call as
+ * BC_ECUDA.  No call falls back to a CPU implementation.
+ */
+#ifndef BALLCORR_H
+#define BALLCORR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    BC_OK = 0,
+    BC_EINVAL = 1,        /* bad argument: NULL, size <= 0, non-finite, r <= 0, R not a rotation */
+    BC_ERANGE = 2,        /* support would wrap onto the grid (P too small) or exceed the plan */
+    BC_ENOMEM = 3,        /* device allocation failed */
+    BC_ESTATE = 4,        /* call out of order (e.g. correlate before upload / spectrum) */
+    BC_EUNSUPPORTED = 5,  /* parameter combination not implemented */
+    BC_ECUDA = 6          /* CUDA runtime error (message in bc_last_error) */
+} bc_status;
+
+typedef enum { BC_FP32 = 0, BC_FP64 = 1 } bc_precision;
+typedef enum { BC_MODE_SPECTRAL = 0, BC_MODE_EXACT = 1 } bc_mode;
+typedef enum { BC_WEIGHTS_REAL = 0, BC_WEIGHTS_COMPLEX = 1 } bc_weight_kind;
+
+typedef enum {
+    BC_OUT_F_FULL = 0,     /* f[n_rot][N][N][N]: float (FP32), double (FP64); complex: (re,im) pairs */
+    BC_OUT_MIN_ARGMIN = 1, /* bc_extremum[n_rot]: min of f (real weights) */
+    BC_OUT_MAX_ARGMAX = 2, /* bc_extremum[n_rot]: max of f (real weights) */
+    BC_OUT_MINMAX = 3,     /* bc_extremum[n_rot][2]: {min, max} (real weights) */
+    BC_OUT_MAX_REAL = 4    /* bc_extremum[n_rot]: max of Re f (any weights; docking score) */
+} bc_out_kind;
+
+/* Per-rotation extremum; idx = (mx*N + my)*N + mz. */
+typedef struct {
+    double val;
+    int64_t idx;
+} bc_extremum;
+
+typedef struct {
+    int32_t N;            /* translations per axis, >= 1 */
+    double h;             /* grid spacing, > 0 */
+    double t0[3];         /* grid origin */
+    int32_t Np;           /* FFT period in grid cells: P = Np*h; Np >= N; factors in {2,3,5} (spectral) */
+    int32_t K;            /* band half-width: modes |k_i| <= K, K < 4096 (spectral) */
+    int32_t precision;    /* bc_precision; SPECTRAL supports BC_FP32 only */
+    int32_t mode;         /* bc_mode */
+    int32_t weights;      /* bc_weight_kind */
+    int32_t max_batch;    /* rotations processed per launch; 0 = library default */
+    double spread_eps;    /* spectral: target aliasing/truncation level of the spreading (0 = 1e-7) */
+} bc_params;
+
+typedef struct bc_ctx bc_ctx;
+
+/* Create a context on `device`.  Validates params (EINVAL / EUNSUPPORTED). */
+bc_status bc_create(int device, const bc_params *params, bc_ctx **out);
+
+/* Release every device and host resource of the context (NULL is a no-op). */
+bc_status bc_destroy(bc_ctx *ctx);
+
+/*
+ * Upload shape `which` (0 = A, the fixed solid; 1 = B, the moving solid).
+ *   xyzr: host or device, n rows of (x, y, z, r) doubles, r > 0, all finite.
+ *   w:    host or device; n doubles (REAL) or 2n interleaved doubles (COMPLEX);
+ *         NULL means every weight is 1.
+ * The data are copied; re-uploading A invalidates the spectrum of A.
+ * Spectral mode additionally checks, once both shapes exist, that no
+ * periodic image of f's support reaches the grid: with the per-axis support
+ * bound S = max_i |a_i,axis| + max_j |b_j| + max r + max s it requires
+ * P >= max(S - t0, t0 + (N-1) h + S) on every axis (P = Np h), else
+ * BC_ERANGE.  The box of each shape must also fit its spreading plan.
+ * Synchronous with respect to the host.
+ */
+bc_status bc_shape_upload(bc_ctx *ctx, int which, const double *xyzr, const double *w, int64_t n);
+
+/* Compute and keep the spectrum of A on the band (spectral mode; a no-op in
+ * exact mode).  Idempotent.  BC_ESTATE if A is missing.  Asynchronous on `stream`. */
+bc_status bc_spectrum_A(bc_ctx *ctx, void *stream);
+
+/*
+ * Correlate A with R B for n_rot rotations.
+ *   R:   host or device, n_rot row-major 3x3 doubles; R R^T = I within 1e-6
+ *        and det R > 0, else BC_EINVAL.
+ *   out: host or device buffer laid out per bc_out_kind.
+ * Device buffers: asynchronous on `stream`.  Host buffers: the call stages
+ * them and returns after the result has reached `out`.
+ * Spectral mode needs bc_spectrum_A first (BC_ESTATE otherwise).
+ */
+bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, int out_kind,
+                                 void *out, void *stream);
+
+/* Last error message of the context (static string if ctx == NULL). */
+const char *bc_last_error(const bc_ctx *ctx);
+const char *bc_status_string(int status);
+
+/*
+ * Introspection (tests / bench): named double-valued properties of the plan.
+ * Keys: "P", "tau_A", "tau_B", "G_A", "G_B", "L_A", "L_B", "c_A", "c_B",
+ * "cut_A", "cut_B", "band_modes", "batch", "bytes_workspace".
+ */
+bc_status bc_query(const bc_ctx *ctx, const char *key, double *value);
+
+/* Number of kernels this context has launched so far. */
+int64_t bc_launch_count(const bc_ctx *ctx);
+
+/*
+ * Per-stage device timing: when enabled, the library records CUDA events on
+ * the launching stream around every kernel of bc_correlate_rotations and
+ * accumulates their durations per stage.  bc_stage_times fills up to `cap`
+ * entries of names/total_ms/launches and returns the number of stages.
+ */
+bc_status bc_set_profiling(bc_ctx *ctx, int enabled);
+int bc_stage_times(bc_ctx *ctx, const char **names, double *total_ms, int64_t *launches, int cap);
+bc_status bc_reset_stage_times(bc_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BALLCORR_H */

@@ -1,0 +1,242 @@
+"""Thin ctypes binding of libballcorr.so (include/ballcorr.h).
+
+Argument marshalling only: every step of the correlation runs in the CUDA
+kernels behind the C ABI.  If the shared library is missing this module
+raises at import time; there is no CPU fallback.
+
+The C entry points are re-exported under their own names (`bc_create`,
+`bc_shape_upload`, `bc_spectrum_A`, `bc_correlate_rotations`, ...);
+`Correlator` wraps them for numpy / torch callers.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libballcorr.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"libballcorr.so not found at {LIB_PATH}: build it with `make` (or __graft_entry__.build()). "
+        "There is no CPU fallback.")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+BC_OK, BC_EINVAL, BC_ERANGE, BC_ENOMEM, BC_ESTATE, BC_EUNSUPPORTED, BC_ECUDA = range(7)
+BC_FP32, BC_FP64 = 0, 1
+BC_MODE_SPECTRAL, BC_MODE_EXACT = 0, 1
+BC_WEIGHTS_REAL, BC_WEIGHTS_COMPLEX = 0, 1
+BC_OUT_F_FULL, BC_OUT_MIN_ARGMIN, BC_OUT_MAX_ARGMAX, BC_OUT_MINMAX, BC_OUT_MAX_REAL = range(5)
+
+OUT_KINDS = {"full": BC_OUT_F_FULL, "min_argmin": BC_OUT_MIN_ARGMIN, "max_argmax": BC_OUT_MAX_ARGMAX,
+             "minmax": BC_OUT_MINMAX, "max_real": BC_OUT_MAX_REAL}
+
+
+class bc_params(ctypes.Structure):
+    _fields_ = [("N", ctypes.c_int32), ("h", ctypes.c_double), ("t0", ctypes.c_double * 3),
+                ("Np", ctypes.c_int32), ("K", ctypes.c_int32), ("precision", ctypes.c_int32),
+                ("mode", ctypes.c_int32), ("weights", ctypes.c_int32), ("max_batch", ctypes.c_int32),
+                ("spread_eps", ctypes.c_double)]
+
+
+EXTREMUM_DTYPE = np.dtype([("val", np.float64), ("idx", np.int64)])
+
+_vp = ctypes.c_void_p
+_lib.bc_create.argtypes = [ctypes.c_int, ctypes.POINTER(bc_params), ctypes.POINTER(_vp)]
+_lib.bc_create.restype = ctypes.c_int
+_lib.bc_destroy.argtypes = [_vp]
+_lib.bc_destroy.restype = ctypes.c_int
+_lib.bc_shape_upload.argtypes = [_vp, ctypes.c_int, _vp, _vp, ctypes.c_int64]
+_lib.bc_shape_upload.restype = ctypes.c_int
+_lib.bc_spectrum_A.argtypes = [_vp, _vp]
+_lib.bc_spectrum_A.restype = ctypes.c_int
+_lib.bc_correlate_rotations.argtypes = [_vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, _vp]
+_lib.bc_correlate_rotations.restype = ctypes.c_int
+_lib.bc_last_error.argtypes = [_vp]
+_lib.bc_last_error.restype = ctypes.c_char_p
+_lib.bc_status_string.argtypes = [ctypes.c_int]
+_lib.bc_status_string.restype = ctypes.c_char_p
+_lib.bc_query.argtypes = [_vp, ctypes.c_char_p, ctypes.POINTER(ctypes.c_double)]
+_lib.bc_query.restype = ctypes.c_int
+_lib.bc_launch_count.argtypes = [_vp]
+_lib.bc_launch_count.restype = ctypes.c_int64
+_lib.bc_set_profiling.argtypes = [_vp, ctypes.c_int]
+_lib.bc_set_profiling.restype = ctypes.c_int
+_lib.bc_stage_times.argtypes = [_vp, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_double),
+                                ctypes.POINTER(ctypes.c_int64), ctypes.c_int]
+_lib.bc_stage_times.restype = ctypes.c_int
+_lib.bc_reset_stage_times.argtypes = [_vp]
+_lib.bc_reset_stage_times.restype = ctypes.c_int
+
+# the C names, re-exported
+bc_create = _lib.bc_create
+bc_destroy = _lib.bc_destroy
+bc_shape_upload = _lib.bc_shape_upload
+bc_spectrum_A = _lib.bc_spectrum_A
+bc_correlate_rotations = _lib.bc_correlate_rotations
+bc_last_error = _lib.bc_last_error
+bc_status_string = _lib.bc_status_string
+bc_query = _lib.bc_query
+bc_launch_count = _lib.bc_launch_count
+bc_set_profiling = _lib.bc_set_profiling
+bc_stage_times = _lib.bc_stage_times
+bc_reset_stage_times = _lib.bc_reset_stage_times
+
+
+class BallCorrError(RuntimeError):
+    def __init__(self, status, msg):
+        self.status = status
+        super().__init__(f"{_lib.bc_status_string(status).decode()}: {msg}")
+
+
+def _ptr(a):
+    """(address, keepalive) of a numpy array or torch tensor (host or device)."""
+    if a is None:
+        return None, None
+    if hasattr(a, "data_ptr"):  # torch tensor
+        if not a.is_contiguous():
+            a = a.contiguous()
+        return a.data_ptr(), a
+    a = np.ascontiguousarray(a)
+    return a.ctypes.data, a
+
+
+def _as_f64(a, cols=None):
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        import torch
+        return a.to(torch.float64).contiguous()
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a
+
+
+def _weights_f64(w, complex_w):
+    if w is None:
+        return None
+    if hasattr(w, "data_ptr"):
+        import torch
+        if complex_w:
+            return torch.view_as_real(w.to(torch.complex128).contiguous()).contiguous()
+        return w.to(torch.float64).contiguous()
+    w = np.asarray(w)
+    if complex_w:
+        w = np.ascontiguousarray(w, dtype=np.complex128).view(np.float64)
+    else:
+        w = np.ascontiguousarray(w, dtype=np.float64)
+    return w
+
+
+def _stream_handle(stream):
+    if stream is None:
+        return None
+    if hasattr(stream, "cuda_stream"):
+        return stream.cuda_stream
+    return int(stream)
+
+
+class Correlator:
+    """One libballcorr context on one device."""
+
+    def __init__(self, N, h, t0, Np=0, K=0, mode="spectral", precision="f32", weights="real",
+                 max_batch=0, spread_eps=0.0, device=0):
+        p = bc_params()
+        p.N = int(N)
+        p.h = float(h)
+        for i in range(3):
+            p.t0[i] = float(t0[i])
+        p.Np = int(Np)
+        p.K = int(K)
+        p.precision = BC_FP64 if precision in ("f64", "fp64", BC_FP64) else BC_FP32
+        p.mode = BC_MODE_EXACT if mode in ("exact", BC_MODE_EXACT) else BC_MODE_SPECTRAL
+        p.weights = BC_WEIGHTS_COMPLEX if weights in ("complex", BC_WEIGHTS_COMPLEX) else BC_WEIGHTS_REAL
+        p.max_batch = int(max_batch)
+        p.spread_eps = float(spread_eps)
+        self.params = p
+        self.N = p.N
+        self.complex = p.weights == BC_WEIGHTS_COMPLEX
+        self.f64 = p.precision == BC_FP64 and p.mode == BC_MODE_EXACT
+        self._ctx = _vp()
+        st = _lib.bc_create(int(device), ctypes.byref(p), ctypes.byref(self._ctx))
+        if st != BC_OK:
+            raise BallCorrError(st, "bc_create failed")
+
+    # -- error helper
+    def _check(self, st):
+        if st != BC_OK:
+            raise BallCorrError(st, _lib.bc_last_error(self._ctx).decode())
+
+    def close(self):
+        if self._ctx:
+            _lib.bc_destroy(self._ctx)
+            self._ctx = _vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- the three calls of the path
+    def shape_upload(self, which, xyzr, w=None):
+        x = _as_f64(xyzr)
+        n = int(x.shape[0]) if x is not None else 0
+        wv = _weights_f64(w, self.complex)
+        px, kx = _ptr(x)
+        pw, kw = _ptr(wv)
+        self._check(_lib.bc_shape_upload(self._ctx, int(which), px, pw, n))
+
+    def spectrum_A(self, stream=None):
+        self._check(_lib.bc_spectrum_A(self._ctx, _stream_handle(stream)))
+
+    def out_shape(self, n_rot, out_kind):
+        kind = OUT_KINDS.get(out_kind, out_kind)
+        if kind == BC_OUT_F_FULL:
+            shp = (n_rot, self.N, self.N, self.N) + ((2,) if self.complex else ())
+            return kind, shp, (np.float64 if self.f64 else np.float32)
+        return kind, (n_rot, 2) if kind == BC_OUT_MINMAX else (n_rot,), EXTREMUM_DTYPE
+
+    def correlate_rotations(self, R, out_kind="full", out=None, stream=None):
+        """R: (n_rot, 3, 3) host numpy / torch (host or cuda).  `out`: optional preallocated
+        numpy array or torch tensor (host or cuda) of the right byte size.  Returns `out`
+        (numpy structured array for reductions when allocated here)."""
+        Rv = _as_f64(R)
+        n_rot = int(Rv.shape[0])
+        kind, shp, dt = self.out_shape(n_rot, out_kind)
+        if out is None:
+            out = np.empty(shp, dtype=dt)
+        pr, kr = _ptr(Rv)
+        po, ko = _ptr(out)
+        self._check(_lib.bc_correlate_rotations(self._ctx, pr, n_rot, kind, po, _stream_handle(stream)))
+        return out
+
+    # -- introspection / profiling
+    def query(self, key):
+        v = ctypes.c_double()
+        self._check(_lib.bc_query(self._ctx, key.encode(), ctypes.byref(v)))
+        return v.value
+
+    def launch_count(self):
+        return int(_lib.bc_launch_count(self._ctx))
+
+    def set_profiling(self, on=True):
+        self._check(_lib.bc_set_profiling(self._ctx, 1 if on else 0))
+
+    def reset_stage_times(self):
+        self._check(_lib.bc_reset_stage_times(self._ctx))
+
+    def stage_times(self):
+        cap = 64
+        names = (ctypes.c_char_p * cap)()
+        ms = (ctypes.c_double * cap)()
+        cnt = (ctypes.c_int64 * cap)()
+        n = _lib.bc_stage_times(self._ctx, names, ms, cnt, cap)
+        return {names[i].decode(): (ms[i], int(cnt[i])) for i in range(min(n, cap))}
+
+
+def extremum_to_numpy(buf):
+    """View a torch uint8/float buffer holding bc_extremum records as a numpy structured array."""
+    return np.frombuffer(bytes(buf), dtype=EXTREMUM_DTYPE)

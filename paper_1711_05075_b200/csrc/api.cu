@@ -1,0 +1,1057 @@
+// api.cu -- the C ABI of libballcorr: contexts, validation, plans, orchestration.
+//
+// Every compute step runs in the kernels of spectral.cu / exact.cu; this file
+// only validates, plans, allocates and launches.  There is no CPU fallback.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "ballcorr.h"
+#include "kernels.cuh"
+
+namespace {
+
+const double kPi = 3.14159265358979323846;
+
+struct ShapePlan {
+    bool ok = false;
+    int L = 0, c = 0, G = 0;
+    int o[3] = {0, 0, 0};
+    double hf = 0, tau = 0, cut = 0;
+    FftPlan fft{};
+    float2 *d_mult[3] = {nullptr, nullptr, nullptr};  // axis x, y, z
+};
+
+struct PendingEvent {
+    const char *name;
+    cudaEvent_t e0, e1;
+};
+
+}  // namespace
+
+struct bc_ctx {
+    int device = 0;
+    bc_params p{};
+    std::string err;
+
+    // shapes (0 = A, 1 = B)
+    bool have[2] = {false, false};
+    int64_t n[2] = {0, 0};
+    std::vector<double> hxyzr[2];
+    std::vector<double> hw[2];  // interleaved (re, im)
+    float4 *d_balls[2] = {nullptr, nullptr};
+    float *d_wre[2] = {nullptr, nullptr};
+    float *d_wim[2] = {nullptr, nullptr};
+    double4 *d_balls64[2] = {nullptr, nullptr};
+    double2 *d_w64[2] = {nullptr, nullptr};
+
+    // spectral
+    double P = 0;
+    int K = 0, M = 0, Kz = 0, Fz = 0;
+    ShapePlan plan[2];
+    FftPlan fft_np{};
+    int *d_csr_off = nullptr, *d_csr_idx = nullptr;
+    float2 *d_Ahat = nullptr;
+    bool have_spec = false;
+    float2 *d_ph[3] = {nullptr, nullptr, nullptr};
+
+    // workspaces
+    void *ws1 = nullptr, *ws2 = nullptr;
+    size_t ws1_bytes = 0, ws2_bytes = 0;
+    unsigned long long *d_keys = nullptr;
+    int keys_cap = 0;
+    float *d_rot = nullptr;
+    double *d_rot64 = nullptr;
+    int64_t rot_cap = 0;
+    void *d_out_stage = nullptr;
+    size_t out_stage_bytes = 0;
+    double *d_acc = nullptr;
+    size_t acc_bytes = 0;
+    double *d_part = nullptr;
+    long long *d_part_idx = nullptr;
+    int part_cap = 0;
+    int batch = 1;
+
+    int64_t launches = 0;
+    bool prof = false;
+    std::vector<PendingEvent> pending;
+    std::vector<cudaEvent_t> event_pool;
+    std::map<std::string, std::pair<double, int64_t>> stage_ms;
+    std::vector<std::string> stage_order;
+};
+
+namespace {
+
+bc_status fail(bc_ctx *ctx, bc_status st, const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    if (ctx) ctx->err = buf;
+    return st;
+}
+
+#define CU(ctx, call)                                                                               \
+    do {                                                                                            \
+        cudaError_t _e = (call);                                                                    \
+        if (_e != cudaSuccess)                                                                      \
+            return fail(ctx, _e == cudaErrorMemoryAllocation ? BC_ENOMEM : BC_ECUDA, "%s: %s (%s:%d)", \
+                        #call, cudaGetErrorString(_e), __FILE__, __LINE__);                         \
+    } while (0)
+
+#define TRY(expr)                      \
+    do {                               \
+        bc_status _s = (expr);         \
+        if (_s != BC_OK) return _s;    \
+    } while (0)
+
+bool friendly(int L)
+{
+    if (L < 1) return false;
+    for (int f : {2, 3, 5})
+        while (L % f == 0) L /= f;
+    return L == 1;
+}
+
+bool make_fft_plan(int L, FftPlan &pl)
+{
+    if (!friendly(L)) return false;
+    pl.L = L;
+    pl.nst = 0;
+    int r = L;
+    while (r % 8 == 0 && pl.nst < BC_FFT_MAX_STAGES) { pl.radix[pl.nst++] = 8; r /= 8; }
+    while (r % 4 == 0 && pl.nst < BC_FFT_MAX_STAGES) { pl.radix[pl.nst++] = 4; r /= 4; }
+    while (r % 2 == 0 && pl.nst < BC_FFT_MAX_STAGES) { pl.radix[pl.nst++] = 2; r /= 2; }
+    while (r % 5 == 0 && pl.nst < BC_FFT_MAX_STAGES) { pl.radix[pl.nst++] = 5; r /= 5; }
+    while (r % 3 == 0 && pl.nst < BC_FFT_MAX_STAGES) { pl.radix[pl.nst++] = 3; r /= 3; }
+    return r == 1;
+}
+
+bool is_device_ptr(const void *ptr)
+{
+    if (!ptr) return false;
+    cudaPointerAttributes at;
+    cudaError_t e = cudaPointerGetAttributes(&at, ptr);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+bc_status fetch_host(bc_ctx *ctx, const double *src, size_t count, std::vector<double> &dst)
+{
+    dst.resize(count);
+    if (count == 0) return BC_OK;
+    if (is_device_ptr(src))
+        CU(ctx, cudaMemcpy(dst.data(), src, count * sizeof(double), cudaMemcpyDeviceToHost));
+    else
+        memcpy(dst.data(), src, count * sizeof(double));
+    return BC_OK;
+}
+
+template <typename T>
+bc_status dalloc(bc_ctx *ctx, T **ptr, size_t bytes)
+{
+    if (*ptr) {
+        cudaFree(*ptr);
+        *ptr = nullptr;
+    }
+    if (bytes == 0) bytes = 16;
+    CU(ctx, cudaMalloc((void **)ptr, bytes));
+    return BC_OK;
+}
+
+template <typename T>
+void dfree(T *&ptr)
+{
+    if (ptr) cudaFree((void *)ptr);
+    ptr = nullptr;
+}
+
+// ------------------------------------------------------------------ profiling helpers
+
+cudaEvent_t take_event(bc_ctx *ctx)
+{
+    if (!ctx->event_pool.empty()) {
+        cudaEvent_t e = ctx->event_pool.back();
+        ctx->event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+struct StageScope {
+    bc_ctx *ctx;
+    cudaStream_t s;
+    const char *name;
+    cudaEvent_t e0 = nullptr;
+    StageScope(bc_ctx *c, cudaStream_t st, const char *nm) : ctx(c), s(st), name(nm)
+    {
+        if (ctx->prof) {
+            e0 = take_event(ctx);
+            cudaEventRecord(e0, s);
+        }
+    }
+    ~StageScope()
+    {
+        if (ctx->prof) {
+            cudaEvent_t e1 = take_event(ctx);
+            cudaEventRecord(e1, s);
+            ctx->pending.push_back({name, e0, e1});
+        }
+    }
+};
+
+void collect_profile(bc_ctx *ctx)
+{
+    if (ctx->pending.empty()) return;
+    cudaEventSynchronize(ctx->pending.back().e1);
+    for (auto &pe : ctx->pending) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, pe.e0, pe.e1);
+        auto it = ctx->stage_ms.find(pe.name);
+        if (it == ctx->stage_ms.end()) {
+            ctx->stage_ms[pe.name] = {ms, 1};
+            ctx->stage_order.push_back(pe.name);
+        } else {
+            it->second.first += ms;
+            it->second.second += 1;
+        }
+        ctx->event_pool.push_back(pe.e0);
+        ctx->event_pool.push_back(pe.e1);
+    }
+    ctx->pending.clear();
+}
+
+// ------------------------------------------------------------------ spectral plan of one shape
+
+// Choose (c, L, G, tau, cut, origin) so that the Gaussian-smoothed density of
+// a shape whose centres lie in [lo, hi] (radii <= rmax) fits a box of L fine
+// cells at spacing hf = P / G, with G = c L >= 4 (K + 1) (spread oversampling
+// sigma_n ~ 2) and alias / truncation level eps.
+bc_status plan_shape(bc_ctx *ctx, int which, const double lo[3], const double hi[3], double rmax)
+{
+    const double P = ctx->P;
+    const int K = ctx->K;
+    const double eps = ctx->p.spread_eps > 0 ? ctx->p.spread_eps : 1e-7;
+    const double lg = std::log(1.0 / eps);
+    const int Gmin = 4 * (K + 1);
+    double extent = 0;
+    for (int a = 0; a < 3; a++) extent = std::max(extent, hi[a] - lo[a]);
+    extent += 2 * rmax;
+
+    ShapePlan best;
+    double best_cost = 1e300;
+    for (int c = 1; c <= 8; c++) {
+        int L = (Gmin + c - 1) / c;
+        for (; L <= 1024; L++) {
+            if (!friendly(L)) continue;
+            const int G = c * L;
+            const double hf = P / G;
+            const double ke = (double)K / P, ka = (double)(G - K) / P;
+            const double tau = std::sqrt(lg / (2 * kPi * kPi * (ka * ka - ke * ke)));
+            const double cut = tau * std::sqrt(2 * lg);
+            if (L * hf >= extent + 2 * cut + 4 * hf) {
+                const double cost = (double)G * ((double)L * L + (double)L * ctx->Kz + (double)ctx->M * ctx->Kz);
+                if (cost < best_cost) {
+                    best_cost = cost;
+                    best = ShapePlan();
+                    best.ok = true;
+                    best.L = L;
+                    best.c = c;
+                    best.G = G;
+                    best.hf = hf;
+                    best.tau = tau;
+                    best.cut = cut;
+                }
+                break;
+            }
+        }
+    }
+    if (!best.ok)
+        return fail(ctx, BC_ERANGE, "shape %c: no spreading box of <= 1024 cells fits extent %.6g with K=%d, P=%.6g",
+                    which ? 'B' : 'A', extent, K, P);
+    for (int a = 0; a < 3; a++) {
+        best.o[a] = (int)std::floor((lo[a] - rmax - best.cut) / best.hf) - 2;
+        if ((best.o[a] + best.L) * best.hf < hi[a] + rmax + best.cut + best.hf)
+            return fail(ctx, BC_ERANGE, "internal: box does not cover shape %c on axis %d", which ? 'B' : 'A', a);
+    }
+    if (!make_fft_plan(best.L, best.fft)) return fail(ctx, BC_EUNSUPPORTED, "box length %d not factorable", best.L);
+
+    // multipliers: hf exp(-2 pi i k o / G) exp(+2 pi^2 tau^2 k^2 / P^2)   (shift + Gaussian deconvolution)
+    ShapePlan &dst = ctx->plan[which];
+    for (int a = 0; a < 3; a++) dfree(dst.d_mult[a]);
+    dst = best;
+    const bool cplx = ctx->p.weights == BC_WEIGHTS_COMPLEX;
+    for (int a = 0; a < 3; a++) {
+        const int klo = (a == 2 && !cplx) ? 0 : -K;
+        const int nk = (a == 2) ? ctx->Kz : ctx->M;
+        std::vector<float2> m(nk);
+        for (int q = 0; q < nk; q++) {
+            const long long k = klo + q;
+            const long long num = ((k * dst.o[a]) % dst.G + dst.G) % dst.G;
+            const double ang = -2 * kPi * (double)num / dst.G;
+            const double amp = dst.hf * std::exp(2 * kPi * kPi * dst.tau * dst.tau * (double)(k * k) / (P * P));
+            m[q] = make_float2((float)(amp * std::cos(ang)), (float)(amp * std::sin(ang)));
+        }
+        TRY(dalloc(ctx, &dst.d_mult[a], sizeof(float2) * nk));
+        CU(ctx, cudaMemcpy(dst.d_mult[a], m.data(), sizeof(float2) * nk, cudaMemcpyHostToDevice));
+    }
+    return BC_OK;
+}
+
+void shape_bounds(const bc_ctx *ctx, int which, double lo[3], double hi[3], double &rmax, double &rho)
+{
+    const std::vector<double> &x = ctx->hxyzr[which];
+    for (int a = 0; a < 3; a++) {
+        lo[a] = 1e300;
+        hi[a] = -1e300;
+    }
+    rmax = 0;
+    rho = 0;
+    for (int64_t i = 0; i < ctx->n[which]; i++) {
+        double nr = 0;
+        for (int a = 0; a < 3; a++) {
+            lo[a] = std::min(lo[a], x[4 * i + a]);
+            hi[a] = std::max(hi[a], x[4 * i + a]);
+            nr += x[4 * i + a] * x[4 * i + a];
+        }
+        rmax = std::max(rmax, x[4 * i + 3]);
+        rho = std::max(rho, std::sqrt(nr));
+    }
+}
+
+bc_status check_support(bc_ctx *ctx)
+{
+    if (ctx->p.mode != BC_MODE_SPECTRAL || !ctx->have[0] || !ctx->have[1]) return BC_OK;
+    if (ctx->n[0] == 0 || ctx->n[1] == 0) return BC_OK;
+    double loA[3], hiA[3], rA, rhoA, loB[3], hiB[3], rB, rhoB;
+    shape_bounds(ctx, 0, loA, hiA, rA, rhoA);
+    shape_bounds(ctx, 1, loB, hiB, rB, rhoB);
+    for (int a = 0; a < 3; a++) {
+        const double S = std::max(std::fabs(loA[a]), std::fabs(hiA[a])) + rhoB + rA + rB;
+        const double need = std::max(S - ctx->p.t0[a], ctx->p.t0[a] + (ctx->p.N - 1) * ctx->p.h + S);
+        if (ctx->P < need)
+            return fail(ctx, BC_ERANGE,
+                        "axis %d: support bound S=%.6g needs period P >= %.6g but P = Np*h = %.6g", a, S, need, ctx->P);
+    }
+    return BC_OK;
+}
+
+bc_status build_csr_A(bc_ctx *ctx)
+{
+    const ShapePlan &pl = ctx->plan[0];
+    const int tpa = (pl.L + 15) / 16;
+    const int ntiles = tpa * tpa * tpa;
+    std::vector<std::vector<int>> lists(ntiles);
+    const std::vector<double> &x = ctx->hxyzr[0];
+    for (int64_t i = 0; i < ctx->n[0]; i++) {
+        double u[3];
+        int t0[3], t1[3];
+        const double rc = (x[4 * i + 3] + pl.cut) / pl.hf;
+        for (int a = 0; a < 3; a++) {
+            u[a] = x[4 * i + a] / pl.hf - pl.o[a];
+            t0[a] = std::max(0, (int)std::floor((u[a] - rc - 1) / 16));
+            t1[a] = std::min(tpa - 1, (int)std::floor((u[a] + rc + 1) / 16));
+        }
+        for (int tx = t0[0]; tx <= t1[0]; tx++)
+            for (int ty = t0[1]; ty <= t1[1]; ty++)
+                for (int tz = t0[2]; tz <= t1[2]; tz++) lists[(tx * tpa + ty) * tpa + tz].push_back((int)i);
+    }
+    std::vector<int> off(ntiles + 1, 0), idx;
+    for (int t = 0; t < ntiles; t++) off[t + 1] = off[t] + (int)lists[t].size();
+    idx.reserve(off[ntiles]);
+    for (int t = 0; t < ntiles; t++) idx.insert(idx.end(), lists[t].begin(), lists[t].end());
+    TRY(dalloc(ctx, &ctx->d_csr_off, sizeof(int) * off.size()));
+    TRY(dalloc(ctx, &ctx->d_csr_idx, sizeof(int) * std::max<size_t>(1, idx.size())));
+    CU(ctx, cudaMemcpy(ctx->d_csr_off, off.data(), sizeof(int) * off.size(), cudaMemcpyHostToDevice));
+    if (!idx.empty()) CU(ctx, cudaMemcpy(ctx->d_csr_idx, idx.data(), sizeof(int) * idx.size(), cudaMemcpyHostToDevice));
+    return BC_OK;
+}
+
+bc_status ensure_ws(bc_ctx *ctx, void **ptr, size_t &cur, size_t need)
+{
+    if (need <= cur && *ptr) return BC_OK;
+    if (*ptr) cudaFree(*ptr);
+    *ptr = nullptr;
+    cur = 0;
+    CU(ctx, cudaMalloc(ptr, need));
+    cur = need;
+    return BC_OK;
+}
+
+// per-rotation sizes (bytes) of the two ping-pong spectral workspaces of shape B
+void spectral_ws_sizes(const bc_ctx *ctx, int which, size_t &s1, size_t &s2)
+{
+    const ShapePlan &pl = ctx->plan[which];
+    const size_t L = pl.L, Kz = ctx->Kz, M = ctx->M, Np = ctx->p.Np, N = ctx->p.N, Fz = ctx->Fz;
+    const bool cplx = ctx->p.weights == BC_WEIGHTS_COMPLEX;
+    const size_t box = L * L * L * (cplx ? 8 : 4);
+    const size_t T1 = L * L * Kz * 8, T2 = L * M * Kz * 8, Bh = M * M * Kz * 8;
+    const size_t F = Np * Np * Fz * 8, X1 = N * Np * Fz * 8, Y1 = N * N * Fz * 8;
+    s1 = std::max(std::max(box, T2), std::max(F, Y1));
+    s2 = std::max(std::max(T1, Bh), X1);
+    s1 = (s1 + 255) / 256 * 256;
+    s2 = (s2 + 255) / 256 * 256;
+}
+
+// spread + three axis passes of one shape -> band spectrum (k layout [kx][ky][kz])
+bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, void *box_T2, void *T1_out,
+                         float2 *spec_out, size_t s1_per, size_t s2_per, cudaStream_t s)
+{
+    const ShapePlan &pl = ctx->plan[which];
+    const bool cplx = ctx->p.weights == BC_WEIGHTS_COMPLEX;
+    const int L = pl.L;
+    {
+        SpreadArgs a{};
+        a.L = L;
+        a.ox = pl.o[0];
+        a.oy = pl.o[1];
+        a.oz = pl.o[2];
+        a.hf = (float)pl.hf;
+        a.inv_hf = (float)(1.0 / pl.hf);
+        a.tau = (float)pl.tau;
+        a.cut = (float)pl.cut;
+        a.n_balls = (int)ctx->n[which];
+        a.balls = ctx->d_balls[which];
+        a.w_re = ctx->d_wre[which];
+        a.w_im = ctx->d_wim[which];
+        a.csr_off = which == 0 ? ctx->d_csr_off : nullptr;
+        a.csr_idx = which == 0 ? ctx->d_csr_idx : nullptr;
+        a.rot = d_rot;
+        a.complex_w = cplx;
+        a.out = box_T2;
+        a.out_batch_stride = (long long)(s1_per / (cplx ? 8 : 4));
+        a.tiles_per_axis = (L + 15) / 16;
+        StageScope sc(ctx, s, which ? "spread_B" : "spread_A");
+        launch_spread(a, nb, s);
+        ctx->launches++;
+    }
+    {
+        AxisArgs a{};
+        a.L = L;
+        a.c = pl.c;
+        a.klo = cplx ? -ctx->K : 0;
+        a.nk = ctx->Kz;
+        a.signed_k = 1;
+        a.sign = -1.f;
+        a.mult = pl.d_mult[2];
+        a.plan = pl.fft;
+        a.in = box_T2;
+        a.in_real = !cplx;
+        a.in_bstride = (long long)(s1_per / (cplx ? 8 : 4));
+        a.out = (float2 *)T1_out;
+        a.out_bstride = (long long)(s2_per / 8);
+        StageScope sc(ctx, s, which ? "axis_z_B" : "axis_z_A");
+        launch_axis_contig(a, L * L, nb, s);
+        ctx->launches++;
+    }
+    {
+        AxisArgs a{};
+        a.L = L;
+        a.c = pl.c;
+        a.klo = -ctx->K;
+        a.nk = ctx->M;
+        a.signed_k = 1;
+        a.sign = -1.f;
+        a.mult = pl.d_mult[1];
+        a.plan = pl.fft;
+        a.O = L;
+        a.I = ctx->Kz;
+        a.in = T1_out;
+        a.in_bstride = (long long)(s2_per / 8);
+        a.out = (float2 *)box_T2;
+        a.out_bstride = (long long)(s1_per / 8);
+        StageScope sc(ctx, s, which ? "axis_y_B" : "axis_y_A");
+        launch_axis_strided(a, nb, s);
+        ctx->launches++;
+    }
+    {
+        AxisArgs a{};
+        a.L = L;
+        a.c = pl.c;
+        a.klo = -ctx->K;
+        a.nk = ctx->M;
+        a.signed_k = 1;
+        a.sign = -1.f;
+        a.mult = pl.d_mult[0];
+        a.plan = pl.fft;
+        a.O = 1;
+        a.I = ctx->M * ctx->Kz;
+        a.in = box_T2;
+        a.in_bstride = (long long)(s1_per / 8);
+        a.out = spec_out;
+        a.out_bstride = (long long)(s2_per / 8);
+        StageScope sc(ctx, s, which ? "axis_x_B" : "axis_x_A");
+        launch_axis_strided(a, nb, s);
+        ctx->launches++;
+    }
+    CU(ctx, cudaGetLastError());
+    return BC_OK;
+}
+
+bc_status upload_shape_device(bc_ctx *ctx, int which)
+{
+    const int64_t n = ctx->n[which];
+    const size_t cnt = (size_t)std::max<int64_t>(n, 1);
+    std::vector<float4> b(cnt);
+    std::vector<float> wr(cnt), wi(cnt);
+    std::vector<double4> b64(cnt);
+    std::vector<double2> w64(cnt);
+    for (int64_t i = 0; i < n; i++) {
+        const double *x = &ctx->hxyzr[which][4 * i];
+        b[i] = make_float4((float)x[0], (float)x[1], (float)x[2], (float)x[3]);
+        b64[i] = make_double4(x[0], x[1], x[2], x[3]);
+        wr[i] = (float)ctx->hw[which][2 * i];
+        wi[i] = (float)ctx->hw[which][2 * i + 1];
+        w64[i] = make_double2(ctx->hw[which][2 * i], ctx->hw[which][2 * i + 1]);
+    }
+    TRY(dalloc(ctx, &ctx->d_balls[which], sizeof(float4) * cnt));
+    TRY(dalloc(ctx, &ctx->d_wre[which], sizeof(float) * cnt));
+    TRY(dalloc(ctx, &ctx->d_wim[which], sizeof(float) * cnt));
+    TRY(dalloc(ctx, &ctx->d_balls64[which], sizeof(double4) * cnt));
+    TRY(dalloc(ctx, &ctx->d_w64[which], sizeof(double2) * cnt));
+    CU(ctx, cudaMemcpy(ctx->d_balls[which], b.data(), sizeof(float4) * cnt, cudaMemcpyHostToDevice));
+    CU(ctx, cudaMemcpy(ctx->d_wre[which], wr.data(), sizeof(float) * cnt, cudaMemcpyHostToDevice));
+    CU(ctx, cudaMemcpy(ctx->d_wim[which], wi.data(), sizeof(float) * cnt, cudaMemcpyHostToDevice));
+    CU(ctx, cudaMemcpy(ctx->d_balls64[which], b64.data(), sizeof(double4) * cnt, cudaMemcpyHostToDevice));
+    CU(ctx, cudaMemcpy(ctx->d_w64[which], w64.data(), sizeof(double2) * cnt, cudaMemcpyHostToDevice));
+    return BC_OK;
+}
+
+bc_status validate_rotations(bc_ctx *ctx, const std::vector<double> &R, int64_t n_rot)
+{
+    for (int64_t r = 0; r < n_rot; r++) {
+        const double *m = &R[9 * r];
+        for (int q = 0; q < 9; q++)
+            if (!std::isfinite(m[q])) return fail(ctx, BC_EINVAL, "rotation %lld has a non-finite entry", (long long)r);
+        for (int i = 0; i < 3; i++)
+            for (int j = 0; j < 3; j++) {
+                double d = 0;
+                for (int k = 0; k < 3; k++) d += m[3 * i + k] * m[3 * j + k];
+                if (std::fabs(d - (i == j ? 1.0 : 0.0)) > 1e-6)
+                    return fail(ctx, BC_EINVAL, "rotation %lld: R R^T deviates from I by %.3g", (long long)r,
+                                std::fabs(d - (i == j ? 1.0 : 0.0)));
+            }
+        const double det = m[0] * (m[4] * m[8] - m[5] * m[7]) - m[1] * (m[3] * m[8] - m[5] * m[6]) +
+                           m[2] * (m[3] * m[7] - m[4] * m[6]);
+        if (det <= 0) return fail(ctx, BC_EINVAL, "rotation %lld has det %.6g <= 0", (long long)r, det);
+    }
+    return BC_OK;
+}
+
+size_t out_elem_bytes(const bc_ctx *ctx, int kind)
+{
+    const bool cplx = ctx->p.weights == BC_WEIGHTS_COMPLEX;
+    const bool f64 = ctx->p.precision == BC_FP64 && ctx->p.mode == BC_MODE_EXACT;
+    if (kind == BC_OUT_F_FULL) {
+        const size_t N3 = (size_t)ctx->p.N * ctx->p.N * ctx->p.N;
+        return N3 * (f64 ? 8 : 4) * (cplx ? 2 : 1);
+    }
+    return sizeof(bc_extremum) * (kind == BC_OUT_MINMAX ? 2 : 1);
+}
+
+}  // namespace
+
+// ============================================================================ public API
+
+extern "C" {
+
+const char *bc_status_string(int st)
+{
+    switch (st) {
+    case BC_OK: return "BC_OK";
+    case BC_EINVAL: return "BC_EINVAL";
+    case BC_ERANGE: return "BC_ERANGE";
+    case BC_ENOMEM: return "BC_ENOMEM";
+    case BC_ESTATE: return "BC_ESTATE";
+    case BC_EUNSUPPORTED: return "BC_EUNSUPPORTED";
+    case BC_ECUDA: return "BC_ECUDA";
+    default: return "BC_UNKNOWN";
+    }
+}
+
+const char *bc_last_error(const bc_ctx *ctx)
+{
+    if (!ctx) return "no context";
+    return ctx->err.c_str();
+}
+
+bc_status bc_create(int device, const bc_params *p, bc_ctx **out)
+{
+    if (!p || !out) return BC_EINVAL;
+    *out = nullptr;
+    if (p->N < 1 || !(p->h > 0) || !std::isfinite(p->h)) return BC_EINVAL;
+    for (int a = 0; a < 3; a++)
+        if (!std::isfinite(p->t0[a])) return BC_EINVAL;
+    if (p->mode != BC_MODE_SPECTRAL && p->mode != BC_MODE_EXACT) return BC_EINVAL;
+    if (p->precision != BC_FP32 && p->precision != BC_FP64) return BC_EINVAL;
+    if (p->weights != BC_WEIGHTS_REAL && p->weights != BC_WEIGHTS_COMPLEX) return BC_EINVAL;
+    if (p->max_batch < 0) return BC_EINVAL;
+    if (p->mode == BC_MODE_SPECTRAL) {
+        if (p->precision != BC_FP32) return BC_EUNSUPPORTED;
+        if (p->Np < p->N || p->Np < 2 || (p->Np % 2) != 0 || !friendly(p->Np) || p->Np > 1024) return BC_EINVAL;
+        if (p->K < 1 || p->K > 2047) return BC_EINVAL;
+        if (p->N > 1625) return BC_EUNSUPPORTED;
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+        cudaGetLastError();
+        return BC_ECUDA;
+    }
+    if (cudaSetDevice(device) != cudaSuccess) return BC_ECUDA;
+    bc_ctx *ctx = new bc_ctx();
+    ctx->device = device;
+    ctx->p = *p;
+    if (p->mode == BC_MODE_SPECTRAL) {
+        const bool cplx = p->weights == BC_WEIGHTS_COMPLEX;
+        ctx->P = p->Np * p->h;
+        ctx->K = p->K;
+        ctx->M = 2 * p->K + 1;
+        ctx->Kz = cplx ? ctx->M : p->K + 1;
+        ctx->Fz = cplx ? p->Np : p->Np / 2 + 1;
+        if (!make_fft_plan(p->Np, ctx->fft_np)) {
+            delete ctx;
+            return BC_EINVAL;
+        }
+        // origin phases exp(2 pi i k t0_a / P), k in [-K, K]
+        for (int a = 0; a < 3; a++) {
+            std::vector<float2> ph(ctx->M);
+            for (int q = 0; q < ctx->M; q++) {
+                const double k = q - p->K;
+                const double x = k * p->t0[a] / ctx->P;
+                const double fr = x - std::floor(x);
+                ph[q] = make_float2((float)std::cos(2 * kPi * fr), (float)std::sin(2 * kPi * fr));
+            }
+            if (dalloc(ctx, &ctx->d_ph[a], sizeof(float2) * ctx->M) != BC_OK ||
+                cudaMemcpy(ctx->d_ph[a], ph.data(), sizeof(float2) * ctx->M, cudaMemcpyHostToDevice) != cudaSuccess) {
+                bc_destroy(ctx);
+                return BC_ENOMEM;
+            }
+        }
+    }
+    *out = ctx;
+    return BC_OK;
+}
+
+bc_status bc_destroy(bc_ctx *ctx)
+{
+    if (!ctx) return BC_OK;
+    cudaSetDevice(ctx->device);
+    for (int w = 0; w < 2; w++) {
+        dfree(ctx->d_balls[w]);
+        dfree(ctx->d_wre[w]);
+        dfree(ctx->d_wim[w]);
+        dfree(ctx->d_balls64[w]);
+        dfree(ctx->d_w64[w]);
+        for (int a = 0; a < 3; a++) dfree(ctx->plan[w].d_mult[a]);
+    }
+    for (int a = 0; a < 3; a++) dfree(ctx->d_ph[a]);
+    dfree(ctx->d_csr_off);
+    dfree(ctx->d_csr_idx);
+    dfree(ctx->d_Ahat);
+    if (ctx->ws1) cudaFree(ctx->ws1);
+    if (ctx->ws2) cudaFree(ctx->ws2);
+    dfree(ctx->d_keys);
+    dfree(ctx->d_rot);
+    dfree(ctx->d_rot64);
+    if (ctx->d_out_stage) cudaFree(ctx->d_out_stage);
+    dfree(ctx->d_acc);
+    dfree(ctx->d_part);
+    dfree(ctx->d_part_idx);
+    for (auto &pe : ctx->pending) {
+        cudaEventDestroy(pe.e0);
+        cudaEventDestroy(pe.e1);
+    }
+    for (auto e : ctx->event_pool) cudaEventDestroy(e);
+    delete ctx;
+    return BC_OK;
+}
+
+bc_status bc_shape_upload(bc_ctx *ctx, int which, const double *xyzr, const double *w, int64_t n)
+{
+    if (!ctx) return BC_EINVAL;
+    if (which != 0 && which != 1) return fail(ctx, BC_EINVAL, "which must be 0 (A) or 1 (B)");
+    if (n < 0 || (n > 0 && !xyzr)) return fail(ctx, BC_EINVAL, "bad shape size or NULL xyzr");
+    if (n > (1ll << 30)) return fail(ctx, BC_EINVAL, "too many balls");
+    CU(ctx, cudaSetDevice(ctx->device));
+    const bool cplx = ctx->p.weights == BC_WEIGHTS_COMPLEX;
+    std::vector<double> x, wv;
+    TRY(fetch_host(ctx, xyzr, (size_t)n * 4, x));
+    if (w) TRY(fetch_host(ctx, w, (size_t)n * (cplx ? 2 : 1), wv));
+    for (int64_t i = 0; i < n; i++) {
+        for (int q = 0; q < 4; q++)
+            if (!std::isfinite(x[4 * i + q])) return fail(ctx, BC_EINVAL, "ball %lld has a non-finite entry", (long long)i);
+        if (!(x[4 * i + 3] > 0)) return fail(ctx, BC_EINVAL, "ball %lld has radius <= 0", (long long)i);
+    }
+    for (double v : wv)
+        if (!std::isfinite(v)) return fail(ctx, BC_EINVAL, "non-finite weight");
+    ctx->hxyzr[which] = x;
+    ctx->hw[which].assign((size_t)n * 2, 0.0);
+    for (int64_t i = 0; i < n; i++) {
+        if (!w) {
+            ctx->hw[which][2 * i] = 1.0;
+        } else if (cplx) {
+            ctx->hw[which][2 * i] = wv[2 * i];
+            ctx->hw[which][2 * i + 1] = wv[2 * i + 1];
+        } else {
+            ctx->hw[which][2 * i] = wv[i];
+        }
+    }
+    ctx->n[which] = n;
+    ctx->have[which] = true;
+    if (which == 0) ctx->have_spec = false;
+    TRY(upload_shape_device(ctx, which));
+    if (ctx->p.mode == BC_MODE_SPECTRAL && n > 0) {
+        double lo[3], hi[3], rmax, rho;
+        shape_bounds(ctx, which, lo, hi, rmax, rho);
+        if (which == 1)
+            for (int a = 0; a < 3; a++) {  // any rotation keeps B inside the ball of radius max|b_j|
+                lo[a] = -rho;
+                hi[a] = rho;
+            }
+        TRY(plan_shape(ctx, which, lo, hi, rmax));
+        if (which == 0) TRY(build_csr_A(ctx));
+    }
+    TRY(check_support(ctx));
+    return BC_OK;
+}
+
+bc_status bc_spectrum_A(bc_ctx *ctx, void *stream)
+{
+    if (!ctx) return BC_EINVAL;
+    if (!ctx->have[0]) return fail(ctx, BC_ESTATE, "shape A has not been uploaded");
+    if (ctx->p.mode != BC_MODE_SPECTRAL || ctx->have_spec) {
+        ctx->have_spec = true;
+        return BC_OK;
+    }
+    CU(ctx, cudaSetDevice(ctx->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t nspec = (size_t)ctx->M * ctx->M * ctx->Kz;
+    TRY(dalloc(ctx, &ctx->d_Ahat, sizeof(float2) * nspec));
+    if (ctx->n[0] == 0) {
+        CU(ctx, cudaMemsetAsync(ctx->d_Ahat, 0, sizeof(float2) * nspec, s));
+        ctx->have_spec = true;
+        return BC_OK;
+    }
+    size_t s1, s2;
+    spectral_ws_sizes(ctx, 0, s1, s2);
+    void *w1 = nullptr, *w2 = nullptr;
+    CU(ctx, cudaMalloc(&w1, s1));
+    cudaError_t e = cudaMalloc(&w2, s2);
+    if (e != cudaSuccess) {
+        cudaFree(w1);
+        return fail(ctx, BC_ENOMEM, "spectrum_A workspace: %s", cudaGetErrorString(e));
+    }
+    bc_status st = shape_spectrum(ctx, 0, nullptr, 1, w1, w2, ctx->d_Ahat, s1, s2, s);
+    cudaError_t se = cudaStreamSynchronize(s);
+    collect_profile(ctx);
+    cudaFree(w1);
+    cudaFree(w2);
+    if (st != BC_OK) return st;
+    if (se != cudaSuccess) return fail(ctx, BC_ECUDA, "spectrum_A: %s", cudaGetErrorString(se));
+    ctx->have_spec = true;
+    return BC_OK;
+}
+
+bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, int out_kind, void *out, void *stream)
+{
+    if (!ctx) return BC_EINVAL;
+    if (!R || !out || n_rot < 1) return fail(ctx, BC_EINVAL, "NULL R/out or n_rot < 1");
+    if (out_kind < BC_OUT_F_FULL || out_kind > BC_OUT_MAX_REAL) return fail(ctx, BC_EINVAL, "bad out_kind");
+    const bool cplx = ctx->p.weights == BC_WEIGHTS_COMPLEX;
+    if (cplx && out_kind != BC_OUT_F_FULL && out_kind != BC_OUT_MAX_REAL)
+        return fail(ctx, BC_EINVAL, "complex weights support F_FULL and MAX_REAL only");
+    if (!ctx->have[0] || !ctx->have[1]) return fail(ctx, BC_ESTATE, "upload both shapes first");
+    if (ctx->p.mode == BC_MODE_SPECTRAL && !ctx->have_spec && ctx->n[0] > 0 && ctx->n[1] > 0)
+        return fail(ctx, BC_ESTATE, "call bc_spectrum_A first");
+    CU(ctx, cudaSetDevice(ctx->device));
+    cudaStream_t s = (cudaStream_t)stream;
+
+    std::vector<double> hR;
+    TRY(fetch_host(ctx, R, (size_t)n_rot * 9, hR));
+    TRY(validate_rotations(ctx, hR, n_rot));
+
+    const size_t out_per = out_elem_bytes(ctx, out_kind);
+    const bool host_out = !is_device_ptr(out);
+    char *dout = (char *)out;
+    if (host_out) {
+        TRY(ensure_ws(ctx, &ctx->d_out_stage, ctx->out_stage_bytes, out_per * n_rot));
+        dout = (char *)ctx->d_out_stage;
+    }
+
+    // empty shape: f == 0 identically
+    if (ctx->n[0] == 0 || ctx->n[1] == 0) {
+        if (out_kind == BC_OUT_F_FULL) {
+            CU(ctx, cudaMemsetAsync(dout, 0, out_per * n_rot, s));
+        } else {
+            std::vector<bc_extremum> z((size_t)n_rot * (out_kind == BC_OUT_MINMAX ? 2 : 1));
+            for (auto &e : z) {
+                e.val = 0.0;
+                e.idx = 0;
+            }
+            CU(ctx, cudaMemcpyAsync(dout, z.data(), z.size() * sizeof(bc_extremum), cudaMemcpyHostToDevice, s));
+            CU(ctx, cudaStreamSynchronize(s));
+        }
+        if (host_out) {
+            CU(ctx, cudaMemcpyAsync(out, dout, out_per * n_rot, cudaMemcpyDeviceToHost, s));
+            CU(ctx, cudaStreamSynchronize(s));
+        }
+        return BC_OK;
+    }
+
+    // rotations to the device (fp32 for the spectral path, fp64 for exact mode)
+    if (n_rot > ctx->rot_cap) {
+        TRY(dalloc(ctx, &ctx->d_rot, sizeof(float) * 9 * n_rot));
+        TRY(dalloc(ctx, &ctx->d_rot64, sizeof(double) * 9 * n_rot));
+        ctx->rot_cap = n_rot;
+    }
+    std::vector<float> fR(hR.begin(), hR.end());
+    CU(ctx, cudaMemcpyAsync(ctx->d_rot, fR.data(), sizeof(float) * 9 * n_rot, cudaMemcpyHostToDevice, s));
+    CU(ctx, cudaMemcpyAsync(ctx->d_rot64, hR.data(), sizeof(double) * 9 * n_rot, cudaMemcpyHostToDevice, s));
+
+    const long long N = ctx->p.N, N3 = N * N * N;
+    if (ctx->p.mode == BC_MODE_EXACT) {
+        int nb = ctx->p.max_batch > 0 ? ctx->p.max_batch : 8;
+        const size_t per = (size_t)N3 * (cplx ? 2 : 1) * sizeof(double);
+        while (nb > 1 && per * nb > ((size_t)4 << 30)) nb /= 2;
+        nb = (int)std::min<int64_t>(nb, n_rot);
+        if (ctx->acc_bytes < per * nb) {
+            TRY(dalloc(ctx, &ctx->d_acc, per * nb));
+            ctx->acc_bytes = per * nb;
+        }
+        if (ctx->part_cap < nb * 64 * 2) {
+            TRY(dalloc(ctx, &ctx->d_part, sizeof(double) * nb * 64 * 2));
+            TRY(dalloc(ctx, &ctx->d_part_idx, sizeof(long long) * nb * 64 * 2));
+            ctx->part_cap = nb * 64 * 2;
+        }
+        for (int64_t r0 = 0; r0 < n_rot; r0 += nb) {
+            const int b = (int)std::min<int64_t>(nb, n_rot - r0);
+            CU(ctx, cudaMemsetAsync(ctx->d_acc, 0, per * b, s));
+            ExactArgs a{};
+            a.nA = (int)ctx->n[0];
+            a.nB = (int)ctx->n[1];
+            a.N = (int)N;
+            a.h = ctx->p.h;
+            a.t0x = ctx->p.t0[0];
+            a.t0y = ctx->p.t0[1];
+            a.t0z = ctx->p.t0[2];
+            a.A = ctx->d_balls64[0];
+            a.B = ctx->d_balls64[1];
+            a.wA = ctx->d_w64[0];
+            a.wB = ctx->d_w64[1];
+            a.rot = ctx->d_rot64 + 9 * r0;
+            a.complex_w = cplx;
+            a.fp64 = ctx->p.precision == BC_FP64;
+            a.acc = ctx->d_acc;
+            a.acc_bstride = (long long)(per / sizeof(double));
+            {
+                StageScope sc(ctx, s, "exact_pairs");
+                launch_exact(a, b, s);
+                ctx->launches++;
+            }
+            ExactOutArgs o{};
+            o.N = (int)N;
+            o.complex_w = cplx;
+            o.fp64 = a.fp64;
+            o.acc = ctx->d_acc;
+            o.acc_bstride = a.acc_bstride;
+            o.out_kind = out_kind;
+            o.out = dout + out_per * r0;
+            o.partials = ctx->d_part;
+            o.partial_idx = ctx->d_part_idx;
+            {
+                StageScope sc(ctx, s, "exact_out");
+                int nl = 0;
+                launch_exact_out(o, b, s, &nl);
+                ctx->launches += nl;
+            }
+            CU(ctx, cudaGetLastError());
+        }
+    } else {
+        size_t s1, s2;
+        spectral_ws_sizes(ctx, 1, s1, s2);
+        int nb = ctx->p.max_batch > 0 ? ctx->p.max_batch : 8;
+        while (nb > 1 && (s1 + s2) * nb > ((size_t)12 << 30)) nb /= 2;
+        nb = (int)std::min<int64_t>(nb, n_rot);
+        ctx->batch = nb;
+        TRY(ensure_ws(ctx, &ctx->ws1, ctx->ws1_bytes, s1 * nb));
+        TRY(ensure_ws(ctx, &ctx->ws2, ctx->ws2_bytes, s2 * nb));
+        if (ctx->keys_cap < 2 * nb) {
+            TRY(dalloc(ctx, &ctx->d_keys, sizeof(unsigned long long) * 2 * nb));
+            ctx->keys_cap = 2 * nb;
+        }
+        const int Np = ctx->p.Np;
+        for (int64_t r0 = 0; r0 < n_rot; r0 += nb) {
+            const int b = (int)std::min<int64_t>(nb, n_rot - r0);
+            // 1-4: spectrum of R B on the band
+            TRY(shape_spectrum(ctx, 1, ctx->d_rot + 9 * r0, b, ctx->ws1, ctx->ws2, (float2 *)ctx->ws2, s1, s2, s));
+            // 5: spectral product with A, origin phase, fold onto Np^3
+            {
+                FoldArgs a{};
+                a.K = ctx->K;
+                a.Kz = ctx->Kz;
+                a.Np = Np;
+                a.Fz = ctx->Fz;
+                a.complex_w = cplx;
+                a.Ahat = ctx->d_Ahat;
+                a.Bhat = (const float2 *)ctx->ws2;
+                a.b_bstride = (long long)(s2 / 8);
+                a.f_bstride = (long long)(s1 / 8);
+                a.phx = ctx->d_ph[0];
+                a.phy = ctx->d_ph[1];
+                a.phz = ctx->d_ph[2];
+                a.F = (float2 *)ctx->ws1;
+                StageScope sc(ctx, s, "fold");
+                launch_fold(a, b, s);
+                ctx->launches++;
+            }
+            // 6-7: inverse transforms along x and y (only the N output rows)
+            {
+                AxisArgs a{};
+                a.L = Np;
+                a.c = 1;
+                a.klo = 0;
+                a.nk = (int)N;
+                a.signed_k = 0;
+                a.sign = 1.f;
+                a.plan = ctx->fft_np;
+                a.O = 1;
+                a.I = Np * ctx->Fz;
+                a.in = ctx->ws1;
+                a.in_bstride = (long long)(s1 / 8);
+                a.out = (float2 *)ctx->ws2;
+                a.out_bstride = (long long)(s2 / 8);
+                StageScope sc(ctx, s, "inv_x");
+                launch_axis_strided(a, b, s);
+                ctx->launches++;
+            }
+            {
+                AxisArgs a{};
+                a.L = Np;
+                a.c = 1;
+                a.klo = 0;
+                a.nk = (int)N;
+                a.signed_k = 0;
+                a.sign = 1.f;
+                a.plan = ctx->fft_np;
+                a.O = (int)N;
+                a.I = ctx->Fz;
+                a.in = ctx->ws2;
+                a.in_bstride = (long long)(s2 / 8);
+                a.out = (float2 *)ctx->ws1;
+                a.out_bstride = (long long)(s1 / 8);
+                StageScope sc(ctx, s, "inv_y");
+                launch_axis_strided(a, b, s);
+                ctx->launches++;
+            }
+            // 8: inverse along z (C2R / C2C), 1/P^3, full output or reduction keys
+            if (out_kind != BC_OUT_F_FULL) {
+                launch_keys_init(ctx->d_keys, 2 * b, s);
+                ctx->launches++;
+            }
+            {
+                LastArgs a{};
+                a.Np = Np;
+                a.N = (int)N;
+                a.Fz = ctx->Fz;
+                a.hermitian = !cplx;
+                a.scale = (float)(1.0 / (ctx->P * ctx->P * ctx->P));
+                a.plan = ctx->fft_np;
+                a.in = (const float2 *)ctx->ws1;
+                a.in_bstride = (long long)(s1 / 8);
+                a.out_kind = out_kind;
+                a.out_full = dout + out_per * r0;
+                a.full_bstride = N3;
+                a.keys = ctx->d_keys;
+                StageScope sc(ctx, s, "inv_z_reduce");
+                launch_last(a, b, s);
+                ctx->launches++;
+            }
+            if (out_kind != BC_OUT_F_FULL) {
+                StageScope sc(ctx, s, "finalize");
+                launch_keys_finalize(ctx->d_keys, b, out_kind, dout + out_per * r0, s);
+                ctx->launches++;
+            }
+            CU(ctx, cudaGetLastError());
+        }
+    }
+    if (host_out) {
+        CU(ctx, cudaMemcpyAsync(out, dout, out_per * n_rot, cudaMemcpyDeviceToHost, s));
+        CU(ctx, cudaStreamSynchronize(s));
+    }
+    if (ctx->prof) collect_profile(ctx);
+    return BC_OK;
+}
+
+bc_status bc_query(const bc_ctx *ctx, const char *key, double *value)
+{
+    if (!ctx || !key || !value) return BC_EINVAL;
+    const std::string k(key);
+    const ShapePlan &A = ctx->plan[0], &B = ctx->plan[1];
+    if (k == "P") *value = ctx->P;
+    else if (k == "tau_A") *value = A.tau;
+    else if (k == "tau_B") *value = B.tau;
+    else if (k == "G_A") *value = A.G;
+    else if (k == "G_B") *value = B.G;
+    else if (k == "L_A") *value = A.L;
+    else if (k == "L_B") *value = B.L;
+    else if (k == "c_A") *value = A.c;
+    else if (k == "c_B") *value = B.c;
+    else if (k == "cut_A") *value = A.cut;
+    else if (k == "cut_B") *value = B.cut;
+    else if (k == "band_modes") *value = (double)ctx->M * ctx->M * ctx->Kz;
+    else if (k == "batch") *value = ctx->batch;
+    else if (k == "bytes_workspace") *value = (double)(ctx->ws1_bytes + ctx->ws2_bytes);
+    else return BC_EINVAL;
+    return BC_OK;
+}
+
+int64_t bc_launch_count(const bc_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+bc_status bc_set_profiling(bc_ctx *ctx, int enabled)
+{
+    if (!ctx) return BC_EINVAL;
+    ctx->prof = enabled != 0;
+    return BC_OK;
+}
+
+int bc_stage_times(bc_ctx *ctx, const char **names, double *total_ms, int64_t *launches, int cap)
+{
+    if (!ctx) return 0;
+    collect_profile(ctx);
+    int n = 0;
+    for (const std::string &nm : ctx->stage_order) {
+        if (n < cap) {
+            auto &v = ctx->stage_ms[nm];
+            if (names) names[n] = ctx->stage_ms.find(nm)->first.c_str();
+            if (total_ms) total_ms[n] = v.first;
+            if (launches) launches[n] = v.second;
+        }
+        n++;
+    }
+    return n;
+}
+
+bc_status bc_reset_stage_times(bc_ctx *ctx)
+{
+    if (!ctx) return BC_EINVAL;
+    collect_profile(ctx);
+    ctx->stage_ms.clear();
+    ctx->stage_order.clear();
+    return BC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,110 @@
+// kernels.cuh -- launch-parameter structs and kernel declarations of libballcorr.
+#pragma once
+
+#include "common.cuh"
+#include "fft.cuh"
+
+// ----------------------------------------------------------------- spreading
+// Gaussian-smoothed ball density on a box of the fine lattice (spacing hf):
+//   rho_s(x_n) = sum_j v_j (1_{B(c_j, s_j)} * G_tau)(x_n),  x_n = (o + n) hf,  n in [0, L)^3
+// (the knot density rho_P of PAPER.md L150 eq_rhoP convolved with the ball
+// primitive, eq_ballconv, and with an isotropic Gaussian G_tau that the
+// spectral deconvolution removes exactly).
+struct SpreadArgs {
+    int L;            // box edge (cells)
+    int ox, oy, oz;   // box origin in fine cells
+    float hf;         // fine spacing
+    float inv_hf;
+    float tau;        // Gaussian sigma (length units)
+    float cut;        // footprint radius beyond the ball radius (length units)
+    int n_balls;      // candidate count when csr == nullptr
+    const float4 *balls;    // (x, y, z, s) fp32
+    const float *w_re;      // weights (real part), nullptr => 1
+    const float *w_im;      // imaginary parts (complex mode), nullptr => 0
+    const int *csr_off;     // per-tile candidate offsets (A) or nullptr (all balls)
+    const int *csr_idx;
+    const float *rot;       // per batch element 9 floats (row-major R) or nullptr (identity)
+    int complex_w;
+    void *out;              // float [b][L][L][L] (real) or float2 (complex)
+    long long out_batch_stride;  // elements
+    int tiles_per_axis;
+};
+
+// ----------------------------------------------------------------- axis transforms
+// One axis of the "box DFT":  X(k) = mult(k) * sum_{n<L} x_n exp(sign 2 pi i k n / G),  G = c L,
+// evaluated through c cosets k = c q + p of an L-point FFT of x_n exp(sign 2 pi i p n / G).
+struct AxisArgs {
+    int L;            // transform length (input samples per line)
+    int c;            // coset count, G = c L
+    int klo, nk;      // output window: k in [klo, klo + nk) (signed in (-G/2, G/2] when signed_k)
+    int signed_k;
+    float sign;       // -1 forward, +1 inverse
+    const float2 *mult;   // nk multipliers (nullptr => 1)
+    FftPlan plan;
+    // strided layout: in[b][O][L][I], out[b][O][nk][I]
+    int O, I;
+    long long in_bstride, out_bstride;
+    const void *in;
+    int in_real;      // input is float (contiguous kernel only)
+    float2 *out;
+};
+
+// contiguous-axis epilogue of the last inverse pass
+struct LastArgs {
+    int Np, N, Fz;       // FFT length, output window, stored input length per line
+    int hermitian;       // 1: C2R from Fz = Np/2+1 stored modes; 0: C2C, Fz = Np
+    float scale;
+    FftPlan plan;
+    const float2 *in;    // [b][N*N lines][Fz]
+    long long in_bstride;
+    int out_kind;        // BC_OUT_*
+    void *out_full;      // float [b][N^3] or float2
+    long long full_bstride;
+    unsigned long long *keys;  // [b][2]: (min key, max key)
+};
+
+struct FoldArgs {
+    int K, Kz, Np, Fz;
+    int complex_w;
+    const float2 *Ahat;       // [kx][ky][kz] (kx, ky in [-K, K]; kz in [0,K] real / [-K,K] complex)
+    const float2 *Bhat;       // [b][kx][ky][kz]
+    long long b_bstride, f_bstride;
+    const float2 *phx, *phy, *phz;  // exp(2 pi i k t0_a / P), index k + K
+    float2 *F;                // [b][Np][Np][Fz]
+};
+
+void launch_spread(const SpreadArgs &a, int batch, cudaStream_t s);
+void launch_axis_contig(const AxisArgs &a, int lines, int batch, cudaStream_t s);
+void launch_axis_strided(const AxisArgs &a, int batch, cudaStream_t s);
+void launch_fold(const FoldArgs &a, int batch, cudaStream_t s);
+void launch_last(const LastArgs &a, int batch, cudaStream_t s);
+void launch_keys_init(unsigned long long *keys, int n, cudaStream_t s);
+void launch_keys_finalize(const unsigned long long *keys, int batch, int out_kind, void *out, cudaStream_t s);
+
+// ----------------------------------------------------------------- exact mode
+struct ExactArgs {
+    int nA, nB, N;
+    double h, t0x, t0y, t0z;
+    const double4 *A;    // (x, y, z, r)
+    const double4 *B;
+    const double2 *wA;   // (re, im)
+    const double2 *wB;
+    const double *rot;   // [b][9]
+    int complex_w;
+    int fp64;            // evaluate V in double (1) or float (0)
+    double *acc;         // [b][N^3] (re) followed by [b][N^3] (im) when complex
+    long long acc_bstride;
+};
+void launch_exact(const ExactArgs &a, int batch, cudaStream_t s);
+
+struct ExactOutArgs {
+    int N;
+    int complex_w, fp64;
+    const double *acc;
+    long long acc_bstride;
+    int out_kind;
+    void *out;           // full output or bc_extremum[]
+    double *partials;    // scratch: [b][nblocks][2] vals
+    long long *partial_idx;
+};
+void launch_exact_out(const ExactOutArgs &a, int batch, cudaStream_t s, int *launches);

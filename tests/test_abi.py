@@ -1,0 +1,78 @@
+"""CPU checks of the C ABI: the library loads, exports every symbol the header
+declares, and validates parameters before touching a device (no compute calls)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "ballcorr.h")
+
+
+@pytest.fixture(scope="module")
+def bc():
+    lib = os.path.join(ROOT, "paper_1711_05075_b200", "lib", "libballcorr.so")
+    if not os.path.exists(lib):
+        import subprocess
+        subprocess.check_call(["make", "-C", ROOT, "-j4"], stdout=subprocess.DEVNULL)
+    from paper_1711_05075_b200 import ballcorr
+    return ballcorr
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(bc_[a-z_A-Z]+)\s*\(", text)))
+
+
+def test_header_declares_the_path(bc):
+    names = declared_functions()
+    for required in ("bc_create", "bc_destroy", "bc_shape_upload", "bc_spectrum_A", "bc_correlate_rotations",
+                     "bc_last_error"):
+        assert required in names
+
+
+def test_library_exports_every_declared_symbol(bc):
+    lib = ctypes.CDLL(bc.LIB_PATH)
+    missing = [n for n in declared_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_status_strings(bc):
+    assert bc.bc_status_string(0) == b"BC_OK"
+    assert bc.bc_status_string(2) == b"BC_ERANGE"
+    assert bc.bc_status_string(99) == b"BC_UNKNOWN"
+
+
+def test_params_struct_layout(bc):
+    # matches the C struct: 4 + pad 4 + 8 + 24 + 4*6 + pad 4? -> check field offsets explicitly
+    P = bc.bc_params
+    assert P.h.offset == 8 and P.t0.offset == 16 and P.Np.offset == 40
+    assert P.spread_eps.offset == 64 and ctypes.sizeof(P) == 72
+
+
+@pytest.mark.parametrize("kw", [
+    dict(N=0, h=0.1, t0=(0, 0, 0)),
+    dict(N=8, h=-1.0, t0=(0, 0, 0)),
+    dict(N=8, h=0.1, t0=(0, 0, 0), Np=7, K=4),          # Np odd
+    dict(N=8, h=0.1, t0=(0, 0, 0), Np=14, K=4),         # 7 is not a {2,3,5} factor
+    dict(N=8, h=0.1, t0=(0, 0, 0), Np=6, K=4),          # Np < N
+    dict(N=8, h=0.1, t0=(0, 0, 0), Np=8, K=0),          # empty band
+])
+def test_create_rejects_bad_params_without_gpu(bc, kw):
+    with pytest.raises(bc.BallCorrError) as e:
+        bc.Correlator(**kw)
+    assert e.value.status == bc.BC_EINVAL
+
+
+def test_spectral_fp64_unsupported(bc):
+    with pytest.raises(bc.BallCorrError) as e:
+        bc.Correlator(N=8, h=0.1, t0=(0, 0, 0), Np=8, K=4, precision="f64")
+    assert e.value.status == bc.BC_EUNSUPPORTED
+
+
+def test_null_context_is_safe(bc):
+    assert bc.bc_destroy(None) == 0
+    assert bc.bc_last_error(None) == b"no context"
+    assert bc.bc_launch_count(None) == 0

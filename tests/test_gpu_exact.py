@@ -1,0 +1,106 @@
+"""Exact (pair-lens) mode on the GPU vs the fp64 lens oracle.
+
+Tolerances (north_star): max|f_gpu - f_cpu| <= 1e-9 max|f_cpu| in fp64 mode and
+1e-4 max|f_cpu| in fp32 mode (fp32 lens evaluation, fp64 accumulation: ~1e-6).
+"""
+import numpy as np
+import pytest
+
+from synth import make_config, random_small_case, random_rotations
+from tests.gpu_helpers import rel_max_err, as_complex, check_extremum
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def bc():
+    import torch
+    assert torch.cuda.is_available()
+    from paper_1711_05075_b200 import ballcorr
+    return ballcorr
+
+
+def make_exact(bc, w, precision=None):
+    c = bc.Correlator(N=w.N, h=w.h, t0=w.t0, mode="exact", precision=precision or w.precision,
+                      weights=w.weights)
+    c.shape_upload(0, w.A_xyzr, w.A_w)
+    c.shape_upload(1, w.B_xyzr, w.B_w)
+    c.spectrum_A()
+    return c
+
+
+def test_tiny_fp64_full_grid(bc, oracle_mod):
+    w = make_config("tiny")
+    c = make_exact(bc, w)
+    f = c.correlate_rotations(w.R, "full")
+    ref = oracle_mod.correlate_grid(w.A_xyzr, w.A_w, w.B_xyzr, w.B_w, w.R[0], w.N, w.h, w.t0)
+    assert f.dtype == np.float64
+    assert rel_max_err(f[0], ref) <= 1e-9
+    assert c.launch_count() >= 2
+
+
+def test_tiny_fp64_rotated_and_reductions(bc, oracle_mod):
+    w = make_config("tiny")
+    R = random_rotations(np.random.default_rng(3), 3)
+    c = make_exact(bc, w)
+    f = c.correlate_rotations(R, "full")
+    mm = c.correlate_rotations(R, "minmax")
+    for r in range(3):
+        ref = oracle_mod.correlate_grid(w.A_xyzr, w.A_w, w.B_xyzr, w.B_w, R[r], w.N, w.h, w.t0)
+        assert rel_max_err(f[r], ref) <= 1e-9
+        tol = 1e-9 * np.abs(ref).max()
+        check_extremum(mm[r, 0]["val"], mm[r, 0]["idx"], ref, "min", tol)
+        check_extremum(mm[r, 1]["val"], mm[r, 1]["idx"], ref, "max", tol)
+        # exact ties at the minimum (f == 0 far from the obstacle): lowest index
+        flat = ref.reshape(-1)
+        if np.count_nonzero(flat == flat.min()) > 1:
+            assert mm[r, 0]["idx"] == int(np.flatnonzero(f[r].reshape(-1) == f[r].min())[0])
+
+
+def test_single_fp32_full_grid(bc, oracle_mod):
+    w = make_config("single")
+    c = make_exact(bc, w)
+    f = c.correlate_rotations(w.R, "full")
+    ref = oracle_mod.correlate_grid(w.A_xyzr, w.A_w, w.B_xyzr, w.B_w, w.R[0], w.N, w.h, w.t0)
+    assert f.dtype == np.float32
+    assert rel_max_err(f[0], ref) <= 1e-4
+
+
+@pytest.mark.parametrize("seed", [21, 22])
+def test_small_complex_exact(bc, oracle_mod, seed):
+    w = random_small_case(seed, n_a=9, n_b=7, n_rot=3, N=14, complex_weights=True)
+    c = make_exact(bc, w, precision="f64")
+    f = as_complex(c.correlate_rotations(w.R, "full"))
+    mr = c.correlate_rotations(w.R, "max_real")
+    for r in range(w.n_rot):
+        ref = oracle_mod.correlate_grid(w.A_xyzr, w.A_w, w.B_xyzr, w.B_w, w.R[r], w.N, w.h, w.t0)
+        assert rel_max_err(f[r], ref) <= 1e-9
+        check_extremum(mr[r]["val"], mr[r]["idx"], ref.real, "max", 1e-9 * np.abs(ref).max())
+
+
+def test_empty_shape_gives_zero(bc):
+    w = random_small_case(30, N=10)
+    c = bc.Correlator(N=w.N, h=w.h, t0=w.t0, mode="exact", precision="f64")
+    c.shape_upload(0, w.A_xyzr, w.A_w)
+    c.shape_upload(1, np.zeros((0, 4)))
+    c.spectrum_A()
+    f = c.correlate_rotations(w.R, "full")
+    assert np.all(f == 0)
+
+
+def test_invalid_rotation_and_radius(bc):
+    w = random_small_case(31, N=10)
+    c = make_exact(bc, w, precision="f64")
+    bad = w.R.copy()
+    bad[0, 0, 0] *= 1.01
+    with pytest.raises(bc.BallCorrError) as e:
+        c.correlate_rotations(bad, "full")
+    assert e.value.status == bc.BC_EINVAL
+    refl = np.diag([1.0, 1.0, -1.0])[None]
+    with pytest.raises(bc.BallCorrError):
+        c.correlate_rotations(refl, "full")
+    bad_b = w.B_xyzr.copy()
+    bad_b[0, 3] = 0.0
+    with pytest.raises(bc.BallCorrError) as e:
+        c.shape_upload(1, bad_b)
+    assert e.value.status == bc.BC_EINVAL

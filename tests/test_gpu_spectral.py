@@ -1,0 +1,135 @@
+"""Spectral mode on the GPU.
+
+Two references:
+* the band-limited reference (oracle/bandlimited.py: direct NDFT x ball transform,
+  product, direct inverse DFT on the same band) pins the implementation -- spreading,
+  box DFT, deconvolution, fold, inverse FFT, reductions -- to fp32 rounding;
+* the lens oracle bounds the discretisation (band) error on the workloads.
+"""
+import numpy as np
+import pytest
+
+from synth import random_small_case, random_rotations
+from tests.gpu_helpers import rel_max_err, as_complex, check_extremum
+
+pytestmark = pytest.mark.gpu
+
+# fp32 pipeline vs fp64 band-limited reference: spreading eps 1e-7 with the
+# Gaussian deconvolution gain and fp32 FFT rounding -> a few 1e-6 of max|f|.
+IMPL_TOL = 2e-5
+
+
+@pytest.fixture(scope="module")
+def bc():
+    import torch
+    assert torch.cuda.is_available()
+    from paper_1711_05075_b200 import ballcorr
+    return ballcorr
+
+
+def spectral(bc, w, Np, K, **kw):
+    c = bc.Correlator(N=w.N, h=w.h, t0=w.t0, Np=Np, K=K, mode="spectral", weights=w.weights, **kw)
+    c.shape_upload(0, w.A_xyzr, w.A_w)
+    c.shape_upload(1, w.B_xyzr, w.B_w)
+    c.spectrum_A()
+    return c
+
+
+@pytest.mark.parametrize("seed,N,Np,K", [(41, 20, 24, 24), (42, 18, 30, 17), (43, 16, 20, 31)])
+def test_real_vs_bandlimited(bc, oracle_mod, seed, N, Np, K):
+    w = random_small_case(seed, n_a=11, n_b=9, n_rot=3, N=N)
+    P = Np * w.h
+    c = spectral(bc, w, Np, K)
+    f = c.correlate_rotations(w.R, "full")
+    for r in range(w.n_rot):
+        ref = oracle_mod.bandlimited_correlation(w.A_xyzr, w.A_w, w.B_xyzr, w.B_w, w.R[r], w.N, w.h, w.t0, P, K)
+        assert rel_max_err(f[r], ref) <= IMPL_TOL, (r, rel_max_err(f[r], ref))
+
+
+@pytest.mark.parametrize("seed", [44, 45])
+def test_complex_vs_bandlimited(bc, oracle_mod, seed):
+    w = random_small_case(seed, n_a=8, n_b=6, n_rot=2, N=16, complex_weights=True)
+    Np, K = 24, 20
+    P = Np * w.h
+    c = spectral(bc, w, Np, K)
+    f = as_complex(c.correlate_rotations(w.R, "full"))
+    mr = c.correlate_rotations(w.R, "max_real")
+    for r in range(w.n_rot):
+        ref = oracle_mod.bandlimited_correlation(w.A_xyzr, w.A_w, w.B_xyzr, w.B_w, w.R[r], w.N, w.h, w.t0, P, K)
+        assert rel_max_err(f[r], ref) <= IMPL_TOL
+        check_extremum(mr[r]["val"], mr[r]["idx"], ref.real, "max", 2 * IMPL_TOL * np.abs(ref).max())
+
+
+def test_reductions_match_full_output(bc):
+    w = random_small_case(46, n_a=12, n_b=10, n_rot=5, N=20)
+    c = spectral(bc, w, 24, 24)
+    f = c.correlate_rotations(w.R, "full")
+    mm = c.correlate_rotations(w.R, "minmax")
+    mn = c.correlate_rotations(w.R, "min_argmin")
+    mx = c.correlate_rotations(w.R, "max_argmax")
+    for r in range(w.n_rot):
+        flat = f[r].reshape(-1)
+        assert mm[r, 0]["val"] == flat.min() and mm[r, 1]["val"] == flat.max()
+        assert mm[r, 0]["idx"] == int(np.argmin(flat)) and mm[r, 1]["idx"] == int(np.argmax(flat))
+        assert mn[r]["idx"] == mm[r, 0]["idx"] and mx[r]["idx"] == mm[r, 1]["idx"]
+
+
+def test_batching_is_bitwise_stable(bc):
+    """Per-rotation results must not depend on how rotations are batched (or sharded)."""
+    w = random_small_case(47, n_a=10, n_b=8, n_rot=7, N=16)
+    f1 = spectral(bc, w, 20, 19, max_batch=1).correlate_rotations(w.R, "full")
+    f3 = spectral(bc, w, 20, 19, max_batch=3).correlate_rotations(w.R, "full")
+    f_sub = spectral(bc, w, 20, 19, max_batch=4).correlate_rotations(w.R[4:], "full")
+    assert np.array_equal(f1, f3)
+    assert np.array_equal(f1[4:], f_sub)
+
+
+def test_device_buffers_and_stream(bc, oracle_mod):
+    import torch
+    w = random_small_case(48, n_a=10, n_b=8, n_rot=2, N=16)
+    c = bc.Correlator(N=w.N, h=w.h, t0=w.t0, Np=20, K=19)
+    c.shape_upload(0, torch.tensor(w.A_xyzr, device="cuda"), torch.tensor(w.A_w, device="cuda"))
+    c.shape_upload(1, torch.tensor(w.B_xyzr, device="cuda"), torch.tensor(w.B_w, device="cuda"))
+    s = torch.cuda.Stream()
+    c.spectrum_A(stream=s)
+    out = torch.empty((2, 16, 16, 16), dtype=torch.float32, device="cuda")
+    c.correlate_rotations(torch.tensor(w.R, device="cuda"), "full", out=out, stream=s)
+    s.synchronize()
+    host = c.correlate_rotations(w.R, "full")
+    assert np.array_equal(out.cpu().numpy(), host)
+
+
+def test_support_wrap_is_rejected(bc):
+    w = random_small_case(49, N=20)
+    c = bc.Correlator(N=w.N, h=w.h, t0=w.t0, Np=20, K=10)  # P = 2.0 < S + 1
+    c.shape_upload(0, w.A_xyzr, w.A_w)
+    with pytest.raises(bc.BallCorrError) as e:
+        c.shape_upload(1, w.B_xyzr, w.B_w)
+    assert e.value.status == bc.BC_ERANGE
+
+
+def test_correlate_before_spectrum_is_estate(bc):
+    w = random_small_case(50, N=12)
+    c = bc.Correlator(N=w.N, h=w.h, t0=w.t0, Np=16, K=8)
+    c.shape_upload(0, w.A_xyzr, w.A_w)
+    c.shape_upload(1, w.B_xyzr, w.B_w)
+    with pytest.raises(bc.BallCorrError) as e:
+        c.correlate_rotations(w.R, "full")
+    assert e.value.status == bc.BC_ESTATE
+
+
+def test_single_ball_pair_vs_lens(bc, oracle_mod):
+    """One ball each, well resolved: the band-limited lens converges to V (sanity of
+    conventions: sign of t, rotation of B about its origin, 1/P^3 normalisation)."""
+    A = np.array([[0.1, -0.05, 0.02, 0.3]])
+    B = np.array([[-0.2, 0.1, 0.05, 0.25]])
+    R = random_rotations(np.random.default_rng(9), 2)
+    N, h, t0 = 24, 2.0 / 24, (-1.0, -1.0, -1.0)
+    c = bc.Correlator(N=N, h=h, t0=t0, Np=36, K=143)
+    c.shape_upload(0, A)
+    c.shape_upload(1, B)
+    c.spectrum_A()
+    f = c.correlate_rotations(R, "full")
+    for r in range(2):
+        ref = oracle_mod.correlate_grid(A, None, B, None, R[r], N, h, t0)
+        assert rel_max_err(f[r], ref) <= 5e-4  # band error 1.3e-4 at K=143 (oracle/bandlimited)
