@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 from synth import make_config, random_small_case, random_rotations
-from tests.gpu_helpers import rel_max_err, as_complex, check_extremum
+from gpu_helpers import rel_max_err, as_complex, check_extremum
 
 pytestmark = pytest.mark.gpu
 

@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 from synth import random_small_case, random_rotations
-from tests.gpu_helpers import rel_max_err, as_complex, check_extremum
+from gpu_helpers import rel_max_err, as_complex, check_extremum
 
 pytestmark = pytest.mark.gpu
 
@@ -100,12 +100,16 @@ def test_device_buffers_and_stream(bc, oracle_mod):
 
 
 def test_support_wrap_is_rejected(bc):
-    w = random_small_case(49, N=20)
-    c = bc.Correlator(N=w.N, h=w.h, t0=w.t0, Np=20, K=10)  # P = 2.0 < S + 1
-    c.shape_upload(0, w.A_xyzr, w.A_w)
+    A = np.array([[0.5, 0.0, 0.0, 0.3]])
+    B = np.array([[0.4, 0.0, 0.0, 0.3]])   # S = 0.5 + 0.4 + 0.3 + 0.3 = 1.5: needs P >= 2.5
+    c = bc.Correlator(N=20, h=0.1, t0=(-1, -1, -1), Np=20, K=10)  # P = 2.0
+    c.shape_upload(0, A)
     with pytest.raises(bc.BallCorrError) as e:
-        c.shape_upload(1, w.B_xyzr, w.B_w)
+        c.shape_upload(1, B)
     assert e.value.status == bc.BC_ERANGE
+    ok = bc.Correlator(N=20, h=0.1, t0=(-1, -1, -1), Np=26, K=10)  # P = 2.6
+    ok.shape_upload(0, A)
+    ok.shape_upload(1, B)
 
 
 def test_correlate_before_spectrum_is_estate(bc):
