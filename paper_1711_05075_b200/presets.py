@@ -1,0 +1,29 @@
+"""Per-workload parameters of the correlator (mode, FFT period, band).
+
+Chosen from the band-error measurements recorded in DESIGN.md §5 (spectral f at
+several bands against the exact pair-lens f, which tests pin to the fp64
+oracle): the smallest band whose error stays well inside the north_star
+tolerance max|f_gpu - f_cpu| <= 1e-4 max|f_cpu|.
+
+* tiny    exact mode, fp64 (the 1e-9 bar is unreachable for any band limit)
+* single  exact mode, fp32 (0.01-radius balls need sigma_f ~ 8 spectrally; exact is cheaper)
+* torus   spectral, Np = 144 (P = 2.25), K = 71: 2.2e-5 measured
+* sweep   spectral, Np = 256 (P = 2), K = 255: 3.8e-5 measured (K = 191: 7.4e-5)
+* docking spectral, Np = 128 (P = 128 A), K = 191: 5.2e-5 measured (K = 127: 1.3e-4 fails)
+"""
+from __future__ import annotations
+
+PRESETS = {
+    "tiny": dict(mode="exact", precision="f64", Np=0, K=0),
+    "single": dict(mode="exact", precision="f32", Np=0, K=0),
+    "torus": dict(mode="spectral", precision="f32", Np=144, K=71),
+    "sweep": dict(mode="spectral", precision="f32", Np=256, K=255),
+    "docking": dict(mode="spectral", precision="f32", Np=128, K=191),
+}
+
+
+def correlator_kwargs(name: str, N: int, h: float, t0, weights: str, **overrides) -> dict:
+    p = dict(PRESETS[name])
+    p.update(overrides)
+    return dict(N=N, h=h, t0=t0, Np=p["Np"], K=p["K"], mode=p["mode"], precision=p["precision"],
+                weights=weights, max_batch=p.get("max_batch", 0), spread_eps=p.get("spread_eps", 0.0))
