@@ -1,7 +1,7 @@
 # libballcorr: hand-written sm_100a CUDA behind a C ABI (include/ballcorr.h)
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -Xptxas -v
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 --expt-relaxed-constexpr -Xcompiler -fPIC -Iinclude -Xptxas -v
 SRC := $(wildcard paper_1711_05075_b200/csrc/*.cu)
 HDR := $(wildcard paper_1711_05075_b200/csrc/*.cuh) include/ballcorr.h
 LIB := paper_1711_05075_b200/lib/libballcorr.so

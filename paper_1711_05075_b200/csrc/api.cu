@@ -25,8 +25,8 @@ struct ShapePlan {
     int L = 0, c = 0, G = 0;
     int o[3] = {0, 0, 0};
     double hf = 0, tau = 0, cut = 0;
-    FftPlan fft{};
     float2 *d_mult[3] = {nullptr, nullptr, nullptr};  // axis x, y, z
+    float2 *d_ctw = nullptr;                           // coset twiddles [c][L]
 };
 
 struct PendingEvent {
@@ -56,11 +56,10 @@ struct bc_ctx {
     double P = 0;
     int K = 0, M = 0, Kz = 0, Fz = 0;
     ShapePlan plan[2];
-    FftPlan fft_np{};
+    std::map<int, float2 *> d_tw;  // exp(-2 pi i m / L) per FFT length
     int *d_csr_off = nullptr, *d_csr_idx = nullptr;
     float2 *d_Ahat = nullptr;
     bool have_spec = false;
-    float2 *d_ph[3] = {nullptr, nullptr, nullptr};
 
     // workspaces
     void *ws1 = nullptr, *ws2 = nullptr;
@@ -120,20 +119,6 @@ bool friendly(int L)
     for (int f : {2, 3, 5})
         while (L % f == 0) L /= f;
     return L == 1;
-}
-
-bool make_fft_plan(int L, FftPlan &pl)
-{
-    if (!friendly(L)) return false;
-    pl.L = L;
-    pl.nst = 0;
-    int r = L;
-    while (r % 8 == 0 && pl.nst < BC_FFT_MAX_STAGES) { pl.radix[pl.nst++] = 8; r /= 8; }
-    while (r % 4 == 0 && pl.nst < BC_FFT_MAX_STAGES) { pl.radix[pl.nst++] = 4; r /= 4; }
-    while (r % 2 == 0 && pl.nst < BC_FFT_MAX_STAGES) { pl.radix[pl.nst++] = 2; r /= 2; }
-    while (r % 5 == 0 && pl.nst < BC_FFT_MAX_STAGES) { pl.radix[pl.nst++] = 5; r /= 5; }
-    while (r % 3 == 0 && pl.nst < BC_FFT_MAX_STAGES) { pl.radix[pl.nst++] = 3; r /= 3; }
-    return r == 1;
 }
 
 bool is_device_ptr(const void *ptr)
@@ -235,6 +220,23 @@ void collect_profile(bc_ctx *ctx)
     ctx->pending.clear();
 }
 
+// ------------------------------------------------------------------ twiddle tables
+
+bc_status ensure_twiddles(bc_ctx *ctx, int L)
+{
+    if (ctx->d_tw.count(L)) return BC_OK;
+    std::vector<float2> t(L);
+    for (int m = 0; m < L; m++) {
+        const double ang = -2 * kPi * (double)m / L;
+        t[m] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+    }
+    float2 *d = nullptr;
+    CU(ctx, cudaMalloc(&d, sizeof(float2) * L));
+    ctx->d_tw[L] = d;
+    CU(ctx, cudaMemcpy(d, t.data(), sizeof(float2) * L, cudaMemcpyHostToDevice));
+    return BC_OK;
+}
+
 // ------------------------------------------------------------------ spectral plan of one shape
 
 // Choose (c, L, G, tau, cut, origin) so that the Gaussian-smoothed density of
@@ -257,7 +259,7 @@ bc_status plan_shape(bc_ctx *ctx, int which, const double lo[3], const double hi
     for (int c = 1; c <= 8; c++) {
         int L = (Gmin + c - 1) / c;
         for (; L <= 1024; L++) {
-            if (!friendly(L)) continue;
+            if (!fft_size_supported(L)) continue;
             const int G = c * L;
             const double hf = P / G;
             const double ke = (double)K / P, ka = (double)(G - K) / P;
@@ -288,11 +290,11 @@ bc_status plan_shape(bc_ctx *ctx, int which, const double lo[3], const double hi
         if ((best.o[a] + best.L) * best.hf < hi[a] + rmax + best.cut + best.hf)
             return fail(ctx, BC_ERANGE, "internal: box does not cover shape %c on axis %d", which ? 'B' : 'A', a);
     }
-    if (!make_fft_plan(best.L, best.fft)) return fail(ctx, BC_EUNSUPPORTED, "box length %d not factorable", best.L);
-
     // multipliers: hf exp(-2 pi i k o / G) exp(+2 pi^2 tau^2 k^2 / P^2)   (shift + Gaussian deconvolution)
+    // and, for A only, the origin phase exp(2 pi i k t0 / P) of the inverse transform
     ShapePlan &dst = ctx->plan[which];
     for (int a = 0; a < 3; a++) dfree(dst.d_mult[a]);
+    dfree(dst.d_ctw);
     dst = best;
     const bool cplx = ctx->p.weights == BC_WEIGHTS_COMPLEX;
     for (int a = 0; a < 3; a++) {
@@ -302,13 +304,26 @@ bc_status plan_shape(bc_ctx *ctx, int which, const double lo[3], const double hi
         for (int q = 0; q < nk; q++) {
             const long long k = klo + q;
             const long long num = ((k * dst.o[a]) % dst.G + dst.G) % dst.G;
-            const double ang = -2 * kPi * (double)num / dst.G;
+            double ang = -2 * kPi * (double)num / dst.G;
+            if (which == 0) {
+                const double x = (double)k * ctx->p.t0[a] / P;
+                ang += 2 * kPi * (x - std::floor(x));
+            }
             const double amp = dst.hf * std::exp(2 * kPi * kPi * dst.tau * dst.tau * (double)(k * k) / (P * P));
             m[q] = make_float2((float)(amp * std::cos(ang)), (float)(amp * std::sin(ang)));
         }
         TRY(dalloc(ctx, &dst.d_mult[a], sizeof(float2) * nk));
         CU(ctx, cudaMemcpy(dst.d_mult[a], m.data(), sizeof(float2) * nk, cudaMemcpyHostToDevice));
     }
+    std::vector<float2> ct((size_t)dst.c * dst.L);
+    for (int p = 0; p < dst.c; p++)
+        for (int n = 0; n < dst.L; n++) {
+            const double ang = -2 * kPi * (double)(((long long)p * n) % dst.G) / dst.G;
+            ct[(size_t)p * dst.L + n] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+        }
+    TRY(dalloc(ctx, &dst.d_ctw, sizeof(float2) * ct.size()));
+    CU(ctx, cudaMemcpy(dst.d_ctw, ct.data(), sizeof(float2) * ct.size(), cudaMemcpyHostToDevice));
+    TRY(ensure_twiddles(ctx, dst.L));
     return BC_OK;
 }
 
@@ -392,28 +407,30 @@ bc_status ensure_ws(bc_ctx *ctx, void **ptr, size_t &cur, size_t need)
     return BC_OK;
 }
 
-// per-rotation sizes (bytes) of the two ping-pong spectral workspaces of shape B
+// per-rotation sizes (bytes) of the two ping-pong spectral workspaces of a shape
+//   ws1: box -> T2 -> X1        ws2: T1 -> F (B) or A_hat staging -> Y1
 void spectral_ws_sizes(const bc_ctx *ctx, int which, size_t &s1, size_t &s2)
 {
     const ShapePlan &pl = ctx->plan[which];
     const size_t L = pl.L, Kz = ctx->Kz, M = ctx->M, Np = ctx->p.Np, N = ctx->p.N, Fz = ctx->Fz;
     const bool cplx = ctx->p.weights == BC_WEIGHTS_COMPLEX;
     const size_t box = L * L * L * (cplx ? 8 : 4);
-    const size_t T1 = L * L * Kz * 8, T2 = L * M * Kz * 8, Bh = M * M * Kz * 8;
+    const size_t T1 = L * L * Kz * 8, T2 = L * M * Kz * 8;
     const size_t F = Np * Np * Fz * 8, X1 = N * Np * Fz * 8, Y1 = N * N * Fz * 8;
-    s1 = std::max(std::max(box, T2), std::max(F, Y1));
-    s2 = std::max(std::max(T1, Bh), X1);
+    s1 = std::max(std::max(box, T2), X1);
+    s2 = std::max(std::max(T1, F), Y1);
     s1 = (s1 + 255) / 256 * 256;
     s2 = (s2 + 255) / 256 * 256;
 }
 
-// spread + three axis passes of one shape -> band spectrum (k layout [kx][ky][kz])
-bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, void *box_T2, void *T1_out,
-                         float2 *spec_out, size_t s1_per, size_t s2_per, cudaStream_t s)
+// spread + z + y passes of one shape; for A also the x pass into A_hat.
+bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, void *ws1, void *ws2,
+                         size_t s1_per, size_t s2_per, cudaStream_t s)
 {
     const ShapePlan &pl = ctx->plan[which];
     const bool cplx = ctx->p.weights == BC_WEIGHTS_COMPLEX;
     const int L = pl.L;
+    const float2 *tw = ctx->d_tw[L];
     {
         SpreadArgs a{};
         a.L = L;
@@ -432,70 +449,63 @@ bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, voi
         a.csr_idx = which == 0 ? ctx->d_csr_idx : nullptr;
         a.rot = d_rot;
         a.complex_w = cplx;
-        a.out = box_T2;
+        a.out = ws1;
         a.out_batch_stride = (long long)(s1_per / (cplx ? 8 : 4));
         a.tiles_per_axis = (L + 15) / 16;
         StageScope sc(ctx, s, which ? "spread_B" : "spread_A");
         launch_spread(a, nb, s);
         ctx->launches++;
     }
+    PassArgs base{};
+    base.L = L;
+    base.c = pl.c;
+    base.G = pl.G;
+    base.signed_k = 1;
+    base.tw = tw;
+    base.ctw = pl.d_ctw;
     {
-        AxisArgs a{};
-        a.L = L;
-        a.c = pl.c;
+        PassArgs a = base;
         a.klo = cplx ? -ctx->K : 0;
         a.nk = ctx->Kz;
-        a.signed_k = 1;
-        a.sign = -1.f;
         a.mult = pl.d_mult[2];
-        a.plan = pl.fft;
-        a.in = box_T2;
+        a.lines = (long long)L * L;
+        a.in = ws1;
         a.in_real = !cplx;
         a.in_bstride = (long long)(s1_per / (cplx ? 8 : 4));
-        a.out = (float2 *)T1_out;
+        a.out = (float2 *)ws2;
         a.out_bstride = (long long)(s2_per / 8);
-        StageScope sc(ctx, s, which ? "axis_z_B" : "axis_z_A");
-        launch_axis_contig(a, L * L, nb, s);
+        StageScope sc(ctx, s, which ? "pass_z_B" : "pass_z_A");
+        launch_pass_contig(a, nb, s);
         ctx->launches++;
     }
     {
-        AxisArgs a{};
-        a.L = L;
-        a.c = pl.c;
+        PassArgs a = base;
         a.klo = -ctx->K;
         a.nk = ctx->M;
-        a.signed_k = 1;
-        a.sign = -1.f;
         a.mult = pl.d_mult[1];
-        a.plan = pl.fft;
         a.O = L;
         a.I = ctx->Kz;
-        a.in = T1_out;
+        a.in = ws2;
         a.in_bstride = (long long)(s2_per / 8);
-        a.out = (float2 *)box_T2;
+        a.out = (float2 *)ws1;
         a.out_bstride = (long long)(s1_per / 8);
-        StageScope sc(ctx, s, which ? "axis_y_B" : "axis_y_A");
-        launch_axis_strided(a, nb, s);
+        StageScope sc(ctx, s, which ? "pass_y_B" : "pass_y_A");
+        launch_pass_strided(a, -1, nb, s);
         ctx->launches++;
     }
-    {
-        AxisArgs a{};
-        a.L = L;
-        a.c = pl.c;
+    if (which == 0) {
+        PassArgs a = base;
         a.klo = -ctx->K;
         a.nk = ctx->M;
-        a.signed_k = 1;
-        a.sign = -1.f;
         a.mult = pl.d_mult[0];
-        a.plan = pl.fft;
         a.O = 1;
         a.I = ctx->M * ctx->Kz;
-        a.in = box_T2;
+        a.in = ws1;
         a.in_bstride = (long long)(s1_per / 8);
-        a.out = spec_out;
-        a.out_bstride = (long long)(s2_per / 8);
-        StageScope sc(ctx, s, which ? "axis_x_B" : "axis_x_A");
-        launch_axis_strided(a, nb, s);
+        a.out = ctx->d_Ahat;
+        a.out_bstride = 0;
+        StageScope sc(ctx, s, "pass_x_A");
+        launch_pass_strided(a, -1, nb, s);
         ctx->launches++;
     }
     CU(ctx, cudaGetLastError());
@@ -603,6 +613,7 @@ bc_status bc_create(int device, const bc_params *p, bc_ctx **out)
     if (p->mode == BC_MODE_SPECTRAL) {
         if (p->precision != BC_FP32) return BC_EUNSUPPORTED;
         if (p->Np < p->N || p->Np < 2 || (p->Np % 2) != 0 || !friendly(p->Np) || p->Np > 1024) return BC_EINVAL;
+        if (!fft_size_supported(p->Np)) return BC_EUNSUPPORTED;
         if (p->K < 1 || p->K > 2047) return BC_EINVAL;
         if (p->N > 1625) return BC_EUNSUPPORTED;
     }
@@ -622,24 +633,9 @@ bc_status bc_create(int device, const bc_params *p, bc_ctx **out)
         ctx->M = 2 * p->K + 1;
         ctx->Kz = cplx ? ctx->M : p->K + 1;
         ctx->Fz = cplx ? p->Np : p->Np / 2 + 1;
-        if (!make_fft_plan(p->Np, ctx->fft_np)) {
-            delete ctx;
-            return BC_EINVAL;
-        }
-        // origin phases exp(2 pi i k t0_a / P), k in [-K, K]
-        for (int a = 0; a < 3; a++) {
-            std::vector<float2> ph(ctx->M);
-            for (int q = 0; q < ctx->M; q++) {
-                const double k = q - p->K;
-                const double x = k * p->t0[a] / ctx->P;
-                const double fr = x - std::floor(x);
-                ph[q] = make_float2((float)std::cos(2 * kPi * fr), (float)std::sin(2 * kPi * fr));
-            }
-            if (dalloc(ctx, &ctx->d_ph[a], sizeof(float2) * ctx->M) != BC_OK ||
-                cudaMemcpy(ctx->d_ph[a], ph.data(), sizeof(float2) * ctx->M, cudaMemcpyHostToDevice) != cudaSuccess) {
-                bc_destroy(ctx);
-                return BC_ENOMEM;
-            }
+        if (ensure_twiddles(ctx, p->Np) != BC_OK) {
+            bc_destroy(ctx);
+            return BC_ENOMEM;
         }
     }
     *out = ctx;
@@ -657,8 +653,9 @@ bc_status bc_destroy(bc_ctx *ctx)
         dfree(ctx->d_balls64[w]);
         dfree(ctx->d_w64[w]);
         for (int a = 0; a < 3; a++) dfree(ctx->plan[w].d_mult[a]);
+        dfree(ctx->plan[w].d_ctw);
     }
-    for (int a = 0; a < 3; a++) dfree(ctx->d_ph[a]);
+    for (auto &kv : ctx->d_tw) cudaFree(kv.second);
     dfree(ctx->d_csr_off);
     dfree(ctx->d_csr_idx);
     dfree(ctx->d_Ahat);
@@ -755,7 +752,7 @@ bc_status bc_spectrum_A(bc_ctx *ctx, void *stream)
         cudaFree(w1);
         return fail(ctx, BC_ENOMEM, "spectrum_A workspace: %s", cudaGetErrorString(e));
     }
-    bc_status st = shape_spectrum(ctx, 0, nullptr, 1, w1, w2, ctx->d_Ahat, s1, s2, s);
+    bc_status st = shape_spectrum(ctx, 0, nullptr, 1, w1, w2, s1, s2, s);
     cudaError_t se = cudaStreamSynchronize(s);
     collect_profile(ctx);
     cudaFree(w1);
@@ -896,65 +893,64 @@ bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, in
         const int Np = ctx->p.Np;
         for (int64_t r0 = 0; r0 < n_rot; r0 += nb) {
             const int b = (int)std::min<int64_t>(nb, n_rot - r0);
-            // 1-4: spectrum of R B on the band
-            TRY(shape_spectrum(ctx, 1, ctx->d_rot + 9 * r0, b, ctx->ws1, ctx->ws2, (float2 *)ctx->ws2, s1, s2, s));
-            // 5: spectral product with A, origin phase, fold onto Np^3
+            // 1-3: spread R B, z and y passes of its box DFT
+            TRY(shape_spectrum(ctx, 1, ctx->d_rot + 9 * r0, b, ctx->ws1, ctx->ws2, s1, s2, s));
+            const ShapePlan &pb = ctx->plan[1];
+            // 4: x pass fused with the spectral product (A' conj(RB)) and the fold onto Np^3
             {
-                FoldArgs a{};
+                FoldXArgs a{};
+                a.L = pb.L;
+                a.c = pb.c;
+                a.G = pb.G;
                 a.K = ctx->K;
+                a.M = ctx->M;
                 a.Kz = ctx->Kz;
                 a.Np = Np;
                 a.Fz = ctx->Fz;
                 a.complex_w = cplx;
+                a.mult = pb.d_mult[0];
+                a.tw = ctx->d_tw[pb.L];
+                a.ctw = pb.d_ctw;
+                a.T2 = (const float2 *)ctx->ws1;
+                a.t2_bstride = (long long)(s1 / 8);
                 a.Ahat = ctx->d_Ahat;
-                a.Bhat = (const float2 *)ctx->ws2;
-                a.b_bstride = (long long)(s2 / 8);
-                a.f_bstride = (long long)(s1 / 8);
-                a.phx = ctx->d_ph[0];
-                a.phy = ctx->d_ph[1];
-                a.phz = ctx->d_ph[2];
-                a.F = (float2 *)ctx->ws1;
-                StageScope sc(ctx, s, "fold");
-                launch_fold(a, b, s);
+                a.F = (float2 *)ctx->ws2;
+                a.f_bstride = (long long)(s2 / 8);
+                StageScope sc(ctx, s, "fold_x");
+                launch_fold_x(a, b, s);
                 ctx->launches++;
             }
-            // 6-7: inverse transforms along x and y (only the N output rows)
+            // 5-6: inverse transforms along x and y (only the N output rows)
+            PassArgs inv{};
+            inv.L = Np;
+            inv.c = 1;
+            inv.G = Np;
+            inv.klo = 0;
+            inv.nk = (int)N;
+            inv.signed_k = 0;
+            inv.tw = ctx->d_tw[Np];
             {
-                AxisArgs a{};
-                a.L = Np;
-                a.c = 1;
-                a.klo = 0;
-                a.nk = (int)N;
-                a.signed_k = 0;
-                a.sign = 1.f;
-                a.plan = ctx->fft_np;
+                PassArgs a = inv;
                 a.O = 1;
                 a.I = Np * ctx->Fz;
-                a.in = ctx->ws1;
-                a.in_bstride = (long long)(s1 / 8);
-                a.out = (float2 *)ctx->ws2;
-                a.out_bstride = (long long)(s2 / 8);
-                StageScope sc(ctx, s, "inv_x");
-                launch_axis_strided(a, b, s);
-                ctx->launches++;
-            }
-            {
-                AxisArgs a{};
-                a.L = Np;
-                a.c = 1;
-                a.klo = 0;
-                a.nk = (int)N;
-                a.signed_k = 0;
-                a.sign = 1.f;
-                a.plan = ctx->fft_np;
-                a.O = (int)N;
-                a.I = ctx->Fz;
                 a.in = ctx->ws2;
                 a.in_bstride = (long long)(s2 / 8);
                 a.out = (float2 *)ctx->ws1;
                 a.out_bstride = (long long)(s1 / 8);
+                StageScope sc(ctx, s, "inv_x");
+                launch_pass_strided(a, 1, b, s);
+                ctx->launches++;
+            }
+            {
+                PassArgs a = inv;
+                a.O = (int)N;
+                a.I = ctx->Fz;
+                a.in = ctx->ws1;
+                a.in_bstride = (long long)(s1 / 8);
+                a.out = (float2 *)ctx->ws2;
+                a.out_bstride = (long long)(s2 / 8);
                 StageScope sc(ctx, s, "inv_y");
-                launch_axis_strided(a, b, s);
+                launch_pass_strided(a, 1, b, s);
                 ctx->launches++;
             }
             // 8: inverse along z (C2R / C2C), 1/P^3, full output or reduction keys
@@ -969,9 +965,9 @@ bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, in
                 a.Fz = ctx->Fz;
                 a.hermitian = !cplx;
                 a.scale = (float)(1.0 / (ctx->P * ctx->P * ctx->P));
-                a.plan = ctx->fft_np;
-                a.in = (const float2 *)ctx->ws1;
-                a.in_bstride = (long long)(s1 / 8);
+                a.tw = ctx->d_tw[Np];
+                a.in = (const float2 *)ctx->ws2;
+                a.in_bstride = (long long)(s2 / 8);
                 a.out_kind = out_kind;
                 a.out_full = dout + out_per * r0;
                 a.full_bstride = N3;

@@ -2,7 +2,6 @@
 #pragma once
 
 #include "common.cuh"
-#include "fft.cuh"
 
 // ----------------------------------------------------------------- spreading
 // Gaussian-smoothed ball density on a box of the fine lattice (spacing hf):
@@ -30,31 +29,46 @@ struct SpreadArgs {
     int tiles_per_axis;
 };
 
-// ----------------------------------------------------------------- axis transforms
-// One axis of the "box DFT":  X(k) = mult(k) * sum_{n<L} x_n exp(sign 2 pi i k n / G),  G = c L,
-// evaluated through c cosets k = c q + p of an L-point FFT of x_n exp(sign 2 pi i p n / G).
-struct AxisArgs {
-    int L;            // transform length (input samples per line)
-    int c;            // coset count, G = c L
-    int klo, nk;      // output window: k in [klo, klo + nk) (signed in (-G/2, G/2] when signed_k)
-    int signed_k;
-    float sign;       // -1 forward, +1 inverse
+// ----------------------------------------------------------------- axis transforms (passes.cu)
+// One axis of the box DFT:  X(k) = mult(k) sum_{n<L} x_n exp(-2 pi i k n / G),  G = c L,
+// through c cosets k = c q + p of an L-point FFT of x_n exp(-2 pi i p n / G);
+// the inverse passes use c = 1, sign +1 and unsigned outputs q in [0, nk).
+struct PassArgs {
+    int L, c, G;
+    int klo, nk, signed_k;
     const float2 *mult;   // nk multipliers (nullptr => 1)
-    FftPlan plan;
-    // strided layout: in[b][O][L][I], out[b][O][nk][I]
+    const float2 *tw;     // exp(-2 pi i m / L), m < L
+    const float2 *ctw;    // coset twiddles exp(-2 pi i p n / G), [c][L]
+    // contiguous: in[b][lines][L] -> out[b][lines][nk]
+    long long lines;
+    int in_real;
+    // strided: in[b][O][L][I] -> out[b][O][nk][I]
     int O, I;
     long long in_bstride, out_bstride;
     const void *in;
-    int in_real;      // input is float (contiguous kernel only)
     float2 *out;
 };
 
-// contiguous-axis epilogue of the last inverse pass
+// fused x-pass of R B + spectral product with A + fold onto Np^3 (passes.cu)
+struct FoldXArgs {
+    int L, c, G;
+    int K, M, Kz, Np, Fz;
+    int complex_w;
+    const float2 *mult;   // x-axis multipliers of B, index kx + K
+    const float2 *tw, *ctw;
+    const float2 *T2;     // [b][ix][ky][kz]
+    long long t2_bstride;
+    const float2 *Ahat;   // [kx][ky][kz], origin phase folded in
+    float2 *F;            // [b][Np][Np][Fz]
+    long long f_bstride;
+};
+
+// contiguous inverse z pass + epilogue
 struct LastArgs {
-    int Np, N, Fz;       // FFT length, output window, stored input length per line
+    int Np, N, Fz;
     int hermitian;       // 1: C2R from Fz = Np/2+1 stored modes; 0: C2C, Fz = Np
     float scale;
-    FftPlan plan;
+    const float2 *tw;    // exp(-2 pi i m / Np)
     const float2 *in;    // [b][N*N lines][Fz]
     long long in_bstride;
     int out_kind;        // BC_OUT_*
@@ -63,20 +77,11 @@ struct LastArgs {
     unsigned long long *keys;  // [b][2]: (min key, max key)
 };
 
-struct FoldArgs {
-    int K, Kz, Np, Fz;
-    int complex_w;
-    const float2 *Ahat;       // [kx][ky][kz] (kx, ky in [-K, K]; kz in [0,K] real / [-K,K] complex)
-    const float2 *Bhat;       // [b][kx][ky][kz]
-    long long b_bstride, f_bstride;
-    const float2 *phx, *phy, *phz;  // exp(2 pi i k t0_a / P), index k + K
-    float2 *F;                // [b][Np][Np][Fz]
-};
-
 void launch_spread(const SpreadArgs &a, int batch, cudaStream_t s);
-void launch_axis_contig(const AxisArgs &a, int lines, int batch, cudaStream_t s);
-void launch_axis_strided(const AxisArgs &a, int batch, cudaStream_t s);
-void launch_fold(const FoldArgs &a, int batch, cudaStream_t s);
+bool fft_size_supported(int L);
+void launch_pass_contig(const PassArgs &a, int batch, cudaStream_t s);
+void launch_pass_strided(const PassArgs &a, int sign, int batch, cudaStream_t s);
+void launch_fold_x(const FoldXArgs &a, int batch, cudaStream_t s);
 void launch_last(const LastArgs &a, int batch, cudaStream_t s);
 void launch_keys_init(unsigned long long *keys, int n, cudaStream_t s);
 void launch_keys_finalize(const unsigned long long *keys, int batch, int out_kind, void *out, cudaStream_t s);

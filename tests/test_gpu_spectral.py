@@ -35,7 +35,7 @@ def spectral(bc, w, Np, K, **kw):
     return c
 
 
-@pytest.mark.parametrize("seed,N,Np,K", [(41, 20, 24, 24), (42, 18, 30, 17), (43, 16, 20, 31)])
+@pytest.mark.parametrize("seed,N,Np,K", [(41, 20, 24, 24), (42, 18, 32, 17), (43, 16, 20, 31)])
 def test_real_vs_bandlimited(bc, oracle_mod, seed, N, Np, K):
     w = random_small_case(seed, n_a=11, n_b=9, n_rot=3, N=N)
     P = Np * w.h
@@ -107,7 +107,7 @@ def test_support_wrap_is_rejected(bc):
     with pytest.raises(bc.BallCorrError) as e:
         c.shape_upload(1, B)
     assert e.value.status == bc.BC_ERANGE
-    ok = bc.Correlator(N=20, h=0.1, t0=(-1, -1, -1), Np=26, K=10)  # P = 2.6
+    ok = bc.Correlator(N=20, h=0.1, t0=(-1, -1, -1), Np=32, K=10)  # P = 3.2
     ok.shape_upload(0, A)
     ok.shape_upload(1, B)
 
