@@ -475,7 +475,7 @@ bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, voi
         a.out = (float2 *)ws2;
         a.out_bstride = (long long)(s2_per / 8);
         StageScope sc(ctx, s, which ? "pass_z_B" : "pass_z_A");
-        launch_pass_contig(a, nb, s);
+        launch_pass(a, 0, nb, s);
         ctx->launches++;
     }
     {
@@ -490,7 +490,7 @@ bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, voi
         a.out = (float2 *)ws1;
         a.out_bstride = (long long)(s1_per / 8);
         StageScope sc(ctx, s, which ? "pass_y_B" : "pass_y_A");
-        launch_pass_strided(a, -1, nb, s);
+        launch_pass(a, 1, nb, s);
         ctx->launches++;
     }
     if (which == 0) {
@@ -505,7 +505,7 @@ bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, voi
         a.out = ctx->d_Ahat;
         a.out_bstride = 0;
         StageScope sc(ctx, s, "pass_x_A");
-        launch_pass_strided(a, -1, nb, s);
+        launch_pass(a, 2, nb, s);
         ctx->launches++;
     }
     CU(ctx, cudaGetLastError());
@@ -938,7 +938,7 @@ bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, in
                 a.out = (float2 *)ctx->ws1;
                 a.out_bstride = (long long)(s1 / 8);
                 StageScope sc(ctx, s, "inv_x");
-                launch_pass_strided(a, 1, b, s);
+                launch_pass(a, 3, b, s);
                 ctx->launches++;
             }
             {
@@ -950,7 +950,7 @@ bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, in
                 a.out = (float2 *)ctx->ws2;
                 a.out_bstride = (long long)(s2 / 8);
                 StageScope sc(ctx, s, "inv_y");
-                launch_pass_strided(a, 1, b, s);
+                launch_pass(a, 3, b, s);
                 ctx->launches++;
             }
             // 8: inverse along z (C2R / C2C), 1/P^3, full output or reduction keys

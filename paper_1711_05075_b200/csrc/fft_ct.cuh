@@ -1,17 +1,20 @@
-// fft_ct.cuh -- compile-time-sized mixed-radix Stockham FFT over shared memory.
+// fft_ct.cuh -- compile-time mixed-radix FFT of lines held in registers.
 //
 // Hand-written replacement of the paper's library FFT stages (PAPER.md L524-L526,
 // "FFTW on the CPU and cuFFT(W) on the GPU"; Appendix C) so that every
-// transform can be fused with the kernel arithmetic around it.
+// transform fuses with the arithmetic around it.
 //
-// A block transforms NL lines of length L; each line is owned by TPL consecutive
-// threads.  Line l lives in shared memory at buf[l * LS + PAD(idx)], with
-// PAD(idx) = idx + idx/16 and LS odd in float2 units (bank spreading).
-// Stage with radix R (Stockham autosort, natural-order output):
+// A line of length L is owned by TPL consecutive threads; thread tl holds the
+// E = L / TPL elements x[m] = line[tl + TPL m] on entry and the outputs
+// X[m] = DFT(line)[tl + TPL m] on exit.  Stockham stages (natural order):
 //     v[r] = a[j + r L/R] * w_L^{r (j mod Ns) L/(Ns R)},  V = DFT_R(v),
 //     b[(j / Ns) Ns R + (j mod Ns) + r Ns] = V[r],        Ns *= R.
-// Sizes and radix schedules are compile-time, so all index arithmetic is
-// strength-reduced; twiddles come from a per-block table tw[m] = exp(-2 pi i m / L).
+// The first stage reads registers, the last writes registers; only the
+// stages in between exchange through shared memory (line buffer with
+// PAD(idx) = idx + idx/16).  Sizes, radices and thread counts are
+// compile-time, so index arithmetic is strength-reduced; stage twiddles come
+// from a per-block table tw[m] = exp(-2 pi i m / L), radix-internal twiddles
+// are compile-time constants.
 #pragma once
 
 #include "common.cuh"
@@ -21,56 +24,67 @@ namespace fct {
 __host__ __device__ constexpr int pad(int idx) { return idx + (idx >> 4); }
 __host__ __device__ constexpr int line_stride(int L) { return (pad(L - 1) + 1) | 1; }
 
-// ---------------------------------------------------------------- schedules
-template <int L> struct Sched;
-#define BC_SCHED(L_, N_, A_, B_, C_, D_) \
-    template <> struct Sched<L_> { static constexpr int n = N_; static constexpr int r[4] = {A_, B_, C_, D_}; };
-BC_SCHED(16, 1, 16, 1, 1, 1)
-BC_SCHED(20, 2, 4, 5, 1, 1)
-BC_SCHED(24, 2, 8, 3, 1, 1)
-BC_SCHED(32, 2, 16, 2, 1, 1)
-BC_SCHED(36, 3, 4, 3, 3, 1)
-BC_SCHED(40, 2, 8, 5, 1, 1)
-BC_SCHED(48, 2, 16, 3, 1, 1)
-BC_SCHED(64, 2, 16, 4, 1, 1)
-BC_SCHED(72, 3, 8, 3, 3, 1)
-BC_SCHED(80, 2, 16, 5, 1, 1)
-BC_SCHED(96, 3, 16, 2, 3, 1)
-BC_SCHED(128, 2, 16, 8, 1, 1)
-BC_SCHED(144, 3, 16, 3, 3, 1)
-BC_SCHED(160, 3, 16, 2, 5, 1)
-BC_SCHED(192, 3, 16, 4, 3, 1)
-BC_SCHED(240, 3, 16, 5, 3, 1)
-BC_SCHED(256, 2, 16, 16, 1, 1)
-BC_SCHED(288, 4, 16, 2, 3, 3)
-BC_SCHED(320, 3, 16, 4, 5, 1)
-BC_SCHED(384, 3, 16, 8, 3, 1)
-BC_SCHED(480, 4, 16, 2, 5, 3)
-BC_SCHED(512, 3, 8, 8, 8, 1)
-BC_SCHED(576, 4, 16, 4, 3, 3)
-BC_SCHED(640, 3, 16, 8, 5, 1)
-BC_SCHED(768, 3, 16, 16, 3, 1)
-BC_SCHED(960, 4, 16, 4, 5, 3)
-BC_SCHED(1024, 3, 16, 16, 4, 1)
-#undef BC_SCHED
-
-// list used by the host dispatchers
-#define BC_FOR_EACH_L(X) X(16) X(20) X(24) X(32) X(36) X(40) X(48) X(64) X(72) X(80) X(96) X(128) X(144) X(160) X(192) X(240) X(256) \
-    X(288) X(320) X(384) X(480) X(512) X(576) X(640) X(768) X(960) X(1024)
-
-template <int L, int S>
-__host__ __device__ constexpr int ns_before()
+// ---------------------------------------------------------------- constexpr trigonometry
+constexpr double kPiD = 3.14159265358979323846264338327950288;
+__host__ __device__ constexpr double csin_red(double x)  // |x| <= pi/4
 {
-    int ns = 1;
-    for (int s = 0; s < S; s++) ns *= Sched<L>::r[s];
-    return ns;
+    double t = x, s = x;
+    for (int n = 1; n < 14; n++) {
+        t *= -x * x / ((2 * n) * (2 * n + 1));
+        s += t;
+    }
+    return s;
 }
+__host__ __device__ constexpr double ccos_red(double x)
+{
+    double t = 1, s = 1;
+    for (int n = 1; n < 14; n++) {
+        t *= -x * x / ((2 * n - 1) * (2 * n));
+        s += t;
+    }
+    return s;
+}
+// cos / sin of 2 pi m / n for integers (exact octant reduction)
+__host__ __device__ constexpr double cos2pi(long long m, long long n)
+{
+    m %= n;
+    if (m < 0) m += n;
+    const long long o8 = (8 * m) / n;  // octant 0..7
+    const double r = 2 * kPiD * ((double)(8 * m - o8 * n) / (8.0 * n));  // in [0, pi/4)
+    switch (o8) {
+    case 0: return ccos_red(r);
+    case 1: return csin_red(kPiD / 4 - r);
+    case 2: return -csin_red(r);
+    case 3: return -ccos_red(kPiD / 4 - r);
+    case 4: return -ccos_red(r);
+    case 5: return -csin_red(kPiD / 4 - r);
+    case 6: return csin_red(r);
+    default: return ccos_red(kPiD / 4 - r);
+    }
+}
+__host__ __device__ constexpr double sin2pi(long long m, long long n) { return cos2pi(4 * m - n, 4 * n); }
+
+template <int N, int SIGN>
+struct WTab {
+    float re[N], im[N];
+    __host__ __device__ constexpr WTab() : re(), im()
+    {
+        for (int m = 0; m < N; m++) {
+            re[m] = (float)cos2pi(m, N);
+            im[m] = (float)(SIGN * sin2pi(m, N));
+        }
+    }
+};
 
 // ---------------------------------------------------------------- small DFTs (SIGN = -1 forward, +1 inverse)
 template <int SIGN>
 BC_DEV float2 mul_si(float2 a) { return SIGN < 0 ? make_float2(a.y, -a.x) : make_float2(-a.y, a.x); }
 
 template <int R, int SIGN> struct Dft;
+
+template <int SIGN> struct Dft<1, SIGN> {
+    static BC_DEV void run(float2 *) {}
+};
 
 template <int SIGN> struct Dft<2, SIGN> {
     static BC_DEV void run(float2 *v) {
@@ -122,63 +136,109 @@ template <int SIGN> struct Dft<5, SIGN> {
     }
 };
 
-// w_n^m = exp(SIGN 2 pi i m / n) for the composite radices
-template <int N, int SIGN>
-BC_DEV float2 wconst(int m)
+// Composite N = N1 N2 (Cooley-Tukey in registers): n = N2 n1 + n2, k = k1 + N1 k2.
+template <int N1, int N2, int SIGN>
+BC_DEV void dft_ct(float2 *v)
 {
-    // cos / sin of 2 pi m / 16 (N = 16) or 2 pi m / 8 (N = 8), m reduced mod N
-    const float c16[16] = {1.0f, 0.92387953251128675613f, 0.70710678118654752440f, 0.38268343236508977173f,
-                           0.0f, -0.38268343236508977173f, -0.70710678118654752440f, -0.92387953251128675613f,
-                           -1.0f, -0.92387953251128675613f, -0.70710678118654752440f, -0.38268343236508977173f,
-                           0.0f, 0.38268343236508977173f, 0.70710678118654752440f, 0.92387953251128675613f};
-    const int mm = (m * (16 / N)) & 15;
-    const float c = c16[mm], s = c16[(mm + 12) & 15];  // sin(x) = cos(x - pi/2)
-    return make_float2(c, SIGN * s);
+    constexpr int N = N1 * N2;
+    constexpr WTab<N, SIGN> W{};
+    float2 y[N2][N1];
+#pragma unroll
+    for (int n2 = 0; n2 < N2; n2++) {
+        float2 t[N1];
+#pragma unroll
+        for (int n1 = 0; n1 < N1; n1++) t[n1] = v[N2 * n1 + n2];
+        Dft<N1, SIGN>::run(t);
+#pragma unroll
+        for (int k1 = 0; k1 < N1; k1++) {
+            const int m = (n2 * k1) % N;
+            y[n2][k1] = (m == 0) ? t[k1] : cmul(t[k1], make_float2(W.re[m], W.im[m]));
+        }
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < N1; k1++) {
+        float2 t[N2];
+#pragma unroll
+        for (int n2 = 0; n2 < N2; n2++) t[n2] = y[n2][k1];
+        Dft<N2, SIGN>::run(t);
+#pragma unroll
+        for (int k2 = 0; k2 < N2; k2++) v[k1 + N1 * k2] = t[k2];
+    }
 }
 
-template <int SIGN> struct Dft<8, SIGN> {
-    static BC_DEV void run(float2 *v) {
-        float2 e[4] = {v[0], v[2], v[4], v[6]};
-        float2 o[4] = {v[1], v[3], v[5], v[7]};
-        Dft<4, SIGN>::run(e);
-        Dft<4, SIGN>::run(o);
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-            const float2 t = q == 0 ? o[0] : cmul(o[q], wconst<8, SIGN>(q));
-            v[q] = cadd(e[q], t);
-            v[q + 4] = csub(e[q], t);
-        }
-    }
-};
+template <int SIGN> struct Dft<6, SIGN> { static BC_DEV void run(float2 *v) { dft_ct<2, 3, SIGN>(v); } };
+template <int SIGN> struct Dft<8, SIGN> { static BC_DEV void run(float2 *v) { dft_ct<2, 4, SIGN>(v); } };
+template <int SIGN> struct Dft<10, SIGN> { static BC_DEV void run(float2 *v) { dft_ct<2, 5, SIGN>(v); } };
+template <int SIGN> struct Dft<12, SIGN> { static BC_DEV void run(float2 *v) { dft_ct<4, 3, SIGN>(v); } };
+template <int SIGN> struct Dft<16, SIGN> { static BC_DEV void run(float2 *v) { dft_ct<4, 4, SIGN>(v); } };
 
-template <int SIGN> struct Dft<16, SIGN> {
-    static BC_DEV void run(float2 *v) {
-        // 16 = 4 x 4: inner DFT4 over n1 (stride 4), twiddle w16^{n2 k1}, outer DFT4 over n2
-        float2 y[4][4];
-#pragma unroll
-        for (int n2 = 0; n2 < 4; n2++) {
-            float2 t[4] = {v[n2], v[4 + n2], v[8 + n2], v[12 + n2]};
-            Dft<4, SIGN>::run(t);
-#pragma unroll
-            for (int k1 = 0; k1 < 4; k1++) y[n2][k1] = (n2 * k1 == 0) ? t[k1] : cmul(t[k1], wconst<16, SIGN>(n2 * k1));
-        }
-#pragma unroll
-        for (int k1 = 0; k1 < 4; k1++) {
-            float2 t[4] = {y[0][k1], y[1][k1], y[2][k1], y[3][k1]};
-            Dft<4, SIGN>::run(t);
-#pragma unroll
-            for (int k2 = 0; k2 < 4; k2++) v[k1 + 4 * k2] = t[k2];
-        }
-    }
-};
+// ---------------------------------------------------------------- plans
+// n stages with radices r[]; TPL threads per line (TPL divides L/r[0] and L/r[n-1]);
+// NL lines per block.
+template <int L> struct Plan;
+#define BC_PLAN(L_, N_, A_, B_, C_, TPL_, NL_)                                                     \
+    template <> struct Plan<L_> {                                                                  \
+        static constexpr int n = N_;                                                               \
+        static constexpr int r[3] = {A_, B_, C_};                                                  \
+        static constexpr int TPL = TPL_;                                                           \
+        static constexpr int NL = NL_;                                                             \
+    };
+//       L   n  radices      TPL NL
+BC_PLAN(16, 2, 4, 4, 1, 4, 16)
+BC_PLAN(20, 3, 2, 5, 2, 10, 16)
+BC_PLAN(24, 3, 2, 3, 4, 6, 16)
+BC_PLAN(32, 2, 8, 4, 1, 4, 16)
+BC_PLAN(36, 2, 6, 6, 1, 6, 16)
+BC_PLAN(40, 3, 2, 5, 4, 10, 16)
+BC_PLAN(48, 2, 12, 4, 1, 4, 16)
+BC_PLAN(64, 2, 8, 8, 1, 8, 16)
+BC_PLAN(72, 2, 12, 6, 1, 6, 16)
+BC_PLAN(80, 3, 4, 5, 4, 20, 8)
+BC_PLAN(96, 3, 4, 6, 4, 24, 8)
+BC_PLAN(128, 2, 16, 8, 1, 8, 16)
+BC_PLAN(144, 2, 12, 12, 1, 12, 8)
+BC_PLAN(160, 3, 8, 5, 4, 20, 8)
+BC_PLAN(192, 3, 8, 3, 8, 24, 8)
+BC_PLAN(240, 3, 12, 5, 4, 20, 8)
+BC_PLAN(256, 2, 16, 16, 1, 16, 8)
+BC_PLAN(288, 3, 12, 2, 12, 24, 8)
+BC_PLAN(320, 3, 16, 5, 4, 20, 8)
+BC_PLAN(384, 3, 16, 3, 8, 24, 8)
+BC_PLAN(512, 3, 16, 2, 16, 32, 4)
+BC_PLAN(576, 3, 12, 4, 12, 48, 4)
+BC_PLAN(640, 3, 16, 5, 8, 40, 4)
+BC_PLAN(768, 3, 16, 3, 16, 48, 4)
+BC_PLAN(1024, 3, 16, 4, 16, 64, 2)
+#undef BC_PLAN
+
+#define BC_FOR_EACH_L(X) X(16) X(20) X(24) X(32) X(36) X(40) X(48) X(64) X(72) X(80) X(96) X(128) \
+    X(144) X(160) X(192) X(240) X(256) X(288) X(320) X(384) X(512) X(576) X(640) X(768) X(1024)
+
+template <int L, int S>
+__host__ __device__ constexpr int ns_before()
+{
+    int ns = 1;
+    for (int s = 0; s < S; s++) ns *= Plan<L>::r[s];
+    return ns;
+}
+
+template <int L>
+__host__ __device__ constexpr bool plan_ok()
+{
+    constexpr int n = Plan<L>::n;
+    int p = 1;
+    for (int s = 0; s < n; s++) p *= Plan<L>::r[s];
+    return p == L && (L / Plan<L>::r[0]) % Plan<L>::TPL == 0 && (L / Plan<L>::r[n - 1]) % Plan<L>::TPL == 0 &&
+           n >= 2;
+}
 
 // ---------------------------------------------------------------- stages
-// FIRST stage reads `src` (optionally multiplying input n by pre[n]); the rest ping-pong a/b.
-template <int L, int TPL, int S, int SIGN>
-BC_DEV void stage(const float2 *__restrict__ src, float2 *__restrict__ dst, const float2 *__restrict__ tw,
-                  const float2 *__restrict__ pre, int tl)
+// middle stage S (0 < S < n-1): shared memory a -> b
+template <int L, int S, int SIGN>
+BC_DEV void mid_stage(const float2 *__restrict__ a, float2 *__restrict__ b, const float2 *__restrict__ tw, int tl)
 {
-    constexpr int R = Sched<L>::r[S];
+    constexpr int TPL = Plan<L>::TPL;
+    constexpr int R = Plan<L>::r[S];
     constexpr int Ns = ns_before<L, S>();
     constexpr int LR = L / R;
     constexpr int TWS = L / (Ns * R);
@@ -190,9 +250,8 @@ BC_DEV void stage(const float2 *__restrict__ src, float2 *__restrict__ dst, cons
         float2 v[R];
 #pragma unroll
         for (int r = 0; r < R; r++) {
-            float2 x = src[pad(j + r * LR)];
-            if (S == 0 && pre) x = cmul(x, pre[j + r * LR]);
-            if (Ns > 1 && r > 0) {
+            float2 x = a[pad(j + r * LR)];
+            if (r > 0) {
                 const float2 w = tw[r * jm * TWS];
                 x = SIGN < 0 ? cmul(x, w) : cmulc(x, w);
             }
@@ -201,48 +260,76 @@ BC_DEV void stage(const float2 *__restrict__ src, float2 *__restrict__ dst, cons
         Dft<R, SIGN>::run(v);
         const int idxD = (j / Ns) * Ns * R + jm;
 #pragma unroll
-        for (int r = 0; r < R; r++) dst[pad(idxD + r * Ns)] = v[r];
+        for (int r = 0; r < R; r++) b[pad(idxD + r * Ns)] = v[r];
     }
 }
 
-// Terminate when S == Sched<L>::n.  (specialisation through a dispatch helper)
-template <int L, int TPL, int S, int SIGN, bool DONE = (S >= Sched<L>::n)>
-struct Run;
-
-template <int L, int TPL, int S, int SIGN>
-struct Run<L, TPL, S, SIGN, true> {
-    static BC_DEV float2 *go(const float2 *, float2 *, float2 *b, const float2 *, const float2 *, int) { return b; }
+template <int L, int S, int SIGN, bool DONE = (S >= Plan<L>::n - 1)>
+struct Mid;
+template <int L, int S, int SIGN>
+struct Mid<L, S, SIGN, true> {
+    static BC_DEV const float2 *go(const float2 *a, float2 *, const float2 *, int) { return a; }
 };
-
-template <int L, int TPL, int S, int SIGN>
-struct Run<L, TPL, S, SIGN, false> {
-    static BC_DEV float2 *go(const float2 *src, float2 *a, float2 *b, const float2 *tw, const float2 *pre, int tl)
+template <int L, int S, int SIGN>
+struct Mid<L, S, SIGN, false> {
+    static BC_DEV const float2 *go(const float2 *a, float2 *b, const float2 *tw, int tl)
     {
-        if (S == 0)
-            stage<L, TPL, 0, SIGN>(src, a, tw, pre, tl);
-        else
-            stage<L, TPL, S, SIGN>(b, a, tw, nullptr, tl);
+        mid_stage<L, S, SIGN>(a, b, tw, tl);
         __syncthreads();
-        return Run<L, TPL, S + 1, SIGN>::go(src, b, a, tw, pre, tl);
+        return Mid<L, S + 1, SIGN>::go(b, (float2 *)a, tw, tl);
     }
 };
 
-// Transform the calling thread-group's line.  `src` = input line (may alias b),
-// a/b = scratch lines (a != src).  pre = optional per-input multiplier (global/L1).
-// All threads of the block must call (block-wide barriers).  The returned
-// pointer is the line buffer holding the natural-order result.
-template <int L>
-__host__ __device__ constexpr bool result_in_a() { return (Sched<L>::n % 2) == 1; }
-
-// threads per line and lines per block used by the pass kernels (E = L / TPL = 16 inputs per thread)
-template <int L>
-__host__ __device__ constexpr int tpl_of() { return L <= 256 ? 16 : (L <= 512 ? 32 : 64); }
-
-// src may alias b (stage 0 reads src, later stages never do).
-template <int L, int TPL, int SIGN>
-BC_DEV float2 *line_fft(const float2 *src, float2 *a, float2 *b, const float2 *tw, const float2 *pre, int tl)
+// FFT of the calling thread-group's line, registers in / registers out (see header).
+// A and B are this line's shared-memory buffers (B used only when n >= 3).
+// Contains block-wide barriers: every thread of the block must call it.  The caller
+// must barrier before writing A/B again (the last stage reads them).
+template <int L, int SIGN>
+BC_DEV void fft_regs(float2 (&x)[L / Plan<L>::TPL], float2 *A, float2 *B, const float2 *tw, int tl)
 {
-    return Run<L, TPL, 0, SIGN>::go(src, a, b, tw, pre, tl);
+    static_assert(plan_ok<L>(), "bad FFT plan");
+    constexpr int TPL = Plan<L>::TPL;
+    constexpr int n = Plan<L>::n;
+    // stage 0 (Ns = 1, no twiddles): registers -> A
+    {
+        constexpr int R = Plan<L>::r[0];
+        constexpr int U = (L / R) / TPL;
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int j = tl + TPL * u;
+            float2 v[R];
+#pragma unroll
+            for (int r = 0; r < R; r++) v[r] = x[u + U * r];
+            Dft<R, SIGN>::run(v);
+#pragma unroll
+            for (int r = 0; r < R; r++) A[pad(j * R + r)] = v[r];
+        }
+    }
+    __syncthreads();
+    const float2 *cur = Mid<L, 1, SIGN>::go(A, B, tw, tl);
+    // last stage (Ns = L / R): shared memory -> registers, output index j + r Ns
+    {
+        constexpr int R = Plan<L>::r[n - 1];
+        constexpr int Ns = L / R;
+        constexpr int U = Ns / TPL;
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int j = tl + TPL * u;
+            float2 v[R];
+#pragma unroll
+            for (int r = 0; r < R; r++) {
+                float2 y = cur[pad(j + r * Ns)];
+                if (r > 0) {
+                    const float2 w = tw[r * j];
+                    y = SIGN < 0 ? cmul(y, w) : cmulc(y, w);
+                }
+                v[r] = y;
+            }
+            Dft<R, SIGN>::run(v);
+#pragma unroll
+            for (int r = 0; r < R; r++) x[u + U * r] = v[r];
+        }
+    }
 }
 
 }  // namespace fct

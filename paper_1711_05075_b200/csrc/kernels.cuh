@@ -58,7 +58,7 @@ struct FoldXArgs {
     const float2 *tw, *ctw;
     const float2 *T2;     // [b][ix][ky][kz]
     long long t2_bstride;
-    const float2 *Ahat;   // [kx][ky][kz], origin phase folded in
+    const float2 *Ahat;   // [ky][kz][kx], origin phase folded in
     float2 *F;            // [b][Np][Np][Fz]
     long long f_bstride;
 };
@@ -79,8 +79,9 @@ struct LastArgs {
 
 void launch_spread(const SpreadArgs &a, int batch, cudaStream_t s);
 bool fft_size_supported(int L);
-void launch_pass_contig(const PassArgs &a, int batch, cudaStream_t s);
-void launch_pass_strided(const PassArgs &a, int sign, int batch, cudaStream_t s);
+// kind: 0 forward contiguous (z), 1 forward strided (y), 2 forward strided -> rows (x of A),
+//       3 inverse strided (x, y of the inverse transform)
+void launch_pass(const PassArgs &a, int kind, int batch, cudaStream_t s);
 void launch_fold_x(const FoldXArgs &a, int batch, cudaStream_t s);
 void launch_last(const LastArgs &a, int batch, cudaStream_t s);
 void launch_keys_init(unsigned long long *keys, int n, cudaStream_t s);

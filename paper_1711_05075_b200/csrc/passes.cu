@@ -2,29 +2,23 @@
 //
 // Per rotation (eq_ccghat), after spreading the smoothed
 // density of R B onto its box (spread.cu):
-//   pass_contig  (z)  box [ix][iy][iz]  -> T1 [ix][iy][kz]
-//   pass_strided (y)  T1               -> T2 [ix][ky][kz]
-//   fold_x            T2 -> x-transform -> f_hat_A'(k) conj(f_hat_RB(k)) -> F[k mod Np]   (fused)
-//   pass_strided (x, inverse) F -> X1 [mx][k'y][k'z]
-//   pass_strided (y, inverse) X1 -> Y1 [mx][my][k'z]
+//   pass (z, contig)   box [ix][iy][iz]  -> T1 [ix][iy][kz]
+//   pass (y, strided)  T1               -> T2 [ix][ky][kz]
+//   fold_x             T2 -> x-transform -> f_hat_A'(k) conj(f_hat_RB(k)) -> F[k mod Np]   (fused)
+//   pass (x, inverse)  F  -> X1 [mx][k'y][k'z]
+//   pass (y, inverse)  X1 -> Y1 [mx][my][k'z]
 //   last (z, inverse, C2R) Y1 -> f(t_m) or per-rotation min / max keys
+// For A (once): z, y, then an x pass writing A' = A_hat * origin phase as [ky][kz][kx].
 // One axis of the box DFT is X(k) = mult(k) sum_{n<L} x_n exp(-2 pi i k n / G), G = c L,
 // evaluated through c cosets k = c q + p of an L-point FFT of x_n exp(-2 pi i p n / G).
-// Each block keeps its raw input lines in registers (L / TPL values per thread) and
-// rewrites the coset-twiddled copy into shared memory before every coset FFT.
+// Lines live in registers (fft_ct.cuh); strided loads / stores are transposed through
+// shared memory so that global accesses stay coalesced.
 #include "kernels.cuh"
 #include "fft_ct.cuh"
 
 #include "ballcorr.h"
 
 using namespace fct;
-
-constexpr int BS = 128;  // threads per block of every FFT pass
-
-template <int L>
-__host__ __device__ constexpr int nl_of() { return BS / tpl_of<L>(); }
-template <int L>
-__host__ __device__ constexpr int epr_of() { return (L * nl_of<L>() + BS - 1) / BS; }  // inputs per thread
 
 __device__ __forceinline__ int coset_kk(int q, int p, int c, int G, int klo, int signed_k)
 {
@@ -33,18 +27,14 @@ __device__ __forceinline__ int coset_kk(int q, int p, int c, int G, int klo, int
     return k - klo;
 }
 
-template <int L>
-__device__ __forceinline__ void load_tw(float2 *tw, const float2 *g)
+// ============================================================================ generic axis pass
+// IN_MODE: 0 contiguous real rows, 1 contiguous complex rows, 2 strided in[b][O][L][I].
+// OUT_MODE: 0 rows out[b][row][nk] (row = line index), 1 strided out[b][O][nk][I].
+template <int L, int SIGN, int IN_MODE, int OUT_MODE>
+__global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL) pass_kernel(PassArgs a)
 {
-    for (int m = threadIdx.x; m < L; m += BS) tw[m] = g[m];
-}
-
-// ============================================================================ contiguous axis (forward z)
-
-template <int L, bool REAL_IN>
-__global__ void __launch_bounds__(BS) pass_contig_kernel(PassArgs a)
-{
-    constexpr int TPL = tpl_of<L>(), NL = nl_of<L>(), LS = line_stride(L), E = epr_of<L>();
+    constexpr int TPL = Plan<L>::TPL, NL = Plan<L>::NL, NT = TPL * NL;
+    constexpr int LS = line_stride(L), E = L / TPL;
     extern __shared__ float2 sm[];
     float2 *tw = sm;
     float2 *A = tw + L;
@@ -52,89 +42,83 @@ __global__ void __launch_bounds__(BS) pass_contig_kernel(PassArgs a)
     float2 *OUT = B + NL * LS;
     const int line = threadIdx.x / TPL, tl = threadIdx.x % TPL;
     const int b = blockIdx.y;
-    const long long gline = (long long)blockIdx.x * NL + line;
-    const bool valid = gline < a.lines;
 
-    load_tw<L>(tw, a.tw);
-    float2 x[E];
-#pragma unroll
-    for (int m = 0; m < E; m++) {
-        const int n = tl + TPL * m;
-        x[m] = make_float2(0.f, 0.f);
-        if (valid && n < L) {
-            if (REAL_IN)
-                x[m].x = ((const float *)a.in)[(long long)b * a.in_bstride + gline * L + n];
-            else
-                x[m] = ((const float2 *)a.in)[(long long)b * a.in_bstride + gline * L + n];
-        }
+    long long row0;  // global row (line) index of this block's first line
+    int o = 0, i0 = 0;
+    if (IN_MODE == 2) {
+        const int itiles = (a.I + NL - 1) / NL;
+        o = blockIdx.x / itiles;
+        i0 = (blockIdx.x % itiles) * NL;
+        row0 = (long long)o * a.I + i0;
+    } else {
+        row0 = (long long)blockIdx.x * NL;
     }
-    for (int p = 0; p < a.c; p++) {
+    const long long nrows = IN_MODE == 2 ? (long long)a.O * a.I : a.lines;
+    const bool valid = IN_MODE == 2 ? (i0 + line < a.I) : (row0 + line < nrows);
+
+    for (int m = threadIdx.x; m < L; m += NT) tw[m] = a.tw[m];
+    float2 x[E];
+    if (IN_MODE == 2) {
+        const float2 *in = (const float2 *)a.in + (long long)b * a.in_bstride + (long long)o * L * a.I;
+        for (int e = threadIdx.x; e < L * NL; e += NT) {
+            const int n = e / NL, i = e % NL;
+            A[i * LS + pad(n)] = (i0 + i < a.I) ? in[(long long)n * a.I + i0 + i] : make_float2(0.f, 0.f);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < E; m++) x[m] = A[line * LS + pad(tl + TPL * m)];
+        __syncthreads();
+    } else {
+        const long long g = (long long)b * a.in_bstride + (row0 + line) * L;
 #pragma unroll
         for (int m = 0; m < E; m++) {
             const int n = tl + TPL * m;
-            if (n < L) A[line * LS + pad(n)] = p ? cmul(x[m], a.ctw[p * L + n]) : x[m];
-        }
-        __syncthreads();
-        const float2 *res = line_fft<L, TPL, -1>(A + line * LS, B + line * LS, A + line * LS, tw, nullptr, tl);
-        for (int q = tl; q < L; q += TPL) {
-            const int kk = coset_kk(q, p, a.c, a.G, a.klo, a.signed_k);
-            if (kk >= 0 && kk < a.nk) OUT[line * a.nk + kk] = cmul(res[pad(q)], a.mult[kk]);
-        }
-        __syncthreads();
-    }
-    const long long base = (long long)b * a.out_bstride + (long long)blockIdx.x * NL * a.nk;
-    for (int e = threadIdx.x; e < NL * a.nk; e += BS) {
-        const int l = e / a.nk;
-        if ((long long)blockIdx.x * NL + l < a.lines) a.out[base + e] = OUT[e];
-    }
-}
-
-// ============================================================================ strided axis (forward / inverse)
-
-template <int L, int SIGN>
-__global__ void __launch_bounds__(BS) pass_strided_kernel(PassArgs a)
-{
-    constexpr int TPL = tpl_of<L>(), NL = nl_of<L>(), LS = line_stride(L), E = epr_of<L>();
-    extern __shared__ float2 sm[];
-    float2 *tw = sm;
-    float2 *A = tw + L;
-    float2 *B = A + NL * LS;
-    const int line = threadIdx.x / TPL, tl = threadIdx.x % TPL;
-    const int b = blockIdx.y;
-    const int itiles = (a.I + NL - 1) / NL;
-    const int o = blockIdx.x / itiles;
-    const int i0 = (blockIdx.x % itiles) * NL;
-    const float2 *in = (const float2 *)a.in + (long long)b * a.in_bstride + (long long)o * L * a.I;
-    float2 *out = a.out + (long long)b * a.out_bstride + (long long)o * a.nk * a.I;
-
-    load_tw<L>(tw, a.tw);
-    float2 x[E];
-#pragma unroll
-    for (int m = 0; m < E; m++) {
-        const int e = threadIdx.x + BS * m;
-        const int n = e / NL, i = e % NL;
-        x[m] = (e < L * NL && i0 + i < a.I) ? in[(long long)n * a.I + i0 + i] : make_float2(0.f, 0.f);
-    }
-    float2 *resbuf = result_in_a<L>() ? B : A;  // stage 0 writes B (line_fft(A, B, A))
-    for (int p = 0; p < a.c; p++) {
-#pragma unroll
-        for (int m = 0; m < E; m++) {
-            const int e = threadIdx.x + BS * m;
-            const int n = e / NL, i = e % NL;
-            if (e < L * NL) A[i * LS + pad(n)] = p ? cmul(x[m], a.ctw[p * L + n]) : x[m];
-        }
-        __syncthreads();
-        line_fft<L, TPL, SIGN>(A + line * LS, B + line * LS, A + line * LS, tw, nullptr, tl);
-        for (int e = threadIdx.x; e < L * NL; e += BS) {
-            const int q = e / NL, i = e % NL;
-            const int kk = coset_kk(q, p, a.c, a.G, a.klo, a.signed_k);
-            if (kk >= 0 && kk < a.nk && i0 + i < a.I) {
-                float2 v = resbuf[i * LS + pad(q)];
-                if (a.mult) v = cmul(v, a.mult[kk]);
-                out[(long long)kk * a.I + i0 + i] = v;
+            x[m] = make_float2(0.f, 0.f);
+            if (valid) {
+                if (IN_MODE == 0)
+                    x[m].x = ((const float *)a.in)[g + n];
+                else
+                    x[m] = ((const float2 *)a.in)[g + n];
             }
         }
-        __syncthreads();
+    }
+
+    float2 *outs = a.out + (long long)b * a.out_bstride;
+    for (int p = 0; p < a.c; p++) {
+        float2 y[E];
+#pragma unroll
+        for (int m = 0; m < E; m++) y[m] = p ? cmul(x[m], a.ctw[p * L + tl + TPL * m]) : x[m];
+        fft_regs<L, SIGN>(y, A + line * LS, B + line * LS, tw, tl);
+        if (OUT_MODE == 0) {
+#pragma unroll
+            for (int m = 0; m < E; m++) {
+                const int kk = coset_kk(tl + TPL * m, p, a.c, a.G, a.klo, a.signed_k);
+                if (kk >= 0 && kk < a.nk) OUT[line * a.nk + kk] = a.mult ? cmul(y[m], a.mult[kk]) : y[m];
+            }
+            __syncthreads();
+        } else {
+            __syncthreads();
+#pragma unroll
+            for (int m = 0; m < E; m++) A[line * LS + pad(tl + TPL * m)] = y[m];
+            __syncthreads();
+            float2 *out = outs + (long long)o * a.nk * a.I;
+            for (int e = threadIdx.x; e < L * NL; e += NT) {
+                const int q = e / NL, i = e % NL;
+                const int kk = coset_kk(q, p, a.c, a.G, a.klo, a.signed_k);
+                if (kk >= 0 && kk < a.nk && i0 + i < a.I) {
+                    const float2 v = A[i * LS + pad(q)];
+                    out[(long long)kk * a.I + i0 + i] = a.mult ? cmul(v, a.mult[kk]) : v;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    if (OUT_MODE == 0) {
+        for (int e = threadIdx.x; e < NL * a.nk; e += NT) {
+            const int l = e / a.nk;
+            const bool ok = IN_MODE == 2 ? (i0 + l < a.I) : (row0 + l < nrows);
+            if (ok) outs[(row0 + l) * a.nk + (e % a.nk)] = OUT[e];
+        }
     }
 }
 
@@ -143,24 +127,22 @@ __global__ void __launch_bounds__(BS) pass_strided_kernel(PassArgs a)
 // Block: target row k'y = blockIdx.x / ztiles, targets k'z in [z0, z0 + 8), all k'x.
 // For every alias group (ky, kz) of those targets, the x-transform of the T2 lines of
 // R B gives f_hat_RB(kx, ky, kz) on the band; times f_hat_A'(k) (A's spectrum with the
-// origin phase exp(2 pi i k.t0/P) folded in) and summed into F[k mod Np].
-// DIRECT: every fold target of a coset is owned by one thread (Np / gcd(c, Np) is a
-// multiple of TPL and G is a multiple of Np), so products accumulate straight into acc; otherwise they are
-// staged per line in Pb[kx] and gathered.
+// origin phase exp(2 pi i k.t0/P) folded in, layout [ky][kz][kx]) and summed into
+// F[k mod Np].  DIRECT: the fold targets of a thread's outputs are owned by that thread
+// (Np / gcd(c, Np) a multiple of TPL and G a multiple of Np), so products accumulate
+// straight into acc; otherwise they are staged in Pb[line][kx] and gathered.
 template <int L, bool CPLX, bool DIRECT>
-__global__ void __launch_bounds__(8 * tpl_of<L>()) fold_x_kernel(FoldXArgs a)
+__global__ void __launch_bounds__(8 * Plan<L>::TPL) fold_x_kernel(FoldXArgs a)
 {
     constexpr int NL = 8;
-    constexpr int TPL = tpl_of<L>();
-    constexpr int NT = NL * TPL;
-    constexpr int LS = line_stride(L);
-    constexpr int E = (L * NL + NT - 1) / NT;
+    constexpr int TPL = Plan<L>::TPL, NT = NL * TPL;
+    constexpr int LS = line_stride(L), E = L / TPL;
     extern __shared__ float2 sm[];
     float2 *tw = sm;
     float2 *A = tw + L;
     float2 *B = A + NL * LS;
-    float2 *acc = B + NL * LS;           // [NL][Np]
-    float2 *Pb = acc + NL * a.Np;        // [NL][M] (gather path only)
+    float2 *acc = B + NL * LS;      // [NL][Np]
+    float2 *Pb = acc + NL * a.Np;   // [NL][M] (gather path only)
     const int line = threadIdx.x / TPL, tl = threadIdx.x % TPL;
     const int b = blockIdx.y;
     const int K = a.K, M = a.M, Np = a.Np, Kz = a.Kz;
@@ -168,14 +150,13 @@ __global__ void __launch_bounds__(8 * tpl_of<L>()) fold_x_kernel(FoldXArgs a)
     const int kyp = blockIdx.x / ztiles;
     const int z0 = (blockIdx.x % ztiles) * NL;
     const float2 *T2 = a.T2 + (long long)b * a.t2_bstride;
-    float2 *resbuf = result_in_a<L>() ? B : A;
 
     for (int m = threadIdx.x; m < L; m += NT) tw[m] = a.tw[m];
     for (int e = threadIdx.x; e < NL * Np; e += NT) acc[e] = make_float2(0.f, 0.f);
 
     const int span = K / Np + 2;
     for (int pass = 0; pass < (CPLX ? 1 : 2); pass++) {
-        const int s = pass ? -1 : 1;   // conj pass: target (-k) mod Np
+        const int s = pass ? -1 : 1;  // conj pass: target (-k) mod Np
         const int zlo = CPLX ? -K : (pass ? 1 : 0);
         for (int nz = -span; nz <= span; nz++) {
             bool any = false;
@@ -184,79 +165,73 @@ __global__ void __launch_bounds__(8 * tpl_of<L>()) fold_x_kernel(FoldXArgs a)
                 any |= (z0 + i < a.Fz) && kz >= zlo && kz <= K;
             }
             if (!any) continue;
+            const int my_kz = s * (z0 + line) + nz * Np;
+            const bool my_ok = (z0 + line < a.Fz) && my_kz >= zlo && my_kz <= K;
             for (int ny = -span; ny <= span; ny++) {
                 const int ky = s * kyp + ny * Np;
                 if (ky < -K || ky > K) continue;
                 // source lines of R B: (ky, kz) for real weights, (-ky, -kz) for complex (f_hat_RB(-k))
                 const int kys = CPLX ? -ky : ky;
-                float2 x[E];
-#pragma unroll
-                for (int m = 0; m < E; m++) {
-                    const int e = threadIdx.x + NT * m;
+                __syncthreads();
+                for (int e = threadIdx.x; e < L * NL; e += NT) {
                     const int n = e / NL, i = e % NL;
                     const int kz = s * (z0 + i) + nz * Np;
-                    x[m] = make_float2(0.f, 0.f);
-                    if (e < L * NL && (z0 + i < a.Fz) && kz >= zlo && kz <= K) {
-                        const int kzs = CPLX ? (-kz + K) : kz;
-                        x[m] = T2[((long long)n * M + (kys + K)) * Kz + kzs];
-                    }
+                    float2 v = make_float2(0.f, 0.f);
+                    if ((z0 + i < a.Fz) && kz >= zlo && kz <= K)
+                        v = T2[((long long)n * M + (kys + K)) * Kz + (CPLX ? (-kz + K) : kz)];
+                    A[i * LS + pad(n)] = v;
                 }
+                __syncthreads();
+                float2 x[E];
+#pragma unroll
+                for (int m = 0; m < E; m++) x[m] = A[line * LS + pad(tl + TPL * m)];
+                __syncthreads();
+                const float2 *arow = a.Ahat + ((long long)(ky + K) * Kz + (CPLX ? my_kz + K : my_kz)) * M;
                 for (int p = 0; p < a.c; p++) {
+                    float2 y[E];
+#pragma unroll
+                    for (int m = 0; m < E; m++) y[m] = p ? cmul(x[m], a.ctw[p * L + tl + TPL * m]) : x[m];
+                    fft_regs<L, -1>(y, A + line * LS, B + line * LS, tw, tl);
 #pragma unroll
                     for (int m = 0; m < E; m++) {
-                        const int e = threadIdx.x + NT * m;
-                        const int n = e / NL, i = e % NL;
-                        if (e < L * NL) A[i * LS + pad(n)] = p ? cmul(x[m], a.ctw[p * L + n]) : x[m];
-                    }
-                    __syncthreads();
-                    line_fft<L, TPL, -1>(A + line * LS, B + line * LS, A + line * LS, tw, nullptr, tl);
-                    for (int e = threadIdx.x; e < L * NL; e += NT) {
-                        const int q = e / NL, i = e % NL;
-                        int kx = a.c * q + p;
+                        int kx = a.c * (tl + TPL * m) + p;
                         if (2 * kx > a.G) kx -= a.G;
                         if (kx < -K || kx > K) continue;
-                        const int kz = s * (z0 + i) + nz * Np;
-                        const bool ok = (z0 + i < a.Fz) && kz >= zlo && kz <= K;
                         float2 P = make_float2(0.f, 0.f);
-                        int kxa = kx;
-                        if (ok) {
-                            const float2 bv = cmul(resbuf[i * LS + pad(q)], a.mult[kx + K]);
-                            if (!CPLX) {
-                                const float2 av = a.Ahat[((long long)(kx + K) * M + (ky + K)) * Kz + kz];
-                                P = cmulc(av, bv);   // f_hat_A'(k) conj(f_hat_RB(k))
-                            } else {
-                                // bv = f_hat_RB(kx, -ky, -kz) = f_hat_RB(-k') at k' = (-kx, ky, kz)
-                                kxa = -kx;
-                                const float2 av = a.Ahat[((long long)(kxa + K) * M + (ky + K)) * Kz + (kz + K)];
-                                P = cmul(av, bv);    // weights not conjugated (reading C-3)
-                            }
+                        const int kxa = CPLX ? -kx : kx;
+                        if (my_ok) {
+                            const float2 bv = cmul(y[m], a.mult[kx + K]);
+                            const float2 av = arow[kxa + K];
+                            // real: f_hat_A'(k) conj(f_hat_RB(k)); complex: bv = f_hat_RB(-k') at
+                            // k' = (-kx, ky, kz), weights not conjugated (reading C-3)
+                            P = CPLX ? cmul(av, bv) : cmulc(av, bv);
                         }
                         if (DIRECT) {
-                            if (ok) {
+                            if (my_ok) {
                                 int t = (s > 0 ? kxa : -kxa) % Np;
                                 if (t < 0) t += Np;
-                                acc[i * Np + t] = cadd(acc[i * Np + t], s > 0 ? P : cconj(P));
+                                acc[line * Np + t] = cadd(acc[line * Np + t], s > 0 ? P : cconj(P));
                             }
                         } else {
-                            Pb[i * M + kxa + K] = P;
+                            Pb[line * M + kxa + K] = P;
                         }
                     }
                     __syncthreads();
                 }
                 if (!DIRECT) {
                     for (int e = threadIdx.x; e < NL * Np; e += NT) {
-                        const int i = e % NL, t = e / NL;
+                        const int i = e / Np, t = e % Np;
                         const int base = s > 0 ? t : (Np - t) % Np;
-                        int kx = base - ((base + K) / Np) * Np;   // smallest alias >= -K
+                        int kx = base - ((base + K) / Np) * Np;  // smallest alias >= -K
                         float2 sum = make_float2(0.f, 0.f);
                         for (; kx <= K; kx += Np) sum = cadd(sum, Pb[i * M + kx + K]);
                         acc[i * Np + t] = cadd(acc[i * Np + t], s > 0 ? sum : cconj(sum));
                     }
-                    __syncthreads();
                 }
             }
         }
     }
+    __syncthreads();
     float2 *F = a.F + (long long)b * a.f_bstride;
     for (int e = threadIdx.x; e < NL * Np; e += NT) {
         const int i = e % NL, t = e / NL;
@@ -276,9 +251,10 @@ __device__ __forceinline__ unsigned long long key_max(float v, unsigned idx)
 }
 
 template <int L, bool HERM>
-__global__ void __launch_bounds__(BS) last_kernel(LastArgs a)
+__global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL) last_kernel(LastArgs a)
 {
-    constexpr int TPL = tpl_of<L>(), NL = nl_of<L>(), LS = line_stride(L);
+    constexpr int TPL = Plan<L>::TPL, NL = Plan<L>::NL, NT = TPL * NL;
+    constexpr int LS = line_stride(L), E = L / TPL;
     extern __shared__ float2 sm[];
     float2 *tw = sm;
     float2 *A = tw + L;
@@ -289,29 +265,31 @@ __global__ void __launch_bounds__(BS) last_kernel(LastArgs a)
     const long long gline = (long long)blockIdx.x * NL + line;
     const bool valid = gline < lines;
 
-    load_tw<L>(tw, a.tw);
-    {
-        const float2 *row = a.in + (long long)b * a.in_bstride + gline * a.Fz;
-        float2 *dst = A + line * LS;
-        for (int n = tl; n < L; n += TPL) {
-            float2 v = make_float2(0.f, 0.f);
-            if (valid) {
-                if (!HERM || n < a.Fz)
-                    v = row[n];
-                else
-                    v = cconj(row[L - n]);
-            }
-            dst[pad(n)] = v;
+    for (int m = threadIdx.x; m < L; m += NT) tw[m] = a.tw[m];
+    const float2 *row = a.in + (long long)b * a.in_bstride + gline * a.Fz;
+    float2 x[E];
+#pragma unroll
+    for (int m = 0; m < E; m++) {
+        const int n = tl + TPL * m;
+        float2 v = make_float2(0.f, 0.f);
+        if (valid) {
+            if (!HERM || n < a.Fz)
+                v = row[n];
+            else
+                v = cconj(row[L - n]);
         }
+        x[m] = v;
     }
-    __syncthreads();
-    const float2 *res = line_fft<L, TPL, +1>(A + line * LS, B + line * LS, A + line * LS, tw, nullptr, tl);
+    fft_regs<L, +1>(x, A + line * LS, B + line * LS, tw, tl);
 
     unsigned long long kmin = ~0ull, kmax = 0ull;
     if (valid) {
-        for (int m = tl; m < a.N; m += TPL) {
-            const float2 v = cscale(res[pad(m)], a.scale);
-            const long long gidx = gline * a.N + m;
+#pragma unroll
+        for (int m = 0; m < E; m++) {
+            const int q = tl + TPL * m;
+            if (q >= a.N) continue;
+            const float2 v = cscale(x[m], a.scale);
+            const long long gidx = gline * a.N + q;
             if (a.out_kind == BC_OUT_F_FULL) {
                 if (HERM)
                     ((float *)a.out_full)[(long long)b * a.full_bstride + gidx] = v.x;
@@ -345,7 +323,7 @@ __global__ void __launch_bounds__(BS) last_kernel(LastArgs a)
 template <int L>
 static size_t fft_smem(size_t extra_f2)
 {
-    return sizeof(float2) * ((size_t)L + 2 * (size_t)nl_of<L>() * line_stride(L) + extra_f2);
+    return sizeof(float2) * ((size_t)L + 2 * (size_t)Plan<L>::NL * line_stride(L) + extra_f2);
 }
 
 template <typename KernelT>
@@ -367,47 +345,30 @@ bool fft_size_supported(int L)
 
 static int gcd_int(int a, int b) { return b ? gcd_int(b, a % b) : a; }
 
-void launch_pass_contig(const PassArgs &a, int batch, cudaStream_t s)
+template <int L, int SIGN, int IN_MODE, int OUT_MODE>
+static void pass_launch(const PassArgs &a, int batch, cudaStream_t s)
 {
-    switch (a.L) {
-#define X(L_)                                                                                 \
-    case L_: {                                                                                \
-        constexpr int NL = nl_of<L_>();                                                       \
-        const size_t sm = fft_smem<L_>((size_t)NL * a.nk);                                    \
-        dim3 grid((unsigned)((a.lines + NL - 1) / NL), batch);                                \
-        if (a.in_real) {                                                                      \
-            set_smem(pass_contig_kernel<L_, true>, sm);                                       \
-            pass_contig_kernel<L_, true><<<grid, BS, sm, s>>>(a);                             \
-        } else {                                                                              \
-            set_smem(pass_contig_kernel<L_, false>, sm);                                      \
-            pass_contig_kernel<L_, false><<<grid, BS, sm, s>>>(a);                            \
-        }                                                                                     \
-        break;                                                                                \
-    }
-        BC_FOR_EACH_L(X)
-#undef X
-    default: break;
-    }
+    constexpr int NL = Plan<L>::NL;
+    const size_t sm = fft_smem<L>(OUT_MODE == 0 ? (size_t)NL * a.nk : 0);
+    const long long blocks = IN_MODE == 2 ? (long long)a.O * ((a.I + NL - 1) / NL) : (a.lines + NL - 1) / NL;
+    set_smem(pass_kernel<L, SIGN, IN_MODE, OUT_MODE>, sm);
+    pass_kernel<L, SIGN, IN_MODE, OUT_MODE><<<dim3((unsigned)blocks, batch), Plan<L>::TPL * NL, sm, s>>>(a);
 }
 
-void launch_pass_strided(const PassArgs &a, int sign, int batch, cudaStream_t s)
+// kind: 0 forward contiguous (z), 1 forward strided -> strided (y), 2 forward strided -> rows (x of A),
+//       3 inverse strided -> strided
+void launch_pass(const PassArgs &a, int kind, int batch, cudaStream_t s)
 {
     switch (a.L) {
-#define X(L_)                                                                                 \
-    case L_: {                                                                                \
-        constexpr int NL = nl_of<L_>();                                                       \
-        const size_t sm = fft_smem<L_>(0);                                                    \
-        const int itiles = (a.I + NL - 1) / NL;                                               \
-        dim3 grid((unsigned)(a.O * itiles), batch);                                           \
-        if (sign < 0) {                                                                       \
-            set_smem(pass_strided_kernel<L_, -1>, sm);                                        \
-            pass_strided_kernel<L_, -1><<<grid, BS, sm, s>>>(a);                              \
-        } else {                                                                              \
-            set_smem(pass_strided_kernel<L_, 1>, sm);                                         \
-            pass_strided_kernel<L_, 1><<<grid, BS, sm, s>>>(a);                               \
-        }                                                                                     \
-        break;                                                                                \
-    }
+#define X(L_)                                                                         \
+    case L_:                                                                          \
+        if (kind == 0) {                                                              \
+            if (a.in_real) pass_launch<L_, -1, 0, 0>(a, batch, s);                    \
+            else pass_launch<L_, -1, 1, 0>(a, batch, s);                              \
+        } else if (kind == 1) pass_launch<L_, -1, 2, 1>(a, batch, s);                 \
+        else if (kind == 2) pass_launch<L_, -1, 2, 0>(a, batch, s);                   \
+        else pass_launch<L_, 1, 2, 1>(a, batch, s);                                   \
+        break;
         BC_FOR_EACH_L(X)
 #undef X
     default: break;
@@ -420,7 +381,7 @@ static void fold_launch(const FoldXArgs &a, dim3 grid, cudaStream_t s)
     const size_t sm = sizeof(float2) * ((size_t)L + 2 * 8 * (size_t)line_stride(L) + 8 * (size_t)a.Np +
                                         (DIRECT ? 0 : 8 * (size_t)a.M));
     set_smem(fold_x_kernel<L, CPLX, DIRECT>, sm);
-    fold_x_kernel<L, CPLX, DIRECT><<<grid, 8 * tpl_of<L>(), sm, s>>>(a);
+    fold_x_kernel<L, CPLX, DIRECT><<<grid, 8 * Plan<L>::TPL, sm, s>>>(a);
 }
 
 void launch_fold_x(const FoldXArgs &a, int batch, cudaStream_t s)
@@ -430,7 +391,7 @@ void launch_fold_x(const FoldXArgs &a, int batch, cudaStream_t s)
     switch (a.L) {
 #define X(L_)                                                                                   \
     case L_: {                                                                                  \
-        const bool direct = ((a.Np / gcd_int(a.c, a.Np)) % tpl_of<L_>()) == 0 && (a.G % a.Np) == 0;                 \
+        const bool direct = ((a.Np / gcd_int(a.c, a.Np)) % Plan<L_>::TPL) == 0 && (a.G % a.Np) == 0; \
         if (a.complex_w) {                                                                      \
             if (direct) fold_launch<L_, true, true>(a, grid, s);                                \
             else fold_launch<L_, true, false>(a, grid, s);                                      \
@@ -451,16 +412,16 @@ void launch_last(const LastArgs &a, int batch, cudaStream_t s)
     switch (a.Np) {
 #define X(L_)                                                                                 \
     case L_: {                                                                                \
-        constexpr int NL = nl_of<L_>();                                                       \
+        constexpr int NL = Plan<L_>::NL;                                                      \
         const size_t sm = fft_smem<L_>(0);                                                    \
         const long long lines = (long long)a.N * a.N;                                         \
         dim3 grid((unsigned)((lines + NL - 1) / NL), batch);                                  \
         if (a.hermitian) {                                                                    \
             set_smem(last_kernel<L_, true>, sm);                                              \
-            last_kernel<L_, true><<<grid, BS, sm, s>>>(a);                                    \
+            last_kernel<L_, true><<<grid, Plan<L_>::TPL * NL, sm, s>>>(a);                    \
         } else {                                                                              \
             set_smem(last_kernel<L_, false>, sm);                                             \
-            last_kernel<L_, false><<<grid, BS, sm, s>>>(a);                                   \
+            last_kernel<L_, false><<<grid, Plan<L_>::TPL * NL, sm, s>>>(a);                   \
         }                                                                                     \
         break;                                                                                \
     }

@@ -59,12 +59,13 @@ __global__ void __launch_bounds__(256) spread_kernel(SpreadArgs a)
     const int cx_ = threadIdx.x >> 4, cy_ = threadIdx.x & 15;
     const int x = X0 + cx_, y = Y0 + cy_;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    float *col_r = accr + threadIdx.x * SP_T;
-    float *col_i = acci + (CPLX ? threadIdx.x * SP_T : 0);
+    // z-major: cell (column t, z) at [z * 256 + t] -> a warp touches 32 consecutive words
+    float *col_r = accr + threadIdx.x;
+    float *col_i = acci + (CPLX ? threadIdx.x : 0);
 #pragma unroll
     for (int z = 0; z < SP_T; z++) {
-        col_r[z] = 0.f;
-        if (CPLX) col_i[z] = 0.f;
+        col_r[z * 256] = 0.f;
+        if (CPLX) col_i[z * 256] = 0.f;
     }
 
     float R[9];
@@ -139,8 +140,8 @@ __global__ void __launch_bounds__(256) spread_kernel(SpreadArgs a)
             for (int z = zlo; z <= zhi; z++) {
                 const float dz = (fz0 + (float)z) - ue.z;
                 const float g = smoothed_ball(we.x, sqrtf(dxy2 + dz * dz) * a.hf, tau);
-                col_r[z] += we.y * g;
-                if (CPLX) col_i[z] += we.z * g;
+                col_r[z * 256] += we.y * g;
+                if (CPLX) col_i[z * 256] += we.z * g;
             }
         }
         __syncthreads();
@@ -154,12 +155,12 @@ __global__ void __launch_bounds__(256) spread_kernel(SpreadArgs a)
             float2 *o = (float2 *)a.out + rowoff;
 #pragma unroll
             for (int z = 0; z < SP_T; z++)
-                if (Z0 + z < L) o[Z0 + z] = make_float2(col_r[z], col_i[z]);
+                if (Z0 + z < L) o[Z0 + z] = make_float2(col_r[z * 256], col_i[z * 256]);
         } else {
             float *o = (float *)a.out + rowoff;
 #pragma unroll
             for (int z = 0; z < SP_T; z++)
-                if (Z0 + z < L) o[Z0 + z] = col_r[z];
+                if (Z0 + z < L) o[Z0 + z] = col_r[z * 256];
         }
     }
 }
