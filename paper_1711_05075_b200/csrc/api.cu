@@ -58,6 +58,9 @@ struct bc_ctx {
     ShapePlan plan[2];
     std::map<int, float2 *> d_tw;  // exp(-2 pi i m / L) per FFT length
     int *d_csr_off = nullptr, *d_csr_idx = nullptr;
+    float4 *d_prof = nullptr;     // per-ball radial profile tables of B (cubic Hermite pieces)
+    int *d_prof_off = nullptr;
+    double dprof = 0;
     float2 *d_Ahat = nullptr;
     bool have_spec = false;
 
@@ -365,6 +368,58 @@ bc_status check_support(bc_ctx *ctx)
     return BC_OK;
 }
 
+// (1_{B(0,s)} * G_tau)(d) in fp64, the same closed form as smoothed_ball() in spread.cu.
+double smoothed_ball_host(double s, double d, double tau)
+{
+    const double a = (s - d) / (std::sqrt(2.0) * tau), b = (s + d) / (std::sqrt(2.0) * tau);
+    const double t1 = a >= 0 ? 0.5 * (std::erf(a) + std::erf(b)) : 0.5 * (std::erfc(-a) - std::erfc(b));
+    const double x = s * d / (tau * tau);
+    double t2;
+    if (x < 1e-2) {
+        const double x2 = x * x;
+        t2 = 2 * s / (tau * std::sqrt(2 * kPi)) * std::exp(-(s * s + d * d) / (2 * tau * tau)) *
+             (1 + x2 / 6 + x2 * x2 / 120);
+    } else {
+        t2 = tau / (d * std::sqrt(2 * kPi)) *
+             (std::exp(-(s - d) * (s - d) / (2 * tau * tau)) - std::exp(-(s + d) * (s + d) / (2 * tau * tau)));
+    }
+    return t1 - t2;
+}
+
+// Per-ball cubic-Hermite tables of the smoothed radial profile of shape B on
+// intervals of width tau/16 out to s + cut (max interpolation error ~2e-8).
+bc_status build_profiles_B(bc_ctx *ctx)
+{
+    const ShapePlan &pl = ctx->plan[1];
+    const double D = pl.tau / 16.0;
+    ctx->dprof = D;
+    std::vector<float4> tab;
+    std::vector<int> off((size_t)std::max<int64_t>(ctx->n[1], 1), 0);
+    for (int64_t j = 0; j < ctx->n[1]; j++) {
+        const double s = ctx->hxyzr[1][4 * j + 3];
+        const int nint = (int)std::ceil((s + pl.cut) / D) + 2;
+        off[j] = (int)tab.size();
+        std::vector<double> v(nint + 1), dv(nint + 1);
+        for (int k = 0; k <= nint; k++) {
+            const double d = k * D, h = 1e-4 * D;
+            v[k] = smoothed_ball_host(s, d, pl.tau);
+            dv[k] = (smoothed_ball_host(s, d + h, pl.tau) - smoothed_ball_host(s, std::fabs(d - h), pl.tau)) / (2 * h) * D;
+        }
+        for (int k = 0; k < nint; k++) {
+            const double p0 = v[k], p1 = v[k + 1], m0 = dv[k], m1 = dv[k + 1];
+            tab.push_back(make_float4((float)p0, (float)m0, (float)(-3 * p0 - 2 * m0 + 3 * p1 - m1),
+                                      (float)(2 * p0 + m0 - 2 * p1 + m1)));
+        }
+        if (tab.size() > (size_t)1 << 30) return fail(ctx, BC_ENOMEM, "profile tables too large");
+    }
+    if (tab.empty()) tab.push_back(make_float4(0, 0, 0, 0));
+    TRY(dalloc(ctx, &ctx->d_prof, sizeof(float4) * tab.size()));
+    TRY(dalloc(ctx, &ctx->d_prof_off, sizeof(int) * off.size()));
+    CU(ctx, cudaMemcpy(ctx->d_prof, tab.data(), sizeof(float4) * tab.size(), cudaMemcpyHostToDevice));
+    CU(ctx, cudaMemcpy(ctx->d_prof_off, off.data(), sizeof(int) * off.size(), cudaMemcpyHostToDevice));
+    return BC_OK;
+}
+
 bc_status build_csr_A(bc_ctx *ctx)
 {
     const ShapePlan &pl = ctx->plan[0];
@@ -452,6 +507,11 @@ bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, voi
         a.out = ws1;
         a.out_batch_stride = (long long)(s1_per / (cplx ? 8 : 4));
         a.tiles_per_axis = (L + 15) / 16;
+        if (which == 1) {
+            a.prof = ctx->d_prof;
+            a.prof_off = ctx->d_prof_off;
+            a.inv_dprof = (float)(1.0 / ctx->dprof);
+        }
         StageScope sc(ctx, s, which ? "spread_B" : "spread_A");
         launch_spread(a, nb, s);
         ctx->launches++;
@@ -658,6 +718,8 @@ bc_status bc_destroy(bc_ctx *ctx)
     for (auto &kv : ctx->d_tw) cudaFree(kv.second);
     dfree(ctx->d_csr_off);
     dfree(ctx->d_csr_idx);
+    dfree(ctx->d_prof);
+    dfree(ctx->d_prof_off);
     dfree(ctx->d_Ahat);
     if (ctx->ws1) cudaFree(ctx->ws1);
     if (ctx->ws2) cudaFree(ctx->ws2);
@@ -721,6 +783,7 @@ bc_status bc_shape_upload(bc_ctx *ctx, int which, const double *xyzr, const doub
             }
         TRY(plan_shape(ctx, which, lo, hi, rmax));
         if (which == 0) TRY(build_csr_A(ctx));
+        if (which == 1) TRY(build_profiles_B(ctx));
     }
     TRY(check_support(ctx));
     return BC_OK;

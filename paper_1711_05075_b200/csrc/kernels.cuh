@@ -27,6 +27,11 @@ struct SpreadArgs {
     void *out;              // float [b][L][L][L] (real) or float2 (complex)
     long long out_batch_stride;  // elements
     int tiles_per_axis;
+    // optional per-ball radial profile tables: cubic pieces c0 + t c1 + t^2 c2 + t^3 c3 on
+    // intervals of width dprof (length units); ball j's pieces start at prof[prof_off[j]]
+    const float4 *prof;
+    const int *prof_off;
+    float inv_dprof;
 };
 
 // ----------------------------------------------------------------- axis transforms (passes.cu)

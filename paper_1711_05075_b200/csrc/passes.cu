@@ -31,7 +31,7 @@ __device__ __forceinline__ int coset_kk(int q, int p, int c, int G, int klo, int
 // IN_MODE: 0 contiguous real rows, 1 contiguous complex rows, 2 strided in[b][O][L][I].
 // OUT_MODE: 0 rows out[b][row][nk] (row = line index), 1 strided out[b][O][nk][I].
 template <int L, int SIGN, int IN_MODE, int OUT_MODE>
-__global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL) pass_kernel(PassArgs a)
+__global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TPL * Plan<L>::NL)) pass_kernel(PassArgs a)
 {
     constexpr int TPL = Plan<L>::TPL, NL = Plan<L>::NL, NT = TPL * NL;
     constexpr int LS = line_stride(L), E = L / TPL;
@@ -60,9 +60,17 @@ __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL) pass_kernel(PassAr
     float2 x[E];
     if (IN_MODE == 2) {
         const float2 *in = (const float2 *)a.in + (long long)b * a.in_bstride + (long long)o * L * a.I;
-        for (int e = threadIdx.x; e < L * NL; e += NT) {
+        // all loads first (E independent loads in flight per thread), then the transpose
+#pragma unroll
+        for (int m = 0; m < E; m++) {
+            const int e = threadIdx.x + NT * m;
             const int n = e / NL, i = e % NL;
-            A[i * LS + pad(n)] = (i0 + i < a.I) ? in[(long long)n * a.I + i0 + i] : make_float2(0.f, 0.f);
+            x[m] = (i0 + i < a.I) ? in[(long long)n * a.I + i0 + i] : make_float2(0.f, 0.f);
+        }
+#pragma unroll
+        for (int m = 0; m < E; m++) {
+            const int e = threadIdx.x + NT * m;
+            A[(e % NL) * LS + pad(e / NL)] = x[m];
         }
         __syncthreads();
 #pragma unroll
@@ -132,7 +140,7 @@ __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL) pass_kernel(PassAr
 // (Np / gcd(c, Np) a multiple of TPL and G a multiple of Np), so products accumulate
 // straight into acc; otherwise they are staged in Pb[line][kx] and gathered.
 template <int L, bool CPLX, bool DIRECT>
-__global__ void __launch_bounds__(8 * Plan<L>::TPL) fold_x_kernel(FoldXArgs a)
+__global__ void __launch_bounds__(8 * Plan<L>::TPL, 512 / (8 * Plan<L>::TPL) > 0 ? 512 / (8 * Plan<L>::TPL) : 1) fold_x_kernel(FoldXArgs a)
 {
     constexpr int NL = 8;
     constexpr int TPL = Plan<L>::TPL, NT = NL * TPL;
@@ -172,17 +180,24 @@ __global__ void __launch_bounds__(8 * Plan<L>::TPL) fold_x_kernel(FoldXArgs a)
                 if (ky < -K || ky > K) continue;
                 // source lines of R B: (ky, kz) for real weights, (-ky, -kz) for complex (f_hat_RB(-k))
                 const int kys = CPLX ? -ky : ky;
-                __syncthreads();
-                for (int e = threadIdx.x; e < L * NL; e += NT) {
+                float2 x[E];
+#pragma unroll
+                for (int m = 0; m < E; m++) {
+                    const int e = threadIdx.x + NT * m;
                     const int n = e / NL, i = e % NL;
                     const int kz = s * (z0 + i) + nz * Np;
                     float2 v = make_float2(0.f, 0.f);
                     if ((z0 + i < a.Fz) && kz >= zlo && kz <= K)
                         v = T2[((long long)n * M + (kys + K)) * Kz + (CPLX ? (-kz + K) : kz)];
-                    A[i * LS + pad(n)] = v;
+                    x[m] = v;
                 }
                 __syncthreads();
-                float2 x[E];
+#pragma unroll
+                for (int m = 0; m < E; m++) {
+                    const int e = threadIdx.x + NT * m;
+                    A[(e % NL) * LS + pad(e / NL)] = x[m];
+                }
+                __syncthreads();
 #pragma unroll
                 for (int m = 0; m < E; m++) x[m] = A[line * LS + pad(tl + TPL * m)];
                 __syncthreads();
@@ -251,7 +266,7 @@ __device__ __forceinline__ unsigned long long key_max(float v, unsigned idx)
 }
 
 template <int L, bool HERM>
-__global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL) last_kernel(LastArgs a)
+__global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TPL * Plan<L>::NL)) last_kernel(LastArgs a)
 {
     constexpr int TPL = Plan<L>::TPL, NL = Plan<L>::NL, NT = TPL * NL;
     constexpr int LS = line_stride(L), E = L / TPL;

@@ -41,13 +41,20 @@ __device__ __forceinline__ float smoothed_ball(float s, float d, float tau)
 
 // Block = 16^3-cell tile, 256 threads; thread t owns the z-column (x, y) of the tile
 // and accumulates into its own shared-memory column (no atomics; balls are added in
-// ball-index order, so the result is bitwise deterministic).
-template <bool CPLX>
+// ball-index order, so the result is bitwise deterministic).  The block first
+// compacts the candidate balls overlapping the tile (order-preserving) into a
+// shared list, then every thread walks the list for its column.
+// TABLE: the radial profile comes from the per-ball cubic-Hermite table
+// (SpreadArgs::prof, built once per shape on the host from the same closed form);
+// otherwise it is evaluated directly (smoothed_ball).
+template <bool CPLX, bool TABLE>
 __global__ void __launch_bounds__(256) spread_kernel(SpreadArgs a)
 {
-    __shared__ float4 sb[256];
-    __shared__ float4 sw[256];
+    constexpr int SP_LCAP = CPLX ? 448 : 768;  // static shared memory stays below 48 KB
+    __shared__ float4 sb[SP_LCAP];
+    __shared__ float4 sw[SP_LCAP];
     __shared__ int wcount[8];
+    __shared__ int list_n;
     __shared__ float accr[SP_T * SP_T * SP_T];
     __shared__ float acci[CPLX ? SP_T * SP_T * SP_T : 1];
 
@@ -81,51 +88,63 @@ __global__ void __launch_bounds__(256) spread_kernel(SpreadArgs a)
     }
     const float fx0 = (float)X0, fy0 = (float)Y0, fz0 = (float)Z0, fe = (float)(SP_T - 1);
     const float tau = a.tau;
+    if (threadIdx.x == 0) list_n = 0;
+    __syncthreads();
 
-    for (int base = 0; base < ncand; base += 256) {
-        const int q = base + threadIdx.x;
-        bool ok = false;
-        float4 u = make_float4(0, 0, 0, 0), wv = make_float4(0, 0, 0, 0);
-        if (q < ncand) {
-            const int j = a.csr_idx ? a.csr_idx[c0 + q] : q;
-            const float4 bl = a.balls[j];
-            float cx = bl.x, cy = bl.y, cz = bl.z;
-            if (a.rot) {  // eq_Mink0 (L235): a rigid motion relocates the centre only
-                cx = R[0] * bl.x + R[1] * bl.y + R[2] * bl.z;
-                cy = R[3] * bl.x + R[4] * bl.y + R[5] * bl.z;
-                cz = R[6] * bl.x + R[7] * bl.y + R[8] * bl.z;
+    int base = 0;
+    while (base < ncand) {
+        // ---- build the list (order-preserving compaction) until full or exhausted
+        while (base < ncand) {
+            const int cnt0 = list_n;
+            if (cnt0 + 256 > SP_LCAP) break;
+            const int q = base + threadIdx.x;
+            bool ok = false;
+            float4 u = make_float4(0, 0, 0, 0), wv = make_float4(0, 0, 0, 0);
+            if (q < ncand) {
+                const int j = a.csr_idx ? a.csr_idx[c0 + q] : q;
+                const float4 bl = a.balls[j];
+                float cx = bl.x, cy = bl.y, cz = bl.z;
+                if (a.rot) {  // eq_Mink0 (L235): a rigid motion relocates the centre only
+                    cx = R[0] * bl.x + R[1] * bl.y + R[2] * bl.z;
+                    cy = R[3] * bl.x + R[4] * bl.y + R[5] * bl.z;
+                    cz = R[6] * bl.x + R[7] * bl.y + R[8] * bl.z;
+                }
+                u.x = cx * a.inv_hf - (float)a.ox;
+                u.y = cy * a.inv_hf - (float)a.oy;
+                u.z = cz * a.inv_hf - (float)a.oz;
+                u.w = (bl.w + a.cut) * a.inv_hf;
+                const float dx = fmaxf(fmaxf(fx0 - u.x, u.x - (fx0 + fe)), 0.f);
+                const float dy = fmaxf(fmaxf(fy0 - u.y, u.y - (fy0 + fe)), 0.f);
+                const float dz = fmaxf(fmaxf(fz0 - u.z, u.z - (fz0 + fe)), 0.f);
+                ok = dx * dx + dy * dy + dz * dz < u.w * u.w;
+                if (ok) {
+                    wv.x = TABLE ? __int_as_float(a.prof_off[j]) : bl.w;
+                    wv.y = a.w_re ? a.w_re[j] : 1.f;
+                    wv.z = (CPLX && a.w_im) ? a.w_im[j] : 0.f;
+                }
             }
-            u.x = cx * a.inv_hf - (float)a.ox;
-            u.y = cy * a.inv_hf - (float)a.oy;
-            u.z = cz * a.inv_hf - (float)a.oz;
-            u.w = (bl.w + a.cut) * a.inv_hf;
-            const float dx = fmaxf(fmaxf(fx0 - u.x, u.x - (fx0 + fe)), 0.f);
-            const float dy = fmaxf(fmaxf(fy0 - u.y, u.y - (fy0 + fe)), 0.f);
-            const float dz = fmaxf(fmaxf(fz0 - u.z, u.z - (fz0 + fe)), 0.f);
-            ok = dx * dx + dy * dy + dz * dz < u.w * u.w;
-            if (ok) {
-                wv.x = bl.w;
-                wv.y = a.w_re ? a.w_re[j] : 1.f;
-                wv.z = (CPLX && a.w_im) ? a.w_im[j] : 0.f;
-            }
-        }
-        // order-preserving compaction (deterministic summation order)
-        const unsigned m = __ballot_sync(0xffffffffu, ok);
-        if (lane == 0) wcount[wid] = __popc(m);
-        __syncthreads();
-        int off = 0, total = 0;
+            const unsigned m = __ballot_sync(0xffffffffu, ok);
+            if (lane == 0) wcount[wid] = __popc(m);
+            __syncthreads();
+            int off = 0, total = 0;
 #pragma unroll
-        for (int w = 0; w < 8; w++) {
-            const int cw = wcount[w];
-            off += (w < wid) ? cw : 0;
-            total += cw;
+            for (int w = 0; w < 8; w++) {
+                const int cw = wcount[w];
+                off += (w < wid) ? cw : 0;
+                total += cw;
+            }
+            if (ok) {
+                const int pos = cnt0 + off + __popc(m & ((1u << lane) - 1u));
+                sb[pos] = u;
+                sw[pos] = wv;
+            }
+            base += 256;
+            __syncthreads();
+            if (threadIdx.x == 0) list_n = cnt0 + total;
+            __syncthreads();
         }
-        if (ok) {
-            const int pos = off + __popc(m & ((1u << lane) - 1u));
-            sb[pos] = u;
-            sw[pos] = wv;
-        }
-        __syncthreads();
+        // ---- accumulate the list into this thread's column
+        const int total = list_n;
         for (int e = 0; e < total; e++) {
             const float4 ue = sb[e];
             const float dx = (float)x - ue.x, dy = (float)y - ue.y;
@@ -139,11 +158,23 @@ __global__ void __launch_bounds__(256) spread_kernel(SpreadArgs a)
             const float4 we = sw[e];
             for (int z = zlo; z <= zhi; z++) {
                 const float dz = (fz0 + (float)z) - ue.z;
-                const float g = smoothed_ball(we.x, sqrtf(dxy2 + dz * dz) * a.hf, tau);
+                const float d = sqrtf(dxy2 + dz * dz) * a.hf;
+                float g;
+                if (TABLE) {
+                    const float uu = d * a.inv_dprof;
+                    const int k = (int)uu;
+                    const float t = uu - (float)k;
+                    const float4 c = a.prof[__float_as_int(we.x) + k];
+                    g = c.x + t * (c.y + t * (c.z + t * c.w));
+                } else {
+                    g = smoothed_ball(we.x, d, tau);
+                }
                 col_r[z * 256] += we.y * g;
                 if (CPLX) col_i[z * 256] += we.z * g;
             }
         }
+        __syncthreads();
+        if (threadIdx.x == 0) list_n = 0;
         __syncthreads();
     }
 
@@ -169,9 +200,12 @@ void launch_spread(const SpreadArgs &a, int batch, cudaStream_t s)
 {
     const int tpa = a.tiles_per_axis;
     dim3 grid(tpa * tpa * tpa, batch);
-    if (a.complex_w)
-        spread_kernel<true><<<grid, 256, 0, s>>>(a);
-    else
-        spread_kernel<false><<<grid, 256, 0, s>>>(a);
+    if (a.prof) {
+        if (a.complex_w) spread_kernel<true, true><<<grid, 256, 0, s>>>(a);
+        else spread_kernel<false, true><<<grid, 256, 0, s>>>(a);
+    } else {
+        if (a.complex_w) spread_kernel<true, false><<<grid, 256, 0, s>>>(a);
+        else spread_kernel<false, false><<<grid, 256, 0, s>>>(a);
+    }
 }
 
