@@ -59,11 +59,11 @@ struct FoldXArgs {
     int L, c, G;
     int K, M, Kz, Np, Fz;
     int complex_w;
-    const float2 *mult;   // x-axis multipliers of B, index kx + K
+    const float2 *mult;   // unused (B's x multipliers are folded into Ahat)
     const float2 *tw, *ctw;
     const float2 *T2;     // [b][ix][ky][kz]
     long long t2_bstride;
-    const float2 *Ahat;   // [ky][kz][kx], origin phase folded in
+    const float2 *Ahat;   // [ky][kz][x in coset-major order of B's x plan]: origin phase and B's x multipliers folded in
     float2 *F;            // [b][Np][Np][Fz]
     long long f_bstride;
 };
@@ -89,6 +89,8 @@ bool fft_size_supported(int L);
 void launch_pass(const PassArgs &a, int kind, int batch, cudaStream_t s);
 void launch_fold_x(const FoldXArgs &a, int batch, cudaStream_t s);
 void launch_last(const LastArgs &a, int batch, cudaStream_t s);
+void launch_permute_cm(const float2 *in, const float2 *mult, float2 *out, long long rows, int K, int L, int c, int G,
+                       int neg, cudaStream_t s);
 void launch_keys_init(unsigned long long *keys, int n, cudaStream_t s);
 void launch_keys_finalize(const unsigned long long *keys, int batch, int out_kind, void *out, cudaStream_t s);
 

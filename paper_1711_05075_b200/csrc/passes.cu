@@ -27,6 +27,31 @@ __device__ __forceinline__ int coset_kk(int q, int p, int c, int G, int klo, int
     return k - klo;
 }
 
+// Coset-major band order of one axis (L, c, G, band |k| <= K): coset p holds the
+// valid q in [0, qp] (k = c q + p > 0) and [qn, L) (k = c q + p - G < 0); they are
+// stored negative part first, so within a coset the order is ascending k and
+// consecutive q map to consecutive positions.  Used for A's x axis so that the
+// fused fold kernel reads A' with unit stride straight from its FFT registers.
+__device__ __forceinline__ int cm_index(int q, int p, int L, int c, int G, int K)
+{
+    int off = 0;
+    for (int pp = 0; pp < p; pp++) {
+        const int qp = K >= pp ? (K - pp) / c : -1;
+        const int qn = (G - K - pp + c - 1) / c;
+        off += (qp + 1) + (L - qn);
+    }
+    const int qn = (G - K - p + c - 1) / c;
+    return off + (q >= qn ? q - qn : q + (L - qn));
+}
+
+// position of band mode k (|k| <= K) in the coset-major order
+__device__ __forceinline__ int cm_of_k(int k, int L, int c, int G, int K)
+{
+    const int kk = k < 0 ? k + G : k;
+    const int p = kk % c;
+    return cm_index((kk - p) / c, p, L, c, G, K);
+}
+
 // ============================================================================ generic axis pass
 // IN_MODE: 0 contiguous real rows, 1 contiguous complex rows, 2 strided in[b][O][L][I].
 // OUT_MODE: 0 rows out[b][row][nk] (row = line index), 1 strided out[b][O][nk][I].
@@ -145,12 +170,15 @@ __global__ void __launch_bounds__(8 * Plan<L>::TPL, 512 / (8 * Plan<L>::TPL) > 0
     constexpr int NL = 8;
     constexpr int TPL = Plan<L>::TPL, NT = NL * TPL;
     constexpr int LS = line_stride(L), E = L / TPL;
+    constexpr bool USE_B = Plan<L>::n >= 3;
     extern __shared__ float2 sm[];
     float2 *tw = sm;
     float2 *A = tw + L;
     float2 *B = A + NL * LS;
-    float2 *acc = B + NL * LS;      // [NL][Np]
-    float2 *Pb = acc + NL * a.Np;   // [NL][M] (gather path only)
+    float2 *acc = B + (USE_B ? NL * LS : 0);  // [NL][Np]
+    float2 *ctw = acc + NL * a.Np;              // [c][L] coset twiddles
+    int2 *tab = (int2 *)(ctw + a.c * L);        // [c][L]: (band position or -1, tD | tC << 16)
+    float2 *Pb = (float2 *)(tab + a.c * L);     // [NL][M] (gather path only)
     const int line = threadIdx.x / TPL, tl = threadIdx.x % TPL;
     const int b = blockIdx.y;
     const int K = a.K, M = a.M, Np = a.Np, Kz = a.Kz;
@@ -161,11 +189,30 @@ __global__ void __launch_bounds__(8 * Plan<L>::TPL, 512 / (8 * Plan<L>::TPL) > 0
 
     for (int m = threadIdx.x; m < L; m += NT) tw[m] = a.tw[m];
     for (int e = threadIdx.x; e < NL * Np; e += NT) acc[e] = make_float2(0.f, 0.f);
+    for (int e = threadIdx.x; e < a.c * L; e += NT) {
+        ctw[e] = a.ctw[e];
+        const int p = e / L, q = e % L;
+        int kx = a.c * q + p;
+        if (2 * kx > a.G) kx -= a.G;
+        int2 t = make_int2(-1, 0);
+        if (kx >= -K && kx <= K) {
+            const int qn = (a.G - K - p + a.c - 1) / a.c;
+            t.x = cm_index(qn, p, L, a.c, a.G, K) + (q >= qn ? q - qn : q + (L - qn));
+            int tD = CPLX ? -kx : kx, tC = -kx;
+            tD %= Np;
+            if (tD < 0) tD += Np;
+            tC %= Np;
+            if (tC < 0) tC += Np;
+            t.y = tD | (tC << 16);
+        }
+        tab[e] = t;
+    }
 
     const int span = K / Np + 2;
     for (int pass = 0; pass < (CPLX ? 1 : 2); pass++) {
         const int s = pass ? -1 : 1;  // conj pass: target (-k) mod Np
         const int zlo = CPLX ? -K : (pass ? 1 : 0);
+        const int tshift = pass ? 16 : 0;
         for (int nz = -span; nz <= span; nz++) {
             bool any = false;
             for (int i = 0; i < NL; i++) {
@@ -201,34 +248,35 @@ __global__ void __launch_bounds__(8 * Plan<L>::TPL, 512 / (8 * Plan<L>::TPL) > 0
 #pragma unroll
                 for (int m = 0; m < E; m++) x[m] = A[line * LS + pad(tl + TPL * m)];
                 __syncthreads();
+                // A'' = A' * conj(mult_x) (real) or A'(-k) * mult_x (complex), coset-major rows
                 const float2 *arow = a.Ahat + ((long long)(ky + K) * Kz + (CPLX ? my_kz + K : my_kz)) * M;
                 for (int p = 0; p < a.c; p++) {
                     float2 y[E];
 #pragma unroll
-                    for (int m = 0; m < E; m++) y[m] = p ? cmul(x[m], a.ctw[p * L + tl + TPL * m]) : x[m];
+                    for (int m = 0; m < E; m++) y[m] = p ? cmul(x[m], ctw[p * L + tl + TPL * m]) : x[m];
                     fft_regs<L, -1>(y, A + line * LS, B + line * LS, tw, tl);
+                    if (my_ok) {
 #pragma unroll
-                    for (int m = 0; m < E; m++) {
-                        int kx = a.c * (tl + TPL * m) + p;
-                        if (2 * kx > a.G) kx -= a.G;
-                        if (kx < -K || kx > K) continue;
-                        float2 P = make_float2(0.f, 0.f);
-                        const int kxa = CPLX ? -kx : kx;
-                        if (my_ok) {
-                            const float2 bv = cmul(y[m], a.mult[kx + K]);
-                            const float2 av = arow[kxa + K];
-                            // real: f_hat_A'(k) conj(f_hat_RB(k)); complex: bv = f_hat_RB(-k') at
+                        for (int m = 0; m < E; m++) {
+                            const int2 t = tab[p * L + tl + TPL * m];
+                            if (t.x < 0) continue;
+                            const float2 av = arow[t.x];
+                            // real: f_hat_A'(k) conj(f_hat_RB(k)); complex: f_hat_A'(k') f_hat_RB(-k'),
                             // k' = (-kx, ky, kz), weights not conjugated (reading C-3)
-                            P = CPLX ? cmul(av, bv) : cmulc(av, bv);
-                        }
-                        if (DIRECT) {
-                            if (my_ok) {
-                                int t = (s > 0 ? kxa : -kxa) % Np;
-                                if (t < 0) t += Np;
-                                acc[line * Np + t] = cadd(acc[line * Np + t], s > 0 ? P : cconj(P));
+                            const float2 P = CPLX ? cmul(av, y[m]) : cmulc(av, y[m]);
+                            if (DIRECT) {
+                                const int tt = (t.y >> tshift) & 0xffff;
+                                acc[line * Np + tt] = cadd(acc[line * Np + tt], s > 0 ? P : cconj(P));
+                            } else {
+                                Pb[line * M + (CPLX ? -1 : 1) * (a.c * (tl + TPL * m) + p - (2 * (a.c * (tl + TPL * m) + p) > a.G ? a.G : 0)) + K] = P;
                             }
-                        } else {
-                            Pb[line * M + kxa + K] = P;
+                        }
+                    } else if (!DIRECT) {
+#pragma unroll
+                        for (int m = 0; m < E; m++) {
+                            int kx = a.c * (tl + TPL * m) + p;
+                            if (2 * kx > a.G) kx -= a.G;
+                            if (kx >= -K && kx <= K) Pb[line * M + kx + K] = make_float2(0.f, 0.f);
                         }
                     }
                     __syncthreads();
@@ -252,6 +300,30 @@ __global__ void __launch_bounds__(8 * Plan<L>::TPL, 512 / (8 * Plan<L>::TPL) > 0
         const int i = e % NL, t = e / NL;
         if (z0 + i < a.Fz) F[((long long)t * Np + kyp) * a.Fz + z0 + i] = acc[i * Np + t];
     }
+}
+
+// ============================================================================ band permutation
+// out[row][cm(s k)] = in[row][k + K], k in [-K, K]: A's spectrum into the coset-major x order
+// of B's plan (s = -1 for complex weights, where the fold reads A'(-k) against RB's line).
+// B's x multipliers (natural order, index k + K) are folded in: real weights store
+// A'(k) conj(mult(k)) at cm(k); complex weights store A'(k) mult(-k) at cm(-k).
+__global__ void permute_cm_kernel(const float2 *__restrict__ in, const float2 *__restrict__ mult,
+                                  float2 *__restrict__ out, long long rows, int K, int L, int c, int G, int neg)
+{
+    const int M = 2 * K + 1;
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= rows * M) return;
+    const long long row = e / M;
+    const int k = (int)(e % M) - K;
+    const float2 v = neg ? cmul(in[e], mult[-k + K]) : cmulc(in[e], mult[k + K]);
+    out[row * M + cm_of_k(neg ? -k : k, L, c, G, K)] = v;
+}
+
+void launch_permute_cm(const float2 *in, const float2 *mult, float2 *out, long long rows, int K, int L, int c, int G,
+                       int neg, cudaStream_t s)
+{
+    const long long n = rows * (2LL * K + 1);
+    permute_cm_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(in, mult, out, rows, K, L, c, G, neg);
 }
 
 // ============================================================================ last inverse pass + epilogue
@@ -393,8 +465,8 @@ void launch_pass(const PassArgs &a, int kind, int batch, cudaStream_t s)
 template <int L, bool CPLX, bool DIRECT>
 static void fold_launch(const FoldXArgs &a, dim3 grid, cudaStream_t s)
 {
-    const size_t sm = sizeof(float2) * ((size_t)L + 2 * 8 * (size_t)line_stride(L) + 8 * (size_t)a.Np +
-                                        (DIRECT ? 0 : 8 * (size_t)a.M));
+    const size_t sm = sizeof(float2) * ((size_t)L + (Plan<L>::n >= 3 ? 2 : 1) * 8 * (size_t)line_stride(L) +
+                                        8 * (size_t)a.Np + 2 * (size_t)a.c * L + (DIRECT ? 0 : 8 * (size_t)a.M));
     set_smem(fold_x_kernel<L, CPLX, DIRECT>, sm);
     fold_x_kernel<L, CPLX, DIRECT><<<grid, 8 * Plan<L>::TPL, sm, s>>>(a);
 }
