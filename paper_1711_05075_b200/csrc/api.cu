@@ -64,7 +64,7 @@ struct bc_ctx {
     float2 *d_Ahat = nullptr;      // A' = A_hat * origin phase, [ky][kz][kx] natural order
     float2 *d_Ahat_cm = nullptr;   // same, x axis in the coset-major order of B's plan
     bool cm_ready = false;
-    float2 *d_mult_cm = nullptr;   // B's x multipliers in coset-major order
+    int MS = 0;                    // row stride of d_Ahat_cm
     bool have_spec = false;
 
     // workspaces
@@ -226,21 +226,6 @@ void collect_profile(bc_ctx *ctx)
     ctx->pending.clear();
 }
 
-// coset-major position of band mode k for an axis plan (L, c, G, K); see passes.cu cm_index
-int cm_of_k_host(int k, int L, int c, int G, int K)
-{
-    const int kk = k < 0 ? k + G : k;
-    const int p = kk % c, q = (kk - p) / c;
-    int off = 0;
-    for (int pp = 0; pp < p; pp++) {
-        const int qp = K >= pp ? (K - pp) / c : -1;
-        const int qn = (G - K - pp + c - 1) / c;
-        off += (qp + 1) + (L - qn);
-    }
-    const int qn = (G - K - p + c - 1) / c;
-    return off + (q >= qn ? q - qn : q + (L - qn));
-}
-
 // ------------------------------------------------------------------ twiddle tables
 
 bc_status ensure_twiddles(bc_ctx *ctx, int L)
@@ -335,12 +320,6 @@ bc_status plan_shape(bc_ctx *ctx, int which, const double lo[3], const double hi
         }
         TRY(dalloc(ctx, &dst.d_mult[a], sizeof(float2) * nk));
         CU(ctx, cudaMemcpy(dst.d_mult[a], m.data(), sizeof(float2) * nk, cudaMemcpyHostToDevice));
-        if (which == 1 && a == 0) {  // B's x multipliers in coset-major order for the fused fold
-            std::vector<float2> mc(nk);
-            for (int q = 0; q < nk; q++) mc[cm_of_k_host(q - K, dst.L, dst.c, dst.G, K)] = m[q];
-            TRY(dalloc(ctx, &ctx->d_mult_cm, sizeof(float2) * nk));
-            CU(ctx, cudaMemcpy(ctx->d_mult_cm, mc.data(), sizeof(float2) * nk, cudaMemcpyHostToDevice));
-        }
     }
     std::vector<float2> ct((size_t)dst.c * dst.L);
     for (int p = 0; p < dst.c; p++)
@@ -746,7 +725,6 @@ bc_status bc_destroy(bc_ctx *ctx)
     dfree(ctx->d_prof_off);
     dfree(ctx->d_Ahat);
     dfree(ctx->d_Ahat_cm);
-    dfree(ctx->d_mult_cm);
     if (ctx->ws1) cudaFree(ctx->ws1);
     if (ctx->ws2) cudaFree(ctx->ws2);
     dfree(ctx->d_keys);
@@ -984,9 +962,11 @@ bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, in
         const int Np = ctx->p.Np;
         if (!ctx->cm_ready) {  // A' into the coset-major x order of B's plan (once per A / B plan)
             const ShapePlan &pb = ctx->plan[1];
-            const size_t nspec = (size_t)ctx->M * ctx->M * ctx->Kz;
+            ctx->MS = cm_row_stride(pb.L, pb.c, pb.G, ctx->K);
+            const size_t nspec = (size_t)ctx->MS * ctx->M * ctx->Kz;
             TRY(dalloc(ctx, &ctx->d_Ahat_cm, sizeof(float2) * nspec));
-            launch_permute_cm(ctx->d_Ahat, pb.d_mult[0], ctx->d_Ahat_cm, (long long)ctx->M * ctx->Kz, ctx->K, pb.L, pb.c, pb.G, cplx, s);
+            launch_permute_cm(ctx->d_Ahat, pb.d_mult[0], ctx->d_Ahat_cm, (long long)ctx->M * ctx->Kz, ctx->K, pb.L, pb.c,
+                              pb.G, cplx, ctx->MS, s);
             ctx->launches++;
             CU(ctx, cudaGetLastError());
             ctx->cm_ready = true;
@@ -1008,7 +988,8 @@ bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, in
                 a.Np = Np;
                 a.Fz = ctx->Fz;
                 a.complex_w = cplx;
-                a.mult = ctx->d_mult_cm;
+                a.mult = nullptr;
+                a.MS = ctx->MS;
                 a.tw = ctx->d_tw[pb.L];
                 a.ctw = pb.d_ctw;
                 a.T2 = (const float2 *)ctx->ws1;

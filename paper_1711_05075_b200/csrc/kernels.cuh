@@ -34,6 +34,48 @@ struct SpreadArgs {
     float inv_dprof;
 };
 
+// ----------------------------------------------------------------- coset-major band order
+// Band |k| <= K of an axis plan (L, c, G): coset p holds q in [0, qp] (k = c q + p >= 0) and
+// [qn, L) (k = c q + p - G < 0), stored negative part first (ascending k).  Every coset
+// segment starts on an even position (16-byte aligned float2 rows for cp.async).
+struct CmSeg {
+    int off, qn, cnt;  // segment start, first negative q, entries
+};
+__host__ __device__ inline CmSeg cm_segment(int p, int L, int c, int G, int K)
+{
+    int off = 0;
+    for (int pp = 0; pp <= p; pp++) {
+        const int qp = K >= pp ? (K - pp) / c : -1;
+        const int qn = (G - K - pp + c - 1) / c;
+        const int cnt = (qp + 1) + (L - qn);
+        if (pp == p) return CmSeg{off, qn, cnt};
+        off += (cnt + 1) & ~1;
+    }
+    return CmSeg{0, 0, 0};
+}
+__host__ __device__ inline int cm_row_stride(int L, int c, int G, int K)
+{
+    const CmSeg s = cm_segment(c - 1, L, c, G, K);
+    return s.off + ((s.cnt + 1) & ~1);
+}
+__host__ __device__ inline int cm_max_seg(int L, int c, int G, int K)
+{
+    int m = 0;
+    for (int p = 0; p < c; p++) {
+        const CmSeg s = cm_segment(p, L, c, G, K);
+        m = s.cnt > m ? s.cnt : m;
+    }
+    return (m + 1) & ~1;
+}
+// position of band mode k within its row
+__host__ __device__ inline int cm_of_k(int k, int L, int c, int G, int K)
+{
+    const int kk = k < 0 ? k + G : k;
+    const int p = kk % c, q = (kk - p) / c;
+    const CmSeg s = cm_segment(p, L, c, G, K);
+    return s.off + (q >= s.qn ? q - s.qn : q + (L - s.qn));
+}
+
 // ----------------------------------------------------------------- axis transforms (passes.cu)
 // One axis of the box DFT:  X(k) = mult(k) sum_{n<L} x_n exp(-2 pi i k n / G),  G = c L,
 // through c cosets k = c q + p of an L-point FFT of x_n exp(-2 pi i p n / G);
@@ -63,7 +105,9 @@ struct FoldXArgs {
     const float2 *tw, *ctw;
     const float2 *T2;     // [b][ix][ky][kz]
     long long t2_bstride;
-    const float2 *Ahat;   // [ky][kz][x in coset-major order of B's x plan]: origin phase and B's x multipliers folded in
+    const float2 *Ahat;   // [ky][kz][x in coset-major order of B's x plan, row stride MS]: origin phase
+                          // and B's x multipliers folded in
+    int MS;               // row stride of Ahat (cm_row_stride)
     float2 *F;            // [b][Np][Np][Fz]
     long long f_bstride;
 };
@@ -90,7 +134,7 @@ void launch_pass(const PassArgs &a, int kind, int batch, cudaStream_t s);
 void launch_fold_x(const FoldXArgs &a, int batch, cudaStream_t s);
 void launch_last(const LastArgs &a, int batch, cudaStream_t s);
 void launch_permute_cm(const float2 *in, const float2 *mult, float2 *out, long long rows, int K, int L, int c, int G,
-                       int neg, cudaStream_t s);
+                       int neg, int MS, cudaStream_t s);
 void launch_keys_init(unsigned long long *keys, int n, cudaStream_t s);
 void launch_keys_finalize(const unsigned long long *keys, int batch, int out_kind, void *out, cudaStream_t s);
 

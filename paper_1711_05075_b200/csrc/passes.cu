@@ -27,31 +27,6 @@ __device__ __forceinline__ int coset_kk(int q, int p, int c, int G, int klo, int
     return k - klo;
 }
 
-// Coset-major band order of one axis (L, c, G, band |k| <= K): coset p holds the
-// valid q in [0, qp] (k = c q + p > 0) and [qn, L) (k = c q + p - G < 0); they are
-// stored negative part first, so within a coset the order is ascending k and
-// consecutive q map to consecutive positions.  Used for A's x axis so that the
-// fused fold kernel reads A' with unit stride straight from its FFT registers.
-__device__ __forceinline__ int cm_index(int q, int p, int L, int c, int G, int K)
-{
-    int off = 0;
-    for (int pp = 0; pp < p; pp++) {
-        const int qp = K >= pp ? (K - pp) / c : -1;
-        const int qn = (G - K - pp + c - 1) / c;
-        off += (qp + 1) + (L - qn);
-    }
-    const int qn = (G - K - p + c - 1) / c;
-    return off + (q >= qn ? q - qn : q + (L - qn));
-}
-
-// position of band mode k (|k| <= K) in the coset-major order
-__device__ __forceinline__ int cm_of_k(int k, int L, int c, int G, int K)
-{
-    const int kk = k < 0 ? k + G : k;
-    const int p = kk % c;
-    return cm_index((kk - p) / c, p, L, c, G, K);
-}
-
 // ============================================================================ generic axis pass
 // IN_MODE: 0 contiguous real rows, 1 contiguous complex rows, 2 strided in[b][O][L][I].
 // OUT_MODE: 0 rows out[b][row][nk] (row = line index), 1 strided out[b][O][nk][I].
@@ -164,6 +139,15 @@ __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TP
 // F[k mod Np].  DIRECT: the fold targets of a thread's outputs are owned by that thread
 // (Np / gcd(c, Np) a multiple of TPL and G a multiple of Np), so products accumulate
 // straight into acc; otherwise they are staged in Pb[line][kx] and gathered.
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
+{
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
 template <int L, bool CPLX, bool DIRECT>
 __global__ void __launch_bounds__(8 * Plan<L>::TPL, 512 / (8 * Plan<L>::TPL) > 0 ? 512 / (8 * Plan<L>::TPL) : 1) fold_x_kernel(FoldXArgs a)
 {
@@ -172,16 +156,18 @@ __global__ void __launch_bounds__(8 * Plan<L>::TPL, 512 / (8 * Plan<L>::TPL) > 0
     constexpr int LS = line_stride(L), E = L / TPL;
     constexpr bool USE_B = Plan<L>::n >= 3;
     extern __shared__ float2 sm[];
+    const int K = a.K, M = a.M, Np = a.Np, Kz = a.Kz;
+    const int SEG = cm_max_seg(L, a.c, a.G, K);
     float2 *tw = sm;
     float2 *A = tw + L;
     float2 *B = A + NL * LS;
-    float2 *acc = B + (USE_B ? NL * LS : 0);  // [NL][Np]
-    float2 *ctw = acc + NL * a.Np;              // [c][L] coset twiddles
-    int2 *tab = (int2 *)(ctw + a.c * L);        // [c][L]: (band position or -1, tD | tC << 16)
+    float2 *acc = B + (USE_B ? NL * LS : 0);    // [NL][Np]
+    float2 *ctw = acc + NL * Np;                // [c][L] coset twiddles
+    float2 *As = ctw + a.c * L;                 // [2][NL][SEG] A'' segments (cp.async double buffer)
+    int2 *tab = (int2 *)(As + 2 * NL * SEG);    // [c][L]: (offset in segment or -1, tD | tC << 16)
     float2 *Pb = (float2 *)(tab + a.c * L);     // [NL][M] (gather path only)
     const int line = threadIdx.x / TPL, tl = threadIdx.x % TPL;
     const int b = blockIdx.y;
-    const int K = a.K, M = a.M, Np = a.Np, Kz = a.Kz;
     const int ztiles = (a.Fz + NL - 1) / NL;
     const int kyp = blockIdx.x / ztiles;
     const int z0 = (blockIdx.x % ztiles) * NL;
@@ -196,8 +182,8 @@ __global__ void __launch_bounds__(8 * Plan<L>::TPL, 512 / (8 * Plan<L>::TPL) > 0
         if (2 * kx > a.G) kx -= a.G;
         int2 t = make_int2(-1, 0);
         if (kx >= -K && kx <= K) {
-            const int qn = (a.G - K - p + a.c - 1) / a.c;
-            t.x = cm_index(qn, p, L, a.c, a.G, K) + (q >= qn ? q - qn : q + (L - qn));
+            const CmSeg sg = cm_segment(p, L, a.c, a.G, K);
+            t.x = q >= sg.qn ? q - sg.qn : q + (L - sg.qn);
             int tD = CPLX ? -kx : kx, tC = -kx;
             tD %= Np;
             if (tD < 0) tD += Np;
@@ -225,6 +211,21 @@ __global__ void __launch_bounds__(8 * Plan<L>::TPL, 512 / (8 * Plan<L>::TPL) > 0
             for (int ny = -span; ny <= span; ny++) {
                 const int ky = s * kyp + ny * Np;
                 if (ky < -K || ky > K) continue;
+                // A'' rows of this group: [ky][kz(i)]; coset p's segment is contiguous
+                auto prefetch = [&](int p, int buf) {
+                    const CmSeg sg = cm_segment(p, L, a.c, a.G, K);
+                    const int chunks = (sg.cnt + 1) >> 1;  // 16-byte chunks per row
+                    for (int e = threadIdx.x; e < NL * chunks; e += NT) {
+                        const int i = e / chunks, ch = e % chunks;
+                        const int kz = s * (z0 + i) + nz * Np;
+                        if ((z0 + i < a.Fz) && kz >= zlo && kz <= K) {
+                            const float2 *src = a.Ahat + ((long long)(ky + K) * Kz + (CPLX ? kz + K : kz)) * a.MS + sg.off;
+                            cp_async16(As + (buf * NL + i) * SEG + 2 * ch, src + 2 * ch);
+                        }
+                    }
+                    cp_async_commit();
+                };
+                prefetch(0, 0);
                 // source lines of R B: (ky, kz) for real weights, (-ky, -kz) for complex (f_hat_RB(-k))
                 const int kys = CPLX ? -ky : ky;
                 float2 x[E];
@@ -248,13 +249,15 @@ __global__ void __launch_bounds__(8 * Plan<L>::TPL, 512 / (8 * Plan<L>::TPL) > 0
 #pragma unroll
                 for (int m = 0; m < E; m++) x[m] = A[line * LS + pad(tl + TPL * m)];
                 __syncthreads();
-                // A'' = A' * conj(mult_x) (real) or A'(-k) * mult_x (complex), coset-major rows
-                const float2 *arow = a.Ahat + ((long long)(ky + K) * Kz + (CPLX ? my_kz + K : my_kz)) * M;
                 for (int p = 0; p < a.c; p++) {
+                    if (p + 1 < a.c) prefetch(p + 1, (p + 1) & 1);
                     float2 y[E];
 #pragma unroll
                     for (int m = 0; m < E; m++) y[m] = p ? cmul(x[m], ctw[p * L + tl + TPL * m]) : x[m];
                     fft_regs<L, -1>(y, A + line * LS, B + line * LS, tw, tl);
+                    if (p + 1 < a.c) cp_async_wait<1>(); else cp_async_wait<0>();
+                    __syncthreads();
+                    const float2 *arow = As + ((p & 1) * NL + line) * SEG;
                     if (my_ok) {
 #pragma unroll
                         for (int m = 0; m < E; m++) {
@@ -268,7 +271,9 @@ __global__ void __launch_bounds__(8 * Plan<L>::TPL, 512 / (8 * Plan<L>::TPL) > 0
                                 const int tt = (t.y >> tshift) & 0xffff;
                                 acc[line * Np + tt] = cadd(acc[line * Np + tt], s > 0 ? P : cconj(P));
                             } else {
-                                Pb[line * M + (CPLX ? -1 : 1) * (a.c * (tl + TPL * m) + p - (2 * (a.c * (tl + TPL * m) + p) > a.G ? a.G : 0)) + K] = P;
+                                int kx = a.c * (tl + TPL * m) + p;
+                                if (2 * kx > a.G) kx -= a.G;
+                                Pb[line * M + (CPLX ? -kx : kx) + K] = P;
                             }
                         }
                     } else if (!DIRECT) {
@@ -308,7 +313,7 @@ __global__ void __launch_bounds__(8 * Plan<L>::TPL, 512 / (8 * Plan<L>::TPL) > 0
 // B's x multipliers (natural order, index k + K) are folded in: real weights store
 // A'(k) conj(mult(k)) at cm(k); complex weights store A'(k) mult(-k) at cm(-k).
 __global__ void permute_cm_kernel(const float2 *__restrict__ in, const float2 *__restrict__ mult,
-                                  float2 *__restrict__ out, long long rows, int K, int L, int c, int G, int neg)
+                                  float2 *__restrict__ out, long long rows, int K, int L, int c, int G, int neg, int MS)
 {
     const int M = 2 * K + 1;
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -316,14 +321,15 @@ __global__ void permute_cm_kernel(const float2 *__restrict__ in, const float2 *_
     const long long row = e / M;
     const int k = (int)(e % M) - K;
     const float2 v = neg ? cmul(in[e], mult[-k + K]) : cmulc(in[e], mult[k + K]);
-    out[row * M + cm_of_k(neg ? -k : k, L, c, G, K)] = v;
+    out[row * MS + cm_of_k(neg ? -k : k, L, c, G, K)] = v;
 }
 
 void launch_permute_cm(const float2 *in, const float2 *mult, float2 *out, long long rows, int K, int L, int c, int G,
-                       int neg, cudaStream_t s)
+                       int neg, int MS, cudaStream_t s)
 {
     const long long n = rows * (2LL * K + 1);
-    permute_cm_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(in, mult, out, rows, K, L, c, G, neg);
+    cudaMemsetAsync(out, 0, sizeof(float2) * rows * MS, s);
+    permute_cm_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(in, mult, out, rows, K, L, c, G, neg, MS);
 }
 
 // ============================================================================ last inverse pass + epilogue
@@ -466,7 +472,8 @@ template <int L, bool CPLX, bool DIRECT>
 static void fold_launch(const FoldXArgs &a, dim3 grid, cudaStream_t s)
 {
     const size_t sm = sizeof(float2) * ((size_t)L + (Plan<L>::n >= 3 ? 2 : 1) * 8 * (size_t)line_stride(L) +
-                                        8 * (size_t)a.Np + 2 * (size_t)a.c * L + (DIRECT ? 0 : 8 * (size_t)a.M));
+                                        8 * (size_t)a.Np + 2 * (size_t)a.c * L + 16 * (size_t)cm_max_seg(L, a.c, a.G, a.K) +
+                                        (DIRECT ? 0 : 8 * (size_t)a.M));
     set_smem(fold_x_kernel<L, CPLX, DIRECT>, sm);
     fold_x_kernel<L, CPLX, DIRECT><<<grid, 8 * Plan<L>::TPL, sm, s>>>(a);
 }
