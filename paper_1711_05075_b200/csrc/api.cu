@@ -65,6 +65,8 @@ struct bc_ctx {
     float2 *d_Ahat_cm = nullptr;   // same, x axis in the coset-major order of B's plan
     bool cm_ready = false;
     int MS = 0;                    // row stride of d_Ahat_cm
+    int *d_xtab = nullptr;         // fused-fold extraction table of B's x plan
+    int2 *d_segs = nullptr;
     bool have_spec = false;
 
     // workspaces
@@ -327,6 +329,26 @@ bc_status plan_shape(bc_ctx *ctx, int which, const double lo[3], const double hi
             const double ang = -2 * kPi * (double)(((long long)p * n) % dst.G) / dst.G;
             ct[(size_t)p * dst.L + n] = make_float2((float)std::cos(ang), (float)std::sin(ang));
         }
+    if (which == 1) {  // extraction table of the fused fold: per FFT output (p, q) of B's x pass
+        std::vector<int> xt((size_t)dst.c * dst.L, -1);
+        std::vector<int2> sg(8, make_int2(0, 0));
+        for (int p = 0; p < dst.c; p++) {
+            const CmSeg s = cm_segment(p, dst.L, dst.c, dst.G, K);
+            sg[p] = make_int2(s.off, s.cnt);
+            for (int q = 0; q < dst.L; q++) {
+                int kx = dst.c * q + p;
+                if (2 * kx > dst.G) kx -= dst.G;
+                if (kx < -K || kx > K) continue;
+                int t = (cplx ? -kx : kx) % ctx->p.Np;
+                if (t < 0) t += ctx->p.Np;
+                xt[(size_t)p * dst.L + q] = (q >= s.qn ? q - s.qn : q + (dst.L - s.qn)) | (t << 16);
+            }
+        }
+        TRY(dalloc(ctx, &ctx->d_xtab, sizeof(int) * xt.size()));
+        TRY(dalloc(ctx, &ctx->d_segs, sizeof(int2) * sg.size()));
+        CU(ctx, cudaMemcpy(ctx->d_xtab, xt.data(), sizeof(int) * xt.size(), cudaMemcpyHostToDevice));
+        CU(ctx, cudaMemcpy(ctx->d_segs, sg.data(), sizeof(int2) * sg.size(), cudaMemcpyHostToDevice));
+    }
     TRY(dalloc(ctx, &dst.d_ctw, sizeof(float2) * ct.size()));
     CU(ctx, cudaMemcpy(dst.d_ctw, ct.data(), sizeof(float2) * ct.size(), cudaMemcpyHostToDevice));
     TRY(ensure_twiddles(ctx, dst.L));
@@ -725,6 +747,8 @@ bc_status bc_destroy(bc_ctx *ctx)
     dfree(ctx->d_prof_off);
     dfree(ctx->d_Ahat);
     dfree(ctx->d_Ahat_cm);
+    dfree(ctx->d_xtab);
+    dfree(ctx->d_segs);
     if (ctx->ws1) cudaFree(ctx->ws1);
     if (ctx->ws2) cudaFree(ctx->ws2);
     dfree(ctx->d_keys);
@@ -990,6 +1014,8 @@ bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, in
                 a.complex_w = cplx;
                 a.mult = nullptr;
                 a.MS = ctx->MS;
+                a.xtab = ctx->d_xtab;
+                a.segs = ctx->d_segs;
                 a.tw = ctx->d_tw[pb.L];
                 a.ctw = pb.d_ctw;
                 a.T2 = (const float2 *)ctx->ws1;

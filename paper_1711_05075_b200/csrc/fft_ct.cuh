@@ -22,7 +22,9 @@
 namespace fct {
 
 __host__ __device__ constexpr int pad(int idx) { return idx + (idx >> 4); }
-__host__ __device__ constexpr int line_stride(int L) { return (pad(L - 1) + 1) | 1; }
+// line stride (float2 units) = 2 mod 16: a half-warp writing 8 lines x 2 consecutive
+// elements during the strided-load transposes hits 16 distinct bank pairs
+__host__ __device__ constexpr int line_stride(int L) { return ((pad(L - 1) + 1 + 13) & ~15) + 2; }
 
 // ---------------------------------------------------------------- constexpr trigonometry
 constexpr double kPiD = 3.14159265358979323846264338327950288;

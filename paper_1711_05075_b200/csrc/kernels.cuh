@@ -108,6 +108,8 @@ struct FoldXArgs {
     const float2 *Ahat;   // [ky][kz][x in coset-major order of B's x plan, row stride MS]: origin phase
                           // and B's x multipliers folded in
     int MS;               // row stride of Ahat (cm_row_stride)
+    const int *xtab;      // [c][L] per FFT output (p, q): segment position | fold target << 16, or -1
+    const int2 *segs;     // [c] (segment offset, entries) of the coset-major rows
     float2 *F;            // [b][Np][Np][Fz]
     long long f_bstride;
 };

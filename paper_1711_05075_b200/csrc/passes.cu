@@ -158,14 +158,16 @@ __global__ void __launch_bounds__(8 * Plan<L>::TPL, 512 / (8 * Plan<L>::TPL) > 0
     extern __shared__ float2 sm[];
     const int K = a.K, M = a.M, Np = a.Np, Kz = a.Kz;
     const int SEG = cm_max_seg(L, a.c, a.G, K);
+    const int AS = Np + (Np >> 3) + 1;          // acc row stride; element t at t + t/8 (bank spread)
     float2 *tw = sm;
     float2 *A = tw + L;
     float2 *B = A + NL * LS;
-    float2 *acc = B + (USE_B ? NL * LS : 0);    // [NL][Np]
-    float2 *ctw = acc + NL * Np;                // [c][L] coset twiddles
+    float2 *acc = B + (USE_B ? NL * LS : 0);    // [NL][AS]
+    float2 *ctw = acc + NL * AS;                // [c][L] coset twiddles
     float2 *As = ctw + a.c * L;                 // [2][NL][SEG] A'' segments (cp.async double buffer)
-    int2 *tab = (int2 *)(As + 2 * NL * SEG);    // [c][L]: (offset in segment or -1, tD | tC << 16)
-    float2 *Pb = (float2 *)(tab + a.c * L);     // [NL][M] (gather path only)
+    int *tab = (int *)(As + 2 * NL * SEG);      // [c][L]: segment position | target << 16, or -1
+    int2 *segs = (int2 *)(tab + a.c * L);       // [c] (offset, entries)
+    float2 *Pb = (float2 *)(segs + 8);          // [NL][M] (gather path only)
     const int line = threadIdx.x / TPL, tl = threadIdx.x % TPL;
     const int b = blockIdx.y;
     const int ztiles = (a.Fz + NL - 1) / NL;
@@ -174,31 +176,18 @@ __global__ void __launch_bounds__(8 * Plan<L>::TPL, 512 / (8 * Plan<L>::TPL) > 0
     const float2 *T2 = a.T2 + (long long)b * a.t2_bstride;
 
     for (int m = threadIdx.x; m < L; m += NT) tw[m] = a.tw[m];
-    for (int e = threadIdx.x; e < NL * Np; e += NT) acc[e] = make_float2(0.f, 0.f);
+    for (int e = threadIdx.x; e < NL * AS; e += NT) acc[e] = make_float2(0.f, 0.f);
     for (int e = threadIdx.x; e < a.c * L; e += NT) {
         ctw[e] = a.ctw[e];
-        const int p = e / L, q = e % L;
-        int kx = a.c * q + p;
-        if (2 * kx > a.G) kx -= a.G;
-        int2 t = make_int2(-1, 0);
-        if (kx >= -K && kx <= K) {
-            const CmSeg sg = cm_segment(p, L, a.c, a.G, K);
-            t.x = q >= sg.qn ? q - sg.qn : q + (L - sg.qn);
-            int tD = CPLX ? -kx : kx, tC = -kx;
-            tD %= Np;
-            if (tD < 0) tD += Np;
-            tC %= Np;
-            if (tC < 0) tC += Np;
-            t.y = tD | (tC << 16);
-        }
-        tab[e] = t;
+        tab[e] = a.xtab[e];
     }
+    if (threadIdx.x < a.c) segs[threadIdx.x] = a.segs[threadIdx.x];
+    __syncthreads();
 
     const int span = K / Np + 2;
     for (int pass = 0; pass < (CPLX ? 1 : 2); pass++) {
         const int s = pass ? -1 : 1;  // conj pass: target (-k) mod Np
         const int zlo = CPLX ? -K : (pass ? 1 : 0);
-        const int tshift = pass ? 16 : 0;
         for (int nz = -span; nz <= span; nz++) {
             bool any = false;
             for (int i = 0; i < NL; i++) {
@@ -212,17 +201,13 @@ __global__ void __launch_bounds__(8 * Plan<L>::TPL, 512 / (8 * Plan<L>::TPL) > 0
                 const int ky = s * kyp + ny * Np;
                 if (ky < -K || ky > K) continue;
                 // A'' rows of this group: [ky][kz(i)]; coset p's segment is contiguous
+                // this thread group copies its own line's row segment (16-byte chunks)
+                const float2 *arow_g = a.Ahat + ((long long)(ky + K) * Kz + (CPLX ? my_kz + K : my_kz)) * a.MS;
                 auto prefetch = [&](int p, int buf) {
-                    const CmSeg sg = cm_segment(p, L, a.c, a.G, K);
-                    const int chunks = (sg.cnt + 1) >> 1;  // 16-byte chunks per row
-                    for (int e = threadIdx.x; e < NL * chunks; e += NT) {
-                        const int i = e / chunks, ch = e % chunks;
-                        const int kz = s * (z0 + i) + nz * Np;
-                        if ((z0 + i < a.Fz) && kz >= zlo && kz <= K) {
-                            const float2 *src = a.Ahat + ((long long)(ky + K) * Kz + (CPLX ? kz + K : kz)) * a.MS + sg.off;
-                            cp_async16(As + (buf * NL + i) * SEG + 2 * ch, src + 2 * ch);
-                        }
-                    }
+                    const int2 sg = segs[p];
+                    if (my_ok)
+                        for (int ch = tl; 2 * ch < sg.y; ch += TPL)
+                            cp_async16(As + (buf * NL + line) * SEG + 2 * ch, arow_g + sg.x + 2 * ch);
                     cp_async_commit();
                 };
                 prefetch(0, 0);
@@ -261,15 +246,17 @@ __global__ void __launch_bounds__(8 * Plan<L>::TPL, 512 / (8 * Plan<L>::TPL) > 0
                     if (my_ok) {
 #pragma unroll
                         for (int m = 0; m < E; m++) {
-                            const int2 t = tab[p * L + tl + TPL * m];
-                            if (t.x < 0) continue;
-                            const float2 av = arow[t.x];
+                            const int t = tab[p * L + tl + TPL * m];
+                            if (t < 0) continue;
+                            const float2 av = arow[t & 0xffff];
                             // real: f_hat_A'(k) conj(f_hat_RB(k)); complex: f_hat_A'(k') f_hat_RB(-k'),
                             // k' = (-kx, ky, kz), weights not conjugated (reading C-3)
                             const float2 P = CPLX ? cmul(av, y[m]) : cmulc(av, y[m]);
                             if (DIRECT) {
-                                const int tt = (t.y >> tshift) & 0xffff;
-                                acc[line * Np + tt] = cadd(acc[line * Np + tt], s > 0 ? P : cconj(P));
+                                int tt = t >> 16;                        // (kx' mod Np), kx' = +-kx
+                                if (s < 0 && tt) tt = Np - tt;           // conj pass: (-kx) mod Np
+                                tt += tt >> 3;
+                                acc[line * AS + tt] = cadd(acc[line * AS + tt], s > 0 ? P : cconj(P));
                             } else {
                                 int kx = a.c * (tl + TPL * m) + p;
                                 if (2 * kx > a.G) kx -= a.G;
@@ -293,7 +280,7 @@ __global__ void __launch_bounds__(8 * Plan<L>::TPL, 512 / (8 * Plan<L>::TPL) > 0
                         int kx = base - ((base + K) / Np) * Np;  // smallest alias >= -K
                         float2 sum = make_float2(0.f, 0.f);
                         for (; kx <= K; kx += Np) sum = cadd(sum, Pb[i * M + kx + K]);
-                        acc[i * Np + t] = cadd(acc[i * Np + t], s > 0 ? sum : cconj(sum));
+                        acc[i * AS + t + (t >> 3)] = cadd(acc[i * AS + t + (t >> 3)], s > 0 ? sum : cconj(sum));
                     }
                 }
             }
@@ -303,7 +290,7 @@ __global__ void __launch_bounds__(8 * Plan<L>::TPL, 512 / (8 * Plan<L>::TPL) > 0
     float2 *F = a.F + (long long)b * a.f_bstride;
     for (int e = threadIdx.x; e < NL * Np; e += NT) {
         const int i = e % NL, t = e / NL;
-        if (z0 + i < a.Fz) F[((long long)t * Np + kyp) * a.Fz + z0 + i] = acc[i * Np + t];
+        if (z0 + i < a.Fz) F[((long long)t * Np + kyp) * a.Fz + z0 + i] = acc[i * AS + t + (t >> 3)];
     }
 }
 
@@ -472,8 +459,9 @@ template <int L, bool CPLX, bool DIRECT>
 static void fold_launch(const FoldXArgs &a, dim3 grid, cudaStream_t s)
 {
     const size_t sm = sizeof(float2) * ((size_t)L + (Plan<L>::n >= 3 ? 2 : 1) * 8 * (size_t)line_stride(L) +
-                                        8 * (size_t)a.Np + 2 * (size_t)a.c * L + 16 * (size_t)cm_max_seg(L, a.c, a.G, a.K) +
-                                        (DIRECT ? 0 : 8 * (size_t)a.M));
+                                        8 * (size_t)(a.Np + (a.Np >> 3) + 1) + (size_t)a.c * L +
+                                        16 * (size_t)cm_max_seg(L, a.c, a.G, a.K) + (DIRECT ? 0 : 8 * (size_t)a.M)) +
+                      sizeof(int) * (size_t)a.c * L + sizeof(int2) * 8;
     set_smem(fold_x_kernel<L, CPLX, DIRECT>, sm);
     fold_x_kernel<L, CPLX, DIRECT><<<grid, 8 * Plan<L>::TPL, sm, s>>>(a);
 }
