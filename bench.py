@@ -118,15 +118,13 @@ def stage_bytes(q, N, Np, K, complex_w):
     X1 = N * Np * Fz * 8
     Y1 = N * N * Fz * 8
     return {
-        "spread_B": box,
-        "axis_z_B": box + T1,
-        "axis_y_B": T1 + T2,
-        "axis_x_B": T2 + Bh,
-        "fold": 2 * Bh + F,
-        "fused_x_fold": T2 + Bh + F,
+        "spread_B": box,              # write the smoothed density box of R B
+        "pass_z_B": box + T1,         # read box, write T1
+        "pass_y_B": T1 + T2,          # read T1, write T2
+        "fold_x": T2 + Bh + F,        # read T2 and A's band spectrum, write the folded product F
         "inv_x": F + X1,
         "inv_y": X1 + Y1,
-        "inv_z_reduce": Y1,
+        "inv_z_reduce": Y1,           # read Y1, write 16 B of keys
     }
 
 
@@ -245,6 +243,13 @@ def run_ours(args, rank, world, local_rank):
     units = n_rot * w.N ** 3 * args.steps * world
     value = units / (ms_max / 1e3)
 
+    # gather the per-rotation (min, argmin) of all ranks (outside the timed region)
+    best = None
+    if world > 1:
+        from paper_1711_05075_b200.sharding import gather_extrema, global_best
+        vals, idxs = gather_extrema(res["val"], res["idx"], n_rot * world, device=dev)
+        best = global_best(vals, idxs, "min")
+
     # e2e through the public API with host buffers (pinned), copies inside the timed region
     R_host = torch.tensor(R, dtype=torch.float64).pin_memory()
     out_host = torch.empty(n_rot * 16, dtype=torch.uint8).pin_memory()
@@ -301,7 +306,8 @@ def run_ours(args, rank, world, local_rank):
         "roofline": roof,
         "cpu_baseline": cpu,
         "stages_ms_per_step": {k: v[0] / args.steps for k, v in stages.items()},
-        "result_sample": {"rot0_min": float(res[0]["val"]), "rot0_argmin": int(res[0]["idx"])},
+        "result_sample": {"rot0_min": float(res[0]["val"]), "rot0_argmin": int(res[0]["idx"]),
+                          "global_best": best},
     }
     print(json.dumps(line), flush=True)
 

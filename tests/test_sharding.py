@@ -1,0 +1,68 @@
+"""Multi-rank host logic on CPU (gloo, world_size 2 and 3): rotation blocks and the
+all-gather of per-rotation results reproduce the single-rank global order exactly."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_1711_05075_b200.sharding import rotation_block, gather_extrema, global_best
+
+
+def test_rotation_blocks_cover_exactly():
+    for n in (1, 7, 64, 512, 3600):
+        for world in (1, 2, 3, 8):
+            seen = []
+            for r in range(world):
+                s, e = rotation_block(n, r, world)
+                assert 0 <= s <= e <= n
+                seen.extend(range(s, e))
+            assert seen == list(range(n))
+            sizes = [rotation_block(n, r, world)[1] - rotation_block(n, r, world)[0] for r in range(world)]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_global_best_tie_break():
+    v = np.array([3.0, 1.0, 1.0, 2.0])
+    i = np.array([5, 9, 2, 0])
+    assert global_best(v, i, "min") == (1, 1.0, 9)
+    assert global_best(v, i, "max") == (0, 3.0, 5)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, n_rot, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(123)
+    all_val = rng.normal(size=n_rot)
+    all_idx = rng.integers(0, 2 ** 31, size=n_rot)
+    s, e = rotation_block(n_rot, rank, world)
+    vals, idxs = gather_extrema(all_val[s:e], all_idx[s:e], n_rot)
+    ok = bool(np.array_equal(vals, all_val) and np.array_equal(idxs, all_idx))
+    q.put((rank, ok))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n_rot", [(2, 512), (3, 64), (2, 7)])
+def test_gather_extrema_gloo(world, n_rot):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n_rot, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    res = dict(q.get(timeout=10) for _ in range(world))
+    assert all(res[r] for r in range(world)), res
+    assert all(p.exitcode == 0 for p in procs)
