@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--rot-per-rank", type=int, default=512)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-slabs", type=int, default=16, help="x-slabs of the 256^3 grid in the oracle sample")
+    ap.add_argument("--cpu-slabs", type=int, default=32, help="x-slabs of the 256^3 grid in the oracle sample")
     return ap.parse_args()
 
 

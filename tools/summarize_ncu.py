@@ -12,10 +12,10 @@ def launch_shares(path):
     rows = [r for r in csv.reader(open(path)) if len(r) > 10]
     hdr, data = rows[0], rows[1:]
     ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
-    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
+    scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6}
     agg = collections.OrderedDict()
     for r in data:
-        name = r[ki].split("(")[0].replace("void ", "")
+        name = r[ki].rsplit("(", 1)[0].replace("void ", "").replace("(int)", "").replace("(bool)", "")
         v = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
         a = agg.setdefault(name, [0.0, 0])
         a[0] += v
@@ -35,7 +35,7 @@ def full_metrics(rep):
     hdr, units, data = rows[0], rows[1], rows[2:]
     res = []
     for r in data:
-        d = {"kernel": r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "")}
+        d = {"kernel": r[hdr.index("Kernel Name")].rsplit("(", 1)[0].replace("void ", "").replace("(int)", "").replace("(bool)", "")}
         for m in METRICS:
             if m in hdr:
                 d[m] = (r[hdr.index(m)], units[hdr.index(m)])
