@@ -698,8 +698,8 @@ bc_status bc_create(int device, const bc_params *p, bc_ctx **out)
     if (p->mode == BC_MODE_SPECTRAL) {
         if (p->precision != BC_FP32) return BC_EUNSUPPORTED;
         if (p->Np < p->N || p->Np < 2 || (p->Np % 2) != 0 || !friendly(p->Np) || p->Np > 1024) return BC_EINVAL;
-        if (!fft_size_supported(p->Np)) return BC_EUNSUPPORTED;
         if (p->K < 1 || p->K > 2047) return BC_EINVAL;
+        if (!fft_size_supported(p->Np)) return BC_EUNSUPPORTED;
         if (p->N > 1625) return BC_EUNSUPPORTED;
     }
     int ndev = 0;
