@@ -95,6 +95,7 @@ typedef struct {
     int32_t weights;      /* bc_weight_kind */
     int32_t max_batch;    /* rotations processed per launch; 0 = library default */
     double spread_eps;    /* spectral: target aliasing/truncation level of the spreading (0 = 1e-7) */
+    double band_radius;   /* spectral: > 0 additionally restricts the band to |k| <= band_radius */
 } bc_params;
 
 typedef struct bc_ctx bc_ctx;

@@ -699,6 +699,7 @@ bc_status bc_create(int device, const bc_params *p, bc_ctx **out)
         if (p->precision != BC_FP32) return BC_EUNSUPPORTED;
         if (p->Np < p->N || p->Np < 2 || (p->Np % 2) != 0 || !friendly(p->Np) || p->Np > 1024) return BC_EINVAL;
         if (p->K < 1 || p->K > 2047) return BC_EINVAL;
+        if (!(p->band_radius >= 0) || !std::isfinite(p->band_radius)) return BC_EINVAL;
         if (!fft_size_supported(p->Np)) return BC_EUNSUPPORTED;
         if (p->N > 1625) return BC_EUNSUPPORTED;
     }
@@ -990,7 +991,7 @@ bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, in
             const size_t nspec = (size_t)ctx->MS * ctx->M * ctx->Kz;
             TRY(dalloc(ctx, &ctx->d_Ahat_cm, sizeof(float2) * nspec));
             launch_permute_cm(ctx->d_Ahat, pb.d_mult[0], ctx->d_Ahat_cm, (long long)ctx->M * ctx->Kz, ctx->K, pb.L, pb.c,
-                              pb.G, cplx, ctx->MS, s);
+                              pb.G, cplx, ctx->MS, ctx->Kz, ctx->p.band_radius, s);
             ctx->launches++;
             CU(ctx, cudaGetLastError());
             ctx->cm_ready = true;

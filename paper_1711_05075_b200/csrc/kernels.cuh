@@ -136,7 +136,7 @@ void launch_pass(const PassArgs &a, int kind, int batch, cudaStream_t s);
 void launch_fold_x(const FoldXArgs &a, int batch, cudaStream_t s);
 void launch_last(const LastArgs &a, int batch, cudaStream_t s);
 void launch_permute_cm(const float2 *in, const float2 *mult, float2 *out, long long rows, int K, int L, int c, int G,
-                       int neg, int MS, cudaStream_t s);
+                       int neg, int MS, int Kz, double band_radius, cudaStream_t s);
 void launch_keys_init(unsigned long long *keys, int n, cudaStream_t s);
 void launch_keys_finalize(const unsigned long long *keys, int batch, int out_kind, void *out, cudaStream_t s);
 

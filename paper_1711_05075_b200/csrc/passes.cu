@@ -300,23 +300,29 @@ __global__ void __launch_bounds__(8 * Plan<L>::TPL, 512 / (8 * Plan<L>::TPL) > 0
 // B's x multipliers (natural order, index k + K) are folded in: real weights store
 // A'(k) conj(mult(k)) at cm(k); complex weights store A'(k) mult(-k) at cm(-k).
 __global__ void permute_cm_kernel(const float2 *__restrict__ in, const float2 *__restrict__ mult,
-                                  float2 *__restrict__ out, long long rows, int K, int L, int c, int G, int neg, int MS)
+                                  float2 *__restrict__ out, long long rows, int K, int L, int c, int G, int neg, int MS,
+                                  int Kz, double R2)
 {
     const int M = 2 * K + 1;
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= rows * M) return;
     const long long row = e / M;
     const int k = (int)(e % M) - K;
-    const float2 v = neg ? cmul(in[e], mult[-k + K]) : cmulc(in[e], mult[k + K]);
+    float2 v = neg ? cmul(in[e], mult[-k + K]) : cmulc(in[e], mult[k + K]);
+    if (R2 > 0) {  // spherical band: zero the modes with |k| > band_radius
+        const long long ky = row / Kz - K, kz = (row % Kz) - (Kz == M ? K : 0);
+        if ((double)(k * (long long)k + ky * ky + kz * kz) > R2) v = make_float2(0.f, 0.f);
+    }
     out[row * MS + cm_of_k(neg ? -k : k, L, c, G, K)] = v;
 }
 
 void launch_permute_cm(const float2 *in, const float2 *mult, float2 *out, long long rows, int K, int L, int c, int G,
-                       int neg, int MS, cudaStream_t s)
+                       int neg, int MS, int Kz, double band_radius, cudaStream_t s)
 {
     const long long n = rows * (2LL * K + 1);
     cudaMemsetAsync(out, 0, sizeof(float2) * rows * MS, s);
-    permute_cm_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(in, mult, out, rows, K, L, c, G, neg, MS);
+    permute_cm_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(in, mult, out, rows, K, L, c, G, neg, MS, Kz,
+                                                                 band_radius > 0 ? band_radius * band_radius : 0.0);
 }
 
 // ============================================================================ last inverse pass + epilogue

@@ -49,7 +49,7 @@ def test_params_struct_layout(bc):
     # matches the C struct: 4 + pad 4 + 8 + 24 + 4*6 + pad 4? -> check field offsets explicitly
     P = bc.bc_params
     assert P.h.offset == 8 and P.t0.offset == 16 and P.Np.offset == 40
-    assert P.spread_eps.offset == 64 and ctypes.sizeof(P) == 72
+    assert P.spread_eps.offset == 64 and P.band_radius.offset == 72 and ctypes.sizeof(P) == 80
 
 
 @pytest.mark.parametrize("kw", [

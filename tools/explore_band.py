@@ -9,7 +9,7 @@ from paper_1711_05075_b200 import ballcorr
 
 name = sys.argv[1]
 nrot = int(sys.argv[2])
-combos = [tuple(int(v) for v in s.split(":")) for s in sys.argv[3:]]
+combos = [tuple(float(v) for v in s.split(":")) for s in sys.argv[3:]]
 w = make_config(name)
 R = w.R[:nrot]
 t = time.time()
@@ -20,8 +20,10 @@ if w.weights == "complex":
     fe = fe[..., 0] + 1j * fe[..., 1]
 print(f"{name}: exact {time.time()-t:.1f}s  max|f| {np.abs(fe).max():.6g}", flush=True)
 ex.close()
-for Np, K in combos:
-    c = ballcorr.Correlator(N=w.N, h=w.h, t0=w.t0, Np=Np, K=K, weights=w.weights, max_batch=2)
+for cmb in combos:
+    Np, K = int(cmb[0]), int(cmb[1])
+    rad = cmb[2] if len(cmb) > 2 else 0.0
+    c = ballcorr.Correlator(N=w.N, h=w.h, t0=w.t0, Np=Np, K=K, weights=w.weights, max_batch=2, band_radius=rad)
     try:
         c.shape_upload(0, w.A_xyzr, w.A_w); c.shape_upload(1, w.B_xyzr, w.B_w); c.spectrum_A()
     except ballcorr.BallCorrError as e:
@@ -32,5 +34,5 @@ for Np, K in combos:
     errs = [np.abs(fs[r] - fe[r]).max() / np.abs(fe[r]).max() for r in range(nrot)]
     re_err = [np.abs(fs[r].real - fe[r].real).max() / np.abs(fe[r].real).max() for r in range(nrot)]
     best = [(fs[r].real.max(), fe[r].real.max(), int(np.argmax(fs[r].real)), int(np.argmax(fe[r].real))) for r in range(nrot)]
-    print(f"Np={Np} K={K} sigma_f={2*K/Np:.2f}: rel err {['%.2e' % e for e in errs]} re {['%.2e' % e for e in re_err]}  max {best[:2]}", flush=True)
+    print(f"Np={Np} K={K} R={rad} sigma_f={2*K/Np:.2f}: rel err {['%.2e' % e for e in errs]} re {['%.2e' % e for e in re_err]}  max {best[:2]}", flush=True)
     c.close()
