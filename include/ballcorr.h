@@ -96,6 +96,9 @@ typedef struct {
     int32_t max_batch;    /* rotations processed per launch; 0 = library default */
     double spread_eps;    /* spectral: target aliasing/truncation level of the spreading (0 = 1e-7) */
     double band_radius;   /* spectral: > 0 additionally restricts the band to |k| <= band_radius */
+    int32_t generic_only; /* spectral: nonzero disables the fused per-plan kernels (spread + z
+                             transform, fold + inverse x) and runs the generic passes instead;
+                             same result up to fp32 rounding order (a test hook) */
 } bc_params;
 
 typedef struct bc_ctx bc_ctx;

@@ -20,8 +20,17 @@ namespace {
 
 const double kPi = 3.14159265358979323846;
 
+// Smoothing window of B in the fused path: the Kaiser-Bessel "blob"
+//   phi(r) = C I0(alpha sqrt(1 - (r/W)^2)),  r < W (fine cells),  unit mass,
+// whose 3D transform is phi_hat(nu) = F(alpha^2 - (2 pi W nu)^2) / F(alpha^2) with
+// F(z^2) = (z cosh z - sinh z) / z^3 (= (sin y - y cos y) / y^3 for z = i y), nu in cycles
+// per cell.  W = 4, alpha = 18.5: alias images at |nu| >= 0.75 are <= 6e-6 of the band
+// (|nu_i| <= 1/4) and the band corner is damped only 22x (the Gaussian it replaces: 400x).
+constexpr double kBlobW = 4.0, kBlobAlpha = 18.5;
+
 struct ShapePlan {
     bool ok = false;
+    bool blob = false;   // B smoothed with the KB blob (fused spread + z path), else the Gaussian
     int L = 0, c = 0, G = 0;
     int o[3] = {0, 0, 0};
     double hf = 0, tau = 0, cut = 0;
@@ -61,6 +70,15 @@ struct bc_ctx {
     float4 *d_prof = nullptr;     // per-ball radial profile tables of B (cubic Hermite pieces)
     int *d_prof_off = nullptr;
     double dprof = 0;
+    // fused spread + z transform of B (spread_z.cu): balls in cell units, per-ball series
+    // constants, the universal (Phi1, Phi2) table, B's support radius
+    float4 *d_bcells = nullptr;
+    float2 *d_g02 = nullptr;
+    float4 *d_phi = nullptr;
+    float *d_dec = nullptr;        // 1 / phi_hat(|k| / G_B) indexed by |k|^2 (blob deconvolution)
+    int phi_n = 0;
+    double phi_U = 0, phi_D = 0;
+    double live_r = 0;
     float2 *d_Ahat = nullptr;      // A' = A_hat * origin phase, [ky][kz][kx] natural order
     float2 *d_Ahat_cm = nullptr;   // same, x axis in the coset-major order of B's plan
     bool cm_ready = false;
@@ -264,7 +282,31 @@ bc_status plan_shape(bc_ctx *ctx, int which, const double lo[3], const double hi
 
     ShapePlan best;
     double best_cost = 1e300;
-    for (int c = 1; c <= 8; c++) {
+    // B with real weights: the fused spread + z kernel with the KB blob when a box size it
+    // supports fits (G >= 4 (K + 1) as for the Gaussian: band |nu_i| <= 1/4 of the fine grid)
+    if (which == 1 && ctx->p.weights == BC_WEIGHTS_REAL && !ctx->p.generic_only) {
+        for (int c = 1; c <= 8; c++)
+            for (int L : {128, 256}) {
+                if (!spread_z_supported(L) || c * L < Gmin) continue;
+                const int G = c * L;
+                const double hf = P / G;
+                if (L * hf < extent + 2 * kBlobW * hf + 4 * hf) continue;
+                const double cost = (double)G * ((double)L * L + (double)L * ctx->Kz + (double)ctx->M * ctx->Kz);
+                if (cost < best_cost) {
+                    best_cost = cost;
+                    best = ShapePlan();
+                    best.ok = true;
+                    best.blob = true;
+                    best.L = L;
+                    best.c = c;
+                    best.G = G;
+                    best.hf = hf;
+                    best.tau = 0;
+                    best.cut = kBlobW * hf;
+                }
+            }
+    }
+    for (int c = 1; c <= 8 && !best.blob; c++) {
         int L = (Gmin + c - 1) / c;
         for (; L <= 1024; L++) {
             if (!fft_size_supported(L)) continue;
@@ -317,7 +359,8 @@ bc_status plan_shape(bc_ctx *ctx, int which, const double lo[3], const double hi
                 const double x = (double)k * ctx->p.t0[a] / P;
                 ang += 2 * kPi * (x - std::floor(x));
             }
-            const double amp = dst.hf * std::exp(2 * kPi * kPi * dst.tau * dst.tau * (double)(k * k) / (P * P));
+            // Gaussian window: separable deconvolution per axis; blob: radial, folded into A''
+            const double amp = dst.blob ? dst.hf : dst.hf * std::exp(2 * kPi * kPi * dst.tau * dst.tau * (double)(k * k) / (P * P));
             m[q] = make_float2((float)(amp * std::cos(ang)), (float)(amp * std::sin(ang)));
         }
         TRY(dalloc(ctx, &dst.d_mult[a], sizeof(float2) * nk));
@@ -445,6 +488,142 @@ bc_status build_profiles_B(bc_ctx *ctx)
     return BC_OK;
 }
 
+// ---- KB blob helpers (fp64, host)
+double blob_F(double z2)
+{
+    if (std::fabs(z2) < 1e-3) return 1.0 / 3 + z2 / 30 + z2 * z2 / 840;
+    if (z2 > 0) {
+        const double z = std::sqrt(z2);
+        return (z * std::cosh(z) - std::sinh(z)) / (z * z * z);
+    }
+    const double y = std::sqrt(-z2);
+    return (std::sin(y) - y * std::cos(y)) / (y * y * y);
+}
+double blob_hat(double nu)  // unit-mass blob transform, nu in cycles per cell
+{
+    const double t = 2 * kPi * kBlobW * nu;
+    return blob_F(kBlobAlpha * kBlobAlpha - t * t) / blob_F(kBlobAlpha * kBlobAlpha);
+}
+double blob_C() { return 1.0 / (4 * kPi * std::pow(kBlobW, 3) * blob_F(kBlobAlpha * kBlobAlpha)); }
+double blob_phi(double r)
+{
+    if (r >= kBlobW) return 0;
+    return blob_C() * std::cyl_bessel_i(0.0, kBlobAlpha * std::sqrt(1 - (r / kBlobW) * (r / kBlobW)));
+}
+double blob_dphi(double r)
+{
+    if (r >= kBlobW || r <= 0) return 0;
+    const double q = std::sqrt(1 - (r / kBlobW) * (r / kBlobW));
+    return blob_C() * std::cyl_bessel_i(1.0, kBlobAlpha * q) * kBlobAlpha * (-r / (kBlobW * kBlobW)) / q;
+}
+// composite 16-point Gauss-Legendre on [a, b] (the integrands below are smooth on [0, W])
+template <typename Fn>
+double gl_integrate(Fn f, double a, double b, int panels = 16)
+{
+    static double x[16], w[16];
+    static bool init = false;
+    if (!init) {
+        for (int i = 0; i < 16; i++) {
+            double z = std::cos(kPi * (i + 0.75) / 16.5), pp = 0;
+            for (int it = 0; it < 100; it++) {
+                double p1 = 1, p2 = 0;
+                for (int j = 1; j <= 16; j++) {
+                    const double p3 = p2;
+                    p2 = p1;
+                    p1 = ((2 * j - 1) * z * p2 - (j - 1) * p3) / j;
+                }
+                pp = 16 * (z * p1 - p2) / (z * z - 1);
+                const double dz = p1 / pp;
+                z -= dz;
+                if (std::fabs(dz) < 1e-16) break;
+            }
+            x[i] = z;
+            w[i] = 2 / ((1 - z * z) * pp * pp);
+        }
+        init = true;
+    }
+    double sum = 0;
+    const double hp = (b - a) / panels;
+    for (int p = 0; p < panels; p++) {
+        const double m = a + (p + 0.5) * hp, r = 0.5 * hp;
+        for (int i = 0; i < 16; i++) sum += w[i] * r * f(m + r * x[i]);
+    }
+    return sum;
+}
+
+// Tables of the fused spread + z kernel (cell units).  For a radial window phi of
+// support W, the window-smoothed ball profile is exactly
+//   g(s, d) = Phi1(s-d) + Phi1(s+d) - (Phi2(s-d) - Phi2(s+d)) / d,
+//   Phi1(u) = sgn(u) 2 pi [int_0^|u| t^2 phi + |u| Q(|u|)],   Phi2(u) = pi int_|u|^W t (t^2 - u^2) phi,
+//   Q(a) = int_a^W t phi,  Phi1 = +-1/2 and Phi2 = 0 for |u| >= W;
+// cubic Hermite pieces of width W/128 on [-W, W] (fp64 -> fp32), and per ball the d -> 0
+// series g = g0 + g2 d^2 with g0(s) = 2 Phi1(s) - 4 pi s Q(s), g2(s) = (2 pi / 3) s^2 phi'(s).
+bc_status build_spread_z_tables(bc_ctx *ctx)
+{
+    const ShapePlan &pl = ctx->plan[1];
+    const double U = kBlobW, D = kBlobW / 128;
+    auto Q = [&](double a) { return a >= U ? 0.0 : gl_integrate([](double t) { return t * blob_phi(t); }, a, U); };
+    auto M2 = [&](double a) { return gl_integrate([](double t) { return t * t * blob_phi(t); }, 0, std::min(a, U)); };
+    auto phi1 = [&](double u) {
+        const double a = std::fabs(u);
+        if (a >= U) return u > 0 ? 0.5 : -0.5;
+        const double v = 2 * kPi * (M2(a) + a * Q(a));
+        return u >= 0 ? v : -v;
+    };
+    auto dphi1 = [&](double u) { return 2 * kPi * Q(std::fabs(u)); };
+    auto phi2 = [&](double u) {
+        const double a = std::fabs(u);
+        if (a >= U) return 0.0;
+        return kPi * gl_integrate([a](double t) { return t * (t * t - a * a) * blob_phi(t); }, a, U);
+    };
+    auto dphi2 = [&](double u) { return -2 * kPi * u * Q(std::fabs(u)); };
+    const int n = (int)std::lround(2 * U / D);
+    std::vector<float4> tab((size_t)2 * n);
+    auto herm = [&](double p0, double m0, double p1, double m1) {
+        return make_float4((float)p0, (float)m0, (float)(-3 * p0 - 2 * m0 + 3 * p1 - m1), (float)(2 * p0 + m0 - 2 * p1 + m1));
+    };
+    std::vector<double> v1(n + 1), d1(n + 1), v2(n + 1), d2(n + 1);
+    for (int i = 0; i <= n; i++) {
+        const double u = -U + i * D;
+        v1[i] = phi1(u);
+        d1[i] = dphi1(u) * D;
+        v2[i] = phi2(u);
+        d2[i] = dphi2(u) * D;
+    }
+    for (int i = 0; i < n; i++) {
+        tab[2 * i] = herm(v1[i], d1[i], v1[i + 1], d1[i + 1]);
+        tab[2 * i + 1] = herm(v2[i], d2[i], v2[i + 1], d2[i + 1]);
+    }
+    const int64_t nb = ctx->n[1];
+    const size_t cnt = (size_t)std::max<int64_t>(nb, 1);
+    std::vector<float4> bc(cnt, make_float4(0, 0, 0, 1));
+    std::vector<float2> g(cnt, make_float2(0, 0));
+    for (int64_t j = 0; j < nb; j++) {
+        const double *x = &ctx->hxyzr[1][4 * j];
+        const double sc = x[3] / pl.hf;
+        bc[j] = make_float4((float)(x[0] / pl.hf), (float)(x[1] / pl.hf), (float)(x[2] / pl.hf), (float)sc);
+        g[j] = make_float2((float)(2 * phi1(sc) - 4 * kPi * sc * Q(sc)), (float)(2 * kPi / 3 * sc * sc * blob_dphi(sc)));
+    }
+    // radial deconvolution 1 / phi_hat(|k| / G) for every |k|^2 of the cube band
+    const size_t nk2 = (size_t)3 * ctx->K * ctx->K + 1;
+    std::vector<float> dec(nk2);
+    for (size_t q = 0; q < nk2; q++) dec[q] = (float)(1.0 / blob_hat(std::sqrt((double)q) / pl.G));
+    TRY(dalloc(ctx, &ctx->d_phi, sizeof(float4) * tab.size()));
+    TRY(dalloc(ctx, &ctx->d_bcells, sizeof(float4) * cnt));
+    TRY(dalloc(ctx, &ctx->d_g02, sizeof(float2) * cnt));
+    TRY(dalloc(ctx, &ctx->d_dec, sizeof(float) * nk2));
+    CU(ctx, cudaMemcpy(ctx->d_phi, tab.data(), sizeof(float4) * tab.size(), cudaMemcpyHostToDevice));
+    CU(ctx, cudaMemcpy(ctx->d_bcells, bc.data(), sizeof(float4) * cnt, cudaMemcpyHostToDevice));
+    CU(ctx, cudaMemcpy(ctx->d_g02, g.data(), sizeof(float2) * cnt, cudaMemcpyHostToDevice));
+    CU(ctx, cudaMemcpy(ctx->d_dec, dec.data(), sizeof(float) * nk2, cudaMemcpyHostToDevice));
+    ctx->phi_n = n;
+    ctx->phi_U = U;
+    ctx->phi_D = D;
+    return BC_OK;
+}
+
+bool use_spread_z(const bc_ctx *ctx) { return ctx->plan[1].ok && ctx->plan[1].blob; }
+
 bc_status build_csr_A(bc_ctx *ctx)
 {
     const ShapePlan &pl = ctx->plan[0];
@@ -511,7 +690,37 @@ bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, voi
     const bool cplx = ctx->p.weights == BC_WEIGHTS_COMPLEX;
     const int L = pl.L;
     const float2 *tw = ctx->d_tw[L];
-    {
+    if (which == 1 && use_spread_z(ctx)) {
+        SpreadZArgs a{};
+        a.L = L;
+        a.K = ctx->K;
+        a.c = pl.c;
+        a.G = pl.G;
+        a.ox = (float)pl.o[0];
+        a.oy = (float)pl.o[1];
+        a.oz = (float)pl.o[2];
+        a.cut = (float)(pl.cut / pl.hf);
+        a.n_balls = (int)ctx->n[1];
+        a.balls = ctx->d_bcells;
+        a.w = ctx->d_wre[1];
+        a.g02 = ctx->d_g02;
+        a.rot = d_rot;
+        a.phi = ctx->d_phi;
+        a.phi_n = ctx->phi_n;
+        a.phi_U = (float)ctx->phi_U;
+        a.phi_invD = (float)(1.0 / ctx->phi_D);
+        a.cx = (float)(-pl.o[0]);
+        a.cy = (float)(-pl.o[1]);
+        a.live_r2 = (float)(ctx->live_r * ctx->live_r);
+        a.mult_z = pl.d_mult[2];
+        a.tw = tw;
+        a.ctw = pl.d_ctw;
+        a.out = (float2 *)ws2;
+        a.out_bstride = (long long)(s2_per / 8);
+        StageScope sc(ctx, s, "spread_z_B");
+        launch_spread_z(a, nb, s);
+        ctx->launches++;
+    } else {
         SpreadArgs a{};
         a.L = L;
         a.ox = pl.o[0];
@@ -548,7 +757,7 @@ bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, voi
     base.signed_k = 1;
     base.tw = tw;
     base.ctw = pl.d_ctw;
-    {
+    if (!(which == 1 && use_spread_z(ctx))) {
         PassArgs a = base;
         a.klo = cplx ? -ctx->K : 0;
         a.nk = ctx->Kz;
@@ -746,6 +955,10 @@ bc_status bc_destroy(bc_ctx *ctx)
     dfree(ctx->d_csr_idx);
     dfree(ctx->d_prof);
     dfree(ctx->d_prof_off);
+    dfree(ctx->d_bcells);
+    dfree(ctx->d_g02);
+    dfree(ctx->d_phi);
+    dfree(ctx->d_dec);
     dfree(ctx->d_Ahat);
     dfree(ctx->d_Ahat_cm);
     dfree(ctx->d_xtab);
@@ -813,7 +1026,11 @@ bc_status bc_shape_upload(bc_ctx *ctx, int which, const double *xyzr, const doub
             }
         TRY(plan_shape(ctx, which, lo, hi, rmax));
         if (which == 0) TRY(build_csr_A(ctx));
-        if (which == 1) TRY(build_profiles_B(ctx));
+        if (which == 1 && !ctx->plan[1].blob) TRY(build_profiles_B(ctx));
+        if (which == 1) {
+            ctx->live_r = (rho + rmax + ctx->plan[1].cut) / ctx->plan[1].hf + 2.0;
+            if (ctx->plan[1].blob) TRY(build_spread_z_tables(ctx));
+        }
     }
     TRY(check_support(ctx));
     return BC_OK;
@@ -985,13 +1202,16 @@ bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, in
             ctx->keys_cap = 2 * nb;
         }
         const int Np = ctx->p.Np;
+        const ShapePlan &pB = ctx->plan[1];
+        const bool fast_fold = !ctx->p.generic_only && fold_fast_supported(pB.L, pB.c, pB.G, ctx->K, Np, cplx);
+        const bool fused_inv = fast_fold || (!ctx->p.generic_only && fold_fuses_inverse(pB.L, Np));
         if (!ctx->cm_ready) {  // A' into the coset-major x order of B's plan (once per A / B plan)
             const ShapePlan &pb = ctx->plan[1];
             ctx->MS = cm_row_stride(pb.L, pb.c, pb.G, ctx->K);
             const size_t nspec = (size_t)ctx->MS * ctx->M * ctx->Kz;
             TRY(dalloc(ctx, &ctx->d_Ahat_cm, sizeof(float2) * nspec));
             launch_permute_cm(ctx->d_Ahat, pb.d_mult[0], ctx->d_Ahat_cm, (long long)ctx->M * ctx->Kz, ctx->K, pb.L, pb.c,
-                              pb.G, cplx, ctx->MS, ctx->Kz, ctx->p.band_radius, s);
+                              pb.G, cplx, ctx->MS, ctx->Kz, ctx->p.band_radius, pb.blob ? ctx->d_dec : nullptr, s);
             ctx->launches++;
             CU(ctx, cudaGetLastError());
             ctx->cm_ready = true;
@@ -1002,7 +1222,25 @@ bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, in
             TRY(shape_spectrum(ctx, 1, ctx->d_rot + 9 * r0, b, ctx->ws1, ctx->ws2, s1, s2, s));
             const ShapePlan &pb = ctx->plan[1];
             // 4: x pass fused with the spectral product (A' conj(RB)) and the fold onto Np^3
-            {
+            if (fast_fold) {
+                FoldFastArgs a{};
+                a.tw = ctx->d_tw[pb.L];
+                a.ctw = pb.d_ctw;
+                a.T2 = (const float2 *)ctx->ws1;
+                a.t2_bstride = (long long)(s1 / 8);
+                a.Ahat = ctx->d_Ahat_cm;
+                a.MS = ctx->MS;
+                for (int p = 0; p < 4; p++) {
+                    const CmSeg sg = cm_segment(p, pb.L, pb.c, pb.G, ctx->K);
+                    a.pos_base[p] = sg.off - sg.qn;
+                }
+                a.X1 = (float2 *)ctx->ws2;
+                a.x1_bstride = (long long)(s2 / 8);
+                a.N = (int)N;
+                StageScope sc(ctx, s, "fold_fast");
+                launch_fold_fast(a, b, s);
+                ctx->launches++;
+            } else {
                 FoldXArgs a{};
                 a.L = pb.L;
                 a.c = pb.c;
@@ -1022,9 +1260,12 @@ bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, in
                 a.T2 = (const float2 *)ctx->ws1;
                 a.t2_bstride = (long long)(s1 / 8);
                 a.Ahat = ctx->d_Ahat_cm;
-                a.F = (float2 *)ctx->ws2;
+                a.F = (float2 *)ctx->ws2;  // F, or X1 when the inverse x pass is fused
                 a.f_bstride = (long long)(s2 / 8);
-                StageScope sc(ctx, s, "fold_x");
+                a.N = (int)N;
+                a.fuse_inv = fused_inv;
+                a.tw_inv = ctx->d_tw[Np];
+                StageScope sc(ctx, s, fused_inv ? "fold_x_inv" : "fold_x");
                 launch_fold_x(a, b, s);
                 ctx->launches++;
             }
@@ -1037,7 +1278,8 @@ bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, in
             inv.nk = (int)N;
             inv.signed_k = 0;
             inv.tw = ctx->d_tw[Np];
-            {
+            // X1 lives in ws1 after a separate inverse x pass, in ws2 when it is fused
+            if (!fused_inv) {
                 PassArgs a = inv;
                 a.O = 1;
                 a.I = Np * ctx->Fz;
@@ -1049,14 +1291,16 @@ bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, in
                 launch_pass(a, 3, b, s);
                 ctx->launches++;
             }
+            void *y1 = fused_inv ? ctx->ws1 : ctx->ws2;
+            const long long y1_bstride = (long long)((fused_inv ? s1 : s2) / 8);
             {
                 PassArgs a = inv;
                 a.O = (int)N;
                 a.I = ctx->Fz;
-                a.in = ctx->ws1;
-                a.in_bstride = (long long)(s1 / 8);
-                a.out = (float2 *)ctx->ws2;
-                a.out_bstride = (long long)(s2 / 8);
+                a.in = fused_inv ? ctx->ws2 : ctx->ws1;
+                a.in_bstride = (long long)((fused_inv ? s2 : s1) / 8);
+                a.out = (float2 *)y1;
+                a.out_bstride = y1_bstride;
                 StageScope sc(ctx, s, "inv_y");
                 launch_pass(a, 3, b, s);
                 ctx->launches++;
@@ -1074,8 +1318,8 @@ bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, in
                 a.hermitian = !cplx;
                 a.scale = (float)(1.0 / (ctx->P * ctx->P * ctx->P));
                 a.tw = ctx->d_tw[Np];
-                a.in = (const float2 *)ctx->ws2;
-                a.in_bstride = (long long)(s2 / 8);
+                a.in = (const float2 *)y1;
+                a.in_bstride = y1_bstride;
                 a.out_kind = out_kind;
                 a.out_full = dout + out_per * r0;
                 a.full_bstride = N3;
@@ -1119,6 +1363,12 @@ bc_status bc_query(const bc_ctx *ctx, const char *key, double *value)
     else if (k == "band_modes") *value = (double)ctx->M * ctx->M * ctx->Kz;
     else if (k == "batch") *value = ctx->batch;
     else if (k == "bytes_workspace") *value = (double)(ctx->ws1_bytes + ctx->ws2_bytes);
+    else if (k == "fused_spread_z") *value = use_spread_z(ctx) ? 1 : 0;
+    else if (k == "blob_B") *value = B.blob ? 1 : 0;
+    else if (k == "fused_fold_inv") *value = (!ctx->p.generic_only && fold_fuses_inverse(B.L, ctx->p.Np)) ? 1 : 0;
+    else if (k == "fold_fast")
+        *value = (!ctx->p.generic_only && fold_fast_supported(B.L, B.c, B.G, ctx->K, ctx->p.Np,
+                                                             ctx->p.weights == BC_WEIGHTS_COMPLEX)) ? 1 : 0;
     else return BC_EINVAL;
     return BC_OK;
 }

@@ -1,0 +1,179 @@
+// fold_fast.cu -- fused x-pass + spectral product + fold + inverse x for the plan shape
+// L = Np = 256, c = 4 cosets, G = 4 (K + 1) (K = 255), real weights (sm_100a).
+//
+// Same arithmetic as fold_x_kernel<256, 256, false, true> (passes.cu; PAPER.md L398-L419
+// eq_ccghat): for the targets (k'y, k'z in [z0, z0 + 8)) the x-transform of every alias
+// line (ky, kz) of R B on the band, times A'' (A's spectrum with the origin phase and B's
+// deconvolution folded in), summed into F[k mod Np] (conjugated at -k for the Hermitian
+// partner half), then the inverse x-FFT of the folded lines, written as X1[mx][k'y][k'z].
+// What this plan shape makes compile-time:
+//  * thread tl of a line holds the FFT outputs q = tl + 16 m of coset p, k = 4 q + p;
+//    the band |k| <= 255 keeps exactly m in {0..3} (k = 4q + p) and {12..15} (k = 4q + p - 1024),
+//    minus (p, q) = (0, 192), and both land on the fold target t = 4 tl + 64 (m & 3) + p:
+//    the thread OWNS its 16 targets, accumulated in registers (no shared-memory atomics);
+//  * the Hermitian partner -t of a target owned by lane tl is owned by lane 15 - tl (p != 0)
+//    or (16 - tl) & 15 (p = 0), in the same 16-lane line: conjugate-pass products move by
+//    warp shuffles;
+//  * A''s coset-major row positions are affine in (tl, m): coalesced 128-byte loads.
+#include "kernels.cuh"
+#include "fft_ct.cuh"
+
+using namespace fct;
+
+namespace {
+
+constexpr int FF_L = 256, FF_C = 4, FF_TPL = 16, FF_NL = 8, FF_NT = FF_NL * FF_TPL;
+constexpr int FF_G = FF_C * FF_L, FF_K = FF_G / 4 - 1, FF_M = 2 * FF_K + 1, FF_KZ = FF_K + 1;
+constexpr int FF_NP = FF_L, FF_FZ = FF_NP / 2 + 1;
+constexpr int FF_LS = line_stride(FF_L);
+static_assert(Plan<FF_L>::TPL == FF_TPL && Plan<FF_L>::n == 2, "fold_fast plan");
+
+}  // namespace
+
+__global__ void __launch_bounds__(FF_NT, 4) fold_fast_kernel(FoldFastArgs a)
+{
+    constexpr int E = FF_L / FF_TPL;  // 16
+    extern __shared__ float2 smf[];
+    float2 *tw = smf;                  // [L]
+    float2 *ctw = tw + FF_L;           // [C][L]
+    float2 *X = ctw + FF_C * FF_L;     // [NL][LS] input lines (x order)
+    float2 *Ab = X + FF_NL * FF_LS;    // [NL][LS] FFT exchange / staging
+    const int line = threadIdx.x / FF_TPL, tl = threadIdx.x % FF_TPL;
+    const int lane = threadIdx.x & 31;
+    const int b = blockIdx.x % a.nb;
+    const int tb = blockIdx.x / a.nb;
+    constexpr int ZT = (FF_FZ + FF_NL - 1) / FF_NL;
+    const int kyp = tb / ZT;
+    const int z0 = (tb % ZT) * FF_NL;
+    const float2 *T2 = a.T2 + (long long)b * a.t2_bstride;
+
+    for (int e = threadIdx.x; e < FF_L; e += FF_NT) tw[e] = a.tw[e];
+    for (int e = threadIdx.x; e < FF_C * FF_L; e += FF_NT) ctw[e] = a.ctw[e];
+
+    // A'' row position of output (m, p) of lane tl: base[p] + tl + 16 m (+ L for m < 4)
+    int pbase[FF_C];
+#pragma unroll
+    for (int p = 0; p < FF_C; p++) pbase[p] = a.pos_base[p] + tl;
+
+    float2 acc[4][FF_C];
+#pragma unroll
+    for (int j = 0; j < 4; j++)
+#pragma unroll
+        for (int p = 0; p < FF_C; p++) acc[j][p] = make_float2(0.f, 0.f);
+
+    const int tz = z0 + line;  // this line's target k'z
+#pragma unroll 1
+    for (int pass = 0; pass < 2; pass++) {
+        // direct: kz = k'z in [0, 128], ky in {k'y, k'y - 256};  conjugate partner: kz = 256 - k'z
+        // (k'z in [1, 128]), ky in {-k'y, 256 - k'y}; out-of-band ky / kz contribute nothing
+#pragma unroll 1
+        for (int al = 0; al < 2; al++) {
+            const int ky = pass == 0 ? (al == 0 ? kyp : kyp - FF_NP) : (al == 0 ? -kyp : FF_NP - kyp);
+            if (ky < -FF_K || ky > FF_K) continue;  // block-uniform
+            // ---- T2 lines (ky, kz(i)) -> X (transposed through registers for coalescing)
+            float2 x[E];
+#pragma unroll
+            for (int m = 0; m < E; m++) {
+                const int e = threadIdx.x + FF_NT * m;
+                const int n = e / FF_NL, i = e % FF_NL;
+                const int kt = z0 + i;
+                const bool ok = pass == 0 ? (kt < FF_FZ) : (kt >= 1 && kt < FF_FZ);
+                const int kz = pass == 0 ? kt : FF_NP - kt;
+                x[m] = ok ? T2[(n * FF_M + ky + FF_K) * FF_KZ + kz] : make_float2(0.f, 0.f);
+            }
+            __syncthreads();  // previous group's last reads of X / Ab are done
+#pragma unroll
+            for (int m = 0; m < E; m++) {
+                const int e = threadIdx.x + FF_NT * m;
+                X[(e % FF_NL) * FF_LS + pad(e / FF_NL)] = x[m];
+            }
+            __syncthreads();
+            const bool my_ok = pass == 0 ? (tz < FF_FZ) : (tz >= 1 && tz < FF_FZ);
+            const int my_kz = pass == 0 ? tz : FF_NP - tz;
+            const float2 *arow = a.Ahat + (long long)((ky + FF_K) * FF_KZ + (my_ok ? my_kz : 0)) * a.MS;
+#pragma unroll
+            for (int p = 0; p < FF_C; p++) {
+                // A'' values of the 8 in-band outputs (issued before the FFT to hide latency)
+                float2 av[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    const int m = u < 4 ? u : u + 8;
+                    const int pos = pbase[p] + 16 * m + (m < 4 ? FF_L : 0);
+                    const bool in_band = my_ok && !(p == 0 && m == 12 && tl == 0);
+                    av[u] = in_band ? __ldg(arow + pos) : make_float2(0.f, 0.f);
+                }
+                float2 y[E];
+#pragma unroll
+                for (int m = 0; m < E; m++) {
+                    const int n = tl + FF_TPL * m;
+                    const float2 v = X[line * FF_LS + pad(n)];
+                    y[m] = p ? cmul(v, ctw[p * FF_L + n]) : v;
+                }
+                fft_regs<FF_L, -1>(y, Ab + line * FF_LS, Ab + line * FF_LS, tw, tl);
+                // S[j] = sum of the products of outputs m = j and m = j + 12 (same target)
+                float2 S[4];
+#pragma unroll
+                for (int j = 0; j < 4; j++) S[j] = cadd(cmulc(av[j], y[j]), cmulc(av[j + 4], y[j + 12]));
+                __syncthreads();  // the next coset's FFT rewrites Ab (fft_regs contract)
+                if (pass == 0) {
+#pragma unroll
+                    for (int j = 0; j < 4; j++) acc[j][p] = cadd(acc[j][p], S[j]);
+                } else {
+                    const int src = (lane & 16) | (p == 0 ? ((16 - tl) & 15) : (15 - tl));
+                    float2 Rv[4];
+#pragma unroll
+                    for (int j = 0; j < 4; j++) {
+                        Rv[j].x = __shfl_sync(0xffffffffu, S[j].x, src);
+                        Rv[j].y = __shfl_sync(0xffffffffu, S[j].y, src);
+                    }
+                    if (p == 0) {
+#pragma unroll
+                        for (int j = 0; j < 4; j++) {
+                            const float2 v = tl == 0 ? Rv[(4 - j) & 3] : Rv[3 - j];
+                            acc[j][0] = cadd(acc[j][0], cconj(v));
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 4; j++) acc[3 - j][(4 - p) & 3] = cadd(acc[3 - j][(4 - p) & 3], cconj(Rv[j]));
+                    }
+                }
+            }
+        }
+    }
+
+    // ---- inverse x of the folded lines: F[t] (t = 4 tl + 64 j + p) -> X1[mx][k'y][k'z]
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 4; j++)
+#pragma unroll
+        for (int p = 0; p < FF_C; p++) X[line * FF_LS + pad(4 * tl + 64 * j + p)] = acc[j][p];
+    __syncthreads();
+    float2 v[E];
+#pragma unroll
+    for (int m = 0; m < E; m++) v[m] = X[line * FF_LS + pad(tl + FF_TPL * m)];
+    fft_regs<FF_NP, +1>(v, Ab + line * FF_LS, Ab + line * FF_LS, tw, tl);
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < E; m++) X[line * FF_LS + pad(tl + FF_TPL * m)] = v[m];
+    __syncthreads();
+    float2 *X1 = a.X1 + (long long)b * a.x1_bstride;
+    for (int e = threadIdx.x; e < FF_NL * a.N; e += FF_NT) {
+        const int i = e % FF_NL, q = e / FF_NL;
+        if (z0 + i < FF_FZ) X1[(q * FF_NP + kyp) * FF_FZ + z0 + i] = X[i * FF_LS + pad(q)];
+    }
+}
+
+bool fold_fast_supported(int L, int c, int G, int K, int Np, int complex_w)
+{
+    return L == FF_L && c == FF_C && G == FF_G && K == FF_K && Np == FF_NP && !complex_w;
+}
+
+void launch_fold_fast(const FoldFastArgs &a_in, int batch, cudaStream_t s)
+{
+    FoldFastArgs a = a_in;
+    a.nb = batch;
+    constexpr int ZT = (FF_FZ + FF_NL - 1) / FF_NL;
+    const size_t sm = sizeof(float2) * ((size_t)FF_L + FF_C * FF_L + 2 * FF_NL * FF_LS);
+    cudaFuncSetAttribute(fold_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    fold_fast_kernel<<<(unsigned)(FF_NP * ZT * batch), FF_NT, sm, s>>>(a);
+}

@@ -34,6 +34,30 @@ struct SpreadArgs {
     float inv_dprof;
 };
 
+// fused spreading + z transform of R B (spread_z.cu), real weights.  Cell units throughout:
+// ball (x, y, z, s) / hf in B's frame; the box origin o (cells); cut = footprint beyond s.
+struct SpreadZArgs {
+    int L, K, c, G;
+    float ox, oy, oz;
+    float cut;
+    int n_balls;
+    const float4 *balls;    // (x, y, z, s) / hf
+    const float *w;         // weights
+    const float2 *g02;      // per ball (g0, g2): g(s, d) ~ g0 + g2 d^2 for d < 0.1 cells (window profile)
+    const float *rot;       // [b][9]
+    const float4 *phi;      // [phi_n][2] cubic pieces of (Phi1, Phi2) on [-U, U]
+    int phi_n;
+    float phi_U, phi_invD;
+    float cx, cy, live_r2;  // support cylinder of R B (any R): centre (cells) and radius^2
+    const float2 *mult_z;   // [K + 1]
+    const float2 *tw;       // exp(-2 pi i m / L)
+    const float2 *ctw;      // [c][L]
+    float2 *out;            // T1 [b][L][L][K + 1]
+    long long out_bstride;  // float2 elements
+};
+bool spread_z_supported(int L);
+void launch_spread_z(const SpreadZArgs &a, int batch, cudaStream_t s);
+
 // ----------------------------------------------------------------- coset-major band order
 // Band |k| <= K of an axis plan (L, c, G): coset p holds q in [0, qp] (k = c q + p >= 0) and
 // [qn, L) (k = c q + p - G < 0), stored negative part first (ascending k).  Every coset
@@ -110,9 +134,30 @@ struct FoldXArgs {
     int MS;               // row stride of Ahat (cm_row_stride)
     const int *xtab;      // [c][L] per FFT output (p, q): segment position | fold target << 16, or -1
     const int2 *segs;     // [c] (segment offset, entries) of the coset-major rows
-    float2 *F;            // [b][Np][Np][Fz]
+    float2 *F;            // [b][Np][Np][Fz], or X1 [b][N][Np][Fz] when the inverse x pass is fused
     long long f_bstride;
+    int N;                // output rows of the fused inverse x pass
+    int fuse_inv;         // request the fused inverse x pass (taken when fold_fuses_inverse(L, Np))
+    const float2 *tw_inv; // exp(-2 pi i m / Np)
+    int nb;               // rotations in the launch (set by launch_fold_x)
 };
+
+// fold_fast.cu: fold_x with the inverse x pass for the plan shape L = Np = 256, c = 4,
+// G = 4 (K + 1), real weights (compile-time band and fold ownership)
+struct FoldFastArgs {
+    const float2 *tw, *ctw;  // exp(-2 pi i m / 256); coset twiddles [4][256]
+    const float2 *T2;        // [b][ix][ky][kz]
+    long long t2_bstride;
+    const float2 *Ahat;      // A'' rows (coset-major, stride MS)
+    int MS;
+    int pos_base[4];         // per coset: segment offset - first negative q
+    float2 *X1;              // [b][N][Np][Fz]
+    long long x1_bstride;
+    int N;
+    int nb;                  // set by launch_fold_fast
+};
+bool fold_fast_supported(int L, int c, int G, int K, int Np, int complex_w);
+void launch_fold_fast(const FoldFastArgs &a, int batch, cudaStream_t s);
 
 // contiguous inverse z pass + epilogue
 struct LastArgs {
@@ -134,9 +179,10 @@ bool fft_size_supported(int L);
 //       3 inverse strided (x, y of the inverse transform)
 void launch_pass(const PassArgs &a, int kind, int batch, cudaStream_t s);
 void launch_fold_x(const FoldXArgs &a, int batch, cudaStream_t s);
+bool fold_fuses_inverse(int L, int Np);
 void launch_last(const LastArgs &a, int batch, cudaStream_t s);
 void launch_permute_cm(const float2 *in, const float2 *mult, float2 *out, long long rows, int K, int L, int c, int G,
-                       int neg, int MS, int Kz, double band_radius, cudaStream_t s);
+                       int neg, int MS, int Kz, double band_radius, const float *dec, cudaStream_t s);
 void launch_keys_init(unsigned long long *keys, int n, cudaStream_t s);
 void launch_keys_finalize(const unsigned long long *keys, int batch, int out_kind, void *out, cudaStream_t s);
 

@@ -13,6 +13,8 @@
 // evaluated through c cosets k = c q + p of an L-point FFT of x_n exp(-2 pi i p n / G).
 // Lines live in registers (fft_ct.cuh); strided loads / stores are transposed through
 // shared memory so that global accesses stay coalesced.
+#include <algorithm>
+
 #include "kernels.cuh"
 #include "fft_ct.cuh"
 
@@ -148,7 +150,11 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-template <int L, bool CPLX, bool DIRECT>
+// Blocks are ordered rotation-fastest (blockIdx.x = target block * nb + rotation), so the
+// nb blocks that read the same A'' rows run together and share them through L2.
+// NP > 0: the inverse x-FFT (length NP, same threads per line as L) is fused: the block
+// transforms its accumulated k'x lines and writes X1[mx][k'y][k'z] (mx < N) instead of F.
+template <int L, int NP, bool CPLX, bool DIRECT>
 __global__ void __launch_bounds__(8 * Plan<L>::TPL, 512 / (8 * Plan<L>::TPL) > 0 ? 512 / (8 * Plan<L>::TPL) : 1) fold_x_kernel(FoldXArgs a)
 {
     constexpr int NL = 8;
@@ -169,10 +175,11 @@ __global__ void __launch_bounds__(8 * Plan<L>::TPL, 512 / (8 * Plan<L>::TPL) > 0
     int2 *segs = (int2 *)(tab + a.c * L);       // [c] (offset, entries)
     float2 *Pb = (float2 *)(segs + 8);          // [NL][M] (gather path only)
     const int line = threadIdx.x / TPL, tl = threadIdx.x % TPL;
-    const int b = blockIdx.y;
+    const int b = blockIdx.x % a.nb;
+    const int tb = blockIdx.x / a.nb;
     const int ztiles = (a.Fz + NL - 1) / NL;
-    const int kyp = blockIdx.x / ztiles;
-    const int z0 = (blockIdx.x % ztiles) * NL;
+    const int kyp = tb / ztiles;
+    const int z0 = (tb % ztiles) * NL;
     const float2 *T2 = a.T2 + (long long)b * a.t2_bstride;
 
     for (int m = threadIdx.x; m < L; m += NT) tw[m] = a.tw[m];
@@ -287,10 +294,35 @@ __global__ void __launch_bounds__(8 * Plan<L>::TPL, 512 / (8 * Plan<L>::TPL) > 0
         }
     }
     __syncthreads();
-    float2 *F = a.F + (long long)b * a.f_bstride;
-    for (int e = threadIdx.x; e < NL * Np; e += NT) {
-        const int i = e % NL, t = e / NL;
-        if (z0 + i < a.Fz) F[((long long)t * Np + kyp) * a.Fz + z0 + i] = acc[i * AS + t + (t >> 3)];
+    if constexpr (NP > 0) {
+        // inverse x: line i = k'z, F[k'x] -> X1[mx][k'y][k'z] for mx < N
+        static_assert(Plan<NP>::TPL == TPL && Plan<NP>::n == 2 && NP <= L, "fused inverse plan");
+        constexpr int EI = NP / TPL;
+        float2 v[EI];
+#pragma unroll
+        for (int m = 0; m < EI; m++) {
+            const int t = tl + TPL * m;
+            v[m] = acc[line * AS + t + (t >> 3)];
+        }
+        for (int m = threadIdx.x; m < NP; m += NT) tw[m] = a.tw_inv[m];
+        __syncthreads();
+        fft_regs<NP, +1>(v, A + line * LS, B + line * LS, tw, tl);
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < EI; m++) A[line * LS + pad(tl + TPL * m)] = v[m];
+        __syncthreads();
+        float2 *X1 = a.F + (long long)b * a.f_bstride;
+        const long long rs = (long long)Np * a.Fz;
+        for (int e = threadIdx.x; e < NL * a.N; e += NT) {
+            const int i = e % NL, q = e / NL;
+            if (z0 + i < a.Fz) X1[(long long)q * rs + (long long)kyp * a.Fz + z0 + i] = A[i * LS + pad(q)];
+        }
+    } else {
+        float2 *F = a.F + (long long)b * a.f_bstride;
+        for (int e = threadIdx.x; e < NL * Np; e += NT) {
+            const int i = e % NL, t = e / NL;
+            if (z0 + i < a.Fz) F[((long long)t * Np + kyp) * a.Fz + z0 + i] = acc[i * AS + t + (t >> 3)];
+        }
     }
 }
 
@@ -299,9 +331,10 @@ __global__ void __launch_bounds__(8 * Plan<L>::TPL, 512 / (8 * Plan<L>::TPL) > 0
 // of B's plan (s = -1 for complex weights, where the fold reads A'(-k) against RB's line).
 // B's x multipliers (natural order, index k + K) are folded in: real weights store
 // A'(k) conj(mult(k)) at cm(k); complex weights store A'(k) mult(-k) at cm(-k).
+// dec != nullptr: B's radial window deconvolution 1 / phi_hat(|k|) (indexed by |k|^2) is folded in.
 __global__ void permute_cm_kernel(const float2 *__restrict__ in, const float2 *__restrict__ mult,
                                   float2 *__restrict__ out, long long rows, int K, int L, int c, int G, int neg, int MS,
-                                  int Kz, double R2)
+                                  int Kz, double R2, const float *__restrict__ dec)
 {
     const int M = 2 * K + 1;
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -309,20 +342,20 @@ __global__ void permute_cm_kernel(const float2 *__restrict__ in, const float2 *_
     const long long row = e / M;
     const int k = (int)(e % M) - K;
     float2 v = neg ? cmul(in[e], mult[-k + K]) : cmulc(in[e], mult[k + K]);
-    if (R2 > 0) {  // spherical band: zero the modes with |k| > band_radius
-        const long long ky = row / Kz - K, kz = (row % Kz) - (Kz == M ? K : 0);
-        if ((double)(k * (long long)k + ky * ky + kz * kz) > R2) v = make_float2(0.f, 0.f);
-    }
+    const long long ky = row / Kz - K, kz = (row % Kz) - (Kz == M ? K : 0);
+    const long long k2 = k * (long long)k + ky * ky + kz * kz;
+    if (dec) v = cscale(v, dec[k2]);
+    if (R2 > 0 && (double)k2 > R2) v = make_float2(0.f, 0.f);  // spherical band: |k| <= band_radius
     out[row * MS + cm_of_k(neg ? -k : k, L, c, G, K)] = v;
 }
 
 void launch_permute_cm(const float2 *in, const float2 *mult, float2 *out, long long rows, int K, int L, int c, int G,
-                       int neg, int MS, int Kz, double band_radius, cudaStream_t s)
+                       int neg, int MS, int Kz, double band_radius, const float *dec, cudaStream_t s)
 {
     const long long n = rows * (2LL * K + 1);
     cudaMemsetAsync(out, 0, sizeof(float2) * rows * MS, s);
     permute_cm_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(in, mult, out, rows, K, L, c, G, neg, MS, Kz,
-                                                                 band_radius > 0 ? band_radius * band_radius : 0.0);
+                                                                 band_radius > 0 ? band_radius * band_radius : 0.0, dec);
 }
 
 // ============================================================================ last inverse pass + epilogue
@@ -336,6 +369,11 @@ __device__ __forceinline__ unsigned long long key_max(float v, unsigned idx)
     return ((unsigned long long)float_order_bits(v) << 32) | (0xffffffffu - idx);
 }
 
+// HERM (real weights, C2R): the lines are taken in pairs (l, l+1) and transformed as one
+// complex line Z = A + i B of their Hermitian-expanded spectra, so Re z = a and Im z = b
+// (the imaginary parts of the DC and Nyquist modes are dropped, as a C2R transform does).
+// The block walks tiles of NL units (line pairs, or single lines for C2C) grid-stride and
+// reduces its keys in registers / shared memory before one atomic per kind.
 template <int L, bool HERM>
 __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TPL * Plan<L>::NL)) last_kernel(LastArgs a)
 {
@@ -345,51 +383,81 @@ __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TP
     float2 *tw = sm;
     float2 *A = tw + L;
     float2 *B = A + NL * LS;
+    __shared__ unsigned long long red[2][NT / 32];
     const int line = threadIdx.x / TPL, tl = threadIdx.x % TPL;
     const int b = blockIdx.y;
     const long long lines = (long long)a.N * a.N;
-    const long long gline = (long long)blockIdx.x * NL + line;
-    const bool valid = gline < lines;
+    const long long units = HERM ? (lines + 1) / 2 : lines;
+    const long long ntiles = (units + NL - 1) / NL;
+    const bool reduce = a.out_kind != BC_OUT_F_FULL;
 
     for (int m = threadIdx.x; m < L; m += NT) tw[m] = a.tw[m];
-    const float2 *row = a.in + (long long)b * a.in_bstride + gline * a.Fz;
-    float2 x[E];
-#pragma unroll
-    for (int m = 0; m < E; m++) {
-        const int n = tl + TPL * m;
-        float2 v = make_float2(0.f, 0.f);
-        if (valid) {
-            if (!HERM || n < a.Fz)
-                v = row[n];
-            else
-                v = cconj(row[L - n]);
-        }
-        x[m] = v;
-    }
-    fft_regs<L, +1>(x, A + line * LS, B + line * LS, tw, tl);
-
     unsigned long long kmin = ~0ull, kmax = 0ull;
-    if (valid) {
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const long long u = tile * NL + line;
+        const bool valid = u < units;
+        const long long l0 = HERM ? 2 * u : u;
+        const bool has1 = HERM && valid && (l0 + 1 < lines);
+        const float2 *row = a.in + (long long)b * a.in_bstride + l0 * a.Fz;
+        float2 x[E];
 #pragma unroll
         for (int m = 0; m < E; m++) {
-            const int q = tl + TPL * m;
-            if (q >= a.N) continue;
-            const float2 v = cscale(x[m], a.scale);
-            const long long gidx = gline * a.N + q;
-            if (a.out_kind == BC_OUT_F_FULL) {
-                if (HERM)
-                    ((float *)a.out_full)[(long long)b * a.full_bstride + gidx] = v.x;
-                else
-                    ((float2 *)a.out_full)[(long long)b * a.full_bstride + gidx] = v;
-            } else {
-                const unsigned gi = (unsigned)gidx;
-                const unsigned long long k1 = key_min(v.x, gi), k2 = key_max(v.x, gi);
-                kmin = k1 < kmin ? k1 : kmin;
-                kmax = k2 > kmax ? k2 : kmax;
+            const int n = tl + TPL * m;
+            float2 v = make_float2(0.f, 0.f);
+            if (valid) {
+                if (!HERM) {
+                    v = row[n];
+                } else {
+                    const bool lo = n < a.Fz;
+                    const int src = lo ? n : L - n;
+                    float2 va = row[src];
+                    float2 vb = has1 ? row[a.Fz + src] : make_float2(0.f, 0.f);
+                    if (n == 0 || 2 * n == L) {
+                        va.y = 0.f;
+                        vb.y = 0.f;
+                    } else if (!lo) {
+                        va.y = -va.y;
+                        vb.y = -vb.y;
+                    }
+                    v = make_float2(va.x - vb.y, va.y + vb.x);  // A + i B
+                }
+            }
+            x[m] = v;
+        }
+        fft_regs<L, +1>(x, A + line * LS, B + line * LS, tw, tl);
+
+        if (valid) {
+#pragma unroll
+            for (int m = 0; m < E; m++) {
+                const int q = tl + TPL * m;
+                if (q >= a.N) continue;
+                const float2 v = cscale(x[m], a.scale);
+                const long long gidx = l0 * a.N + q;
+                if (!reduce) {
+                    if (HERM) {
+                        float *o = (float *)a.out_full + (long long)b * a.full_bstride + gidx;
+                        o[0] = v.x;
+                        if (has1) o[a.N] = v.y;
+                    } else {
+                        ((float2 *)a.out_full)[(long long)b * a.full_bstride + gidx] = v;
+                    }
+                } else {
+                    const unsigned gi = (unsigned)gidx;
+                    unsigned long long k1 = key_min(v.x, gi), k2 = key_max(v.x, gi);
+                    kmin = k1 < kmin ? k1 : kmin;
+                    kmax = k2 > kmax ? k2 : kmax;
+                    if (HERM && has1) {
+                        k1 = key_min(v.y, gi + (unsigned)a.N);
+                        k2 = key_max(v.y, gi + (unsigned)a.N);
+                        kmin = k1 < kmin ? k1 : kmin;
+                        kmax = k2 > kmax ? k2 : kmax;
+                    }
+                }
             }
         }
+        __syncthreads();  // the next tile's first FFT stage rewrites A
     }
-    if (a.out_kind != BC_OUT_F_FULL) {
+    if (reduce) {
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
             const unsigned long long o1 = __shfl_xor_sync(0xffffffffu, kmin, off);
@@ -398,6 +466,15 @@ __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TP
             kmax = o2 > kmax ? o2 : kmax;
         }
         if ((threadIdx.x & 31) == 0) {
+            red[0][threadIdx.x >> 5] = kmin;
+            red[1][threadIdx.x >> 5] = kmax;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < NT / 32; w++) {
+                kmin = red[0][w] < kmin ? red[0][w] : kmin;
+                kmax = red[1][w] > kmax ? red[1][w] : kmax;
+            }
             if (kmin != ~0ull) atomicMin(&a.keys[2 * b + 0], kmin);
             if (kmax != 0ull) atomicMax(&a.keys[2 * b + 1], kmax);
         }
@@ -461,31 +538,46 @@ void launch_pass(const PassArgs &a, int kind, int batch, cudaStream_t s)
     }
 }
 
-template <int L, bool CPLX, bool DIRECT>
+template <int L, int NP, bool CPLX, bool DIRECT>
 static void fold_launch(const FoldXArgs &a, dim3 grid, cudaStream_t s)
 {
     const size_t sm = sizeof(float2) * ((size_t)L + (Plan<L>::n >= 3 ? 2 : 1) * 8 * (size_t)line_stride(L) +
                                         8 * (size_t)(a.Np + (a.Np >> 3) + 1) + (size_t)a.c * L +
                                         16 * (size_t)cm_max_seg(L, a.c, a.G, a.K) + (DIRECT ? 0 : 8 * (size_t)a.M)) +
                       sizeof(int) * (size_t)a.c * L + sizeof(int2) * 8;
-    set_smem(fold_x_kernel<L, CPLX, DIRECT>, sm);
-    fold_x_kernel<L, CPLX, DIRECT><<<grid, 8 * Plan<L>::TPL, sm, s>>>(a);
+    set_smem(fold_x_kernel<L, NP, CPLX, DIRECT>, sm);
+    fold_x_kernel<L, NP, CPLX, DIRECT><<<grid, 8 * Plan<L>::TPL, sm, s>>>(a);
 }
 
-void launch_fold_x(const FoldXArgs &a, int batch, cudaStream_t s)
+bool fold_fuses_inverse(int L, int Np) { return L == 256 && Np == 256; }
+
+void launch_fold_x(const FoldXArgs &a_in, int batch, cudaStream_t s)
 {
+    FoldXArgs a = a_in;
+    a.nb = batch;
     const int ztiles = (a.Fz + 7) / 8;
-    dim3 grid((unsigned)(a.Np * ztiles), batch);
+    dim3 grid((unsigned)(a.Np * ztiles * batch), 1);
+    if (a.fuse_inv && fold_fuses_inverse(a.L, a.Np)) {
+        const bool direct = ((a.Np / gcd_int(a.c, a.Np)) % Plan<256>::TPL) == 0 && (a.G % a.Np) == 0;
+        if (a.complex_w) {
+            if (direct) fold_launch<256, 256, true, true>(a, grid, s);
+            else fold_launch<256, 256, true, false>(a, grid, s);
+        } else {
+            if (direct) fold_launch<256, 256, false, true>(a, grid, s);
+            else fold_launch<256, 256, false, false>(a, grid, s);
+        }
+        return;
+    }
     switch (a.L) {
 #define X(L_)                                                                                   \
     case L_: {                                                                                  \
         const bool direct = ((a.Np / gcd_int(a.c, a.Np)) % Plan<L_>::TPL) == 0 && (a.G % a.Np) == 0; \
         if (a.complex_w) {                                                                      \
-            if (direct) fold_launch<L_, true, true>(a, grid, s);                                \
-            else fold_launch<L_, true, false>(a, grid, s);                                      \
+            if (direct) fold_launch<L_, 0, true, true>(a, grid, s);                             \
+            else fold_launch<L_, 0, true, false>(a, grid, s);                                   \
         } else {                                                                                \
-            if (direct) fold_launch<L_, false, true>(a, grid, s);                               \
-            else fold_launch<L_, false, false>(a, grid, s);                                     \
+            if (direct) fold_launch<L_, 0, false, true>(a, grid, s);                            \
+            else fold_launch<L_, 0, false, false>(a, grid, s);                                  \
         }                                                                                       \
         break;                                                                                  \
     }
@@ -503,7 +595,10 @@ void launch_last(const LastArgs &a, int batch, cudaStream_t s)
         constexpr int NL = Plan<L_>::NL;                                                      \
         const size_t sm = fft_smem<L_>(0);                                                    \
         const long long lines = (long long)a.N * a.N;                                         \
-        dim3 grid((unsigned)((lines + NL - 1) / NL), batch);                                  \
+        const long long units = a.hermitian ? (lines + 1) / 2 : lines;                        \
+        const long long tiles = (units + NL - 1) / NL;                                        \
+        const long long cap = std::max(1LL, 4LL * 148 * 4 / std::max(batch, 1));             \
+        dim3 grid((unsigned)std::min(tiles, cap), batch);                                     \
         if (a.hermitian) {                                                                    \
             set_smem(last_kernel<L_, true>, sm);                                              \
             last_kernel<L_, true><<<grid, Plan<L_>::TPL * NL, sm, s>>>(a);                    \

@@ -3,6 +3,7 @@ declares, and validates parameters before touching a device (no compute calls)."
 import ctypes
 import os
 import re
+import subprocess
 
 import pytest
 
@@ -45,11 +46,19 @@ def test_status_strings(bc):
     assert bc.bc_status_string(99) == b"BC_UNKNOWN"
 
 
-def test_params_struct_layout(bc):
-    # matches the C struct: 4 + pad 4 + 8 + 24 + 4*6 + pad 4? -> check field offsets explicitly
+def test_params_struct_layout(bc, tmp_path):
+    """ctypes' bc_params agrees with the C compiler's layout of include/ballcorr.h."""
     P = bc.bc_params
-    assert P.h.offset == 8 and P.t0.offset == 16 and P.Np.offset == 40
-    assert P.spread_eps.offset == 64 and P.band_radius.offset == 72 and ctypes.sizeof(P) == 80
+    names = [f[0] for f in P._fields_]
+    src = tmp_path / "layout.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "ballcorr.h"\nint main(void){\n' +
+                   "".join(f'printf("%zu\\n", offsetof(bc_params, {n}));\n' for n in names) +
+                   'printf("%zu\\n", sizeof(bc_params));return 0;}\n')
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split()]
+    assert got[:-1] == [getattr(P, n).offset for n in names]
+    assert got[-1] == ctypes.sizeof(P)
 
 
 @pytest.mark.parametrize("kw", [

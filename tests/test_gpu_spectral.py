@@ -137,3 +137,26 @@ def test_single_ball_pair_vs_lens(bc, oracle_mod):
     for r in range(2):
         ref = oracle_mod.correlate_grid(A, None, B, None, R[r], N, h, t0)
         assert rel_max_err(f[r], ref) <= 5e-4  # band error 1.3e-4 at K=143 (oracle/bandlimited)
+
+
+@pytest.mark.parametrize("seed", [51, 52])
+def test_blob_fused_path_vs_bandlimited(bc, oracle_mod, seed):
+    """Real weights on a box size the fused spread + z kernel supports (L_B = 128 here): B is
+    smoothed with the KB blob window, deconvolved radially inside A's band spectrum."""
+    w = random_small_case(seed, n_a=11, n_b=9, n_rot=2, N=16)
+    Np, K = 32, 63
+    P = Np * w.h
+    c = spectral(bc, w, Np, K)
+    assert c.query("blob_B") == 1 and c.query("fused_spread_z") == 1 and c.query("L_B") == 128
+    f = c.correlate_rotations(w.R, "full")
+    mm = c.correlate_rotations(w.R, "minmax")
+    for r in range(w.n_rot):
+        ref = oracle_mod.bandlimited_correlation(w.A_xyzr, w.A_w, w.B_xyzr, w.B_w, w.R[r], w.N, w.h, w.t0, P, K)
+        assert rel_max_err(f[r], ref) <= IMPL_TOL, (r, rel_max_err(f[r], ref))
+        check_extremum(mm[r, 0]["val"], mm[r, 0]["idx"], ref, "min", 2 * IMPL_TOL * np.abs(ref).max())
+        check_extremum(mm[r, 1]["val"], mm[r, 1]["idx"], ref, "max", 2 * IMPL_TOL * np.abs(ref).max())
+    # the generic (Gaussian window, unfused) plan of the same problem agrees
+    g = spectral(bc, w, Np, K, generic_only=True)
+    assert g.query("blob_B") == 0
+    fg = g.correlate_rotations(w.R, "full")
+    assert rel_max_err(f, fg) <= IMPL_TOL

@@ -111,3 +111,24 @@ def test_docking_sampled(bc, oracle_mod):
         # best real score: the GPU argmax has an oracle score within tolerance of the GPU max
         k = int(np.searchsorted(idx, int(best[j]["idx"])))
         assert abs(ref[k].real - best[j]["val"]) <= TOL_F32 * np.abs(ref).max()
+
+
+def test_sweep_fused_matches_generic(bc):
+    """The fused kernels the sweep plan takes (spread + z transform, fold + inverse x) give
+    the generic passes' result up to fp32 rounding order (both paths are checked against
+    the oracle elsewhere: generic on the band-limited cases, fused on the sampled sweep)."""
+    w = make_config("sweep", n_rot=512)
+    fused = correlator(bc, w)
+    assert fused.query("fused_spread_z") == 1 and fused.query("fold_fast") == 1
+    generic = correlator(bc, w, generic_only=True)
+    assert generic.query("fused_spread_z") == 0 and generic.query("fold_fast") == 0
+    rots = w.R[[3, 200]]
+    a = fused.correlate_rotations(rots, "full")
+    b = generic.correlate_rotations(rots, "full")
+    for r in range(len(rots)):
+        assert rel_max_err(a[r], b[r]) <= 2e-5, rel_max_err(a[r], b[r])
+    ma = fused.correlate_rotations(rots, "minmax")
+    for r in range(len(rots)):
+        assert ma[r, 0]["val"] == pytest.approx(float(a[r].min()), abs=1e-12)
+        assert ma[r, 1]["val"] == pytest.approx(float(a[r].max()), abs=1e-12)
+        assert a[r].reshape(-1)[ma[r, 1]["idx"]] == ma[r, 1]["val"]
