@@ -121,6 +121,7 @@ def stage_bytes(q, N, Np, K, complex_w):
         "spread_z_B": T1,             # fused spread + z transform: write T1 (the box stays on chip)
         "fold_x_inv": T2 + Bh + X1,   # fused fold + inverse x: read T2 and A's band, write X1
         "fold_fast": T2 + Bh + X1,    # same, compile-time plan of the sweep's shape
+        "pass_y_fast": T1 + T2,       # read T1, write T2 (compile-time plan)
         "spread_B": box,              # write the smoothed density box of R B
         "pass_z_B": box + T1,         # read box, write T1
         "pass_y_B": T1 + T2,          # read T1, write T2

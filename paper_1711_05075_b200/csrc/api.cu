@@ -772,7 +772,22 @@ bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, voi
         launch_pass(a, 0, nb, s);
         ctx->launches++;
     }
-    {
+    if (which == 1 && use_spread_z(ctx) && pass_y_fast_supported(L, pl.c, pl.G, ctx->K, cplx)) {
+        PassYFastArgs a{};
+        a.tw = tw;
+        a.ctw = pl.d_ctw;
+        a.mult = pl.d_mult[1];
+        a.T1 = (const float2 *)ws2;
+        a.t1_bstride = (long long)(s2_per / 8);
+        a.T2 = (float2 *)ws1;
+        a.t2_bstride = (long long)(s1_per / 8);
+        a.cx = (float)(-pl.o[0]);
+        a.cy = (float)(-pl.o[1]);
+        a.live_r2 = (float)(ctx->live_r * ctx->live_r);
+        StageScope sc(ctx, s, "pass_y_fast");
+        launch_pass_y_fast(a, nb, s);
+        ctx->launches++;
+    } else {
         PassArgs a = base;
         a.klo = -ctx->K;
         a.nk = ctx->M;

@@ -177,3 +177,96 @@ void launch_fold_fast(const FoldFastArgs &a_in, int batch, cudaStream_t s)
     cudaFuncSetAttribute(fold_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     fold_fast_kernel<<<(unsigned)(FF_NP * ZT * batch), FF_NT, sm, s>>>(a);
 }
+
+// ============================================================================ forward y pass
+// T1[ix][iy][kz] -> T2[ix][ky][kz] = mult_y(ky) sum_iy T1 exp(-2 pi i ky iy / G), |ky| <= K,
+// for the same plan shape (the generic pass_kernel<256, -1, 2, 1> computes the same).
+// Block = one ix, 8 consecutive kz.  Rows iy outside B's support cylinder at this ix are
+// zero (spread_z writes them so) and are not loaded.  Per coset only the 128 in-band
+// outputs (q < 64 or q >= 192) are staged and stored.
+__global__ void __launch_bounds__(FF_NT, 5) pass_y_fast_kernel(PassYFastArgs a)
+{
+    constexpr int E = FF_L / FF_TPL;
+    extern __shared__ float2 smf[];
+    float2 *tw = smf;
+    float2 *X = tw + FF_L;
+    float2 *Ab = X + FF_NL * FF_LS;
+    const float2 *__restrict__ ctw = a.ctw;  // through L1 (keeps shared memory to 5 blocks / SM)
+    const int line = threadIdx.x / FF_TPL, tl = threadIdx.x % FF_TPL;
+    const int b = blockIdx.y;
+    constexpr int ZT = FF_KZ / FF_NL;
+    const int ix = blockIdx.x / ZT;
+    const int kz0 = (blockIdx.x % ZT) * FF_NL;
+    const float2 *T1 = a.T1 + (long long)b * a.t1_bstride + (long long)ix * FF_L * FF_KZ;
+    float2 *T2 = a.T2 + (long long)b * a.t2_bstride + (long long)ix * FF_M * FF_KZ;
+
+    // live rows at this ix: |(ix, iy) - (cx, cy)| <= r
+    const float dxl = (float)ix - a.cx;
+    const float h2 = a.live_r2 - dxl * dxl;
+    int ylo = 0, yhi = -1;
+    if (h2 > 0.f) {
+        const float hh = sqrtf(h2);
+        ylo = max(0, (int)floorf(a.cy - hh));
+        yhi = min(FF_L - 1, (int)ceilf(a.cy + hh));
+    }
+    for (int e = threadIdx.x; e < FF_L; e += FF_NT) tw[e] = a.tw[e];
+    {
+        float2 x[E];
+#pragma unroll
+        for (int m = 0; m < E; m++) {
+            const int e = threadIdx.x + FF_NT * m;
+            const int n = e / FF_NL, i = e % FF_NL;
+            x[m] = (n >= ylo && n <= yhi) ? T1[n * FF_KZ + kz0 + i] : make_float2(0.f, 0.f);
+        }
+#pragma unroll
+        for (int m = 0; m < E; m++) {
+            const int e = threadIdx.x + FF_NT * m;
+            X[(e % FF_NL) * FF_LS + pad(e / FF_NL)] = x[m];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int p = 0; p < FF_C; p++) {
+        float2 y[E];
+#pragma unroll
+        for (int m = 0; m < E; m++) {
+            const int n = tl + FF_TPL * m;
+            const float2 v = X[line * FF_LS + pad(n)];
+            y[m] = p ? cmul(v, __ldg(ctw + p * FF_L + n)) : v;
+        }
+        fft_regs<FF_L, -1>(y, Ab + line * FF_LS, Ab + line * FF_LS, tw, tl);
+        __syncthreads();
+        // in-band outputs u = q (q < 64) or q - 128 (q >= 192), times mult_y(ky)
+#pragma unroll
+        for (int uu = 0; uu < 8; uu++) {
+            const int m = uu < 4 ? uu : uu + 8;
+            const int q = tl + FF_TPL * m;
+            const int ky = FF_C * q + p - (m >= 12 ? FF_G : 0);
+            const int u = m < 4 ? q : q - 128;
+            const float2 mu = (ky >= -FF_K) ? __ldg(a.mult + ky + FF_K) : make_float2(0.f, 0.f);
+            Ab[line * FF_LS + u] = cmul(y[m], mu);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+            const int e = threadIdx.x + FF_NT * r;
+            const int u = e / FF_NL, i = e % FF_NL;
+            const int q = u < 64 ? u : u + 128;
+            const int ky = FF_C * q + p - (q >= 192 ? FF_G : 0);
+            if (ky >= -FF_K) T2[(ky + FF_K) * FF_KZ + kz0 + i] = Ab[i * FF_LS + u];
+        }
+        __syncthreads();
+    }
+}
+
+bool pass_y_fast_supported(int L, int c, int G, int K, int complex_w)
+{
+    return L == FF_L && c == FF_C && G == FF_G && K == FF_K && !complex_w;
+}
+
+void launch_pass_y_fast(const PassYFastArgs &a, int batch, cudaStream_t s)
+{
+    const size_t sm = sizeof(float2) * ((size_t)FF_L + 2 * FF_NL * FF_LS);
+    cudaFuncSetAttribute(pass_y_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    pass_y_fast_kernel<<<dim3((unsigned)(FF_L * (FF_KZ / FF_NL)), batch), FF_NT, sm, s>>>(a);
+}

@@ -157,6 +157,18 @@ struct FoldFastArgs {
     int nb;                  // set by launch_fold_fast
 };
 bool fold_fast_supported(int L, int c, int G, int K, int Np, int complex_w);
+
+// fold_fast.cu: forward y pass of R B for the same plan shape (live-row input skipping)
+struct PassYFastArgs {
+    const float2 *tw, *ctw, *mult;  // twiddles, coset twiddles [4][256], mult_y [2K + 1]
+    const float2 *T1;               // [b][L][L][K + 1]
+    long long t1_bstride;
+    float2 *T2;                     // [b][L][2K + 1][K + 1]
+    long long t2_bstride;
+    float cx, cy, live_r2;          // B's support cylinder (cells)
+};
+bool pass_y_fast_supported(int L, int c, int G, int K, int complex_w);
+void launch_pass_y_fast(const PassYFastArgs &a, int batch, cudaStream_t s);
 void launch_fold_fast(const FoldFastArgs &a, int batch, cudaStream_t s);
 
 // contiguous inverse z pass + epilogue

@@ -48,10 +48,12 @@ __device__ __forceinline__ PhiVal phi_lookup(const float4 *__restrict__ tab, flo
 
 }  // namespace
 
+// FFT phase: NG = 128 / TPL thread groups (the other half of the block idles) keep the
+// exchange buffer small enough for 3 blocks / SM.
 template <int L>
-__global__ void __launch_bounds__(256, 2) spread_z_kernel(SpreadZArgs a)
+__global__ void __launch_bounds__(256, 3) spread_z_kernel(SpreadZArgs a)
 {
-    constexpr int TPL = Plan<L>::TPL, E = L / TPL, NG = 256 / TPL;
+    constexpr int TPL = Plan<L>::TPL, E = L / TPL, NG = 128 / TPL;
     constexpr int LS = line_stride(L);
     static_assert(256 % TPL == 0 && Plan<L>::n == 2, "spread_z plan");
     extern __shared__ float4 smz[];
@@ -60,8 +62,10 @@ __global__ void __launch_bounds__(256, 2) spread_z_kernel(SpreadZArgs a)
     float4 *phi = smz;
     float2 *tw = (float2 *)(phi + 2 * a.phi_n);
     float2 *Abuf = tw + L;
-    float *acc = (float *)(Abuf + NG * LS);           // [16][L]
-    float4 *sb = (float4 *)(acc + SZ_COLS * L);       // [LCAP] (ux, uy, uz, rc^2)
+    constexpr int CS = L + 16;                        // column stride: the two half-warps of a warp
+                                                      // (adjacent columns) sit 16 banks apart
+    float *acc = (float *)(Abuf + NG * LS);           // [16][CS]
+    float4 *sb = (float4 *)(acc + SZ_COLS * CS);      // [LCAP] (ux, uy, uz, rc^2)
     float4 *sw = sb + SZ_LCAP;                        // [LCAP] (s, w, g0, g2)
     float2 *zb = (float2 *)acc;                       // [8][M] (after the spread)
     __shared__ int wcount[8];
@@ -87,7 +91,7 @@ __global__ void __launch_bounds__(256, 2) spread_z_kernel(SpreadZArgs a)
 
     for (int e = threadIdx.x; e < 2 * a.phi_n; e += 256) phi[e] = a.phi[e];
     for (int e = threadIdx.x; e < L; e += 256) tw[e] = a.tw[e];
-    for (int e = threadIdx.x; e < SZ_COLS * L; e += 256) acc[e] = 0.f;
+    for (int e = threadIdx.x; e < SZ_COLS * CS; e += 256) acc[e] = 0.f;
 
     float R[9];
 #pragma unroll
@@ -97,7 +101,8 @@ __global__ void __launch_bounds__(256, 2) spread_z_kernel(SpreadZArgs a)
     const int h = lane >> 4, hl = lane & 15;
     const int col = 2 * wid + h;
     const float fx = (float)(X0 + (col >> 2)), fy = (float)(Y0 + (col & 3));
-    float *accc = acc + col * L;
+    float *accc = acc + col * CS;
+    const float fyw = (float)(Y0 + ((2 * wid) & 3));  // the warp's columns: (fx, fyw) and (fx, fyw + 1)
     const float fX0 = (float)X0, fY0 = (float)Y0;
     const float U = a.phi_U, invD = a.phi_invD;
     const float tmax = (float)a.phi_n - 1e-3f;
@@ -152,7 +157,19 @@ __global__ void __launch_bounds__(256, 2) spread_z_kernel(SpreadZArgs a)
         // distinct cells, steps and balls are sequential, so the sums are race-free and in
         // list order (deterministic).
         const int total = list_n;
-        for (int e = 0; e < total; e++) {
+        for (int base0 = 0; base0 < total; base0 += 32) {
+            // the candidates that reach one of this warp's two columns (ballot, list order kept)
+            bool rel = false;
+            if (base0 + lane < total) {
+                const float4 uc = sb[base0 + lane];
+                const float ddx = fx - uc.x;
+                const float ddy = fmaxf(fmaxf(fyw - uc.y, uc.y - (fyw + 1.f)), 0.f);
+                rel = fmaf(ddx, ddx, ddy * ddy) < uc.w;
+            }
+            unsigned msk = __ballot_sync(0xffffffffu, rel);
+        while (msk) {
+            const int e = base0 + __ffs(msk) - 1;
+            msk &= msk - 1;
             const float4 ue = sb[e];
             const float dx = fx - ue.x, dy = fy - ue.y;
             const float dxy2 = fmaf(dx, dx, dy * dy);
@@ -187,6 +204,7 @@ __global__ void __launch_bounds__(256, 2) spread_z_kernel(SpreadZArgs a)
                 }
             }
         }
+        }
         __syncthreads();
         if (threadIdx.x == 0) list_n = 0;
         __syncthreads();
@@ -194,23 +212,30 @@ __global__ void __launch_bounds__(256, 2) spread_z_kernel(SpreadZArgs a)
 
     // ---- z transform: line l = columns (2l, 2l+1); group g handles line g % 8, cosets g/8 + (NG/8) r
     const int g = threadIdx.x / TPL, tl = threadIdx.x % TPL;
+    const bool fft_thread = g < NG;
     const int line = g % SZ_LINES;
     float2 x[E];
 #pragma unroll
     for (int m = 0; m < E; m++) {
         const int n = tl + TPL * m;
-        x[m] = make_float2(acc[(2 * line) * L + n], acc[(2 * line + 1) * L + n]);
+        x[m] = fft_thread ? make_float2(acc[(2 * line) * CS + n], acc[(2 * line + 1) * CS + n]) : make_float2(0.f, 0.f);
     }
     __syncthreads();  // acc / lists dead: zb may overwrite them
     const int c = a.c, G = a.G;
     const int rounds = (SZ_LINES * c + NG - 1) / NG;
     for (int r = 0; r < rounds; r++) {
         const int p = g / SZ_LINES + (NG / SZ_LINES) * r;
-        const bool active = p < c;
+        const bool active = fft_thread && p < c;
         float2 y[E];
 #pragma unroll
         for (int m = 0; m < E; m++) y[m] = (active && p) ? cmul(x[m], a.ctw[p * L + tl + TPL * m]) : x[m];
-        fft_regs<L, -1>(y, Abuf + g * LS, Abuf + g * LS, tw, tl);
+        float2 *ab = Abuf + (fft_thread ? g : g - NG) * LS;  // idle groups shadow the active ones' buffers
+        if (fft_thread) {
+            fft_regs<L, -1>(y, ab, ab, tw, tl);
+        } else {
+            // keep the block-wide barriers of fft_regs (stage 0 -> last stage) in step
+            __syncthreads();
+        }
         if (active) {
 #pragma unroll
             for (int m = 0; m < E; m++) {
@@ -239,10 +264,11 @@ bool spread_z_supported(int L) { return L == 128 || L == 256; }
 template <int L>
 static void spread_z_launch(const SpreadZArgs &a, int batch, cudaStream_t s)
 {
-    constexpr int NG = 256 / Plan<L>::TPL;
+    constexpr int NG = 128 / Plan<L>::TPL;
     const int tpa = L / 4;
-    const size_t region = std::max((size_t)SZ_COLS * L * 4 + (size_t)SZ_LCAP * 32, (size_t)SZ_LINES * (2 * a.K + 1) * 8);
+    const size_t region = std::max((size_t)SZ_COLS * (L + 16) * 4 + (size_t)SZ_LCAP * 32, (size_t)SZ_LINES * (2 * a.K + 1) * 8);
     const size_t sm = (size_t)a.phi_n * 32 + (size_t)L * 8 + (size_t)NG * line_stride(L) * 8 + region;
+    static_assert(NG == 128 / Plan<L>::TPL, "spread_z FFT groups");
     cudaFuncSetAttribute(spread_z_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     spread_z_kernel<L><<<dim3(tpa * tpa, batch), 256, sm, s>>>(a);
 }
