@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -103,13 +104,17 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- algorithmic bytes
 
-def stage_bytes(q, N, Np, K, complex_w):
-    """Compulsory bytes per rotation of each kernel of the spectral path:
-    its input read once plus its output written once."""
+def stage_work(q, N, Np, K, complex_w):
+    """Algorithmic work per rotation of each kernel of the spectral path:
+    compulsory bytes (input read once + output written once) and FP32 flops
+    (5 n log2 n per complex n-point FFT, 6 per complex multiply, 2 per complex add,
+    30 per window-profile evaluation of a spread cell)."""
     M = 2 * K + 1
     Kz = M if complex_w else K + 1
     Fz = Np if complex_w else Np // 2 + 1
-    L = int(q("L_B"))
+    L, c = int(q("L_B")), int(q("c_B"))
+    lg = math.log2
+    fft = lambda n: 5.0 * n * lg(n)
     box = L ** 3 * (8 if complex_w else 4)
     T1 = L * L * Kz * 8
     T2 = L * M * Kz * 8
@@ -117,19 +122,29 @@ def stage_bytes(q, N, Np, K, complex_w):
     F = Np * Np * Fz * 8
     X1 = N * Np * Fz * 8
     Y1 = N * N * Fz * 8
+    axis = lambda lines: lines * c * (fft(L) + 6 * L)       # c coset transforms + coset twiddles
+    tiles = q("live_tiles_B")
+    spread_z_flops = 30 * q("spread_cells_B") + tiles * 8 * axis(1) + tiles * 16 * Kz * 8
+    fold_flops = axis(M * Kz) + 8.0 * M * M * Kz + Np * Fz * fft(Np)
     return {
-        "spread_z_B": T1,             # fused spread + z transform: write T1 (the box stays on chip)
-        "fold_x_inv": T2 + Bh + X1,   # fused fold + inverse x: read T2 and A's band, write X1
-        "fold_fast": T2 + Bh + X1,    # same, compile-time plan of the sweep's shape
-        "pass_y_fast": T1 + T2,       # read T1, write T2 (compile-time plan)
-        "spread_B": box,              # write the smoothed density box of R B
-        "pass_z_B": box + T1,         # read box, write T1
-        "pass_y_B": T1 + T2,          # read T1, write T2
-        "fold_x": T2 + Bh + F,        # read T2 and A's band spectrum, write the folded product F
-        "inv_x": F + X1,
-        "inv_y": X1 + Y1,
-        "inv_z_reduce": Y1,           # read Y1, write 16 B of keys
+        "spread_z_B": (T1, spread_z_flops),            # fused spread + z transform: write T1
+        "pass_y_fast": (T1 + T2, axis(L * Kz) + 6.0 * L * M * Kz),
+        "fold_fast": (T2 + Bh + X1, fold_flops),       # read T2 and A's band, write X1
+        "fold_x_inv": (T2 + Bh + X1, fold_flops),
+        "spread_B": (box, 30 * q("spread_cells_B")),
+        "pass_z_B": (box + T1, axis(L * L)),
+        "pass_y_B": (T1 + T2, axis(L * Kz) + 6.0 * L * M * Kz),
+        "fold_x": (T2 + Bh + F, axis(M * Kz) + 8.0 * M * M * Kz),
+        "inv_x": (F + X1, Np * Fz * fft(Np)),
+        "inv_y": (X1 + Y1, N * Fz * fft(Np)),
+        "inv_z_reduce": (Y1, (N * N / 2) * fft(Np) + N ** 3),
     }
+
+
+def alu_peak_tflops():
+    """FP32 peak from the unit counts of B200_PROFILING.md: 148 SMs x 128 FP32 lanes x
+    2 flop (FFMA) x 1.965 GHz (clocks.max.sm)."""
+    return 148 * 128 * 2 * 1.965e9 / 1e12
 
 
 def measured_peaks():
@@ -275,22 +290,40 @@ def run_ours(args, rank, world, local_rank):
 
     if rank != 0:
         return
-    # roofline of the dominant kernel (largest share of device time in the timed region)
+    # roofline of the dominant kernel (largest share of device time in the timed region):
+    # HBM-bound if its algorithmic flop/byte is below the FP32 ridge, else ALU-bound
     q = ctx.query
-    sb = stage_bytes(q, w.N, kw["Np"], kw["K"], w.weights == "complex")
+    work = stage_work(q, w.N, kw["Np"], kw["K"], w.weights == "complex")
     peak, peak_kind = measured_peaks()
-    dom = max(stages.items(), key=lambda kv: kv[1][0]) if stages else None
-    roof = None
-    if dom is not None and dom[0] in sb:
-        name, (tot_ms, nl) = dom
-        batch = int(q("batch"))
-        per_launch_bytes = sb[name] * batch
+    alu_peak = alu_peak_tflops()
+    ridge = alu_peak * 1e12 / (peak * 1e9)
+    batch = int(q("batch"))
+    per_stage = {}
+    for name, (tot_ms, nl) in stages.items():
+        if name not in work:
+            continue
+        by, fl = work[name]
         avg_s = tot_ms / nl / 1e3
-        achieved = per_launch_bytes / avg_s / 1e9
-        roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
-                "alg_bytes_per_launch": per_launch_bytes, "avg_launch_ms": avg_s * 1e3,
-                "share_of_step": tot_ms / ms}
+        per_stage[name] = {"ms_per_rot": tot_ms / (args.steps * n_rot), "share": tot_ms / ms,
+                           "hbm_GBps": by * batch / avg_s / 1e9, "hbm_frac": by * batch / avg_s / 1e9 / peak,
+                           "fp32_TFLOPs": fl * batch / avg_s / 1e12, "alu_frac": fl * batch / avg_s / 1e12 / alu_peak,
+                           "flop_per_byte": fl / by}
+    roof = None
+    if per_stage:
+        name = max(per_stage, key=lambda k: per_stage[k]["share"])
+        st = per_stage[name]
+        tot_ms, nl = stages[name]
+        by, fl = work[name]
+        alu = fl / by > ridge
+        roof = {"bound": "alu" if alu else "hbm", "kernel": name,
+                "achieved": st["fp32_TFLOPs"] if alu else st["hbm_GBps"],
+                "peak": alu_peak if alu else peak, "unit": "TFLOP/s" if alu else "GB/s",
+                "frac": st["alu_frac"] if alu else st["hbm_frac"], "traffic": None,
+                "peak_source": ("derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz" if alu else peak_kind),
+                "alg_bytes_per_launch": by * batch, "alg_flops_per_launch": fl * batch,
+                "avg_launch_ms": tot_ms / nl, "share_of_step": st["share"],
+                "hbm_view": {"achieved_GBps": st["hbm_GBps"], "peak_GBps": peak, "frac": st["hbm_frac"]},
+                "ridge_flop_per_byte": ridge}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_oracle_sample(w, R[0], args.cpu_slabs)
@@ -310,6 +343,7 @@ def run_ours(args, rank, world, local_rank):
         "roofline": roof,
         "cpu_baseline": cpu,
         "stages_ms_per_step": {k: v[0] / args.steps for k, v in stages.items()},
+        "stages": per_stage,
         "result_sample": {"rot0_min": float(res[0]["val"]), "rot0_argmin": int(res[0]["idx"]),
                           "global_best": best},
     }

@@ -146,8 +146,11 @@ const char *bc_status_string(int status);
 
 /*
  * Introspection (tests / bench): named double-valued properties of the plan.
- * Keys: "P", "tau_A", "tau_B", "G_A", "G_B", "L_A", "L_B", "c_A", "c_B",
- * "cut_A", "cut_B", "band_modes", "batch", "bytes_workspace".
+ * Keys: "P", "K", "Np", "tau_A", "tau_B", "G_A", "G_B", "L_A", "L_B", "c_A", "c_B",
+ * "cut_A", "cut_B", "band_modes", "batch", "bytes_workspace", "blob_B" (B smoothed with the
+ * KB blob window), "fused_spread_z", "fused_fold_inv", "fold_fast" (which fused kernels the
+ * plan takes), "spread_cells_B" (sum of B's footprint volumes in fine cells), "live_tiles_B".
+ * Unknown keys: BC_EINVAL.
  */
 bc_status bc_query(const bc_ctx *ctx, const char *key, double *value);
 

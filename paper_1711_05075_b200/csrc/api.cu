@@ -79,6 +79,8 @@ struct bc_ctx {
     int phi_n = 0;
     double phi_U = 0, phi_D = 0;
     double live_r = 0;
+    double spread_cells_B = 0;     // sum_j (4/3) pi (s_j / hf + W)^3: window-smoothed footprint cells of B
+    int64_t live_tiles_B = 0;      // 4x4 column tiles of B's box inside its support cylinder
     float2 *d_Ahat = nullptr;      // A' = A_hat * origin phase, [ky][kz][kx] natural order
     float2 *d_Ahat_cm = nullptr;   // same, x axis in the coset-major order of B's plan
     bool cm_ready = false;
@@ -1043,7 +1045,21 @@ bc_status bc_shape_upload(bc_ctx *ctx, int which, const double *xyzr, const doub
         if (which == 0) TRY(build_csr_A(ctx));
         if (which == 1 && !ctx->plan[1].blob) TRY(build_profiles_B(ctx));
         if (which == 1) {
-            ctx->live_r = (rho + rmax + ctx->plan[1].cut) / ctx->plan[1].hf + 2.0;
+            const ShapePlan &pb = ctx->plan[1];
+            ctx->live_r = (rho + rmax + pb.cut) / pb.hf + 2.0;
+            ctx->spread_cells_B = 0;
+            for (int64_t j = 0; j < n; j++) {
+                const double rc = (ctx->hxyzr[1][4 * j + 3] + pb.cut) / pb.hf;
+                ctx->spread_cells_B += 4.0 / 3.0 * kPi * rc * rc * rc;
+            }
+            ctx->live_tiles_B = 0;  // same test as spread_z_kernel's zero-tile exit
+            for (int X0 = 0; X0 < pb.L; X0 += 4)
+                for (int Y0 = 0; Y0 < pb.L; Y0 += 4) {
+                    const double cx = -pb.o[0], cy = -pb.o[1];
+                    const double dx = std::max(std::max(X0 - cx, cx - (X0 + 3)), 0.0);
+                    const double dy = std::max(std::max(Y0 - cy, cy - (Y0 + 3)), 0.0);
+                    if (dx * dx + dy * dy <= ctx->live_r * ctx->live_r) ctx->live_tiles_B++;
+                }
             if (ctx->plan[1].blob) TRY(build_spread_z_tables(ctx));
         }
     }
@@ -1380,6 +1396,10 @@ bc_status bc_query(const bc_ctx *ctx, const char *key, double *value)
     else if (k == "bytes_workspace") *value = (double)(ctx->ws1_bytes + ctx->ws2_bytes);
     else if (k == "fused_spread_z") *value = use_spread_z(ctx) ? 1 : 0;
     else if (k == "blob_B") *value = B.blob ? 1 : 0;
+    else if (k == "spread_cells_B") *value = ctx->spread_cells_B;
+    else if (k == "live_tiles_B") *value = (double)ctx->live_tiles_B;
+    else if (k == "K") *value = ctx->K;
+    else if (k == "Np") *value = ctx->p.Np;
     else if (k == "fused_fold_inv") *value = (!ctx->p.generic_only && fold_fuses_inverse(B.L, ctx->p.Np)) ? 1 : 0;
     else if (k == "fold_fast")
         *value = (!ctx->p.generic_only && fold_fast_supported(B.L, B.c, B.G, ctx->K, ctx->p.Np,

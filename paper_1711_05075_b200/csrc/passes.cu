@@ -392,7 +392,11 @@ __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TP
     const bool reduce = a.out_kind != BC_OUT_F_FULL;
 
     for (int m = threadIdx.x; m < L; m += NT) tw[m] = a.tw[m];
-    unsigned long long kmin = ~0ull, kmax = 0ull;
+    // running extrema of this thread: values in fp32 with their linear index; a thread visits
+    // its outputs in increasing index order, so strict comparisons keep the lowest index on
+    // ties, as the 64-bit keys (built once at the end) do across threads
+    float vmin = INFINITY, vmax = -INFINITY;
+    unsigned imin = 0xffffffffu, imax = 0xffffffffu;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const long long u = tile * NL + line;
         const bool valid = u < units;
@@ -443,20 +447,26 @@ __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TP
                     }
                 } else {
                     const unsigned gi = (unsigned)gidx;
-                    unsigned long long k1 = key_min(v.x, gi), k2 = key_max(v.x, gi);
-                    kmin = k1 < kmin ? k1 : kmin;
-                    kmax = k2 > kmax ? k2 : kmax;
-                    if (HERM && has1) {
-                        k1 = key_min(v.y, gi + (unsigned)a.N);
-                        k2 = key_max(v.y, gi + (unsigned)a.N);
-                        kmin = k1 < kmin ? k1 : kmin;
-                        kmax = k2 > kmax ? k2 : kmax;
-                    }
+                    if (v.x < vmin) { vmin = v.x; imin = gi; }
+                    if (v.x > vmax) { vmax = v.x; imax = gi; }
+                }
+            }
+            if (HERM && has1 && reduce) {  // line l0 + 1: indices above all of line l0's
+#pragma unroll
+                for (int m = 0; m < E; m++) {
+                    const int q = tl + TPL * m;
+                    if (q >= a.N) continue;
+                    const float vy = x[m].y * a.scale;
+                    const unsigned gi = (unsigned)((l0 + 1) * a.N + q);
+                    if (vy < vmin) { vmin = vy; imin = gi; }
+                    if (vy > vmax) { vmax = vy; imax = gi; }
                 }
             }
         }
         __syncthreads();  // the next tile's first FFT stage rewrites A
     }
+    unsigned long long kmin = imin != 0xffffffffu ? key_min(vmin, imin) : ~0ull;
+    unsigned long long kmax = imax != 0xffffffffu ? key_max(vmax, imax) : 0ull;
     if (reduce) {
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
