@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -74,6 +75,11 @@ struct bc_ctx {
     // constants, the universal (Phi1, Phi2) table, B's support radius
     float4 *d_bcells = nullptr;
     float2 *d_g02 = nullptr;
+    float4 *d_recB = nullptr;      // (s, w, g0, g2) per ball of B (cells)
+    double rc_max_B = 0;           // max (s + W) / hf over B
+    float4 *d_recA = nullptr;      // per-rotation binning workspace (spread_z.cu)
+    int *d_szcnt = nullptr, *d_szoff = nullptr, *d_szlist = nullptr;
+    int sz_cap = 0;                // rotations the binning workspace holds
     float4 *d_phi = nullptr;
     float *d_dec = nullptr;        // 1 / phi_hat(|k| / G_B) indexed by |k|^2 (blob deconvolution)
     int phi_n = 0;
@@ -610,6 +616,15 @@ bc_status build_spread_z_tables(bc_ctx *ctx)
     const size_t nk2 = (size_t)3 * ctx->K * ctx->K + 1;
     std::vector<float> dec(nk2);
     for (size_t q = 0; q < nk2; q++) dec[q] = (float)(1.0 / blob_hat(std::sqrt((double)q) / pl.G));
+    std::vector<float4> rb(cnt, make_float4(0, 0, 0, 0));
+    ctx->rc_max_B = 0;
+    for (int64_t j = 0; j < nb; j++) {
+        rb[j] = make_float4(bc[j].w, (float)ctx->hw[1][2 * j], g[j].x, g[j].y);
+        ctx->rc_max_B = std::max(ctx->rc_max_B, ctx->hxyzr[1][4 * j + 3] / pl.hf + kBlobW);
+    }
+    TRY(dalloc(ctx, &ctx->d_recB, sizeof(float4) * cnt));
+    CU(ctx, cudaMemcpy(ctx->d_recB, rb.data(), sizeof(float4) * cnt, cudaMemcpyHostToDevice));
+    ctx->sz_cap = 0;  // binning workspace is sized for this shape at the next correlate
     TRY(dalloc(ctx, &ctx->d_phi, sizeof(float4) * tab.size()));
     TRY(dalloc(ctx, &ctx->d_bcells, sizeof(float4) * cnt));
     TRY(dalloc(ctx, &ctx->d_g02, sizeof(float2) * cnt));
@@ -693,20 +708,49 @@ bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, voi
     const int L = pl.L;
     const float2 *tw = ctx->d_tw[L];
     if (which == 1 && use_spread_z(ctx)) {
+        const int n = (int)ctx->n[1];
+        const int nbins = spread_z_bins(L);
+        const long long lstride = (long long)n * spread_z_bins_per_ball((float)ctx->rc_max_B);
+        if (ctx->sz_cap < nb) {
+            TRY(dalloc(ctx, &ctx->d_recA, sizeof(float4) * (size_t)n * nb));
+            TRY(dalloc(ctx, &ctx->d_szcnt, sizeof(int) * (size_t)nbins * nb));
+            TRY(dalloc(ctx, &ctx->d_szoff, sizeof(int) * (size_t)nbins * nb));
+            TRY(dalloc(ctx, &ctx->d_szlist, sizeof(int) * (size_t)lstride * nb));
+            ctx->sz_cap = nb;
+        }
+        {
+            SzBinArgs bn{};
+            bn.n = n;
+            bn.balls = ctx->d_bcells;
+            bn.rot = d_rot;
+            bn.ox = (float)pl.o[0];
+            bn.oy = (float)pl.o[1];
+            bn.oz = (float)pl.o[2];
+            bn.cut = (float)(pl.cut / pl.hf);
+            bn.recA = ctx->d_recA;
+            bn.bpa = L / 8;
+            bn.nbins = nbins;
+            bn.counts = ctx->d_szcnt;
+            bn.offs = ctx->d_szoff;
+            bn.lists = ctx->d_szlist;
+            bn.list_stride = lstride;
+            StageScope sc(ctx, s, "bin_B");
+            launch_spread_z_bin(bn, nb, s);
+            ctx->launches += 3;
+        }
         SpreadZArgs a{};
         a.L = L;
         a.K = ctx->K;
         a.c = pl.c;
         a.G = pl.G;
-        a.ox = (float)pl.o[0];
-        a.oy = (float)pl.o[1];
-        a.oz = (float)pl.o[2];
-        a.cut = (float)(pl.cut / pl.hf);
-        a.n_balls = (int)ctx->n[1];
-        a.balls = ctx->d_bcells;
-        a.w = ctx->d_wre[1];
-        a.g02 = ctx->d_g02;
-        a.rot = d_rot;
+        a.n_balls = n;
+        a.recA = ctx->d_recA;
+        a.recB = ctx->d_recB;
+        a.counts = ctx->d_szcnt;
+        a.offs = ctx->d_szoff;
+        a.lists = ctx->d_szlist;
+        a.nbins = nbins;
+        a.list_stride = lstride;
         a.phi = ctx->d_phi;
         a.phi_n = ctx->phi_n;
         a.phi_U = (float)ctx->phi_U;
@@ -976,6 +1020,11 @@ bc_status bc_destroy(bc_ctx *ctx)
     dfree(ctx->d_g02);
     dfree(ctx->d_phi);
     dfree(ctx->d_dec);
+    dfree(ctx->d_recB);
+    dfree(ctx->d_recA);
+    dfree(ctx->d_szcnt);
+    dfree(ctx->d_szoff);
+    dfree(ctx->d_szlist);
     dfree(ctx->d_Ahat);
     dfree(ctx->d_Ahat_cm);
     dfree(ctx->d_xtab);

@@ -36,15 +36,30 @@ struct SpreadArgs {
 
 // fused spreading + z transform of R B (spread_z.cu), real weights.  Cell units throughout:
 // ball (x, y, z, s) / hf in B's frame; the box origin o (cells); cut = footprint beyond s.
+// per-rotation binning of B's balls for spread_z (8 x 8-column bins, ball order)
+struct SzBinArgs {
+    int n;                  // balls
+    const float4 *balls;    // (x, y, z, s) / hf, B frame
+    const float *rot;       // [b][9]
+    float ox, oy, oz, cut;  // box origin (cells), window support W (cells)
+    float4 *recA;           // [b][n] (u_x, u_y, u_z, (s + W)^2), box cells
+    int bpa, nbins;         // bins per axis, bins
+    int *counts, *offs;     // [b][nbins]
+    int *lists;             // [b][list_stride] ball indices
+    long long list_stride;
+};
+int spread_z_bins(int L);
+int spread_z_bins_per_ball(float rc_max);
+void launch_spread_z_bin(const SzBinArgs &a, int batch, cudaStream_t s);
+
 struct SpreadZArgs {
     int L, K, c, G;
-    float ox, oy, oz;
-    float cut;
     int n_balls;
-    const float4 *balls;    // (x, y, z, s) / hf
-    const float *w;         // weights
-    const float2 *g02;      // per ball (g0, g2): g(s, d) ~ g0 + g2 d^2 for d < 0.1 cells (window profile)
-    const float *rot;       // [b][9]
+    const float4 *recA;     // [b][n] rotated balls (SzBinArgs)
+    const float4 *recB;     // [n] (s, w, g0, g2): radius (cells), weight, d -> 0 series g0 + g2 d^2
+    const int *counts, *offs, *lists;  // the bins (SzBinArgs)
+    int nbins;
+    long long list_stride;
     const float4 *phi;      // [phi_n][2] cubic pieces of (Phi1, Phi2) on [-U, U]
     int phi_n;
     float phi_U, phi_invD;

@@ -29,7 +29,7 @@ namespace {
 
 constexpr int SZ_COLS = 16;    // columns per block (4 x 4)
 constexpr int SZ_LINES = 8;    // complex lines (column pairs)
-constexpr int SZ_LCAP = 256;   // candidate list chunk
+constexpr int SZ_BIN = 8;      // binning: 8 x 8 columns
 
 struct PhiVal {
     float p1, p2;
@@ -48,6 +48,89 @@ __device__ __forceinline__ PhiVal phi_lookup(const float4 *__restrict__ tab, flo
 
 }  // namespace
 
+// ============================================================================ per-rotation binning
+// recA[b][j] = (R b_j / hf - o, (s_j + W)^2) in box cells; the moving ball's footprint disk
+// (radius s_j + W around its centre) is listed, in ball order, in every 8 x 8-column bin
+// of the box it reaches.  Counting pass, then a fill pass whose blocks find their own
+// offsets by summing the counts of the bins before them (no separate scan, deterministic).
+__global__ void szb_rotate_kernel(SzBinArgs a)
+{
+    const int j = blockIdx.x * blockDim.x + threadIdx.x, b = blockIdx.y;
+    if (j >= a.n) return;
+    const float *R = a.rot + 9 * b;
+    const float4 bl = a.balls[j];  // (x, y, z, s) in cells, B frame
+    // eq_Mink0 (L235): the rigid motion relocates the centre only
+    const float rc = bl.w + a.cut;
+    a.recA[(long long)b * a.n + j] = make_float4(R[0] * bl.x + R[1] * bl.y + R[2] * bl.z - a.ox,
+                                                 R[3] * bl.x + R[4] * bl.y + R[5] * bl.z - a.oy,
+                                                 R[6] * bl.x + R[7] * bl.y + R[8] * bl.z - a.oz, rc * rc);
+}
+
+__device__ __forceinline__ bool szb_hits(float4 u, int bin, int bpa)
+{
+    const float x0 = (float)((bin / bpa) * SZ_BIN), y0 = (float)((bin % bpa) * SZ_BIN);
+    const float dx = fmaxf(fmaxf(x0 - u.x, u.x - (x0 + (SZ_BIN - 1))), 0.f);
+    const float dy = fmaxf(fmaxf(y0 - u.y, u.y - (y0 + (SZ_BIN - 1))), 0.f);
+    return dx * dx + dy * dy < u.w;
+}
+
+__global__ void __launch_bounds__(256) szb_count_kernel(SzBinArgs a)
+{
+    const int bin = blockIdx.x, b = blockIdx.y;
+    const float4 *rec = a.recA + (long long)b * a.n;
+    int cnt = 0;
+    for (int j = threadIdx.x; j < a.n; j += 256) cnt += szb_hits(rec[j], bin, a.bpa) ? 1 : 0;
+    __shared__ int red[8];
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int w = 0; w < 8; w++) t += red[w];
+        a.counts[b * a.nbins + bin] = t;
+    }
+}
+
+__global__ void __launch_bounds__(256) szb_fill_kernel(SzBinArgs a)
+{
+    const int bin = blockIdx.x, b = blockIdx.y;
+    const float4 *rec = a.recA + (long long)b * a.n;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __shared__ int red[8];
+    __shared__ int base_s;
+    int s = 0;
+    for (int k = threadIdx.x; k < bin; k += 256) s += a.counts[b * a.nbins + k];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) red[wid] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int w = 0; w < 8; w++) t += red[w];
+        a.offs[b * a.nbins + bin] = t;
+        base_s = t;
+    }
+    __syncthreads();
+    int pos0 = base_s;
+    int *lst = a.lists + (long long)b * a.list_stride;
+    for (int j0 = 0; j0 < a.n; j0 += 256) {
+        const int j = j0 + threadIdx.x;
+        const bool ok = j < a.n && szb_hits(rec[j], bin, a.bpa);
+        const unsigned m = __ballot_sync(0xffffffffu, ok);
+        __syncthreads();
+        if (lane == 0) red[wid] = __popc(m);
+        __syncthreads();
+        int off = 0, total = 0;
+#pragma unroll
+        for (int w = 0; w < 8; w++) {
+            off += (w < wid) ? red[w] : 0;
+            total += red[w];
+        }
+        if (ok) lst[pos0 + off + __popc(m & ((1u << lane) - 1u))] = j;
+        pos0 += total;
+    }
+}
+
+// ============================================================================ spread + z transform
 // FFT phase: NG = 128 / TPL thread groups (the other half of the block idles) keep the
 // exchange buffer small enough for 3 blocks / SM.
 template <int L>
@@ -58,18 +141,14 @@ __global__ void __launch_bounds__(256, 3) spread_z_kernel(SpreadZArgs a)
     static_assert(256 % TPL == 0 && Plan<L>::n == 2, "spread_z plan");
     extern __shared__ float4 smz[];
     const int K = a.K, M = 2 * a.K + 1, Kz = a.K + 1;
-    // layout: phi table | tw | Abuf (NG lines) | region {acc + lists  /  zb}
+    // layout: phi table | tw | Abuf (NG lines) | region {acc  /  zb}
     float4 *phi = smz;
     float2 *tw = (float2 *)(phi + 2 * a.phi_n);
     float2 *Abuf = tw + L;
     constexpr int CS = L + 16;                        // column stride: the two half-warps of a warp
                                                       // (adjacent columns) sit 16 banks apart
     float *acc = (float *)(Abuf + NG * LS);           // [16][CS]
-    float4 *sb = (float4 *)(acc + SZ_COLS * CS);      // [LCAP] (ux, uy, uz, rc^2)
-    float4 *sw = sb + SZ_LCAP;                        // [LCAP] (s, w, g0, g2)
     float2 *zb = (float2 *)acc;                       // [8][M] (after the spread)
-    __shared__ int wcount[8];
-    __shared__ int list_n;
 
     const int b = blockIdx.y;
     const int tpa = L / 4;
@@ -93,84 +172,41 @@ __global__ void __launch_bounds__(256, 3) spread_z_kernel(SpreadZArgs a)
     for (int e = threadIdx.x; e < L; e += 256) tw[e] = a.tw[e];
     for (int e = threadIdx.x; e < SZ_COLS * CS; e += 256) acc[e] = 0.f;
 
-    float R[9];
-#pragma unroll
-    for (int q = 0; q < 9; q++) R[q] = a.rot[9 * b + q];
-
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int h = lane >> 4, hl = lane & 15;
     const int col = 2 * wid + h;
     const float fx = (float)(X0 + (col >> 2)), fy = (float)(Y0 + (col & 3));
     float *accc = acc + col * CS;
     const float fyw = (float)(Y0 + ((2 * wid) & 3));  // the warp's columns: (fx, fyw) and (fx, fyw + 1)
-    const float fX0 = (float)X0, fY0 = (float)Y0;
     const float U = a.phi_U, invD = a.phi_invD;
     const float tmax = (float)a.phi_n - 1e-3f;
-    if (threadIdx.x == 0) list_n = 0;
+    const int bin = (X0 / SZ_BIN) * (L / SZ_BIN) + Y0 / SZ_BIN;
+    const int cnt = a.counts[b * a.nbins + bin];
+    const int *lst = a.lists + (long long)b * a.list_stride + a.offs[b * a.nbins + bin];
+    const float4 *recA = a.recA + (long long)b * a.n_balls;
     __syncthreads();
 
-    const int nb_ = a.n_balls;
-    int base = 0;
-    while (base < nb_) {
-        // ---- candidate list (order-preserving compaction) until full or exhausted
-        while (base < nb_) {
-            const int cnt0 = list_n;
-            if (cnt0 + 256 > SZ_LCAP) break;
-            const int j = base + threadIdx.x;
-            bool ok = false;
-            float4 u = make_float4(0, 0, 0, 0);
-            if (j < nb_) {
-                const float4 bl = a.balls[j];  // (x, y, z, s) in cells, B frame
-                // eq_Mink0 (L235): the rigid motion relocates the centre only
-                u.x = R[0] * bl.x + R[1] * bl.y + R[2] * bl.z - a.ox;
-                u.y = R[3] * bl.x + R[4] * bl.y + R[5] * bl.z - a.oy;
-                u.z = R[6] * bl.x + R[7] * bl.y + R[8] * bl.z - a.oz;
-                const float rc = bl.w + a.cut;
-                u.w = rc * rc;
-                const float dx = fmaxf(fmaxf(fX0 - u.x, u.x - (fX0 + 3.f)), 0.f);
-                const float dy = fmaxf(fmaxf(fY0 - u.y, u.y - (fY0 + 3.f)), 0.f);
-                ok = dx * dx + dy * dy < u.w;
-            }
-            const unsigned m = __ballot_sync(0xffffffffu, ok);
-            if (lane == 0) wcount[wid] = __popc(m);
-            __syncthreads();
-            int off = 0, total = 0;
-#pragma unroll
-            for (int w = 0; w < 8; w++) {
-                const int cw = wcount[w];
-                off += (w < wid) ? cw : 0;
-                total += cw;
-            }
-            if (ok) {
-                const int pos = cnt0 + off + __popc(m & ((1u << lane) - 1u));
-                sb[pos] = u;
-                const float2 g = a.g02[j];
-                sw[pos] = make_float4(a.balls[j].w, a.w[j], g.x, g.y);
-            }
-            base += 256;
-            __syncthreads();
-            if (threadIdx.x == 0) list_n = cnt0 + total;
-            __syncthreads();
+    // ---- accumulate the bin's balls (ball order) into this lane's cells.  The warp keeps the
+    // balls whose footprint reaches one of its two columns (ballot); a half-warp covers the
+    // ball's chord of its column in 16-cell steps from the chord start: within a step the lanes
+    // touch distinct cells, steps and balls are sequential, so the sums are race-free and in
+    // ball order (deterministic).
+    for (int base0 = 0; base0 < cnt; base0 += 32) {
+        int jl = -1;
+        bool rel = false;
+        if (base0 + lane < cnt) {
+            jl = lst[base0 + lane];
+            const float4 uc = recA[jl];
+            const float ddx = fx - uc.x;
+            const float ddy = fmaxf(fmaxf(fyw - uc.y, uc.y - (fyw + 1.f)), 0.f);
+            rel = fmaf(ddx, ddx, ddy * ddy) < uc.w;
         }
-        // ---- accumulate the list into this lane's cells.  A half-warp covers the ball's chord
-        // of its column in 16-cell steps from the chord start: within a step the lanes touch
-        // distinct cells, steps and balls are sequential, so the sums are race-free and in
-        // list order (deterministic).
-        const int total = list_n;
-        for (int base0 = 0; base0 < total; base0 += 32) {
-            // the candidates that reach one of this warp's two columns (ballot, list order kept)
-            bool rel = false;
-            if (base0 + lane < total) {
-                const float4 uc = sb[base0 + lane];
-                const float ddx = fx - uc.x;
-                const float ddy = fmaxf(fmaxf(fyw - uc.y, uc.y - (fyw + 1.f)), 0.f);
-                rel = fmaf(ddx, ddx, ddy * ddy) < uc.w;
-            }
-            unsigned msk = __ballot_sync(0xffffffffu, rel);
+        unsigned msk = __ballot_sync(0xffffffffu, rel);
         while (msk) {
-            const int e = base0 + __ffs(msk) - 1;
+            const int src = __ffs(msk) - 1;
             msk &= msk - 1;
-            const float4 ue = sb[e];
+            const int j = __shfl_sync(0xffffffffu, jl, src);
+            const float4 ue = recA[j];
             const float dx = fx - ue.x, dy = fy - ue.y;
             const float dxy2 = fmaf(dx, dx, dy * dy);
             const float hz2 = ue.w - dxy2;
@@ -183,7 +219,7 @@ __global__ void __launch_bounds__(256, 3) spread_z_kernel(SpreadZArgs a)
             }
             const int nmax = max(nit, __shfl_xor_sync(0xffffffffu, nit, 16));
             if (nmax <= 0) continue;
-            const float4 we = sw[e];  // (s, w, g0, g2)
+            const float4 we = a.recB[j];  // (s, w, g0, g2)
             for (int it = 0; it < nmax; it++) {
                 const int z = zlo + (it << 4) + hl;
                 if (z <= zhi) {
@@ -204,11 +240,8 @@ __global__ void __launch_bounds__(256, 3) spread_z_kernel(SpreadZArgs a)
                 }
             }
         }
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) list_n = 0;
-        __syncthreads();
     }
+    __syncthreads();
 
     // ---- z transform: line l = columns (2l, 2l+1); group g handles line g % 8, cosets g/8 + (NG/8) r
     const int g = threadIdx.x / TPL, tl = threadIdx.x % TPL;
@@ -266,11 +299,20 @@ static void spread_z_launch(const SpreadZArgs &a, int batch, cudaStream_t s)
 {
     constexpr int NG = 128 / Plan<L>::TPL;
     const int tpa = L / 4;
-    const size_t region = std::max((size_t)SZ_COLS * (L + 16) * 4 + (size_t)SZ_LCAP * 32, (size_t)SZ_LINES * (2 * a.K + 1) * 8);
+    const size_t region = std::max((size_t)SZ_COLS * (L + 16) * 4, (size_t)SZ_LINES * (2 * a.K + 1) * 8);
     const size_t sm = (size_t)a.phi_n * 32 + (size_t)L * 8 + (size_t)NG * line_stride(L) * 8 + region;
-    static_assert(NG == 128 / Plan<L>::TPL, "spread_z FFT groups");
     cudaFuncSetAttribute(spread_z_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     spread_z_kernel<L><<<dim3(tpa * tpa, batch), 256, sm, s>>>(a);
+}
+
+int spread_z_bins(int L) { return (L / SZ_BIN) * (L / SZ_BIN); }
+int spread_z_bins_per_ball(float rc_max) { const int t = (int)(2 * rc_max / SZ_BIN) + 2; return t * t; }
+
+void launch_spread_z_bin(const SzBinArgs &a, int batch, cudaStream_t s)
+{
+    szb_rotate_kernel<<<dim3((a.n + 255) / 256, batch), 256, 0, s>>>(a);
+    szb_count_kernel<<<dim3(a.nbins, batch), 256, 0, s>>>(a);
+    szb_fill_kernel<<<dim3(a.nbins, batch), 256, 0, s>>>(a);
 }
 
 void launch_spread_z(const SpreadZArgs &a, int batch, cudaStream_t s)
