@@ -728,7 +728,7 @@ bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, voi
             bn.oz = (float)pl.o[2];
             bn.cut = (float)(pl.cut / pl.hf);
             bn.recA = ctx->d_recA;
-            bn.bpa = L / 8;
+            bn.bpa = spread_z_bins_per_axis(L);
             bn.nbins = nbins;
             bn.counts = ctx->d_szcnt;
             bn.offs = ctx->d_szoff;

@@ -36,7 +36,7 @@ struct SpreadArgs {
 
 // fused spreading + z transform of R B (spread_z.cu), real weights.  Cell units throughout:
 // ball (x, y, z, s) / hf in B's frame; the box origin o (cells); cut = footprint beyond s.
-// per-rotation binning of B's balls for spread_z (8 x 8-column bins, ball order)
+// per-rotation binning of B's balls for spread_z (16 x 16-column bins, ball order)
 struct SzBinArgs {
     int n;                  // balls
     const float4 *balls;    // (x, y, z, s) / hf, B frame
@@ -49,6 +49,7 @@ struct SzBinArgs {
     long long list_stride;
 };
 int spread_z_bins(int L);
+int spread_z_bins_per_axis(int L);
 int spread_z_bins_per_ball(float rc_max);
 void launch_spread_z_bin(const SzBinArgs &a, int batch, cudaStream_t s);
 

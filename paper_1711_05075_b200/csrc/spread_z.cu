@@ -29,7 +29,7 @@ namespace {
 
 constexpr int SZ_COLS = 16;    // columns per block (4 x 4)
 constexpr int SZ_LINES = 8;    // complex lines (column pairs)
-constexpr int SZ_BIN = 8;      // binning: 8 x 8 columns
+constexpr int SZ_BIN = 16;     // binning: 16 x 16 columns
 
 struct PhiVal {
     float p1, p2;
@@ -50,7 +50,7 @@ __device__ __forceinline__ PhiVal phi_lookup(const float4 *__restrict__ tab, flo
 
 // ============================================================================ per-rotation binning
 // recA[b][j] = (R b_j / hf - o, (s_j + W)^2) in box cells; the moving ball's footprint disk
-// (radius s_j + W around its centre) is listed, in ball order, in every 8 x 8-column bin
+// (radius s_j + W around its centre) is listed, in ball order, in every 16 x 16-column bin
 // of the box it reaches.  Counting pass, then a fill pass whose blocks find their own
 // offsets by summing the counts of the bins before them (no separate scan, deterministic).
 __global__ void szb_rotate_kernel(SzBinArgs a)
@@ -306,6 +306,7 @@ static void spread_z_launch(const SpreadZArgs &a, int batch, cudaStream_t s)
 }
 
 int spread_z_bins(int L) { return (L / SZ_BIN) * (L / SZ_BIN); }
+int spread_z_bins_per_axis(int L) { return L / SZ_BIN; }
 int spread_z_bins_per_ball(float rc_max) { const int t = (int)(2 * rc_max / SZ_BIN) + 2; return t * t; }
 
 void launch_spread_z_bin(const SzBinArgs &a, int batch, cudaStream_t s)
