@@ -266,29 +266,46 @@ BC_DEV void mid_stage(const float2 *__restrict__ a, float2 *__restrict__ b, cons
     }
 }
 
-template <int L, int S, int SIGN, bool DONE = (S >= Plan<L>::n - 1)>
+// Exchange barrier: block-wide, or warp-wide when every line lives inside one warp
+// (WS: TPL divides 32, lines start at multiples of TPL) and only its own threads touch its
+// buffers.
+template <bool WS>
+BC_DEV void line_sync()
+{
+    if (WS)
+        __syncwarp();
+    else
+        __syncthreads();
+}
+template <int L>
+__host__ __device__ constexpr bool warp_local() { return 32 % Plan<L>::TPL == 0; }
+
+template <int L, int S, int SIGN, bool WS, bool DONE = (S >= Plan<L>::n - 1)>
 struct Mid;
-template <int L, int S, int SIGN>
-struct Mid<L, S, SIGN, true> {
+template <int L, int S, int SIGN, bool WS>
+struct Mid<L, S, SIGN, WS, true> {
     static BC_DEV const float2 *go(const float2 *a, float2 *, const float2 *, int) { return a; }
 };
-template <int L, int S, int SIGN>
-struct Mid<L, S, SIGN, false> {
+template <int L, int S, int SIGN, bool WS>
+struct Mid<L, S, SIGN, WS, false> {
     static BC_DEV const float2 *go(const float2 *a, float2 *b, const float2 *tw, int tl)
     {
         mid_stage<L, S, SIGN>(a, b, tw, tl);
-        __syncthreads();
-        return Mid<L, S + 1, SIGN>::go(b, (float2 *)a, tw, tl);
+        line_sync<WS>();
+        return Mid<L, S + 1, SIGN, WS>::go(b, (float2 *)a, tw, tl);
     }
 };
 
 // FFT of the calling thread-group's line, registers in / registers out (see header).
 // A and B are this line's shared-memory buffers (B used only when n >= 3).
-// Contains block-wide barriers: every thread of the block must call it.  The caller
-// must barrier before writing A/B again (the last stage reads them).
-template <int L, int SIGN>
+// Contains barriers (block-wide, or warp-wide with WS = true, which requires
+// warp_local<L>()): every thread of the block (warp) must call it.  The caller must
+// barrier before writing A/B again (the last stage reads them); the twiddle table tw must
+// be visible to the calling threads before the call.
+template <int L, int SIGN, bool WS = false>
 BC_DEV void fft_regs(float2 (&x)[L / Plan<L>::TPL], float2 *A, float2 *B, const float2 *tw, int tl)
 {
+    static_assert(!WS || warp_local<L>(), "warp-synchronous FFT needs lines inside one warp");
     static_assert(plan_ok<L>(), "bad FFT plan");
     constexpr int TPL = Plan<L>::TPL;
     constexpr int n = Plan<L>::n;
@@ -307,8 +324,8 @@ BC_DEV void fft_regs(float2 (&x)[L / Plan<L>::TPL], float2 *A, float2 *B, const 
             for (int r = 0; r < R; r++) A[pad(j * R + r)] = v[r];
         }
     }
-    __syncthreads();
-    const float2 *cur = Mid<L, 1, SIGN>::go(A, B, tw, tl);
+    line_sync<WS>();
+    const float2 *cur = Mid<L, 1, SIGN, WS>::go(A, B, tw, tl);
     // last stage (Ns = L / R): shared memory -> registers, output index j + r Ns
     {
         constexpr int R = Plan<L>::r[n - 1];

@@ -109,12 +109,12 @@ __global__ void __launch_bounds__(FF_NT, 4) fold_fast_kernel(FoldFastArgs a)
                     const float2 v = X[line * FF_LS + pad(n)];
                     y[m] = p ? cmul(v, ctw[p * FF_L + n]) : v;
                 }
-                fft_regs<FF_L, -1>(y, Ab + line * FF_LS, Ab + line * FF_LS, tw, tl);
+                fft_regs<FF_L, -1, true>(y, Ab + line * FF_LS, Ab + line * FF_LS, tw, tl);
                 // S[j] = sum of the products of outputs m = j and m = j + 12 (same target)
                 float2 S[4];
 #pragma unroll
                 for (int j = 0; j < 4; j++) S[j] = cadd(cmulc(av[j], y[j]), cmulc(av[j + 4], y[j + 12]));
-                __syncthreads();  // the next coset's FFT rewrites Ab (fft_regs contract)
+                __syncwarp();  // the next coset's FFT rewrites this line's Ab (fft_regs contract)
                 if (pass == 0) {
 #pragma unroll
                     for (int j = 0; j < 4; j++) acc[j][p] = cadd(acc[j][p], S[j]);
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(FF_NT, 4) fold_fast_kernel(FoldFastArgs a)
     float2 v[E];
 #pragma unroll
     for (int m = 0; m < E; m++) v[m] = X[line * FF_LS + pad(tl + FF_TPL * m)];
-    fft_regs<FF_NP, +1>(v, Ab + line * FF_LS, Ab + line * FF_LS, tw, tl);
+    fft_regs<FF_NP, +1, true>(v, Ab + line * FF_LS, Ab + line * FF_LS, tw, tl);
     __syncthreads();
 #pragma unroll
     for (int m = 0; m < E; m++) X[line * FF_LS + pad(tl + FF_TPL * m)] = v[m];
@@ -234,8 +234,8 @@ __global__ void __launch_bounds__(FF_NT, 5) pass_y_fast_kernel(PassYFastArgs a)
             const float2 v = X[line * FF_LS + pad(n)];
             y[m] = p ? cmul(v, __ldg(ctw + p * FF_L + n)) : v;
         }
-        fft_regs<FF_L, -1>(y, Ab + line * FF_LS, Ab + line * FF_LS, tw, tl);
-        __syncthreads();
+        fft_regs<FF_L, -1, true>(y, Ab + line * FF_LS, Ab + line * FF_LS, tw, tl);
+        __syncwarp();
         // in-band outputs u = q (q < 64) or q - 128 (q >= 192), times mult_y(ky)
 #pragma unroll
         for (int uu = 0; uu < 8; uu++) {

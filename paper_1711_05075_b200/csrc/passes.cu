@@ -392,6 +392,8 @@ __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TP
     const bool reduce = a.out_kind != BC_OUT_F_FULL;
 
     for (int m = threadIdx.x; m < L; m += NT) tw[m] = a.tw[m];
+    __syncthreads();
+    constexpr bool WS = warp_local<L>();
     // running extrema of this thread: values in fp32 with their linear index; a thread visits
     // its outputs in increasing index order, so strict comparisons keep the lowest index on
     // ties, as the 64-bit keys (built once at the end) do across threads
@@ -428,7 +430,7 @@ __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TP
             }
             x[m] = v;
         }
-        fft_regs<L, +1>(x, A + line * LS, B + line * LS, tw, tl);
+        fft_regs<L, +1, WS>(x, A + line * LS, B + line * LS, tw, tl);
 
         if (valid) {
 #pragma unroll
@@ -463,7 +465,7 @@ __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TP
                 }
             }
         }
-        __syncthreads();  // the next tile's first FFT stage rewrites A
+        line_sync<WS>();  // the next tile's first FFT stage rewrites this line's A
     }
     unsigned long long kmin = imin != 0xffffffffu ? key_min(vmin, imin) : ~0ull;
     unsigned long long kmax = imax != 0xffffffffu ? key_max(vmax, imax) : 0ull;

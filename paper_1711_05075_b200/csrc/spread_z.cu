@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(256, 3) spread_z_kernel(SpreadZArgs a)
 {
     constexpr int TPL = Plan<L>::TPL, E = L / TPL, NG = 128 / TPL;
     constexpr int LS = line_stride(L);
-    static_assert(256 % TPL == 0 && Plan<L>::n == 2, "spread_z plan");
+    static_assert(256 % TPL == 0 && Plan<L>::n == 2 && warp_local<L>(), "spread_z plan");
     extern __shared__ float4 smz[];
     const int K = a.K, M = 2 * a.K + 1, Kz = a.K + 1;
     // layout: phi table | tw | Abuf (NG lines) | region {acc  /  zb}
@@ -262,13 +262,7 @@ __global__ void __launch_bounds__(256, 3) spread_z_kernel(SpreadZArgs a)
         float2 y[E];
 #pragma unroll
         for (int m = 0; m < E; m++) y[m] = (active && p) ? cmul(x[m], a.ctw[p * L + tl + TPL * m]) : x[m];
-        float2 *ab = Abuf + (fft_thread ? g : g - NG) * LS;  // idle groups shadow the active ones' buffers
-        if (fft_thread) {
-            fft_regs<L, -1>(y, ab, ab, tw, tl);
-        } else {
-            // keep the block-wide barriers of fft_regs (stage 0 -> last stage) in step
-            __syncthreads();
-        }
+        if (fft_thread) fft_regs<L, -1, true>(y, Abuf + g * LS, Abuf + g * LS, tw, tl);  // warp-uniform branch
         if (active) {
 #pragma unroll
             for (int m = 0; m < E; m++) {
@@ -277,8 +271,9 @@ __global__ void __launch_bounds__(256, 3) spread_z_kernel(SpreadZArgs a)
                 if (k >= -K && k <= K) zb[line * M + k + K] = y[m];
             }
         }
-        __syncthreads();
+        __syncwarp();  // the next round's FFT rewrites this group's buffer
     }
+    __syncthreads();  // zb complete
     // ---- unpack the column pairs, multiply by mult_z, store T1 rows (contiguous in kz)
     for (int e = threadIdx.x; e < SZ_LINES * Kz; e += 256) {
         const int l = e / Kz, k = e % Kz;
