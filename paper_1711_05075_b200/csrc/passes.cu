@@ -493,6 +493,168 @@ __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TP
     }
 }
 
+// ---------------------------------------------------------------- TMA-fed variant (real weights)
+// Same arithmetic as last_kernel<L, true>; the 2 NL rows of a tile are contiguous in Y1, so
+// one thread arms an mbarrier with the byte count and issues a 1D bulk copy
+// (cp.async.bulk ... mbarrier::complete_tx) of the NEXT tile into the other half of a
+// double buffer while the block transforms the current one from shared memory.
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+template <int L>
+__global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TPL * Plan<L>::NL)) last_tma_kernel(LastArgs a)
+{
+    constexpr int TPL = Plan<L>::TPL, NL = Plan<L>::NL, NT = TPL * NL;
+    constexpr int LS = line_stride(L), E = L / TPL;
+    constexpr bool WS = warp_local<L>();
+    extern __shared__ __align__(16) float2 sm[];
+    const int Fz = a.Fz;
+    float2 *stage = sm;                          // [2][2 NL][Fz]
+    float2 *tw = stage + 2 * 2 * NL * Fz;
+    float2 *A = tw + L;
+    float2 *B = A + NL * LS;
+    __shared__ unsigned long long bar[2];
+    __shared__ unsigned long long red[2][NT / 32];
+    const int line = threadIdx.x / TPL, tl = threadIdx.x % TPL;
+    const int b = blockIdx.y;
+    const long long lines = (long long)a.N * a.N;
+    const long long ntiles = (lines + 2 * NL - 1) / (2 * NL);
+    const bool reduce = a.out_kind != BC_OUT_F_FULL;
+    const float2 *in = a.in + (long long)b * a.in_bstride;
+
+    auto issue = [&](long long tile, int s) {  // one thread: arm + copy tile -> stage s
+        const long long l0 = tile * 2 * NL;
+        const long long nl = lines - l0 < 2 * NL ? lines - l0 : 2 * NL;
+        const unsigned bytes = (unsigned)(nl * Fz * sizeof(float2));
+        mbar_expect_tx(&bar[s], bytes);
+        bulk_g2s(stage + (size_t)s * 2 * NL * Fz, in + l0 * Fz, bytes, &bar[s]);
+    };
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    for (int m = threadIdx.x; m < L; m += NT) tw[m] = a.tw[m];
+    __syncthreads();
+    if (threadIdx.x == 0 && blockIdx.x < ntiles) issue(blockIdx.x, 0);
+
+    float vmin = INFINITY, vmax = -INFINITY;
+    unsigned imin = 0xffffffffu, imax = 0xffffffffu;
+    int it = 0;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
+        const int s = it & 1;
+        if (threadIdx.x == 0 && tile + gridDim.x < ntiles) issue(tile + gridDim.x, s ^ 1);
+        mbar_wait(&bar[s], (it >> 1) & 1);
+        const float2 *st = stage + (size_t)s * 2 * NL * Fz;
+        const long long l0 = tile * 2 * NL + 2 * line;
+        const bool valid = l0 < lines;
+        const bool has1 = l0 + 1 < lines;
+        const float2 *ra = st + (2 * line) * Fz, *rb = ra + Fz;
+        float2 x[E];
+#pragma unroll
+        for (int m = 0; m < E; m++) {
+            const int n = tl + TPL * m;
+            float2 v = make_float2(0.f, 0.f);
+            if (valid) {
+                const bool lo = n < Fz;
+                const int src = lo ? n : L - n;
+                float2 va = ra[src];
+                float2 vb = has1 ? rb[src] : make_float2(0.f, 0.f);
+                if (n == 0 || 2 * n == L) {
+                    va.y = 0.f;
+                    vb.y = 0.f;
+                } else if (!lo) {
+                    va.y = -va.y;
+                    vb.y = -vb.y;
+                }
+                v = make_float2(va.x - vb.y, va.y + vb.x);  // A + i B
+            }
+            x[m] = v;
+        }
+        fft_regs<L, +1, WS>(x, A + line * LS, B + line * LS, tw, tl);
+        if (valid) {
+#pragma unroll
+            for (int m = 0; m < E; m++) {
+                const int q = tl + TPL * m;
+                if (q >= a.N) continue;
+                const float2 v = cscale(x[m], a.scale);
+                const long long gidx = l0 * a.N + q;
+                if (!reduce) {
+                    float *o = (float *)a.out_full + (long long)b * a.full_bstride + gidx;
+                    o[0] = v.x;
+                    if (has1) o[a.N] = v.y;
+                } else {
+                    const unsigned gi = (unsigned)gidx;
+                    if (v.x < vmin) { vmin = v.x; imin = gi; }
+                    if (v.x > vmax) { vmax = v.x; imax = gi; }
+                }
+            }
+            if (has1 && reduce) {
+#pragma unroll
+                for (int m = 0; m < E; m++) {
+                    const int q = tl + TPL * m;
+                    if (q >= a.N) continue;
+                    const float vy = x[m].y * a.scale;
+                    const unsigned gi = (unsigned)((l0 + 1) * a.N + q);
+                    if (vy < vmin) { vmin = vy; imin = gi; }
+                    if (vy > vmax) { vmax = vy; imax = gi; }
+                }
+            }
+        }
+        __syncthreads();  // stage s fully read (it is refilled next iteration); FFT buffers free
+    }
+    unsigned long long kmin = imin != 0xffffffffu ? key_min(vmin, imin) : ~0ull;
+    unsigned long long kmax = imax != 0xffffffffu ? key_max(vmax, imax) : 0ull;
+    if (reduce) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const unsigned long long o1 = __shfl_xor_sync(0xffffffffu, kmin, off);
+            const unsigned long long o2 = __shfl_xor_sync(0xffffffffu, kmax, off);
+            kmin = o1 < kmin ? o1 : kmin;
+            kmax = o2 > kmax ? o2 : kmax;
+        }
+        if ((threadIdx.x & 31) == 0) {
+            red[0][threadIdx.x >> 5] = kmin;
+            red[1][threadIdx.x >> 5] = kmax;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < NT / 32; w++) {
+                kmin = red[0][w] < kmin ? red[0][w] : kmin;
+                kmax = red[1][w] > kmax ? red[1][w] : kmax;
+            }
+            if (kmin != ~0ull) atomicMin(&a.keys[2 * b + 0], kmin);
+            if (kmax != 0ull) atomicMax(&a.keys[2 * b + 1], kmax);
+        }
+    }
+}
+
 // ============================================================================ host dispatch
 
 template <int L>
@@ -601,6 +763,19 @@ void launch_fold_x(const FoldXArgs &a_in, int batch, cudaStream_t s)
 
 void launch_last(const LastArgs &a, int batch, cudaStream_t s)
 {
+    // TMA-fed C2R path: the tile rows must be 16-byte aligned (the stage offsets and
+    // the row blocks are multiples of 2 NL rows; Fz * 8 bytes per row)
+    if (a.hermitian && a.Np == 256 && ((uintptr_t)a.in % 16) == 0 && (a.in_bstride * 8) % 16 == 0) {
+        constexpr int NL = Plan<256>::NL;
+        const size_t sm = sizeof(float2) * (2 * 2 * NL * (size_t)a.Fz + 256 +
+                                            (Plan<256>::n >= 3 ? 2 : 1) * (size_t)NL * line_stride(256));
+        const long long lines = (long long)a.N * a.N;
+        const long long tiles = (lines + 2 * NL - 1) / (2 * NL);
+        const long long cap = std::max(1LL, 4LL * 148 * 4 / std::max(batch, 1));
+        set_smem(last_tma_kernel<256>, sm);
+        last_tma_kernel<256><<<dim3((unsigned)std::min(tiles, cap), batch), Plan<256>::TPL * NL, sm, s>>>(a);
+        return;
+    }
     switch (a.Np) {
 #define X(L_)                                                                                 \
     case L_: {                                                                                \
