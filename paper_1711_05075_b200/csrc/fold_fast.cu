@@ -50,11 +50,7 @@ __global__ void __launch_bounds__(FF_NT, 4) fold_fast_kernel(FoldFastArgs a)
     for (int e = threadIdx.x; e < FF_L; e += FF_NT) tw[e] = a.tw[e];
     for (int e = threadIdx.x; e < FF_C * FF_L; e += FF_NT) ctw[e] = a.ctw[e];
 
-    // A'' row position of output (m, p) of lane tl: base[p] + tl + 16 m (+ L for m < 4)
-    int pbase[FF_C];
-#pragma unroll
-    for (int p = 0; p < FF_C; p++) pbase[p] = a.pos_base[p] + tl;
-
+    // A'' row position of output (m, p) of lane tl: pos_base[p] + tl + 16 m (+ L for m < 4)
     float2 acc[4][FF_C];
 #pragma unroll
     for (int j = 0; j < 4; j++)
@@ -91,14 +87,19 @@ __global__ void __launch_bounds__(FF_NT, 4) fold_fast_kernel(FoldFastArgs a)
             const bool my_ok = pass == 0 ? (tz < FF_FZ) : (tz >= 1 && tz < FF_FZ);
             const int my_kz = pass == 0 ? tz : FF_NP - tz;
             const float2 *arow = a.Ahat + (long long)((ky + FF_K) * FF_KZ + (my_ok ? my_kz : 0)) * a.MS;
-#pragma unroll
+            // one copy of the FFT (runtime coset loop keeps the code in the instruction cache);
+            // only the register-accumulator update is specialised per coset
+#pragma unroll 1
             for (int p = 0; p < FF_C; p++) {
                 // A'' values of the 8 in-band outputs (issued before the FFT to hide latency)
+                // (select chain: a runtime index into the kernel-parameter array would force a
+                // local-memory copy of the argument block)
+                const int pb = (p == 0 ? a.pos_base[0] : p == 1 ? a.pos_base[1] : p == 2 ? a.pos_base[2] : a.pos_base[3]) + tl;
                 float2 av[8];
 #pragma unroll
                 for (int u = 0; u < 8; u++) {
                     const int m = u < 4 ? u : u + 8;
-                    const int pos = pbase[p] + 16 * m + (m < 4 ? FF_L : 0);
+                    const int pos = pb + 16 * m + (m < 4 ? FF_L : 0);
                     const bool in_band = my_ok && !(p == 0 && m == 12 && tl == 0);
                     av[u] = in_band ? __ldg(arow + pos) : make_float2(0.f, 0.f);
                 }
@@ -116,8 +117,14 @@ __global__ void __launch_bounds__(FF_NT, 4) fold_fast_kernel(FoldFastArgs a)
                 for (int j = 0; j < 4; j++) S[j] = cadd(cmulc(av[j], y[j]), cmulc(av[j + 4], y[j + 12]));
                 __syncwarp();  // the next coset's FFT rewrites this line's Ab (fft_regs contract)
                 if (pass == 0) {
-#pragma unroll
-                    for (int j = 0; j < 4; j++) acc[j][p] = cadd(acc[j][p], S[j]);
+                    switch (p) {
+#define FF_DIRECT(P_)                                                               \
+    case P_:                                                                        \
+        _Pragma("unroll") for (int j = 0; j < 4; j++) acc[j][P_] = cadd(acc[j][P_], S[j]); \
+        break;
+                        FF_DIRECT(0) FF_DIRECT(1) FF_DIRECT(2) FF_DIRECT(3)
+#undef FF_DIRECT
+                    }
                 } else {
                     const int src = (lane & 16) | (p == 0 ? ((16 - tl) & 15) : (15 - tl));
                     float2 Rv[4];
@@ -126,15 +133,20 @@ __global__ void __launch_bounds__(FF_NT, 4) fold_fast_kernel(FoldFastArgs a)
                         Rv[j].x = __shfl_sync(0xffffffffu, S[j].x, src);
                         Rv[j].y = __shfl_sync(0xffffffffu, S[j].y, src);
                     }
-                    if (p == 0) {
+                    switch (p) {
+                    case 0:
 #pragma unroll
                         for (int j = 0; j < 4; j++) {
                             const float2 v = tl == 0 ? Rv[(4 - j) & 3] : Rv[3 - j];
                             acc[j][0] = cadd(acc[j][0], cconj(v));
                         }
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < 4; j++) acc[3 - j][(4 - p) & 3] = cadd(acc[3 - j][(4 - p) & 3], cconj(Rv[j]));
+                        break;
+#define FF_CONJ(P_)                                                                                          \
+    case P_:                                                                                                 \
+        _Pragma("unroll") for (int j = 0; j < 4; j++) acc[3 - j][4 - P_] = cadd(acc[3 - j][4 - P_], cconj(Rv[j])); \
+        break;
+                        FF_CONJ(1) FF_CONJ(2) FF_CONJ(3)
+#undef FF_CONJ
                     }
                 }
             }
