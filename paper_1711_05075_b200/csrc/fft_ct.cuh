@@ -234,6 +234,25 @@ __host__ __device__ constexpr bool plan_ok()
            n >= 2;
 }
 
+// ---------------------------------------------------------------- twiddle table in shared memory
+// Flat table tw[m] = exp(-2 pi i m / L) for plans with middle stages; for two-stage plans the
+// last stage is the only user and reads w^{r j} with lanes at consecutive j, so the table is
+// stored as tw[(r - 1) Ns + j] = w^{r j} (r in [1, R), j in [0, Ns)): conflict-free, where the
+// flat table at lane stride r would serialise up to 8-way.
+template <int L>
+BC_DEV void load_twiddles(float2 *tw_s, const float2 *tw_g, int tid, int nt)
+{
+    if (Plan<L>::n == 2) {
+        constexpr int R = Plan<L>::r[Plan<L>::n - 1], Ns = L / R;
+        for (int e = tid; e < (R - 1) * Ns; e += nt) {
+            const int r = e / Ns + 1, j = e % Ns;
+            tw_s[e] = tw_g[(r * j) % L];
+        }
+    } else {
+        for (int e = tid; e < L; e += nt) tw_s[e] = tw_g[e];
+    }
+}
+
 // ---------------------------------------------------------------- stages
 // middle stage S (0 < S < n-1): shared memory a -> b
 template <int L, int S, int SIGN>
@@ -339,7 +358,7 @@ BC_DEV void fft_regs(float2 (&x)[L / Plan<L>::TPL], float2 *A, float2 *B, const 
             for (int r = 0; r < R; r++) {
                 float2 y = cur[pad(j + r * Ns)];
                 if (r > 0) {
-                    const float2 w = tw[r * j];
+                    const float2 w = n == 2 ? tw[(r - 1) * Ns + j] : tw[r * j];
                     y = SIGN < 0 ? cmul(y, w) : cmulc(y, w);
                 }
                 v[r] = y;

@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(FF_NT, 4) fold_fast_kernel(FoldFastArgs a)
     const int z0 = (tb % ZT) * FF_NL;
     const float2 *T2 = a.T2 + (long long)b * a.t2_bstride;
 
-    for (int e = threadIdx.x; e < FF_L; e += FF_NT) tw[e] = a.tw[e];
+    load_twiddles<FF_L>(tw, a.tw, threadIdx.x, FF_NT);
     for (int e = threadIdx.x; e < FF_C * FF_L; e += FF_NT) ctw[e] = a.ctw[e];
 
     // A'' row position of output (m, p) of lane tl: pos_base[p] + tl + 16 m (+ L for m < 4)
@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(FF_NT, 5) pass_y_fast_kernel(PassYFastArgs a)
         ylo = max(0, (int)floorf(a.cy - hh));
         yhi = min(FF_L - 1, (int)ceilf(a.cy + hh));
     }
-    for (int e = threadIdx.x; e < FF_L; e += FF_NT) tw[e] = a.tw[e];
+    load_twiddles<FF_L>(tw, a.tw, threadIdx.x, FF_NT);
     {
         float2 x[E];
 #pragma unroll

@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TP
     const long long nrows = IN_MODE == 2 ? (long long)a.O * a.I : a.lines;
     const bool valid = IN_MODE == 2 ? (i0 + line < a.I) : (row0 + line < nrows);
 
-    for (int m = threadIdx.x; m < L; m += NT) tw[m] = a.tw[m];
+    load_twiddles<L>(tw, a.tw, threadIdx.x, NT);
     float2 x[E];
     if (IN_MODE == 2) {
         const float2 *in = (const float2 *)a.in + (long long)b * a.in_bstride + (long long)o * L * a.I;
@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(8 * Plan<L>::TPL, 512 / (8 * Plan<L>::TPL) > 0
     const int z0 = (tb % ztiles) * NL;
     const float2 *T2 = a.T2 + (long long)b * a.t2_bstride;
 
-    for (int m = threadIdx.x; m < L; m += NT) tw[m] = a.tw[m];
+    load_twiddles<L>(tw, a.tw, threadIdx.x, NT);
     for (int e = threadIdx.x; e < NL * AS; e += NT) acc[e] = make_float2(0.f, 0.f);
     for (int e = threadIdx.x; e < a.c * L; e += NT) {
         ctw[e] = a.ctw[e];
@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(8 * Plan<L>::TPL, 512 / (8 * Plan<L>::TPL) > 0
             const int t = tl + TPL * m;
             v[m] = acc[line * AS + t + (t >> 3)];
         }
-        for (int m = threadIdx.x; m < NP; m += NT) tw[m] = a.tw_inv[m];
+        load_twiddles<NP>(tw, a.tw_inv, threadIdx.x, NT);
         __syncthreads();
         fft_regs<NP, +1>(v, A + line * LS, B + line * LS, tw, tl);
         __syncthreads();
@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TP
     const long long ntiles = (units + NL - 1) / NL;
     const bool reduce = a.out_kind != BC_OUT_F_FULL;
 
-    for (int m = threadIdx.x; m < L; m += NT) tw[m] = a.tw[m];
+    load_twiddles<L>(tw, a.tw, threadIdx.x, NT);
     __syncthreads();
     constexpr bool WS = warp_local<L>();
     // running extrema of this thread: values in fp32 with their linear index; a thread visits
@@ -560,7 +560,7 @@ __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TP
         mbar_init(&bar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    for (int m = threadIdx.x; m < L; m += NT) tw[m] = a.tw[m];
+    load_twiddles<L>(tw, a.tw, threadIdx.x, NT);
     __syncthreads();
     if (threadIdx.x == 0 && blockIdx.x < ntiles) issue(blockIdx.x, 0);
 

@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(256, 3) spread_z_kernel(SpreadZArgs a)
     }
 
     for (int e = threadIdx.x; e < 2 * a.phi_n; e += 256) phi[e] = a.phi[e];
-    for (int e = threadIdx.x; e < L; e += 256) tw[e] = a.tw[e];
+    load_twiddles<L>(tw, a.tw, threadIdx.x, 256);
     for (int e = threadIdx.x; e < SZ_COLS * CS; e += 256) acc[e] = 0.f;
 
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
