@@ -22,6 +22,8 @@ using namespace fct;
 
 namespace {
 
+__constant__ WTab<64, -1> c_w64 = WTab<64, -1>();  // e^{-2 pi i e / 64}
+
 constexpr int FF_L = 256, FF_C = 4, FF_TPL = 16, FF_NL = 8, FF_NT = FF_NL * FF_TPL;
 constexpr int FF_G = FF_C * FF_L, FF_K = FF_G / 4 - 1, FF_M = 2 * FF_K + 1, FF_KZ = FF_K + 1;
 constexpr int FF_NP = FF_L, FF_FZ = FF_NP / 2 + 1;
@@ -237,14 +239,17 @@ __global__ void __launch_bounds__(FF_NT, 5) pass_y_fast_kernel(PassYFastArgs a)
         }
     }
     __syncthreads();
-#pragma unroll
-    for (int p = 0; p < FF_C; p++) {
+#pragma unroll 1
+    for (int p = 0; p < FF_C; p++) {  // runtime loop: one FFT copy in the instruction cache
+        // coset twiddle e^{-2 pi i p (tl + 16 m) / 1024} = c1 * e^{-2 pi i p m / 64}: one L1 load
+        // per thread and a warp-uniform constant per element (the kernel is L1-bound)
+        const float2 c1 = __ldg(ctw + p * FF_L + tl);
         float2 y[E];
 #pragma unroll
         for (int m = 0; m < E; m++) {
-            const int n = tl + FF_TPL * m;
-            const float2 v = X[line * FF_LS + pad(n)];
-            y[m] = p ? cmul(v, __ldg(ctw + p * FF_L + n)) : v;
+            const float2 v = X[line * FF_LS + pad(tl + FF_TPL * m)];
+            const int e = (p * m) & 63;
+            y[m] = p ? cmul(v, cmul(c1, make_float2(c_w64.re[e], c_w64.im[e]))) : v;
         }
         fft_regs<FF_L, -1, true>(y, Ab + line * FF_LS, Ab + line * FF_LS, tw, tl);
         __syncwarp();
