@@ -16,7 +16,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libballcorr.so")
+# BALLCORR_LIB: an alternative in-tree build (development A/B timing); default lib/libballcorr.so
+LIB_PATH = os.environ.get("BALLCORR_LIB") or os.path.join(_HERE, "lib", "libballcorr.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
