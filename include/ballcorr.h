@@ -140,6 +140,20 @@ bc_status bc_spectrum_A(bc_ctx *ctx, void *stream);
 bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, int out_kind,
                                  void *out, void *stream);
 
+/*
+ * Time-critical single-configuration query: f_R(t) at n
+ * arbitrary configurations (R_q, t_q), off the translation grid, evaluated EXACTLY as the
+ * pair-lens sum of the combinatorial route (eq_ORP / eq_convgP) over the pairs
+ * that overlap (uniform grid of A's centres); fp64, any mode.  The spectral grid of
+ * bc_correlate_rotations approximates the same f within its band error.
+ *   R:   host or device, n row-major 3x3 doubles (validated as for bc_correlate_rotations).
+ *   t:   host or device, n x 3 doubles (finite).
+ *   out: host or device, n doubles (REAL weights) or 2n interleaved (COMPLEX: Re, Im).
+ * Device out: asynchronous on `stream`; host out: returns after the values are written.
+ */
+bc_status bc_evaluate_points(bc_ctx *ctx, const double *R, const double *t, int64_t n, double *out,
+                             void *stream);
+
 /* Last error message of the context (static string if ctx == NULL). */
 const char *bc_last_error(const bc_ctx *ctx);
 const char *bc_status_string(int status);

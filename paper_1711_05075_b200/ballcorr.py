@@ -57,6 +57,8 @@ _lib.bc_spectrum_A.argtypes = [_vp, _vp]
 _lib.bc_spectrum_A.restype = ctypes.c_int
 _lib.bc_correlate_rotations.argtypes = [_vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, _vp]
 _lib.bc_correlate_rotations.restype = ctypes.c_int
+_lib.bc_evaluate_points.argtypes = [_vp, _vp, _vp, ctypes.c_int64, _vp, _vp]
+_lib.bc_evaluate_points.restype = ctypes.c_int
 _lib.bc_last_error.argtypes = [_vp]
 _lib.bc_last_error.restype = ctypes.c_char_p
 _lib.bc_status_string.argtypes = [ctypes.c_int]
@@ -216,6 +218,24 @@ class Correlator:
         po, ko = _ptr(out)
         self._check(_lib.bc_correlate_rotations(self._ctx, pr, n_rot, kind, po, _stream_handle(stream)))
         return out
+
+    def evaluate_points(self, R, t, out=None, stream=None):
+        """f_R(t) at n arbitrary configurations (exact pair-lens sum, fp64): R (n, 3, 3) and
+        t (n, 3), host numpy / torch (host or cuda).  Returns float64 (n,) or complex128 (n,)
+        when allocated here; `out` may be a preallocated float64 buffer (n or (n, 2))."""
+        Rv = _as_f64(R)
+        tv = _as_f64(t)
+        n = int(Rv.shape[0])
+        if tuple(tv.shape) != (n, 3):
+            raise ValueError("t must have shape (n, 3)")
+        ret_complex = out is None and self.complex
+        if out is None:
+            out = np.empty((n, 2) if self.complex else (n,), dtype=np.float64)
+        pr, kr = _ptr(Rv)
+        pt, kt = _ptr(tv)
+        po, ko = _ptr(out)
+        self._check(_lib.bc_evaluate_points(self._ctx, pr, pt, n, po, _stream_handle(stream)))
+        return out[:, 0] + 1j * out[:, 1] if ret_complex else out
 
     # -- introspection / profiling
     def query(self, key):

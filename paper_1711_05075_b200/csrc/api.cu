@@ -112,6 +112,14 @@ struct bc_ctx {
     int part_cap = 0;
     int batch = 1;
 
+    // single-configuration query: uniform grid of A's centres (built on first use)
+    bool qgrid_ready = false;
+    int *d_qstart = nullptr, *d_qidx = nullptr;
+    int qn[3] = {0, 0, 0};
+    double qg0[3] = {0, 0, 0}, qcs = 0;
+    double *d_qR = nullptr, *d_qt = nullptr, *d_qpart = nullptr, *d_qout = nullptr;
+    int64_t q_cap = 0;
+
     int64_t launches = 0;
     bool prof = false;
     std::vector<PendingEvent> pending;
@@ -641,6 +649,51 @@ bc_status build_spread_z_tables(bc_ctx *ctx)
 
 bool use_spread_z(const bc_ctx *ctx) { return ctx->plan[1].ok && ctx->plan[1].blob; }
 
+// Uniform grid of A's centres for bc_evaluate_points: cell size cs >= max r_A + max s_B, so
+// every A ball overlapping a B ball centred at c lies in the 27 cells around c.  CSR, ball
+// order within each cell (deterministic sums).  At most 128 cells per axis.
+bc_status build_query_grid(bc_ctx *ctx)
+{
+    const std::vector<double> &x = ctx->hxyzr[0];
+    const int64_t nA = ctx->n[0];
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300}, ra = 0, sb = 0;
+    for (int64_t i = 0; i < nA; i++) {
+        for (int d = 0; d < 3; d++) {
+            lo[d] = std::min(lo[d], x[4 * i + d]);
+            hi[d] = std::max(hi[d], x[4 * i + d]);
+        }
+        ra = std::max(ra, x[4 * i + 3]);
+    }
+    for (int64_t j = 0; j < ctx->n[1]; j++) sb = std::max(sb, ctx->hxyzr[1][4 * j + 3]);
+    double cs = ra + sb;
+    for (int d = 0; d < 3; d++) cs = std::max(cs, (hi[d] - lo[d]) / 127.0);
+    cs *= 1.0 + 1e-9;
+    int nc = 1;
+    for (int d = 0; d < 3; d++) {
+        ctx->qg0[d] = lo[d];
+        ctx->qn[d] = std::max(1, (int)std::floor((hi[d] - lo[d]) / cs) + 1);
+        nc *= ctx->qn[d];
+    }
+    ctx->qcs = cs;
+    std::vector<int> cell((size_t)nA), start((size_t)nc + 1, 0), idx((size_t)std::max<int64_t>(nA, 1));
+    for (int64_t i = 0; i < nA; i++) {
+        int g[3];
+        for (int d = 0; d < 3; d++)
+            g[d] = std::min(ctx->qn[d] - 1, std::max(0, (int)std::floor((x[4 * i + d] - lo[d]) / cs)));
+        cell[i] = (g[0] * ctx->qn[1] + g[1]) * ctx->qn[2] + g[2];
+        start[cell[i] + 1]++;
+    }
+    for (int c = 0; c < nc; c++) start[c + 1] += start[c];
+    std::vector<int> fill(start.begin(), start.end() - 1);
+    for (int64_t i = 0; i < nA; i++) idx[fill[cell[i]]++] = (int)i;
+    TRY(dalloc(ctx, &ctx->d_qstart, sizeof(int) * start.size()));
+    TRY(dalloc(ctx, &ctx->d_qidx, sizeof(int) * idx.size()));
+    CU(ctx, cudaMemcpy(ctx->d_qstart, start.data(), sizeof(int) * start.size(), cudaMemcpyHostToDevice));
+    CU(ctx, cudaMemcpy(ctx->d_qidx, idx.data(), sizeof(int) * idx.size(), cudaMemcpyHostToDevice));
+    ctx->qgrid_ready = true;
+    return BC_OK;
+}
+
 bc_status build_csr_A(bc_ctx *ctx)
 {
     const ShapePlan &pl = ctx->plan[0];
@@ -1025,6 +1078,12 @@ bc_status bc_destroy(bc_ctx *ctx)
     dfree(ctx->d_szcnt);
     dfree(ctx->d_szoff);
     dfree(ctx->d_szlist);
+    dfree(ctx->d_qstart);
+    dfree(ctx->d_qidx);
+    dfree(ctx->d_qR);
+    dfree(ctx->d_qt);
+    dfree(ctx->d_qpart);
+    dfree(ctx->d_qout);
     dfree(ctx->d_Ahat);
     dfree(ctx->d_Ahat_cm);
     dfree(ctx->d_xtab);
@@ -1079,6 +1138,7 @@ bc_status bc_shape_upload(bc_ctx *ctx, int which, const double *xyzr, const doub
     }
     ctx->n[which] = n;
     ctx->have[which] = true;
+    ctx->qgrid_ready = false;
     if (which == 0) ctx->have_spec = false;
     ctx->cm_ready = false;
     TRY(upload_shape_device(ctx, which));
@@ -1421,6 +1481,78 @@ bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, in
         CU(ctx, cudaStreamSynchronize(s));
     }
     if (ctx->prof) collect_profile(ctx);
+    return BC_OK;
+}
+
+bc_status bc_evaluate_points(bc_ctx *ctx, const double *R, const double *t, int64_t n, double *out, void *stream)
+{
+    if (!ctx) return BC_EINVAL;
+    if (!R || !t || !out || n < 1) return fail(ctx, BC_EINVAL, "NULL R/t/out or n < 1");
+    if (!ctx->have[0] || !ctx->have[1]) return fail(ctx, BC_ESTATE, "upload both shapes first");
+    CU(ctx, cudaSetDevice(ctx->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool cplx = ctx->p.weights == BC_WEIGHTS_COMPLEX;
+    std::vector<double> hR, ht;
+    TRY(fetch_host(ctx, R, (size_t)n * 9, hR));
+    TRY(fetch_host(ctx, t, (size_t)n * 3, ht));
+    TRY(validate_rotations(ctx, hR, n));
+    for (double v : ht)
+        if (!std::isfinite(v)) return fail(ctx, BC_EINVAL, "non-finite translation");
+    const size_t out_per = cplx ? 2 : 1;
+    const bool host_out = !is_device_ptr(out);
+    if (ctx->n[0] == 0 || ctx->n[1] == 0) {
+        if (host_out)
+            std::fill(out, out + out_per * n, 0.0);
+        else
+            CU(ctx, cudaMemsetAsync(out, 0, sizeof(double) * out_per * n, s));
+        return BC_OK;
+    }
+    if (!ctx->qgrid_ready) TRY(build_query_grid(ctx));
+    const int64_t chunk = std::min<int64_t>(n, 65535);
+    const int nblk = query_blocks((int)ctx->n[1]);
+    if (ctx->q_cap < chunk) {
+        TRY(dalloc(ctx, &ctx->d_qR, sizeof(double) * 9 * chunk));
+        TRY(dalloc(ctx, &ctx->d_qt, sizeof(double) * 3 * chunk));
+        TRY(dalloc(ctx, &ctx->d_qpart, sizeof(double) * 2 * nblk * chunk));
+        TRY(dalloc(ctx, &ctx->d_qout, sizeof(double) * 2 * chunk));
+        ctx->q_cap = chunk;
+    }
+    for (int64_t q0 = 0; q0 < n; q0 += chunk) {
+        const int nq = (int)std::min<int64_t>(chunk, n - q0);
+        CU(ctx, cudaMemcpyAsync(ctx->d_qR, hR.data() + 9 * q0, sizeof(double) * 9 * nq, cudaMemcpyHostToDevice, s));
+        CU(ctx, cudaMemcpyAsync(ctx->d_qt, ht.data() + 3 * q0, sizeof(double) * 3 * nq, cudaMemcpyHostToDevice, s));
+        QueryArgs qa{};
+        qa.nq = nq;
+        qa.nB = (int)ctx->n[1];
+        qa.R = ctx->d_qR;
+        qa.t = ctx->d_qt;
+        qa.A = ctx->d_balls64[0];
+        qa.B = ctx->d_balls64[1];
+        qa.wA = ctx->d_w64[0];
+        qa.wB = ctx->d_w64[1];
+        qa.start = ctx->d_qstart;
+        qa.idx = ctx->d_qidx;
+        qa.nx = ctx->qn[0];
+        qa.ny = ctx->qn[1];
+        qa.nz = ctx->qn[2];
+        qa.gx0 = ctx->qg0[0];
+        qa.gy0 = ctx->qg0[1];
+        qa.gz0 = ctx->qg0[2];
+        qa.inv_cs = 1.0 / ctx->qcs;
+        qa.partial = ctx->d_qpart;
+        qa.out = host_out ? ctx->d_qout : out + out_per * q0;
+        qa.complex_w = cplx;
+        {
+            StageScope sc(ctx, s, "evaluate_points");
+            launch_query(qa, s);
+            ctx->launches += 2;
+        }
+        CU(ctx, cudaGetLastError());
+        if (host_out) {
+            CU(ctx, cudaMemcpyAsync(out + out_per * q0, ctx->d_qout, sizeof(double) * out_per * nq, cudaMemcpyDeviceToHost, s));
+            CU(ctx, cudaStreamSynchronize(s));
+        }
+    }
     return BC_OK;
 }
 

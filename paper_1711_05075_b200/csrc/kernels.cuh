@@ -241,3 +241,19 @@ struct ExactOutArgs {
     long long *partial_idx;
 };
 void launch_exact_out(const ExactOutArgs &a, int batch, cudaStream_t s, int *launches);
+
+// ----------------------------------------------------------------- single-configuration query (query.cu)
+struct QueryArgs {
+    int nq, nB;
+    const double *R, *t;            // [nq][9], [nq][3]
+    const double4 *A, *B;           // (x, y, z, r)
+    const double2 *wA, *wB;         // (re, im)
+    const int *start, *idx;         // A's uniform grid: CSR over cells (ball order within a cell)
+    int nx, ny, nz;
+    double gx0, gy0, gz0, inv_cs;
+    double *partial;                // [nq][blocks][2]
+    double *out;                    // [nq] (real) or [nq][2] (complex)
+    int complex_w;
+};
+int query_blocks(int nB);
+void launch_query(const QueryArgs &a, cudaStream_t s);
