@@ -572,12 +572,12 @@ double gl_integrate(Fn f, double a, double b, int panels = 16)
 //   g(s, d) = Phi1(s-d) + Phi1(s+d) - (Phi2(s-d) - Phi2(s+d)) / d,
 //   Phi1(u) = sgn(u) 2 pi [int_0^|u| t^2 phi + |u| Q(|u|)],   Phi2(u) = pi int_|u|^W t (t^2 - u^2) phi,
 //   Q(a) = int_a^W t phi,  Phi1 = +-1/2 and Phi2 = 0 for |u| >= W;
-// cubic Hermite pieces of width W/128 on [-W, W] (fp64 -> fp32), and per ball the d -> 0
+// cubic Hermite pieces of width W/48 on [-W, W] (fp64 -> fp32), and per ball the d -> 0
 // series g = g0 + g2 d^2 with g0(s) = 2 Phi1(s) - 4 pi s Q(s), g2(s) = (2 pi / 3) s^2 phi'(s).
 bc_status build_spread_z_tables(bc_ctx *ctx)
 {
     const ShapePlan &pl = ctx->plan[1];
-    const double U = kBlobW, D = kBlobW / 128;
+    const double U = kBlobW, D = kBlobW / 48;  // cubic Hermite error ~2e-7 of the unit density
     auto Q = [&](double a) { return a >= U ? 0.0 : gl_integrate([](double t) { return t * blob_phi(t); }, a, U); };
     auto M2 = [&](double a) { return gl_integrate([](double t) { return t * t * blob_phi(t); }, 0, std::min(a, U)); };
     auto phi1 = [&](double u) {

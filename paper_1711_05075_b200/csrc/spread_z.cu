@@ -131,22 +131,25 @@ __global__ void __launch_bounds__(256) szb_fill_kernel(SzBinArgs a)
 }
 
 // ============================================================================ spread + z transform
-// FFT phase: NG = 128 / TPL thread groups (the other half of the block idles) keep the
-// exchange buffer small enough for 3 blocks / SM.
+// Block = 128 threads, 4 x 4 columns (full z).  Spreading: warp w owns the 4 columns
+// (X0 + w, Y0 + g), g = lane / 8; the 8 lanes of a group step along the ball's chord of
+// their column 8 cells at a time (a ~15-cell chord takes 2 steps at ~94% lane use), so one
+// ball visit serves 4 columns.  FFT phase: 128 / TPL thread groups, one pair-line each.
 template <int L>
-__global__ void __launch_bounds__(256, 3) spread_z_kernel(SpreadZArgs a)
+__global__ void __launch_bounds__(128, 4) spread_z_kernel(SpreadZArgs a)
 {
-    constexpr int TPL = Plan<L>::TPL, E = L / TPL, NG = 128 / TPL;
+    constexpr int NT = 128;
+    constexpr int TPL = Plan<L>::TPL, E = L / TPL, NG = NT / TPL;
     constexpr int LS = line_stride(L);
-    static_assert(256 % TPL == 0 && Plan<L>::n == 2 && warp_local<L>(), "spread_z plan");
+    static_assert(NT % TPL == 0 && NG >= SZ_LINES && Plan<L>::n == 2 && warp_local<L>(), "spread_z plan");
     extern __shared__ float4 smz[];
     const int K = a.K, M = 2 * a.K + 1, Kz = a.K + 1;
     // layout: phi table | tw | Abuf (NG lines) | region {acc  /  zb}
     float4 *phi = smz;
     float2 *tw = (float2 *)(phi + 2 * a.phi_n);
     float2 *Abuf = tw + L;
-    constexpr int CS = L + 16;                        // column stride: the two half-warps of a warp
-                                                      // (adjacent columns) sit 16 banks apart
+    constexpr int CS = L + 8;                         // column stride: the 4 lane groups of a warp
+                                                      // (4 columns) sit 8 banks apart
     float *acc = (float *)(Abuf + NG * LS);           // [16][CS]
     float2 *zb = (float2 *)acc;                       // [8][M] (after the spread)
 
@@ -160,7 +163,7 @@ __global__ void __launch_bounds__(256, 3) spread_z_kernel(SpreadZArgs a)
         const float dx = fmaxf(fmaxf((float)X0 - a.cx, a.cx - (float)(X0 + 3)), 0.f);
         const float dy = fmaxf(fmaxf((float)Y0 - a.cy, a.cy - (float)(Y0 + 3)), 0.f);
         if (dx * dx + dy * dy > a.live_r2) {
-            for (int e = threadIdx.x; e < SZ_COLS * Kz; e += 256) {
+            for (int e = threadIdx.x; e < SZ_COLS * Kz; e += NT) {
                 const int col = e / Kz, k = e % Kz;
                 T1[((long long)(X0 + (col >> 2)) * L + Y0 + (col & 3)) * Kz + k] = make_float2(0.f, 0.f);
             }
@@ -168,16 +171,16 @@ __global__ void __launch_bounds__(256, 3) spread_z_kernel(SpreadZArgs a)
         }
     }
 
-    for (int e = threadIdx.x; e < 2 * a.phi_n; e += 256) phi[e] = a.phi[e];
-    load_twiddles<L>(tw, a.tw, threadIdx.x, 256);
-    for (int e = threadIdx.x; e < SZ_COLS * CS; e += 256) acc[e] = 0.f;
+    for (int e = threadIdx.x; e < 2 * a.phi_n; e += NT) phi[e] = a.phi[e];
+    load_twiddles<L>(tw, a.tw, threadIdx.x, NT);
+    for (int e = threadIdx.x; e < SZ_COLS * CS; e += NT) acc[e] = 0.f;
 
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int h = lane >> 4, hl = lane & 15;
-    const int col = 2 * wid + h;
-    const float fx = (float)(X0 + (col >> 2)), fy = (float)(Y0 + (col & 3));
+    const int gi = lane >> 3, hl = lane & 7;
+    const int col = 4 * wid + gi;                     // = (cx << 2) | cy
+    const float fx = (float)(X0 + wid), fy = (float)(Y0 + gi);
+    const float fy0 = (float)Y0;
     float *accc = acc + col * CS;
-    const float fyw = (float)(Y0 + ((2 * wid) & 3));  // the warp's columns: (fx, fyw) and (fx, fyw + 1)
     const float U = a.phi_U, invD = a.phi_invD;
     const float tmax = (float)a.phi_n - 1e-3f;
     const int bin = (X0 / SZ_BIN) * (L / SZ_BIN) + Y0 / SZ_BIN;
@@ -187,8 +190,7 @@ __global__ void __launch_bounds__(256, 3) spread_z_kernel(SpreadZArgs a)
     __syncthreads();
 
     // ---- accumulate the bin's balls (ball order) into this lane's cells.  The warp keeps the
-    // balls whose footprint reaches one of its two columns (ballot); a half-warp covers the
-    // ball's chord of its column in 16-cell steps from the chord start: within a step the lanes
+    // balls whose footprint reaches one of its four columns (ballot); within a step the lanes
     // touch distinct cells, steps and balls are sequential, so the sums are race-free and in
     // ball order (deterministic).
     for (int base0 = 0; base0 < cnt; base0 += 32) {
@@ -198,7 +200,7 @@ __global__ void __launch_bounds__(256, 3) spread_z_kernel(SpreadZArgs a)
             jl = lst[base0 + lane];
             const float4 uc = recA[jl];
             const float ddx = fx - uc.x;
-            const float ddy = fmaxf(fmaxf(fyw - uc.y, uc.y - (fyw + 1.f)), 0.f);
+            const float ddy = fmaxf(fmaxf(fy0 - uc.y, uc.y - (fy0 + 3.f)), 0.f);
             rel = fmaf(ddx, ddx, ddy * ddy) < uc.w;
         }
         unsigned msk = __ballot_sync(0xffffffffu, rel);
@@ -215,13 +217,14 @@ __global__ void __launch_bounds__(256, 3) spread_z_kernel(SpreadZArgs a)
                 const float hz = hz2 * rsqrtf(hz2);
                 zlo = max(0, (int)ceilf(ue.z - hz));
                 zhi = min(L - 1, (int)floorf(ue.z + hz));
-                nit = (zhi - zlo + 16) >> 4;
+                nit = (zhi - zlo + 8) >> 3;
             }
-            const int nmax = max(nit, __shfl_xor_sync(0xffffffffu, nit, 16));
+            int nmax = max(nit, __shfl_xor_sync(0xffffffffu, nit, 8));
+            nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, 16));
             if (nmax <= 0) continue;
             const float4 we = a.recB[j];  // (s, w, g0, g2)
             for (int it = 0; it < nmax; it++) {
-                const int z = zlo + (it << 4) + hl;
+                const int z = zlo + (it << 3) + hl;
                 if (z <= zhi) {
                     const float dz = (float)z - ue.z;
                     const float d2 = fmaf(dz, dz, dxy2);
@@ -245,24 +248,23 @@ __global__ void __launch_bounds__(256, 3) spread_z_kernel(SpreadZArgs a)
 
     // ---- z transform: line l = columns (2l, 2l+1); group g handles line g % 8, cosets g/8 + (NG/8) r
     const int g = threadIdx.x / TPL, tl = threadIdx.x % TPL;
-    const bool fft_thread = g < NG;
     const int line = g % SZ_LINES;
     float2 x[E];
 #pragma unroll
     for (int m = 0; m < E; m++) {
         const int n = tl + TPL * m;
-        x[m] = fft_thread ? make_float2(acc[(2 * line) * CS + n], acc[(2 * line + 1) * CS + n]) : make_float2(0.f, 0.f);
+        x[m] = make_float2(acc[(2 * line) * CS + n], acc[(2 * line + 1) * CS + n]);
     }
-    __syncthreads();  // acc / lists dead: zb may overwrite them
+    __syncthreads();  // acc dead: zb may overwrite it
     const int c = a.c, G = a.G;
     const int rounds = (SZ_LINES * c + NG - 1) / NG;
     for (int r = 0; r < rounds; r++) {
         const int p = g / SZ_LINES + (NG / SZ_LINES) * r;
-        const bool active = fft_thread && p < c;
+        const bool active = p < c;
         float2 y[E];
 #pragma unroll
         for (int m = 0; m < E; m++) y[m] = (active && p) ? cmul(x[m], a.ctw[p * L + tl + TPL * m]) : x[m];
-        if (fft_thread) fft_regs<L, -1, true>(y, Abuf + g * LS, Abuf + g * LS, tw, tl);  // warp-uniform branch
+        fft_regs<L, -1, true>(y, Abuf + g * LS, Abuf + g * LS, tw, tl);
         if (active) {
 #pragma unroll
             for (int m = 0; m < E; m++) {
@@ -275,7 +277,7 @@ __global__ void __launch_bounds__(256, 3) spread_z_kernel(SpreadZArgs a)
     }
     __syncthreads();  // zb complete
     // ---- unpack the column pairs, multiply by mult_z, store T1 rows (contiguous in kz)
-    for (int e = threadIdx.x; e < SZ_LINES * Kz; e += 256) {
+    for (int e = threadIdx.x; e < SZ_LINES * Kz; e += NT) {
         const int l = e / Kz, k = e % Kz;
         const float2 Z = zb[l * M + K + k], Zm = zb[l * M + K - k];
         const float2 mu = a.mult_z[k];
@@ -294,10 +296,10 @@ static void spread_z_launch(const SpreadZArgs &a, int batch, cudaStream_t s)
 {
     constexpr int NG = 128 / Plan<L>::TPL;
     const int tpa = L / 4;
-    const size_t region = std::max((size_t)SZ_COLS * (L + 16) * 4, (size_t)SZ_LINES * (2 * a.K + 1) * 8);
+    const size_t region = std::max((size_t)SZ_COLS * (L + 8) * 4, (size_t)SZ_LINES * (2 * a.K + 1) * 8);
     const size_t sm = (size_t)a.phi_n * 32 + (size_t)L * 8 + (size_t)NG * line_stride(L) * 8 + region;
     cudaFuncSetAttribute(spread_z_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    spread_z_kernel<L><<<dim3(tpa * tpa, batch), 256, sm, s>>>(a);
+    spread_z_kernel<L><<<dim3(tpa * tpa, batch), 128, sm, s>>>(a);
 }
 
 int spread_z_bins(int L) { return (L / SZ_BIN) * (L / SZ_BIN); }
