@@ -606,9 +606,9 @@ bc_status build_spread_z_tables(bc_ctx *ctx)
         v2[i] = phi2(u);
         d2[i] = dphi2(u) * D;
     }
-    for (int i = 0; i < n; i++) {
-        tab[2 * i] = herm(v1[i], d1[i], v1[i + 1], d1[i + 1]);
-        tab[2 * i + 1] = herm(v2[i], d2[i], v2[i + 1], d2[i + 1]);
+    for (int i = 0; i < n; i++) {  // [n] Phi1 pieces, then [n] Phi2 pieces
+        tab[i] = herm(v1[i], d1[i], v1[i + 1], d1[i + 1]);
+        tab[n + i] = herm(v2[i], d2[i], v2[i + 1], d2[i + 1]);
     }
     const int64_t nb = ctx->n[1];
     const size_t cnt = (size_t)std::max<int64_t>(nb, 1);

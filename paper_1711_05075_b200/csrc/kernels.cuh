@@ -61,7 +61,7 @@ struct SpreadZArgs {
     const int *counts, *offs, *lists;  // the bins (SzBinArgs)
     int nbins;
     long long list_stride;
-    const float4 *phi;      // [phi_n][2] cubic pieces of (Phi1, Phi2) on [-U, U]
+    const float4 *phi;      // cubic pieces on [-U, U]: [phi_n] of Phi1, then [phi_n] of Phi2
     int phi_n;
     float phi_U, phi_invD;
     float cx, cy, live_r2;  // support cylinder of R B (any R): centre (cells) and radius^2

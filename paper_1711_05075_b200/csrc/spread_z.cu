@@ -37,12 +37,14 @@ struct PhiVal {
 
 // (Phi1, Phi2)(u) from the cubic pieces; u is clamped to the table, whose end knots carry the
 // exact limits (Phi1(+-U) = +-1/2, Phi2(+-U) = 0, zero slopes), so no range branch is needed.
-__device__ __forceinline__ PhiVal phi_lookup(const float4 *__restrict__ tab, float tmax, float U, float invD, float u)
+// tab = [n] Phi1 pieces followed by [n] Phi2 pieces (split arrays: a 16-byte load at a random
+// piece hits one of 8 bank groups, where interleaved 32-byte records would hit one of 4)
+__device__ __forceinline__ PhiVal phi_lookup(const float4 *__restrict__ tab, int n, float tmax, float U, float invD, float u)
 {
     const float t = fminf(fmaxf((u + U) * invD, 0.f), tmax);
     const int i = (int)t;
     const float f = t - (float)i;
-    const float4 a = tab[2 * i], b = tab[2 * i + 1];
+    const float4 a = tab[i], b = tab[n + i];
     return PhiVal{fmaf(f, fmaf(f, fmaf(f, a.w, a.z), a.y), a.x), fmaf(f, fmaf(f, fmaf(f, b.w, b.z), b.y), b.x)};
 }
 
@@ -183,6 +185,7 @@ __global__ void __launch_bounds__(128, 4) spread_z_kernel(SpreadZArgs a)
     float *accc = acc + col * CS;
     const float U = a.phi_U, invD = a.phi_invD;
     const float tmax = (float)a.phi_n - 1e-3f;
+    const int nphi = a.phi_n;
     const int bin = (X0 / SZ_BIN) * (L / SZ_BIN) + Y0 / SZ_BIN;
     const int cnt = a.counts[b * a.nbins + bin];
     const int *lst = a.lists + (long long)b * a.list_stride + a.offs[b * a.nbins + bin];
@@ -234,9 +237,9 @@ __global__ void __launch_bounds__(128, 4) spread_z_kernel(SpreadZArgs a)
                     } else {
                         const float rd = rsqrtf(d2);
                         const float d = d2 * rd;
-                        const PhiVal p = phi_lookup(phi, tmax, U, invD, we.x - d);
+                        const PhiVal p = phi_lookup(phi, nphi, tmax, U, invD, we.x - d);
                         PhiVal q = PhiVal{0.5f, 0.f};
-                        if (we.x + d < U) q = phi_lookup(phi, tmax, U, invD, we.x + d);
+                        if (we.x + d < U) q = phi_lookup(phi, nphi, tmax, U, invD, we.x + d);
                         g = p.p1 + q.p1 - (p.p2 - q.p2) * rd;
                     }
                     accc[z] = fmaf(we.y, g, accc[z]);
