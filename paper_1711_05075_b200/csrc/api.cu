@@ -811,6 +811,8 @@ bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, voi
         a.cx = (float)(-pl.o[0]);
         a.cy = (float)(-pl.o[1]);
         a.live_r2 = (float)(ctx->live_r * ctx->live_r);
+        a.zero_r2 = (float)((ctx->live_r + 1) * (ctx->live_r + 1));
+        a.skip_zero = pass_y_fast_supported(L, pl.c, pl.G, ctx->K, cplx) ? 1 : 0;
         a.mult_z = pl.d_mult[2];
         a.tw = tw;
         a.ctw = pl.d_ctw;
@@ -1167,7 +1169,7 @@ bc_status bc_shape_upload(bc_ctx *ctx, int which, const double *xyzr, const doub
                     const double cx = -pb.o[0], cy = -pb.o[1];
                     const double dx = std::max(std::max(X0 - cx, cx - (X0 + 3)), 0.0);
                     const double dy = std::max(std::max(Y0 - cy, cy - (Y0 + 3)), 0.0);
-                    if (dx * dx + dy * dy <= ctx->live_r * ctx->live_r) ctx->live_tiles_B++;
+                    if (dx * dx + dy * dy <= (ctx->live_r + 1) * (ctx->live_r + 1)) ctx->live_tiles_B++;
                 }
             if (ctx->plan[1].blob) TRY(build_spread_z_tables(ctx));
         }

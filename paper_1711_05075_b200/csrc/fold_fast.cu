@@ -218,10 +218,10 @@ __global__ void __launch_bounds__(FF_NT, 5) pass_y_fast_kernel(PassYFastArgs a)
     const float dxl = (float)ix - a.cx;
     const float h2 = a.live_r2 - dxl * dxl;
     int ylo = 0, yhi = -1;
-    if (h2 > 0.f) {
+    if (h2 > 0.f) {  // rows within live_r (spread_z writes every tile within live_r + 1)
         const float hh = sqrtf(h2);
-        ylo = max(0, (int)floorf(a.cy - hh));
-        yhi = min(FF_L - 1, (int)ceilf(a.cy + hh));
+        ylo = max(0, (int)ceilf(a.cy - hh));
+        yhi = min(FF_L - 1, (int)floorf(a.cy + hh));
     }
     load_twiddles<FF_L>(tw, a.tw, threadIdx.x, FF_NT);
     {

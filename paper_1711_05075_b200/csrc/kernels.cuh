@@ -65,6 +65,8 @@ struct SpreadZArgs {
     int phi_n;
     float phi_U, phi_invD;
     float cx, cy, live_r2;  // support cylinder of R B (any R): centre (cells) and radius^2
+    float zero_r2;          // tiles farther than sqrt(zero_r2) from the axis are zero
+    int skip_zero;          // 1: do not write the zero tiles (the y pass never reads them)
     const float2 *mult_z;   // [K + 1]
     const float2 *tw;       // exp(-2 pi i m / L)
     const float2 *ctw;      // [c][L]

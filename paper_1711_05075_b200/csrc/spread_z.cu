@@ -160,11 +160,14 @@ __global__ void __launch_bounds__(128, 4) spread_z_kernel(SpreadZArgs a)
     const int X0 = (blockIdx.x / tpa) * 4, Y0 = (blockIdx.x % tpa) * 4;
     float2 *T1 = a.out + (long long)b * a.out_bstride;
 
-    // tiles outside B's (rotation-invariant) support cylinder: T1 rows are zero
+    // tiles outside B's (rotation-invariant) support cylinder: T1 rows are zero.  When the
+    // consumer is pass_y_fast (skip_zero) they are never read (it loads only rows within
+    // live_r, and zero tiles lie beyond live_r + 1), so nothing is written.
     {
         const float dx = fmaxf(fmaxf((float)X0 - a.cx, a.cx - (float)(X0 + 3)), 0.f);
         const float dy = fmaxf(fmaxf((float)Y0 - a.cy, a.cy - (float)(Y0 + 3)), 0.f);
-        if (dx * dx + dy * dy > a.live_r2) {
+        if (dx * dx + dy * dy > a.zero_r2) {
+            if (a.skip_zero) return;
             for (int e = threadIdx.x; e < SZ_COLS * Kz; e += NT) {
                 const int col = e / Kz, k = e % Kz;
                 T1[((long long)(X0 + (col >> 2)) * L + Y0 + (col & 3)) * Kz + k] = make_float2(0.f, 0.f);
@@ -260,6 +263,7 @@ __global__ void __launch_bounds__(128, 4) spread_z_kernel(SpreadZArgs a)
     }
     __syncthreads();  // acc dead: zb may overwrite it
     const int c = a.c, G = a.G;
+    const bool band4 = c == 4 && G == 1024 && K == 255;  // block-uniform
     const int rounds = (SZ_LINES * c + NG - 1) / NG;
     for (int r = 0; r < rounds; r++) {
         const int p = g / SZ_LINES + (NG / SZ_LINES) * r;
@@ -268,7 +272,16 @@ __global__ void __launch_bounds__(128, 4) spread_z_kernel(SpreadZArgs a)
 #pragma unroll
         for (int m = 0; m < E; m++) y[m] = (active && p) ? cmul(x[m], a.ctw[p * L + tl + TPL * m]) : x[m];
         fft_regs<L, -1, true>(y, Abuf + g * LS, Abuf + g * LS, tw, tl);
-        if (active) {
+        if (L == 256 && band4) {
+            // plan L = 256, c = 4, K = 255: outputs m < 4 (k = 4q + p) and m >= 12
+            // (k = 4q + p - 1024) are the band, minus (p, q) = (0, 192)
+#pragma unroll
+            for (int m = 0; m < E; m++) {
+                if (m >= 4 && m < 12) continue;
+                const int k = 4 * (tl + TPL * m) + p - (m >= 12 ? 1024 : 0);
+                if (m != 12 || p != 0 || tl != 0) zb[line * M + k + K] = y[m];
+            }
+        } else if (active) {
 #pragma unroll
             for (int m = 0; m < E; m++) {
                 int k = c * (tl + TPL * m) + p;
