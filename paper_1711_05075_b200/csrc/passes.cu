@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TP
         float2 y[E];
 #pragma unroll
         for (int m = 0; m < E; m++) y[m] = p ? cmul(x[m], a.ctw[p * L + tl + TPL * m]) : x[m];
-        fft_regs<L, SIGN>(y, A + line * LS, B + line * LS, tw, tl);
+        fft_regs<L, SIGN, warp_local<L>()>(y, A + line * LS, B + line * LS, tw, tl);
         if (OUT_MODE == 0) {
 #pragma unroll
             for (int m = 0; m < E; m++) {
