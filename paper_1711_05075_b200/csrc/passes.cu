@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TP
     const bool valid = IN_MODE == 2 ? (i0 + line < a.I) : (row0 + line < nrows);
 
     load_twiddles<L>(tw, a.tw, threadIdx.x, NT);
+    __syncthreads();  // the table is read across warps (warp-synchronous FFTs do not order it)
     float2 x[E];
     if (IN_MODE == 2) {
         const float2 *in = (const float2 *)a.in + (long long)b * a.in_bstride + (long long)o * L * a.I;
