@@ -15,6 +15,8 @@
 //    or (16 - tl) & 15 (p = 0), in the same 16-lane line: conjugate-pass products move by
 //    warp shuffles;
 //  * A''s coset-major row positions are affine in (tl, m): coalesced 128-byte loads.
+#include <algorithm>
+
 #include "kernels.cuh"
 #include "fft_ct.cuh"
 
@@ -42,15 +44,48 @@ __global__ void __launch_bounds__(FF_NT, 4) fold_fast_kernel(FoldFastArgs a)
     float2 *Ab = X + FF_NL * FF_LS;    // [NL][LS] FFT exchange / staging
     const int line = threadIdx.x / FF_TPL, tl = threadIdx.x % FF_TPL;
     const int lane = threadIdx.x & 31;
-    const int b = blockIdx.x % a.nb;
-    const int tb = blockIdx.x / a.nb;
     constexpr int ZT = (FF_FZ + FF_NL - 1) / FF_NL;
-    const int kyp = tb / ZT;
-    const int z0 = (tb % ZT) * FF_NL;
-    const float2 *T2 = a.T2 + (long long)b * a.t2_bstride;
 
     load_twiddles<FF_L>(tw, a.tw, threadIdx.x, FF_NT);
     for (int e = threadIdx.x; e < FF_C * FF_L; e += FF_NT) ctw[e] = a.ctw[e];
+
+    // persistent blocks: work items w = (target block) * nb + rotation, rotation-fastest (the
+    // nb items sharing A'' rows run together and share them through L2); the tables above are
+    // loaded once per block
+    const int n_items = FF_NP * ZT * a.nb;
+#pragma unroll 1
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+    const int b = w % a.nb;
+    const int tb = w / a.nb;
+    const int kyp = tb / ZT;
+    const int z0 = (tb % ZT) * FF_NL;
+    const float2 *T2 = a.T2 + (long long)b * a.t2_bstride;
+    // the alias groups of this target block: (pass, ky) with ky in the band (block-uniform),
+    // packed 16 bits each ((ky + 512) * 2 + pass) so a runtime group index needs no local memory
+    unsigned long long groups = 0;
+    int ng = 0;
+#pragma unroll
+    for (int pass = 0; pass < 2; pass++)
+#pragma unroll
+        for (int al = 0; al < 2; al++) {
+            const int ky = pass == 0 ? (al == 0 ? kyp : kyp - FF_NP) : (al == 0 ? -kyp : FF_NP - kyp);
+            if (ky >= -FF_K && ky <= FF_K) {
+                groups |= (unsigned long long)((ky + 512) * 2 + pass) << (16 * ng);
+                ng++;
+            }
+        }
+    auto group_ky = [&](int g) { return (int)((groups >> (16 * g)) & 0xffff) / 2 - 512; };
+    auto group_pass = [&](int g) { return (int)((groups >> (16 * g)) & 1); };
+    // L2 prefetch of a group's T2 rows: 256 rows x 64 bytes, two rows per thread
+    auto prefetch_group = [&](int g) {
+        const int ky = group_ky(g), pass = group_pass(g);
+        const int kz = pass == 0 ? z0 : FF_NP - z0 - (FF_NL - 1);  // lowest kz of the 8 lines
+        for (int n = threadIdx.x; n < FF_L; n += FF_NT) {
+            const float2 *p = T2 + (n * FF_M + ky + FF_K) * FF_KZ + max(kz, 0);
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+        }
+    };
+    prefetch_group(0);
 
     // A'' row position of output (m, p) of lane tl: pos_base[p] + tl + 16 m (+ L for m < 4)
     float2 acc[4][FF_C];
@@ -60,14 +95,13 @@ __global__ void __launch_bounds__(FF_NT, 4) fold_fast_kernel(FoldFastArgs a)
         for (int p = 0; p < FF_C; p++) acc[j][p] = make_float2(0.f, 0.f);
 
     const int tz = z0 + line;  // this line's target k'z
+    // direct: kz = k'z in [0, 128], ky in {k'y, k'y - 256};  conjugate partner: kz = 256 - k'z
+    // (k'z in [1, 128]), ky in {-k'y, 256 - k'y}; out-of-band ky / kz contribute nothing
 #pragma unroll 1
-    for (int pass = 0; pass < 2; pass++) {
-        // direct: kz = k'z in [0, 128], ky in {k'y, k'y - 256};  conjugate partner: kz = 256 - k'z
-        // (k'z in [1, 128]), ky in {-k'y, 256 - k'y}; out-of-band ky / kz contribute nothing
-#pragma unroll 1
-        for (int al = 0; al < 2; al++) {
-            const int ky = pass == 0 ? (al == 0 ? kyp : kyp - FF_NP) : (al == 0 ? -kyp : FF_NP - kyp);
-            if (ky < -FF_K || ky > FF_K) continue;  // block-uniform
+    for (int g = 0; g < ng; g++) {
+        const int ky = group_ky(g), pass = group_pass(g);
+        if (g + 1 < ng) prefetch_group(g + 1);
+        {
             // ---- T2 lines (ky, kz(i)) -> X (transposed through registers for coalescing)
             float2 x[E];
 #pragma unroll
@@ -175,6 +209,8 @@ __global__ void __launch_bounds__(FF_NT, 4) fold_fast_kernel(FoldFastArgs a)
         const int i = e % FF_NL, q = e / FF_NL;
         if (z0 + i < FF_FZ) X1[(q * FF_NP + kyp) * FF_FZ + z0 + i] = X[i * FF_LS + pad(q)];
     }
+    __syncthreads();  // X is rewritten by the next item's first group
+    }
 }
 
 bool fold_fast_supported(int L, int c, int G, int K, int Np, int complex_w)
@@ -189,7 +225,12 @@ void launch_fold_fast(const FoldFastArgs &a_in, int batch, cudaStream_t s)
     constexpr int ZT = (FF_FZ + FF_NL - 1) / FF_NL;
     const size_t sm = sizeof(float2) * ((size_t)FF_L + FF_C * FF_L + 2 * FF_NL * FF_LS);
     cudaFuncSetAttribute(fold_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    fold_fast_kernel<<<(unsigned)(FF_NP * ZT * batch), FF_NT, sm, s>>>(a);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long long items = (long long)FF_NP * ZT * batch;
+    const long long grid = std::min<long long>(items, (long long)sms * 4 * 4);  // 4 blocks / SM, 4 waves of items or more
+    fold_fast_kernel<<<(unsigned)grid, FF_NT, sm, s>>>(a);
 }
 
 // ============================================================================ forward y pass
