@@ -132,3 +132,21 @@ def test_sweep_fused_matches_generic(bc):
         assert ma[r, 0]["val"] == pytest.approx(float(a[r].min()), abs=1e-12)
         assert ma[r, 1]["val"] == pytest.approx(float(a[r].max()), abs=1e-12)
         assert a[r].reshape(-1)[ma[r, 1]["idx"]] == ma[r, 1]["val"]
+
+
+def test_sweep_batching_is_bitwise_stable(bc):
+    """The fused plan sums in a fixed order (lane-owned spread cells, register-owned fold
+    targets, order-independent 64-bit extremum keys), so the per-rotation results do not
+    depend on how rotations are batched -- the property the rotation sharding over GPUs
+    (each rank its own batches) relies on.  11 rotations: ragged batches of 8 + 3 and 3 x 3 + 2,
+    and single rotations."""
+    w = make_config("sweep", n_rot=11)
+    r8 = correlator(bc, w, max_batch=8).correlate_rotations(w.R, "minmax")
+    r3 = correlator(bc, w, max_batch=3).correlate_rotations(w.R, "minmax")
+    c1 = correlator(bc, w, max_batch=1)
+    r1 = np.concatenate([c1.correlate_rotations(w.R[i:i + 1], "minmax") for i in (0, 9, 10)])
+    assert np.array_equal(r8, r3)
+    assert np.array_equal(r8[[0, 9, 10]], r1)
+    f8 = correlator(bc, w, max_batch=8).correlate_rotations(w.R[7:10], "full")
+    f1 = c1.correlate_rotations(w.R[8:9], "full")
+    assert np.array_equal(f8[1], f1[0])
