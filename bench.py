@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-slabs", type=int, default=32, help="x-slabs of the 256^3 grid in the oracle sample")
+    ap.add_argument("--max-batch", type=int, default=0, help="rotations per launch (0 = library default)")
+    ap.add_argument("--concurrency", type=int, default=0, help="batches in flight (0 = library default)")
     return ap.parse_args()
 
 
@@ -213,7 +215,8 @@ def run_ours(args, rank, world, local_rank):
     w = make_config(WORKLOAD, n_rot=args.rot_per_rank)
     R = w.R if rank == 0 else random_rotations(np.random.default_rng((0, rank)), args.rot_per_rank)
     n_rot = len(R)
-    kw = correlator_kwargs(WORKLOAD, w.N, w.h, w.t0, w.weights)
+    kw = correlator_kwargs(WORKLOAD, w.N, w.h, w.t0, w.weights, max_batch=args.max_batch,
+                           concurrency=args.concurrency)
     ctx = ballcorr.Correlator(device=local_rank, **kw)
     stream = torch.cuda.current_stream(dev)
     t = time.perf_counter()
@@ -233,8 +236,6 @@ def run_ours(args, rank, world, local_rank):
     sampler = ClockSampler(local_rank)
     sampler.start()
     time.sleep(0.3)
-    ctx.set_profiling(True)
-    ctx.reset_stage_times()
     l0 = ctx.launch_count()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -250,9 +251,21 @@ def run_ours(args, rank, world, local_rank):
         dist.barrier()
     ms = e0.elapsed_time(e1)
     launches = ctx.launch_count() - l0
+    clocks = sampler.stop()
+    # per-stage device times: one more (untimed) step with the library's per-launch CUDA
+    # events on; profiling serialises the batches (no concurrent slots), so shares refer to
+    # this profiled step
+    ctx.set_profiling(True)
+    ctx.reset_stage_times()
+    p0 = torch.cuda.Event(enable_timing=True)
+    p1 = torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    ctx.correlate_rotations(R_dev, kind, out=out, stream=stream)
+    p1.record(stream)
+    torch.cuda.synchronize()
+    prof_ms = p0.elapsed_time(p1)
     stages = ctx.stage_times()
     ctx.set_profiling(False)
-    clocks = sampler.stop()
     t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
@@ -304,7 +317,7 @@ def run_ours(args, rank, world, local_rank):
             continue
         by, fl = work[name]
         avg_s = tot_ms / nl / 1e3
-        per_stage[name] = {"ms_per_rot": tot_ms / (args.steps * n_rot), "share": tot_ms / ms,
+        per_stage[name] = {"ms_per_rot": tot_ms / n_rot, "share": tot_ms / prof_ms,
                            "hbm_GBps": by * batch / avg_s / 1e9, "hbm_frac": by * batch / avg_s / 1e9 / peak,
                            "fp32_TFLOPs": fl * batch / avg_s / 1e12, "alu_frac": fl * batch / avg_s / 1e12 / alu_peak,
                            "flop_per_byte": fl / by}
@@ -342,7 +355,8 @@ def run_ours(args, rank, world, local_rank):
                 "d2h_bytes_per_step": int(n_rot * 16)},
         "roofline": roof,
         "cpu_baseline": cpu,
-        "stages_ms_per_step": {k: v[0] / args.steps for k, v in stages.items()},
+        "stages_ms_per_step": {k: v[0] for k, v in stages.items()},
+        "profiled_step_ms": prof_ms,
         "stages": per_stage,
         "result_sample": {"rot0_min": float(res[0]["val"]), "rot0_argmin": int(res[0]["idx"]),
                           "global_best": best},

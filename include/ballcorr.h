@@ -99,6 +99,9 @@ typedef struct {
     int32_t generic_only; /* spectral: nonzero disables the fused per-plan kernels (spread + z
                              transform, fold + inverse x) and runs the generic passes instead;
                              same result up to fp32 rounding order (a test hook) */
+    int32_t concurrency;  /* spectral: rotation batches in flight on internal streams forked from
+                             and joined to the caller's stream (0 or 1 = one batch at a time, on
+                             the caller's stream; 2 = two) */
 } bc_params;
 
 typedef struct bc_ctx bc_ctx;

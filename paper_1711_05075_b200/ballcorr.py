@@ -41,7 +41,7 @@ class bc_params(ctypes.Structure):
                 ("Np", ctypes.c_int32), ("K", ctypes.c_int32), ("precision", ctypes.c_int32),
                 ("mode", ctypes.c_int32), ("weights", ctypes.c_int32), ("max_batch", ctypes.c_int32),
                 ("spread_eps", ctypes.c_double), ("band_radius", ctypes.c_double),
-                ("generic_only", ctypes.c_int32)]
+                ("generic_only", ctypes.c_int32), ("concurrency", ctypes.c_int32)]
 
 
 EXTREMUM_DTYPE = np.dtype([("val", np.float64), ("idx", np.int64)])
@@ -146,7 +146,7 @@ class Correlator:
     """One libballcorr context on one device."""
 
     def __init__(self, N, h, t0, Np=0, K=0, mode="spectral", precision="f32", weights="real",
-                 max_batch=0, spread_eps=0.0, band_radius=0.0, generic_only=False, device=0):
+                 max_batch=0, spread_eps=0.0, band_radius=0.0, generic_only=False, concurrency=0, device=0):
         p = bc_params()
         p.N = int(N)
         p.h = float(h)
@@ -161,6 +161,7 @@ class Correlator:
         p.spread_eps = float(spread_eps)
         p.band_radius = float(band_radius)
         p.generic_only = int(bool(generic_only))
+        p.concurrency = int(concurrency)
         self.params = p
         self.N = p.N
         self.complex = p.weights == BC_WEIGHTS_COMPLEX

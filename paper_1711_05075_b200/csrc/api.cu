@@ -39,6 +39,20 @@ struct ShapePlan {
     float2 *d_ctw = nullptr;                           // coset twiddles [c][L]
 };
 
+// One rotation batch in flight: workspaces, reduction keys, B's binning buffers and (for
+// concurrent batches) an internal stream.
+struct Slot {
+    void *ws1 = nullptr, *ws2 = nullptr;
+    size_t ws1_bytes = 0, ws2_bytes = 0;
+    unsigned long long *keys = nullptr;
+    int keys_cap = 0;
+    float4 *recA = nullptr;
+    int *szcnt = nullptr, *szoff = nullptr, *szlist = nullptr;
+    int sz_cap = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t done = nullptr;
+};
+
 struct PendingEvent {
     const char *name;
     cudaEvent_t e0, e1;
@@ -77,9 +91,7 @@ struct bc_ctx {
     float2 *d_g02 = nullptr;
     float4 *d_recB = nullptr;      // (s, w, g0, g2) per ball of B (cells)
     double rc_max_B = 0;           // max (s + W) / hf over B
-    float4 *d_recA = nullptr;      // per-rotation binning workspace (spread_z.cu)
-    int *d_szcnt = nullptr, *d_szoff = nullptr, *d_szlist = nullptr;
-    int sz_cap = 0;                // rotations the binning workspace holds
+
     float4 *d_phi = nullptr;
     float *d_dec = nullptr;        // 1 / phi_hat(|k| / G_B) indexed by |k|^2 (blob deconvolution)
     int phi_n = 0;
@@ -96,10 +108,8 @@ struct bc_ctx {
     bool have_spec = false;
 
     // workspaces
-    void *ws1 = nullptr, *ws2 = nullptr;
-    size_t ws1_bytes = 0, ws2_bytes = 0;
-    unsigned long long *d_keys = nullptr;
-    int keys_cap = 0;
+    Slot slot[2];                  // batches in flight (slot 1 only with concurrent batches)
+    cudaEvent_t ev_fork = nullptr;
     float *d_rot = nullptr;
     double *d_rot64 = nullptr;
     int64_t rot_cap = 0;
@@ -632,7 +642,7 @@ bc_status build_spread_z_tables(bc_ctx *ctx)
     }
     TRY(dalloc(ctx, &ctx->d_recB, sizeof(float4) * cnt));
     CU(ctx, cudaMemcpy(ctx->d_recB, rb.data(), sizeof(float4) * cnt, cudaMemcpyHostToDevice));
-    ctx->sz_cap = 0;  // binning workspace is sized for this shape at the next correlate
+    ctx->slot[0].sz_cap = ctx->slot[1].sz_cap = 0;  // binning workspace resized at the next correlate
     TRY(dalloc(ctx, &ctx->d_phi, sizeof(float4) * tab.size()));
     TRY(dalloc(ctx, &ctx->d_bcells, sizeof(float4) * cnt));
     TRY(dalloc(ctx, &ctx->d_g02, sizeof(float2) * cnt));
@@ -754,7 +764,7 @@ void spectral_ws_sizes(const bc_ctx *ctx, int which, size_t &s1, size_t &s2)
 
 // spread + z + y passes of one shape; for A also the x pass into A_hat.
 bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, void *ws1, void *ws2,
-                         size_t s1_per, size_t s2_per, cudaStream_t s)
+                         size_t s1_per, size_t s2_per, cudaStream_t s, Slot &sl)
 {
     const ShapePlan &pl = ctx->plan[which];
     const bool cplx = ctx->p.weights == BC_WEIGHTS_COMPLEX;
@@ -764,12 +774,12 @@ bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, voi
         const int n = (int)ctx->n[1];
         const int nbins = spread_z_bins(L);
         const long long lstride = (long long)n * spread_z_bins_per_ball((float)ctx->rc_max_B);
-        if (ctx->sz_cap < nb) {
-            TRY(dalloc(ctx, &ctx->d_recA, sizeof(float4) * (size_t)n * nb));
-            TRY(dalloc(ctx, &ctx->d_szcnt, sizeof(int) * (size_t)nbins * nb));
-            TRY(dalloc(ctx, &ctx->d_szoff, sizeof(int) * (size_t)nbins * nb));
-            TRY(dalloc(ctx, &ctx->d_szlist, sizeof(int) * (size_t)lstride * nb));
-            ctx->sz_cap = nb;
+        if (sl.sz_cap < nb) {
+            TRY(dalloc(ctx, &sl.recA, sizeof(float4) * (size_t)n * nb));
+            TRY(dalloc(ctx, &sl.szcnt, sizeof(int) * (size_t)nbins * nb));
+            TRY(dalloc(ctx, &sl.szoff, sizeof(int) * (size_t)nbins * nb));
+            TRY(dalloc(ctx, &sl.szlist, sizeof(int) * (size_t)lstride * nb));
+            sl.sz_cap = nb;
         }
         {
             SzBinArgs bn{};
@@ -780,12 +790,12 @@ bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, voi
             bn.oy = (float)pl.o[1];
             bn.oz = (float)pl.o[2];
             bn.cut = (float)(pl.cut / pl.hf);
-            bn.recA = ctx->d_recA;
+            bn.recA = sl.recA;
             bn.bpa = spread_z_bins_per_axis(L);
             bn.nbins = nbins;
-            bn.counts = ctx->d_szcnt;
-            bn.offs = ctx->d_szoff;
-            bn.lists = ctx->d_szlist;
+            bn.counts = sl.szcnt;
+            bn.offs = sl.szoff;
+            bn.lists = sl.szlist;
             bn.list_stride = lstride;
             StageScope sc(ctx, s, "bin_B");
             launch_spread_z_bin(bn, nb, s);
@@ -797,11 +807,11 @@ bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, voi
         a.c = pl.c;
         a.G = pl.G;
         a.n_balls = n;
-        a.recA = ctx->d_recA;
+        a.recA = sl.recA;
         a.recB = ctx->d_recB;
-        a.counts = ctx->d_szcnt;
-        a.offs = ctx->d_szoff;
-        a.lists = ctx->d_szlist;
+        a.counts = sl.szcnt;
+        a.offs = sl.szoff;
+        a.lists = sl.szlist;
         a.nbins = nbins;
         a.list_stride = lstride;
         a.phi = ctx->d_phi;
@@ -1020,6 +1030,7 @@ bc_status bc_create(int device, const bc_params *p, bc_ctx **out)
     if (p->precision != BC_FP32 && p->precision != BC_FP64) return BC_EINVAL;
     if (p->weights != BC_WEIGHTS_REAL && p->weights != BC_WEIGHTS_COMPLEX) return BC_EINVAL;
     if (p->max_batch < 0) return BC_EINVAL;
+    if (p->concurrency < 0 || p->concurrency > 2) return BC_EINVAL;
     if (p->mode == BC_MODE_SPECTRAL) {
         if (p->precision != BC_FP32) return BC_EUNSUPPORTED;
         if (p->Np < p->N || p->Np < 2 || (p->Np % 2) != 0 || !friendly(p->Np) || p->Np > 1024) return BC_EINVAL;
@@ -1076,10 +1087,18 @@ bc_status bc_destroy(bc_ctx *ctx)
     dfree(ctx->d_phi);
     dfree(ctx->d_dec);
     dfree(ctx->d_recB);
-    dfree(ctx->d_recA);
-    dfree(ctx->d_szcnt);
-    dfree(ctx->d_szoff);
-    dfree(ctx->d_szlist);
+    for (Slot &sl : ctx->slot) {
+        if (sl.ws1) cudaFree(sl.ws1);
+        if (sl.ws2) cudaFree(sl.ws2);
+        dfree(sl.keys);
+        dfree(sl.recA);
+        dfree(sl.szcnt);
+        dfree(sl.szoff);
+        dfree(sl.szlist);
+        if (sl.stream) cudaStreamDestroy(sl.stream);
+        if (sl.done) cudaEventDestroy(sl.done);
+    }
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     dfree(ctx->d_qstart);
     dfree(ctx->d_qidx);
     dfree(ctx->d_qR);
@@ -1090,9 +1109,7 @@ bc_status bc_destroy(bc_ctx *ctx)
     dfree(ctx->d_Ahat_cm);
     dfree(ctx->d_xtab);
     dfree(ctx->d_segs);
-    if (ctx->ws1) cudaFree(ctx->ws1);
-    if (ctx->ws2) cudaFree(ctx->ws2);
-    dfree(ctx->d_keys);
+
     dfree(ctx->d_rot);
     dfree(ctx->d_rot64);
     if (ctx->d_out_stage) cudaFree(ctx->d_out_stage);
@@ -1205,7 +1222,7 @@ bc_status bc_spectrum_A(bc_ctx *ctx, void *stream)
         return fail(ctx, BC_ENOMEM, "spectrum_A workspace: %s", cudaGetErrorString(e));
     }
     ctx->cm_ready = false;
-    bc_status st = shape_spectrum(ctx, 0, nullptr, 1, w1, w2, s1, s2, s);
+    bc_status st = shape_spectrum(ctx, 0, nullptr, 1, w1, w2, s1, s2, s, ctx->slot[0]);
     cudaError_t se = cudaStreamSynchronize(s);
     collect_profile(ctx);
     cudaFree(w1);
@@ -1333,15 +1350,28 @@ bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, in
     } else {
         size_t s1, s2;
         spectral_ws_sizes(ctx, 1, s1, s2);
-        int nb = ctx->p.max_batch > 0 ? ctx->p.max_batch : 8;
+        int nb = ctx->p.max_batch > 0 ? ctx->p.max_batch : 16;
         while (nb > 1 && (s1 + s2) * nb > ((size_t)12 << 30)) nb /= 2;
         nb = (int)std::min<int64_t>(nb, n_rot);
         ctx->batch = nb;
-        TRY(ensure_ws(ctx, &ctx->ws1, ctx->ws1_bytes, s1 * nb));
-        TRY(ensure_ws(ctx, &ctx->ws2, ctx->ws2_bytes, s2 * nb));
-        if (ctx->keys_cap < 2 * nb) {
-            TRY(dalloc(ctx, &ctx->d_keys, sizeof(unsigned long long) * 2 * nb));
-            ctx->keys_cap = 2 * nb;
+        // concurrent batches (opt-in, concurrency = 2): two slots on internal streams forked
+        // from / joined to `s`, so that blocks of different kernels (the spread of one batch,
+        // the fold of the other) share the SMs.  Measured 3.6 % slower on the sweep (L1 / L2
+        // contention), hence off by default.  Not while profiling (stage times would overlap).
+        const int64_t n_batches = (n_rot + nb - 1) / nb;
+        const int nslots = (!ctx->prof && n_batches > 1 && ctx->p.concurrency == 2) ? 2 : 1;
+        for (int q = 0; q < nslots; q++) {
+            Slot &sl = ctx->slot[q];
+            TRY(ensure_ws(ctx, &sl.ws1, sl.ws1_bytes, s1 * nb));
+            TRY(ensure_ws(ctx, &sl.ws2, sl.ws2_bytes, s2 * nb));
+            if (sl.keys_cap < 2 * nb) {
+                TRY(dalloc(ctx, &sl.keys, sizeof(unsigned long long) * 2 * nb));
+                sl.keys_cap = 2 * nb;
+            }
+            if (nslots > 1 && !sl.stream) {
+                CU(ctx, cudaStreamCreateWithFlags(&sl.stream, cudaStreamNonBlocking));
+                CU(ctx, cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
+            }
         }
         const int Np = ctx->p.Np;
         const ShapePlan &pB = ctx->plan[1];
@@ -1358,17 +1388,27 @@ bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, in
             CU(ctx, cudaGetLastError());
             ctx->cm_ready = true;
         }
+        if (nslots > 1) {  // fork: the slots' streams wait for the uploads / A'' on `s`
+            if (!ctx->ev_fork) CU(ctx, cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+            CU(ctx, cudaEventRecord(ctx->ev_fork, s));
+            for (int q = 0; q < nslots; q++) CU(ctx, cudaStreamWaitEvent(ctx->slot[q].stream, ctx->ev_fork, 0));
+        }
+        const cudaStream_t s_user = s;
         for (int64_t r0 = 0; r0 < n_rot; r0 += nb) {
             const int b = (int)std::min<int64_t>(nb, n_rot - r0);
+            Slot &sl = ctx->slot[nslots > 1 ? (int)((r0 / nb) % nslots) : 0];
+            const cudaStream_t s = nslots > 1 ? sl.stream : s_user;
+            void *const ws1 = sl.ws1, *const ws2 = sl.ws2;
+            unsigned long long *const keys = sl.keys;
             // 1-3: spread R B, z and y passes of its box DFT
-            TRY(shape_spectrum(ctx, 1, ctx->d_rot + 9 * r0, b, ctx->ws1, ctx->ws2, s1, s2, s));
+            TRY(shape_spectrum(ctx, 1, ctx->d_rot + 9 * r0, b, ws1, ws2, s1, s2, s, sl));
             const ShapePlan &pb = ctx->plan[1];
             // 4: x pass fused with the spectral product (A' conj(RB)) and the fold onto Np^3
             if (fast_fold) {
                 FoldFastArgs a{};
                 a.tw = ctx->d_tw[pb.L];
                 a.ctw = pb.d_ctw;
-                a.T2 = (const float2 *)ctx->ws1;
+                a.T2 = (const float2 *)ws1;
                 a.t2_bstride = (long long)(s1 / 8);
                 a.Ahat = ctx->d_Ahat_cm;
                 a.MS = ctx->MS;
@@ -1376,7 +1416,7 @@ bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, in
                     const CmSeg sg = cm_segment(p, pb.L, pb.c, pb.G, ctx->K);
                     a.pos_base[p] = sg.off - sg.qn;
                 }
-                a.X1 = (float2 *)ctx->ws2;
+                a.X1 = (float2 *)ws2;
                 a.x1_bstride = (long long)(s2 / 8);
                 a.N = (int)N;
                 StageScope sc(ctx, s, "fold_fast");
@@ -1399,10 +1439,10 @@ bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, in
                 a.segs = ctx->d_segs;
                 a.tw = ctx->d_tw[pb.L];
                 a.ctw = pb.d_ctw;
-                a.T2 = (const float2 *)ctx->ws1;
+                a.T2 = (const float2 *)ws1;
                 a.t2_bstride = (long long)(s1 / 8);
                 a.Ahat = ctx->d_Ahat_cm;
-                a.F = (float2 *)ctx->ws2;  // F, or X1 when the inverse x pass is fused
+                a.F = (float2 *)ws2;  // F, or X1 when the inverse x pass is fused
                 a.f_bstride = (long long)(s2 / 8);
                 a.N = (int)N;
                 a.fuse_inv = fused_inv;
@@ -1425,21 +1465,21 @@ bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, in
                 PassArgs a = inv;
                 a.O = 1;
                 a.I = Np * ctx->Fz;
-                a.in = ctx->ws2;
+                a.in = ws2;
                 a.in_bstride = (long long)(s2 / 8);
-                a.out = (float2 *)ctx->ws1;
+                a.out = (float2 *)ws1;
                 a.out_bstride = (long long)(s1 / 8);
                 StageScope sc(ctx, s, "inv_x");
                 launch_pass(a, 3, b, s);
                 ctx->launches++;
             }
-            void *y1 = fused_inv ? ctx->ws1 : ctx->ws2;
+            void *y1 = fused_inv ? ws1 : ws2;
             const long long y1_bstride = (long long)((fused_inv ? s1 : s2) / 8);
             {
                 PassArgs a = inv;
                 a.O = (int)N;
                 a.I = ctx->Fz;
-                a.in = fused_inv ? ctx->ws2 : ctx->ws1;
+                a.in = fused_inv ? ws2 : ws1;
                 a.in_bstride = (long long)((fused_inv ? s2 : s1) / 8);
                 a.out = (float2 *)y1;
                 a.out_bstride = y1_bstride;
@@ -1449,7 +1489,7 @@ bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, in
             }
             // 8: inverse along z (C2R / C2C), 1/P^3, full output or reduction keys
             if (out_kind != BC_OUT_F_FULL) {
-                launch_keys_init(ctx->d_keys, 2 * b, s);
+                launch_keys_init(keys, 2 * b, s);
                 ctx->launches++;
             }
             {
@@ -1465,17 +1505,23 @@ bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, in
                 a.out_kind = out_kind;
                 a.out_full = dout + out_per * r0;
                 a.full_bstride = N3;
-                a.keys = ctx->d_keys;
+                a.keys = keys;
                 StageScope sc(ctx, s, "inv_z_reduce");
                 launch_last(a, b, s);
                 ctx->launches++;
             }
             if (out_kind != BC_OUT_F_FULL) {
                 StageScope sc(ctx, s, "finalize");
-                launch_keys_finalize(ctx->d_keys, b, out_kind, dout + out_per * r0, s);
+                launch_keys_finalize(keys, b, out_kind, dout + out_per * r0, s);
                 ctx->launches++;
             }
             CU(ctx, cudaGetLastError());
+        }
+        if (nslots > 1) {  // join
+            for (int q = 0; q < nslots; q++) {
+                CU(ctx, cudaEventRecord(ctx->slot[q].done, ctx->slot[q].stream));
+                CU(ctx, cudaStreamWaitEvent(s_user, ctx->slot[q].done, 0));
+            }
         }
     }
     if (host_out) {
@@ -1576,7 +1622,8 @@ bc_status bc_query(const bc_ctx *ctx, const char *key, double *value)
     else if (k == "cut_B") *value = B.cut;
     else if (k == "band_modes") *value = (double)ctx->M * ctx->M * ctx->Kz;
     else if (k == "batch") *value = ctx->batch;
-    else if (k == "bytes_workspace") *value = (double)(ctx->ws1_bytes + ctx->ws2_bytes);
+    else if (k == "bytes_workspace")
+        *value = (double)(ctx->slot[0].ws1_bytes + ctx->slot[0].ws2_bytes + ctx->slot[1].ws1_bytes + ctx->slot[1].ws2_bytes);
     else if (k == "fused_spread_z") *value = use_spread_z(ctx) ? 1 : 0;
     else if (k == "blob_B") *value = B.blob ? 1 : 0;
     else if (k == "spread_cells_B") *value = ctx->spread_cells_B;

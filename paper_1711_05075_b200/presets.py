@@ -27,4 +27,4 @@ def correlator_kwargs(name: str, N: int, h: float, t0, weights: str, **overrides
     p.update(overrides)
     return dict(N=N, h=h, t0=t0, Np=p["Np"], K=p["K"], mode=p["mode"], precision=p["precision"],
                 weights=weights, max_batch=p.get("max_batch", 0), spread_eps=p.get("spread_eps", 0.0),
-                generic_only=p.get("generic_only", False))
+                generic_only=p.get("generic_only", False), concurrency=p.get("concurrency", 0))
