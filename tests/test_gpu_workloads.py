@@ -150,3 +150,27 @@ def test_sweep_batching_is_bitwise_stable(bc):
     f8 = correlator(bc, w, max_batch=8).correlate_rotations(w.R[7:10], "full")
     f1 = c1.correlate_rotations(w.R[8:9], "full")
     assert np.array_equal(f8[1], f1[0])
+
+
+def test_sweep_plan_ragged_grid(bc, oracle_mod):
+    """The sweep's fused plan with an output grid smaller than the period (N = 200 < Np = 256,
+    a ragged last tile in every inverse pass): sampled points and the extrema against the
+    lens oracle."""
+    from paper_1711_05075_b200.presets import correlator_kwargs
+    w = make_config("sweep", n_rot=3)
+    N, h = 200, w.h
+    t0 = (-0.78, -0.78, -0.78)
+    c = bc.Correlator(**correlator_kwargs("sweep", N, h, t0, w.weights))
+    c.shape_upload(0, w.A_xyzr, w.A_w)
+    c.shape_upload(1, w.B_xyzr, w.B_w)
+    assert c.query("fold_fast") == 1 and c.query("fused_spread_z") == 1
+    c.spectrum_A()
+    r = 2
+    f = c.correlate_rotations(w.R[r:r + 1], "full")[0]
+    mm = c.correlate_rotations(w.R[r:r + 1], "minmax")[0]
+    assert f.shape == (N, N, N)
+    idx = sample_indices(f, 40, 20, seed=9, extra=[int(mm[1]["idx"]), N ** 3 - 1])
+    ref = oracle_mod.correlate_points(w.A_xyzr, w.A_w, w.B_xyzr, w.B_w, w.R[r], N, h, t0, idx)
+    got = f.reshape(-1)[idx]
+    assert np.abs(got - ref).max() <= TOL_F32 * np.abs(ref).max()
+    assert mm[1]["val"] == float(f.max()) and mm[0]["val"] == float(f.min())
