@@ -153,8 +153,15 @@ BC_DEV void dft_ct(float2 *v)
         Dft<N1, SIGN>::run(t);
 #pragma unroll
         for (int k1 = 0; k1 < N1; k1++) {
+            // after unrolling m is a constant: multiples of a quarter turn are swaps / negations
             const int m = (n2 * k1) % N;
-            y[n2][k1] = (m == 0) ? t[k1] : cmul(t[k1], make_float2(W.re[m], W.im[m]));
+            float2 v;
+            if (m == 0) v = t[k1];
+            else if (4 * m == N) v = mul_si<SIGN>(t[k1]);
+            else if (2 * m == N) v = make_float2(-t[k1].x, -t[k1].y);
+            else if (4 * m == 3 * N) v = mul_si<-SIGN>(t[k1]);
+            else v = cmul(t[k1], make_float2(W.re[m], W.im[m]));
+            y[n2][k1] = v;
         }
     }
 #pragma unroll
