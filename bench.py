@@ -149,6 +149,20 @@ def alu_peak_tflops():
     return 148 * 128 * 2 * 1.965e9 / 1e12
 
 
+STAGE_KERNEL = {"fold_fast": "fold_fast_kernel", "spread_z_B": "spread_z_kernel", "pass_y_fast": "pass_y_fast_kernel",
+                "inv_y": "pass_kernel", "inv_z_reduce": "last_tma_kernel"}
+
+
+def ncu_traffic(stage, rotations):
+    """DRAM bytes per launch of `stage` from the committed ncu --set full capture
+    (profiles/r1/ncu_traffic.json, per rotation), or None."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "r1", "ncu_traffic.json")))
+        return d["dram_bytes_per_rotation"][STAGE_KERNEL[stage]] * rotations
+    except Exception:
+        return None
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -331,7 +345,9 @@ def run_ours(args, rank, world, local_rank):
         roof = {"bound": "alu" if alu else "hbm", "kernel": name,
                 "achieved": st["fp32_TFLOPs"] if alu else st["hbm_GBps"],
                 "peak": alu_peak if alu else peak, "unit": "TFLOP/s" if alu else "GB/s",
-                "frac": st["alu_frac"] if alu else st["hbm_frac"], "traffic": None,
+                "frac": st["alu_frac"] if alu else st["hbm_frac"], "traffic": ncu_traffic(name, batch),
+                "traffic_source": "profiles/r1/ncu_traffic.json (ncu --set full, dram__bytes_read.sum + "
+                                  "dram__bytes_write.sum per rotation x rotations per launch)",
                 "peak_source": ("derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz" if alu else peak_kind),
                 "alg_bytes_per_launch": by * batch, "alg_flops_per_launch": fl * batch,
                 "avg_launch_ms": tot_ms / nl, "share_of_step": st["share"],

@@ -50,7 +50,28 @@ def full_metrics(rep):
     return res
 
 
+def traffic_json(rep, rotations_per_launch, path):
+    """DRAM bytes (read + write) per rotation of each captured kernel, for bench.py's
+    roofline "traffic" field (the capture's launches hold `rotations_per_launch` rotations)."""
+    import json
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    res = {}
+    for d in full_metrics(rep):
+        k = d["kernel"].split("<")[0].strip()
+        tot = 0.0
+        for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            v, u = d[m]
+            tot += float(v) * scale.get(u, 1)
+        res.setdefault(k, []).append(tot / rotations_per_launch)
+    out = {k: sum(v) / len(v) for k, v in res.items()}
+    json.dump({"dram_bytes_per_rotation": out, "source": rep, "rotations_per_launch": rotations_per_launch},
+              open(path, "w"), indent=1)
+
+
 def main():
+    if sys.argv[1] == "--traffic":
+        traffic_json(sys.argv[2], int(sys.argv[3]), sys.argv[4])
+        return
     launches, rep, out = sys.argv[1], sys.argv[2], sys.argv[3]
     agg = launch_shares(launches)
     tot = sum(a[0] for a in agg.values())
