@@ -755,9 +755,10 @@ void spectral_ws_sizes(const bc_ctx *ctx, int which, size_t &s1, size_t &s2)
     const bool cplx = ctx->p.weights == BC_WEIGHTS_COMPLEX;
     const size_t box = L * L * L * (cplx ? 8 : 4);
     const size_t T1 = L * L * Kz * 8, T2 = L * M * Kz * 8;
-    const size_t F = Np * Np * Fz * 8, X1 = N * Np * Fz * 8, Y1 = N * N * Fz * 8;
+    const size_t Fzp = (Fz + 7) & ~(size_t)7;  // padded row pitch of X1 / Y1 on the fast plan
+    const size_t F = Np * Np * Fz * 8, X1 = N * Np * Fzp * 8, Y1 = N * N * Fzp * 8;
     s1 = std::max(std::max(box, T2), X1);
-    s2 = std::max(std::max(T1, F), Y1);
+    s2 = std::max(std::max(std::max(T1, F), Y1), X1);  // X1 sits in ws2 when the inverse x is fused
     s1 = (s1 + 255) / 256 * 256;
     s2 = (s2 + 255) / 256 * 256;
 }
@@ -1377,6 +1378,9 @@ bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, in
         const ShapePlan &pB = ctx->plan[1];
         const bool fast_fold = !ctx->p.generic_only && fold_fast_supported(pB.L, pB.c, pB.G, ctx->K, Np, cplx);
         const bool fused_inv = fast_fold || (!ctx->p.generic_only && fold_fuses_inverse(pB.L, Np));
+        // row pitch of X1 / Y1: padded to 8 modes on the fast plan (64-byte row pieces stay
+        // 32-byte-sector aligned), the stored count elsewhere
+        const int zpitch = fast_fold ? (ctx->Fz + 7) & ~7 : ctx->Fz;
         if (!ctx->cm_ready) {  // A' into the coset-major x order of B's plan (once per A / B plan)
             const ShapePlan &pb = ctx->plan[1];
             ctx->MS = cm_row_stride(pb.L, pb.c, pb.G, ctx->K);
@@ -1418,6 +1422,7 @@ bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, in
                 }
                 a.X1 = (float2 *)ws2;
                 a.x1_bstride = (long long)(s2 / 8);
+                a.x1_pitch = zpitch;
                 a.N = (int)N;
                 StageScope sc(ctx, s, "fold_fast");
                 launch_fold_fast(a, b, s);
@@ -1483,6 +1488,7 @@ bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, in
                 a.in_bstride = (long long)((fused_inv ? s2 : s1) / 8);
                 a.out = (float2 *)y1;
                 a.out_bstride = y1_bstride;
+                a.pitch_in = a.pitch_out = zpitch;
                 StageScope sc(ctx, s, "inv_y");
                 launch_pass(a, 3, b, s);
                 ctx->launches++;
@@ -1502,6 +1508,7 @@ bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, in
                 a.tw = ctx->d_tw[Np];
                 a.in = (const float2 *)y1;
                 a.in_bstride = y1_bstride;
+                a.pitch = zpitch;
                 a.out_kind = out_kind;
                 a.out_full = dout + out_per * r0;
                 a.full_bstride = N3;

@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(FF_NT, 4) fold_fast_kernel(FoldFastArgs a)
     float2 *X1 = a.X1 + (long long)b * a.x1_bstride;
     for (int e = threadIdx.x; e < FF_NL * a.N; e += FF_NT) {
         const int i = e % FF_NL, q = e / FF_NL;
-        if (z0 + i < FF_FZ) X1[(q * FF_NP + kyp) * FF_FZ + z0 + i] = X[i * FF_LS + pad(q)];
+        if (z0 + i < FF_FZ) X1[(q * FF_NP + kyp) * a.x1_pitch + z0 + i] = X[i * FF_LS + pad(q)];
     }
     __syncthreads();  // X is rewritten by the next item's first group
     }

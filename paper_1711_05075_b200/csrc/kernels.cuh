@@ -131,8 +131,9 @@ struct PassArgs {
     // contiguous: in[b][lines][L] -> out[b][lines][nk]
     long long lines;
     int in_real;
-    // strided: in[b][O][L][I] -> out[b][O][nk][I]
+    // strided: in[b][O][L][I] -> out[b][O][nk][I] (row pitches pitch_in / pitch_out, 0 = I)
     int O, I;
+    int pitch_in, pitch_out;
     long long in_bstride, out_bstride;
     const void *in;
     float2 *out;
@@ -169,8 +170,9 @@ struct FoldFastArgs {
     const float2 *Ahat;      // A'' rows (coset-major, stride MS)
     int MS;
     int pos_base[4];         // per coset: segment offset - first negative q
-    float2 *X1;              // [b][N][Np][Fz]
+    float2 *X1;              // [b][N][Np][x1_pitch]
     long long x1_bstride;
+    int x1_pitch;            // row pitch (>= Np/2 + 1; 136 keeps 64-byte row pieces sector-aligned)
     int N;
     int nb;                  // set by launch_fold_fast
 };
@@ -192,6 +194,7 @@ void launch_fold_fast(const FoldFastArgs &a, int batch, cudaStream_t s);
 // contiguous inverse z pass + epilogue
 struct LastArgs {
     int Np, N, Fz;
+    int pitch;           // row pitch of `in` in float2 (0 = Fz)
     int hermitian;       // 1: C2R from Fz = Np/2+1 stored modes; 0: C2C, Fz = Np
     float scale;
     const float2 *tw;    // exp(-2 pi i m / Np)

@@ -62,13 +62,14 @@ __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TP
     __syncthreads();  // the table is read across warps (warp-synchronous FFTs do not order it)
     float2 x[E];
     if (IN_MODE == 2) {
-        const float2 *in = (const float2 *)a.in + (long long)b * a.in_bstride + (long long)o * L * a.I;
+        const int pin = a.pitch_in ? a.pitch_in : a.I;
+        const float2 *in = (const float2 *)a.in + (long long)b * a.in_bstride + (long long)o * L * pin;
         // all loads first (E independent loads in flight per thread), then the transpose
 #pragma unroll
         for (int m = 0; m < E; m++) {
             const int e = threadIdx.x + NT * m;
             const int n = e / NL, i = e % NL;
-            x[m] = (i0 + i < a.I) ? in[(long long)n * a.I + i0 + i] : make_float2(0.f, 0.f);
+            x[m] = (i0 + i < a.I) ? in[(long long)n * pin + i0 + i] : make_float2(0.f, 0.f);
         }
 #pragma unroll
         for (int m = 0; m < E; m++) {
@@ -112,13 +113,14 @@ __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TP
 #pragma unroll
             for (int m = 0; m < E; m++) A[line * LS + pad(tl + TPL * m)] = y[m];
             __syncthreads();
-            float2 *out = outs + (long long)o * a.nk * a.I;
+            const int pout = a.pitch_out ? a.pitch_out : a.I;
+            float2 *out = outs + (long long)o * a.nk * pout;
             for (int e = threadIdx.x; e < L * NL; e += NT) {
                 const int q = e / NL, i = e % NL;
                 const int kk = coset_kk(q, p, a.c, a.G, a.klo, a.signed_k);
                 if (kk >= 0 && kk < a.nk && i0 + i < a.I) {
                     const float2 v = A[i * LS + pad(q)];
-                    out[(long long)kk * a.I + i0 + i] = a.mult ? cmul(v, a.mult[kk]) : v;
+                    out[(long long)kk * pout + i0 + i] = a.mult ? cmul(v, a.mult[kk]) : v;
                 }
             }
             __syncthreads();
@@ -405,7 +407,8 @@ __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TP
         const bool valid = u < units;
         const long long l0 = HERM ? 2 * u : u;
         const bool has1 = HERM && valid && (l0 + 1 < lines);
-        const float2 *row = a.in + (long long)b * a.in_bstride + l0 * a.Fz;
+        const int pitch = a.pitch ? a.pitch : a.Fz;
+        const float2 *row = a.in + (long long)b * a.in_bstride + l0 * pitch;
         float2 x[E];
 #pragma unroll
         for (int m = 0; m < E; m++) {
@@ -418,7 +421,7 @@ __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TP
                     const bool lo = n < a.Fz;
                     const int src = lo ? n : L - n;
                     float2 va = row[src];
-                    float2 vb = has1 ? row[a.Fz + src] : make_float2(0.f, 0.f);
+                    float2 vb = has1 ? row[pitch + src] : make_float2(0.f, 0.f);
                     if (n == 0 || 2 * n == L) {
                         va.y = 0.f;
                         vb.y = 0.f;
@@ -535,9 +538,9 @@ __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TP
     constexpr int LS = line_stride(L), E = L / TPL;
     constexpr bool WS = warp_local<L>();
     extern __shared__ __align__(16) float2 sm[];
-    const int Fz = a.Fz;
-    float2 *stage = sm;                          // [2][2 NL][Fz]
-    float2 *tw = stage + 2 * 2 * NL * Fz;
+    const int Fz = a.Fz, Pz = a.pitch ? a.pitch : a.Fz;  // stored modes, row pitch
+    float2 *stage = sm;                          // [2][2 NL][Pz]
+    float2 *tw = stage + 2 * 2 * NL * Pz;
     float2 *A = tw + L;
     float2 *B = A + NL * LS;
     __shared__ unsigned long long bar[2];
@@ -552,9 +555,9 @@ __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TP
     auto issue = [&](long long tile, int s) {  // one thread: arm + copy tile -> stage s
         const long long l0 = tile * 2 * NL;
         const long long nl = lines - l0 < 2 * NL ? lines - l0 : 2 * NL;
-        const unsigned bytes = (unsigned)(nl * Fz * sizeof(float2));
+        const unsigned bytes = (unsigned)(nl * Pz * sizeof(float2));
         mbar_expect_tx(&bar[s], bytes);
-        bulk_g2s(stage + (size_t)s * 2 * NL * Fz, in + l0 * Fz, bytes, &bar[s]);
+        bulk_g2s(stage + (size_t)s * 2 * NL * Pz, in + l0 * Pz, bytes, &bar[s]);
     };
     if (threadIdx.x == 0) {
         mbar_init(&bar[0], 1);
@@ -572,11 +575,11 @@ __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TP
         const int s = it & 1;
         if (threadIdx.x == 0 && tile + gridDim.x < ntiles) issue(tile + gridDim.x, s ^ 1);
         mbar_wait(&bar[s], (it >> 1) & 1);
-        const float2 *st = stage + (size_t)s * 2 * NL * Fz;
+        const float2 *st = stage + (size_t)s * 2 * NL * Pz;
         const long long l0 = tile * 2 * NL + 2 * line;
         const bool valid = l0 < lines;
         const bool has1 = l0 + 1 < lines;
-        const float2 *ra = st + (2 * line) * Fz, *rb = ra + Fz;
+        const float2 *ra = st + (2 * line) * Pz, *rb = ra + Pz;
         float2 x[E];
 #pragma unroll
         for (int m = 0; m < E; m++) {
@@ -766,9 +769,10 @@ void launch_last(const LastArgs &a, int batch, cudaStream_t s)
 {
     // TMA-fed C2R path: the tile rows must be 16-byte aligned (the stage offsets and
     // the row blocks are multiples of 2 NL rows; Fz * 8 bytes per row)
-    if (a.hermitian && a.Np == 256 && ((uintptr_t)a.in % 16) == 0 && (a.in_bstride * 8) % 16 == 0) {
+    if (a.hermitian && a.Np == 256 && ((uintptr_t)a.in % 16) == 0 && (a.in_bstride * 8) % 16 == 0 &&
+        ((a.pitch ? a.pitch : a.Fz) * 8 * 2 * Plan<256>::NL) % 16 == 0) {
         constexpr int NL = Plan<256>::NL;
-        const size_t sm = sizeof(float2) * (2 * 2 * NL * (size_t)a.Fz + 256 +
+        const size_t sm = sizeof(float2) * (2 * 2 * NL * (size_t)(a.pitch ? a.pitch : a.Fz) + 256 +
                                             (Plan<256>::n >= 3 ? 2 : 1) * (size_t)NL * line_stride(256));
         const long long lines = (long long)a.N * a.N;
         const long long tiles = (lines + 2 * NL - 1) / (2 * NL);
