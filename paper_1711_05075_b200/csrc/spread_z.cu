@@ -229,24 +229,24 @@ __global__ void __launch_bounds__(128, 4) spread_z_kernel(SpreadZArgs a)
             nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, 16));
             if (nmax <= 0) continue;
             const float4 we = a.recB[j];  // (s, w, g0, g2)
-            for (int it = 0; it < nmax; it++) {
-                const int z = zlo + (it << 3) + hl;
-                if (z <= zhi) {
-                    const float dz = (float)z - ue.z;
-                    const float d2 = fmaf(dz, dz, dxy2);
-                    float g;
-                    if (d2 < 0.01f) {
-                        g = fmaf(we.w, d2, we.z);
-                    } else {
-                        const float rd = rsqrtf(d2);
-                        const float d = d2 * rd;
-                        const PhiVal p = phi_lookup(phi, nphi, tmax, U, invD, we.x - d);
-                        PhiVal q = PhiVal{0.5f, 0.f};
-                        if (we.x + d < U) q = phi_lookup(phi, nphi, tmax, U, invD, we.x + d);
-                        g = p.p1 + q.p1 - (p.p2 - q.p2) * rd;
-                    }
-                    accc[z] = fmaf(we.y, g, accc[z]);
-                }
+            // two cells per lane per step (z and z + 8: independent evaluation chains)
+            auto prof = [&](float d2) {
+                if (d2 < 0.01f) return fmaf(we.w, d2, we.z);
+                const float rd = rsqrtf(d2);
+                const float d = d2 * rd;
+                const PhiVal p = phi_lookup(phi, nphi, tmax, U, invD, we.x - d);
+                PhiVal q = PhiVal{0.5f, 0.f};
+                if (we.x + d < U) q = phi_lookup(phi, nphi, tmax, U, invD, we.x + d);
+                return p.p1 + q.p1 - (p.p2 - q.p2) * rd;
+            };
+            for (int it = 0; it < nmax; it += 2) {
+                const int z0 = zlo + (it << 3) + hl, z1 = z0 + 8;
+                const bool ok0 = z0 <= zhi, ok1 = z1 <= zhi;
+                const float dz0 = (float)z0 - ue.z, dz1 = (float)z1 - ue.z;
+                const float g0 = ok0 ? prof(fmaf(dz0, dz0, dxy2)) : 0.f;
+                const float g1 = ok1 ? prof(fmaf(dz1, dz1, dxy2)) : 0.f;
+                if (ok0) accc[z0] = fmaf(we.y, g0, accc[z0]);
+                if (ok1) accc[z1] = fmaf(we.y, g1, accc[z1]);
             }
         }
     }
