@@ -200,11 +200,13 @@ __global__ void __launch_bounds__(128, 4) spread_z_kernel(SpreadZArgs a)
     // touch distinct cells, steps and balls are sequential, so the sums are race-free and in
     // ball order (deterministic).
     for (int base0 = 0; base0 < cnt; base0 += 32) {
-        int jl = -1;
+        // lane k tests candidate base0 + k and keeps its two records for the broadcast below
         bool rel = false;
+        float4 uc = make_float4(0.f, 0.f, 0.f, 0.f), wc = uc;
         if (base0 + lane < cnt) {
-            jl = lst[base0 + lane];
-            const float4 uc = recA[jl];
+            const int jl = lst[base0 + lane];
+            uc = recA[jl];
+            wc = a.recB[jl];
             const float ddx = fx - uc.x;
             const float ddy = fmaxf(fmaxf(fy0 - uc.y, uc.y - (fy0 + 3.f)), 0.f);
             rel = fmaf(ddx, ddx, ddy * ddy) < uc.w;
@@ -213,8 +215,8 @@ __global__ void __launch_bounds__(128, 4) spread_z_kernel(SpreadZArgs a)
         while (msk) {
             const int src = __ffs(msk) - 1;
             msk &= msk - 1;
-            const int j = __shfl_sync(0xffffffffu, jl, src);
-            const float4 ue = recA[j];
+            const float4 ue = make_float4(__shfl_sync(0xffffffffu, uc.x, src), __shfl_sync(0xffffffffu, uc.y, src),
+                                          __shfl_sync(0xffffffffu, uc.z, src), __shfl_sync(0xffffffffu, uc.w, src));
             const float dx = fx - ue.x, dy = fy - ue.y;
             const float dxy2 = fmaf(dx, dx, dy * dy);
             const float hz2 = ue.w - dxy2;
@@ -228,7 +230,9 @@ __global__ void __launch_bounds__(128, 4) spread_z_kernel(SpreadZArgs a)
             int nmax = max(nit, __shfl_xor_sync(0xffffffffu, nit, 8));
             nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, 16));
             if (nmax <= 0) continue;
-            const float4 we = a.recB[j];  // (s, w, g0, g2)
+            const float4 we = make_float4(__shfl_sync(0xffffffffu, wc.x, src), __shfl_sync(0xffffffffu, wc.y, src),
+                                          __shfl_sync(0xffffffffu, wc.z, src),
+                                          __shfl_sync(0xffffffffu, wc.w, src));  // (s, w, g0, g2)
             // two cells per lane per step (z and z + 8: independent evaluation chains)
             auto prof = [&](float d2) {
                 if (d2 < 0.01f) return fmaf(we.w, d2, we.z);
