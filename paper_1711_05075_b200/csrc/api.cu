@@ -543,12 +543,10 @@ double blob_dphi(double r)
     return blob_C() * std::cyl_bessel_i(1.0, kBlobAlpha * q) * kBlobAlpha * (-r / (kBlobW * kBlobW)) / q;
 }
 // composite 16-point Gauss-Legendre on [a, b] (the integrands below are smooth on [0, W])
-template <typename Fn>
-double gl_integrate(Fn f, double a, double b, int panels = 16)
-{
-    static double x[16], w[16];
-    static bool init = false;
-    if (!init) {
+struct GL16 {
+    double x[16], w[16];
+    GL16()
+    {
         for (int i = 0; i < 16; i++) {
             double z = std::cos(kPi * (i + 0.75) / 16.5), pp = 0;
             for (int it = 0; it < 100; it++) {
@@ -566,8 +564,13 @@ double gl_integrate(Fn f, double a, double b, int panels = 16)
             x[i] = z;
             w[i] = 2 / ((1 - z * z) * pp * pp);
         }
-        init = true;
     }
+};
+template <typename Fn>
+double gl_integrate(Fn f, double a, double b, int panels = 16)
+{
+    static const GL16 gl;  // thread-safe one-time initialisation (C++11 static)
+    const double *x = gl.x, *w = gl.w;
     double sum = 0;
     const double hp = (b - a) / panels;
     for (int p = 0; p < panels; p++) {
