@@ -44,7 +44,11 @@ __global__ void __launch_bounds__(FF_NT, 4) fold_fast_kernel(FoldFastArgs a)
     float2 *Ab = X + FF_NL * FF_LS;    // [NL][LS] FFT exchange / staging
     const int line = threadIdx.x / FF_TPL, tl = threadIdx.x % FF_TPL;
     const int lane = threadIdx.x & 31;
-    constexpr int ZT = (FF_FZ + FF_NL - 1) / FF_NL;
+    // targets: 16 tiles of 8 k'z per k'y row cover k'z in [0, 128); the Nyquist plane k'z = 128
+    // is done by 32 items whose 8 lines are 8 consecutive k'y rows (a 17th tile per row would
+    // carry 1 valid line in 8)
+    constexpr int ZT = (FF_FZ - 1) / FF_NL;            // 16
+    constexpr int NREG = FF_NP * ZT, NNYQ = FF_NP / FF_NL;
 
     load_twiddles<FF_L>(tw, a.tw, threadIdx.x, FF_NT);
     for (int e = threadIdx.x; e < FF_C * FF_L; e += FF_NT) ctw[e] = a.ctw[e];
@@ -52,40 +56,41 @@ __global__ void __launch_bounds__(FF_NT, 4) fold_fast_kernel(FoldFastArgs a)
     // persistent blocks: work items w = (target block) * nb + rotation, rotation-fastest (the
     // nb items sharing A'' rows run together and share them through L2); the tables above are
     // loaded once per block
-    const int n_items = FF_NP * ZT * a.nb;
+    const int n_items = (NREG + NNYQ) * a.nb;
 #pragma unroll 1
     for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
     const int b = w % a.nb;
     const int tb = w / a.nb;
-    const int kyp = tb / ZT;
-    const int z0 = (tb % ZT) * FF_NL;
+    const bool nyq = tb >= NREG;
+    const int kyp = nyq ? FF_NL * (tb - NREG) : tb / ZT;   // k'y of line 0
+    const int z0 = nyq ? FF_FZ - 1 : (tb % ZT) * FF_NL;     // k'z of line 0
+    // line i: target (k'y, k'z) = (kyp + i, 128) on the Nyquist plane, (kyp, z0 + i) elsewhere
+    auto line_kyp = [&](int i) { return nyq ? kyp + i : kyp; };
+    auto line_kz = [&](int i) { return nyq ? z0 : z0 + i; };
     const float2 *T2 = a.T2 + (long long)b * a.t2_bstride;
-    // the alias groups of this target block: (pass, ky) with ky in the band (block-uniform),
-    // packed 16 bits each ((ky + 512) * 2 + pass) so a runtime group index needs no local memory
-    unsigned long long groups = 0;
-    int ng = 0;
+    // the alias slots (pass, al): ky = +-k'y (+ 256 al); a slot is skipped when out of band for
+    // the whole block (block-uniform); on the Nyquist plane validity is per line
+    auto slot_ky = [&](int kp, int pass, int al) {
+        return pass == 0 ? (al == 0 ? kp : kp - FF_NP) : (al == 0 ? -kp : FF_NP - kp);
+    };
+    unsigned slots = 0;
 #pragma unroll
-    for (int pass = 0; pass < 2; pass++)
-#pragma unroll
-        for (int al = 0; al < 2; al++) {
-            const int ky = pass == 0 ? (al == 0 ? kyp : kyp - FF_NP) : (al == 0 ? -kyp : FF_NP - kyp);
-            if (ky >= -FF_K && ky <= FF_K) {
-                groups |= (unsigned long long)((ky + 512) * 2 + pass) << (16 * ng);
-                ng++;
-            }
-        }
-    auto group_ky = [&](int g) { return (int)((groups >> (16 * g)) & 0xffff) / 2 - 512; };
-    auto group_pass = [&](int g) { return (int)((groups >> (16 * g)) & 1); };
-    // L2 prefetch of a group's T2 rows: 256 rows x 64 bytes, two rows per thread
-    auto prefetch_group = [&](int g) {
-        const int ky = group_ky(g), pass = group_pass(g);
+    for (int sidx = 0; sidx < 4; sidx++) {
+        const int ky0 = slot_ky(kyp, sidx >> 1, sidx & 1), ky7 = slot_ky(kyp + FF_NL - 1, sidx >> 1, sidx & 1);
+        const bool any = (ky0 >= -FF_K && ky0 <= FF_K) || (nyq && ky7 >= -FF_K && ky7 <= FF_K);
+        if (any) slots |= 1u << sidx;
+    }
+    // L2 prefetch of a slot's T2 rows: 256 rows x 64 bytes, two rows per thread (regular items)
+    auto prefetch_slot = [&](int sidx) {
+        if (nyq) return;
+        const int ky = slot_ky(kyp, sidx >> 1, sidx & 1), pass = sidx >> 1;
         const int kz = pass == 0 ? z0 : FF_NP - z0 - (FF_NL - 1);  // lowest kz of the 8 lines
         for (int n = threadIdx.x; n < FF_L; n += FF_NT) {
             const float2 *p = T2 + (n * FF_M + ky + FF_K) * FF_KZ + max(kz, 0);
             asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
         }
     };
-    prefetch_group(0);
+    if (slots) prefetch_slot(__ffs(slots) - 1);
 
     // A'' row position of output (m, p) of lane tl: pos_base[p] + tl + 16 m (+ L for m < 4)
     float2 acc[4][FF_C];
@@ -94,13 +99,16 @@ __global__ void __launch_bounds__(FF_NT, 4) fold_fast_kernel(FoldFastArgs a)
 #pragma unroll
         for (int p = 0; p < FF_C; p++) acc[j][p] = make_float2(0.f, 0.f);
 
-    const int tz = z0 + line;  // this line's target k'z
+    const int tz = line_kz(line);    // this line's target k'z
+    const int tkyp = line_kyp(line); // and k'y
     // direct: kz = k'z in [0, 128], ky in {k'y, k'y - 256};  conjugate partner: kz = 256 - k'z
     // (k'z in [1, 128]), ky in {-k'y, 256 - k'y}; out-of-band ky / kz contribute nothing
 #pragma unroll 1
-    for (int g = 0; g < ng; g++) {
-        const int ky = group_ky(g), pass = group_pass(g);
-        if (g + 1 < ng) prefetch_group(g + 1);
+    for (unsigned rest = slots; rest; rest &= rest - 1) {
+        const int sidx = __ffs(rest) - 1;
+        const int pass = sidx >> 1, al = sidx & 1;
+        if (rest & (rest - 1)) prefetch_slot(__ffs(rest & (rest - 1)) - 1);
+        const int ky = slot_ky(tkyp, pass, al);  // this thread's line
         {
             // ---- T2 lines (ky, kz(i)) -> X (transposed through registers for coalescing)
             float2 x[E];
@@ -108,10 +116,11 @@ __global__ void __launch_bounds__(FF_NT, 4) fold_fast_kernel(FoldFastArgs a)
             for (int m = 0; m < E; m++) {
                 const int e = threadIdx.x + FF_NT * m;
                 const int n = e / FF_NL, i = e % FF_NL;
-                const int kt = z0 + i;
-                const bool ok = pass == 0 ? (kt < FF_FZ) : (kt >= 1 && kt < FF_FZ);
+                const int kt = line_kz(i);
+                const int kyi = slot_ky(line_kyp(i), pass, al);
+                const bool ok = (pass == 0 ? (kt < FF_FZ) : (kt >= 1 && kt < FF_FZ)) && kyi >= -FF_K && kyi <= FF_K;
                 const int kz = pass == 0 ? kt : FF_NP - kt;
-                x[m] = ok ? T2[(n * FF_M + ky + FF_K) * FF_KZ + kz] : make_float2(0.f, 0.f);
+                x[m] = ok ? T2[(n * FF_M + kyi + FF_K) * FF_KZ + kz] : make_float2(0.f, 0.f);
             }
             __syncthreads();  // previous group's last reads of X / Ab are done
 #pragma unroll
@@ -120,7 +129,7 @@ __global__ void __launch_bounds__(FF_NT, 4) fold_fast_kernel(FoldFastArgs a)
                 X[(e % FF_NL) * FF_LS + pad(e / FF_NL)] = x[m];
             }
             __syncthreads();
-            const bool my_ok = pass == 0 ? (tz < FF_FZ) : (tz >= 1 && tz < FF_FZ);
+            const bool my_ok = (pass == 0 ? (tz < FF_FZ) : (tz >= 1 && tz < FF_FZ)) && ky >= -FF_K && ky <= FF_K;
             const int my_kz = pass == 0 ? tz : FF_NP - tz;
             const float2 *arow = a.Ahat + (long long)((ky + FF_K) * FF_KZ + (my_ok ? my_kz : 0)) * a.MS;
             // one copy of the FFT (runtime coset loop keeps the code in the instruction cache);
@@ -207,7 +216,7 @@ __global__ void __launch_bounds__(FF_NT, 4) fold_fast_kernel(FoldFastArgs a)
     float2 *X1 = a.X1 + (long long)b * a.x1_bstride;
     for (int e = threadIdx.x; e < FF_NL * a.N; e += FF_NT) {
         const int i = e % FF_NL, q = e / FF_NL;
-        if (z0 + i < FF_FZ) X1[(q * FF_NP + kyp) * a.x1_pitch + z0 + i] = X[i * FF_LS + pad(q)];
+        X1[(q * FF_NP + line_kyp(i)) * a.x1_pitch + line_kz(i)] = X[i * FF_LS + pad(q)];
     }
     __syncthreads();  // X is rewritten by the next item's first group
     }
@@ -222,13 +231,13 @@ void launch_fold_fast(const FoldFastArgs &a_in, int batch, cudaStream_t s)
 {
     FoldFastArgs a = a_in;
     a.nb = batch;
-    constexpr int ZT = (FF_FZ + FF_NL - 1) / FF_NL;
+    constexpr int ZT = (FF_FZ - 1) / FF_NL;
     const size_t sm = sizeof(float2) * ((size_t)FF_L + FF_C * FF_L + 2 * FF_NL * FF_LS);
     cudaFuncSetAttribute(fold_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const long long items = (long long)FF_NP * ZT * batch;
+    const long long items = (long long)(FF_NP * ZT + FF_NP / FF_NL) * batch;
     const long long grid = std::min<long long>(items, (long long)sms * 4 * 4);  // 4 blocks / SM, 4 waves of items or more
     fold_fast_kernel<<<(unsigned)grid, FF_NT, sm, s>>>(a);
 }
