@@ -273,6 +273,10 @@ __global__ void __launch_bounds__(FF_NT, 5) pass_y_fast_kernel(PassYFastArgs a)
         ylo = max(0, (int)ceilf(a.cy - hh));
         yhi = min(FF_L - 1, (int)floorf(a.cy + hh));
     }
+    if (ylo > yhi) {  // x plane outside B's support cylinder: its T2 rows are zero, no transform
+        for (int e = threadIdx.x; e < FF_M * FF_NL; e += FF_NT) T2[(e / FF_NL) * FF_KZ + kz0 + e % FF_NL] = make_float2(0.f, 0.f);
+        return;
+    }
     load_twiddles<FF_L>(tw, a.tw, threadIdx.x, FF_NT);
     {
         float2 x[E];
