@@ -827,6 +827,12 @@ bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, voi
         a.live_r2 = (float)(ctx->live_r * ctx->live_r);
         a.zero_r2 = (float)((ctx->live_r + 1) * (ctx->live_r + 1));
         a.skip_zero = pass_y_fast_supported(L, pl.c, pl.G, ctx->K, cplx) ? 1 : 0;
+        // the sweep's plan: spread to the box (ws1, free until the y pass writes T2 there) and
+        // transform it in a second kernel -- the spread alone runs at twice the occupancy
+        if (a.skip_zero) {
+            a.box = (float *)ws1;
+            a.box_bstride = (long long)(s1_per / 4);
+        }
         a.mult_z = pl.d_mult[2];
         a.tw = tw;
         a.ctw = pl.d_ctw;
@@ -834,7 +840,7 @@ bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, voi
         a.out_bstride = (long long)(s2_per / 8);
         StageScope sc(ctx, s, "spread_z_B");
         launch_spread_z(a, nb, s);
-        ctx->launches++;
+        ctx->launches += a.box ? 2 : 1;
     } else {
         SpreadArgs a{};
         a.L = L;

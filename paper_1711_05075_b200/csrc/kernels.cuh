@@ -72,6 +72,8 @@ struct SpreadZArgs {
     const float2 *ctw;      // [c][L]
     float2 *out;            // T1 [b][L][L][K + 1]
     long long out_bstride;  // float2 elements
+    float *box;             // non-null: spread to this fp32 box [b][L][L][L] (stride box_bstride),
+    long long box_bstride;  // then a separate tile z transform (two kernels, see spread_z.cu)
 };
 bool spread_z_supported(int L);
 void launch_spread_z(const SpreadZArgs &a, int batch, cudaStream_t s);

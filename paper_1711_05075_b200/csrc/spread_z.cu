@@ -137,23 +137,90 @@ __global__ void __launch_bounds__(256) szb_fill_kernel(SzBinArgs a)
 // (X0 + w, Y0 + g), g = lane / 8; the 8 lanes of a group step along the ball's chord of
 // their column 8 cells at a time (a ~15-cell chord takes 2 steps at ~94% lane use), so one
 // ball visit serves 4 columns.  FFT phase: 128 / TPL thread groups, one pair-line each.
-template <int L>
-__global__ void __launch_bounds__(128, 4) spread_z_kernel(SpreadZArgs a)
+// The z transform of one 4 x 4 column tile held in shared memory (acc[16][CS] fp32):
+// columns (2l, 2l+1) form one complex line z = a + i b; group g (TPL threads) handles line
+// g % 8 and cosets g / 8 + (NG / 8) r; the band of Z(k), |k| <= K, goes to zb[8][2K + 1]
+// (aliasing acc once the lines are in registers); A(k) = (Z(k) + conj Z(-k)) / 2,
+// B(k) = (Z(k) - conj Z(-k)) / 2i, times mult_z, are stored as T1 rows.
+template <int L, int NT>
+__device__ __forceinline__ void tile_z_transform(const SpreadZArgs &a, float *acc, float2 *Abuf, const float2 *tw,
+                                                 float2 *T1, int X0, int Y0)
+{
+    constexpr int TPL = Plan<L>::TPL, E = L / TPL, NG = NT / TPL;
+    constexpr int LS = line_stride(L);
+    constexpr int CS = L + 8;
+    const int K = a.K, M = 2 * a.K + 1, Kz = a.K + 1;
+    float2 *zb = (float2 *)acc;
+    const int g = threadIdx.x / TPL, tl = threadIdx.x % TPL;
+    const int line = g % SZ_LINES;
+    float2 x[E];
+#pragma unroll
+    for (int m = 0; m < E; m++) {
+        const int n = tl + TPL * m;
+        x[m] = make_float2(acc[(2 * line) * CS + n], acc[(2 * line + 1) * CS + n]);
+    }
+    __syncthreads();  // acc dead: zb may overwrite it
+    const int c = a.c, G = a.G;
+    const bool band4 = c == 4 && G == 1024 && K == 255;  // block-uniform
+    const int rounds = (SZ_LINES * c + NG - 1) / NG;
+    for (int r = 0; r < rounds; r++) {
+        const int p = g / SZ_LINES + (NG / SZ_LINES) * r;
+        const bool active = p < c;
+        float2 y[E];
+#pragma unroll
+        for (int m = 0; m < E; m++) y[m] = (active && p) ? cmul(x[m], a.ctw[p * L + tl + TPL * m]) : x[m];
+        fft_regs<L, -1, true>(y, Abuf + g * LS, Abuf + g * LS, tw, tl);
+        if (L == 256 && band4) {
+            // plan L = 256, c = 4, K = 255: outputs m < 4 (k = 4q + p) and m >= 12
+            // (k = 4q + p - 1024) are the band, minus (p, q) = (0, 192)
+#pragma unroll
+            for (int m = 0; m < E; m++) {
+                if (m >= 4 && m < 12) continue;
+                const int k = 4 * (tl + TPL * m) + p - (m >= 12 ? 1024 : 0);
+                if (m != 12 || p != 0 || tl != 0) zb[line * M + k + K] = y[m];
+            }
+        } else if (active) {
+#pragma unroll
+            for (int m = 0; m < E; m++) {
+                int k = c * (tl + TPL * m) + p;
+                if (2 * k > G) k -= G;
+                if (k >= -K && k <= K) zb[line * M + k + K] = y[m];
+            }
+        }
+        __syncwarp();  // the next round's FFT rewrites this group's buffer
+    }
+    __syncthreads();  // zb complete
+    for (int e = threadIdx.x; e < SZ_LINES * Kz; e += NT) {
+        const int l = e / Kz, k = e % Kz;
+        const float2 Z = zb[l * M + K + k], Zm = zb[l * M + K - k];
+        const float2 mu = a.mult_z[k];
+        const float2 Xa = cmul(make_float2(0.5f * (Z.x + Zm.x), 0.5f * (Z.y - Zm.y)), mu);
+        const float2 Xb = cmul(make_float2(0.5f * (Z.y + Zm.y), -0.5f * (Z.x - Zm.x)), mu);
+        const int ca = 2 * l, cb = 2 * l + 1;
+        T1[((long long)(X0 + (ca >> 2)) * L + Y0 + (ca & 3)) * Kz + k] = Xa;
+        T1[((long long)(X0 + (cb >> 2)) * L + Y0 + (cb & 3)) * Kz + k] = Xb;
+    }
+}
+
+// BOX = false: spread + z transform of the tile (one kernel).  BOX = true: spread only, the
+// tile's 16 fp32 columns are written to the box (a.box) for pass_z_fast; without the FFT's
+// registers and buffers the spread runs at twice the occupancy.
+template <int L, bool BOX>
+__global__ void __launch_bounds__(128, BOX ? 8 : 4) spread_z_kernel(SpreadZArgs a)
 {
     constexpr int NT = 128;
-    constexpr int TPL = Plan<L>::TPL, E = L / TPL, NG = NT / TPL;
+    constexpr int TPL = Plan<L>::TPL, NG = NT / TPL;
     constexpr int LS = line_stride(L);
     static_assert(NT % TPL == 0 && NG >= SZ_LINES && Plan<L>::n == 2 && warp_local<L>(), "spread_z plan");
     extern __shared__ float4 smz[];
-    const int K = a.K, M = 2 * a.K + 1, Kz = a.K + 1;
-    // layout: phi table | tw | Abuf (NG lines) | region {acc  /  zb}
+    const int Kz = a.K + 1;
+    // layout: phi table | tw | Abuf (NG lines) | region {acc  /  zb}   (BOX: phi table | acc)
     float4 *phi = smz;
     float2 *tw = (float2 *)(phi + 2 * a.phi_n);
     float2 *Abuf = tw + L;
     constexpr int CS = L + 8;                         // column stride: the 4 lane groups of a warp
                                                       // (4 columns) sit 8 banks apart
-    float *acc = (float *)(Abuf + NG * LS);           // [16][CS]
-    float2 *zb = (float2 *)acc;                       // [8][M] (after the spread)
+    float *acc = BOX ? (float *)(phi + 2 * a.phi_n) : (float *)(Abuf + NG * LS);  // [16][CS]
 
     const int b = blockIdx.y;
     const int tpa = L / 4;
@@ -177,7 +244,7 @@ __global__ void __launch_bounds__(128, 4) spread_z_kernel(SpreadZArgs a)
     }
 
     for (int e = threadIdx.x; e < 2 * a.phi_n; e += NT) phi[e] = a.phi[e];
-    load_twiddles<L>(tw, a.tw, threadIdx.x, NT);
+    if (!BOX) load_twiddles<L>(tw, a.tw, threadIdx.x, NT);
     for (int e = threadIdx.x; e < SZ_COLS * CS; e += NT) acc[e] = 0.f;
 
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -256,57 +323,60 @@ __global__ void __launch_bounds__(128, 4) spread_z_kernel(SpreadZArgs a)
     }
     __syncthreads();
 
-    // ---- z transform: line l = columns (2l, 2l+1); group g handles line g % 8, cosets g/8 + (NG/8) r
-    const int g = threadIdx.x / TPL, tl = threadIdx.x % TPL;
-    const int line = g % SZ_LINES;
-    float2 x[E];
-#pragma unroll
-    for (int m = 0; m < E; m++) {
-        const int n = tl + TPL * m;
-        x[m] = make_float2(acc[(2 * line) * CS + n], acc[(2 * line + 1) * CS + n]);
-    }
-    __syncthreads();  // acc dead: zb may overwrite it
-    const int c = a.c, G = a.G;
-    const bool band4 = c == 4 && G == 1024 && K == 255;  // block-uniform
-    const int rounds = (SZ_LINES * c + NG - 1) / NG;
-    for (int r = 0; r < rounds; r++) {
-        const int p = g / SZ_LINES + (NG / SZ_LINES) * r;
-        const bool active = p < c;
-        float2 y[E];
-#pragma unroll
-        for (int m = 0; m < E; m++) y[m] = (active && p) ? cmul(x[m], a.ctw[p * L + tl + TPL * m]) : x[m];
-        fft_regs<L, -1, true>(y, Abuf + g * LS, Abuf + g * LS, tw, tl);
-        if (L == 256 && band4) {
-            // plan L = 256, c = 4, K = 255: outputs m < 4 (k = 4q + p) and m >= 12
-            // (k = 4q + p - 1024) are the band, minus (p, q) = (0, 192)
-#pragma unroll
-            for (int m = 0; m < E; m++) {
-                if (m >= 4 && m < 12) continue;
-                const int k = 4 * (tl + TPL * m) + p - (m >= 12 ? 1024 : 0);
-                if (m != 12 || p != 0 || tl != 0) zb[line * M + k + K] = y[m];
-            }
-        } else if (active) {
-#pragma unroll
-            for (int m = 0; m < E; m++) {
-                int k = c * (tl + TPL * m) + p;
-                if (2 * k > G) k -= G;
-                if (k >= -K && k <= K) zb[line * M + k + K] = y[m];
-            }
+    if (BOX) {  // the tile's 16 columns (1 KB each) to the box
+        float *box = a.box + (long long)b * a.box_bstride;
+        for (int e = threadIdx.x; e < SZ_COLS * L; e += NT) {
+            const int cc = e / L, z = e % L;
+            box[((long long)(X0 + (cc >> 2)) * L + Y0 + (cc & 3)) * L + z] = acc[cc * CS + z];
         }
-        __syncwarp();  // the next round's FFT rewrites this group's buffer
+    } else {
+        tile_z_transform<L, NT>(a, acc, Abuf, tw, T1, X0, Y0);
     }
-    __syncthreads();  // zb complete
-    // ---- unpack the column pairs, multiply by mult_z, store T1 rows (contiguous in kz)
-    for (int e = threadIdx.x; e < SZ_LINES * Kz; e += NT) {
-        const int l = e / Kz, k = e % Kz;
-        const float2 Z = zb[l * M + K + k], Zm = zb[l * M + K - k];
-        const float2 mu = a.mult_z[k];
-        const float2 Xa = cmul(make_float2(0.5f * (Z.x + Zm.x), 0.5f * (Z.y - Zm.y)), mu);
-        const float2 Xb = cmul(make_float2(0.5f * (Z.y + Zm.y), -0.5f * (Z.x - Zm.x)), mu);
-        const int ca = 2 * l, cb = 2 * l + 1;
-        T1[((long long)(X0 + (ca >> 2)) * L + Y0 + (ca & 3)) * Kz + k] = Xa;
-        T1[((long long)(X0 + (cb >> 2)) * L + Y0 + (cb & 3)) * Kz + k] = Xb;
+}
+
+// z transform of the box written by spread_z_kernel<L, true>, tile by tile (4 x 4 columns):
+// the same FFT phase as the fused kernel, its input read from HBM (1 KB column rows).
+template <int L>
+__global__ void __launch_bounds__(128, 4) pass_z_fast_kernel(SpreadZArgs a)
+{
+    constexpr int NT = 128;
+    constexpr int TPL = Plan<L>::TPL, NG = NT / TPL;
+    constexpr int LS = line_stride(L);
+    constexpr int CS = L + 8;
+    extern __shared__ float4 smz[];
+    const int Kz = a.K + 1;
+    float2 *tw = (float2 *)smz;
+    float2 *Abuf = tw + L;
+    float *acc = (float *)(Abuf + NG * LS);  // [16][CS], then zb
+    const int b = blockIdx.y;
+    const int tpa = L / 4;
+    const int X0 = (blockIdx.x / tpa) * 4, Y0 = (blockIdx.x % tpa) * 4;
+    float2 *T1 = a.out + (long long)b * a.out_bstride;
+    {   // same zero-tile test as the spread (which wrote nothing for these tiles)
+        const float dx = fmaxf(fmaxf((float)X0 - a.cx, a.cx - (float)(X0 + 3)), 0.f);
+        const float dy = fmaxf(fmaxf((float)Y0 - a.cy, a.cy - (float)(Y0 + 3)), 0.f);
+        if (dx * dx + dy * dy > a.zero_r2) {
+            if (a.skip_zero) return;
+            for (int e = threadIdx.x; e < SZ_COLS * Kz; e += NT) {
+                const int col = e / Kz, k = e % Kz;
+                T1[((long long)(X0 + (col >> 2)) * L + Y0 + (col & 3)) * Kz + k] = make_float2(0.f, 0.f);
+            }
+            return;
+        }
     }
+    load_twiddles<L>(tw, a.tw, threadIdx.x, NT);
+    const float *box = a.box + (long long)b * a.box_bstride;
+    for (int e = threadIdx.x; e < SZ_COLS * L / 4; e += NT) {
+        const int cc = e / (L / 4), z4 = e % (L / 4);
+        const float4 v = *reinterpret_cast<const float4 *>(box + ((long long)(X0 + (cc >> 2)) * L + Y0 + (cc & 3)) * L + 4 * z4);
+        float *d = acc + cc * CS + 4 * z4;
+        d[0] = v.x;
+        d[1] = v.y;
+        d[2] = v.z;
+        d[3] = v.w;
+    }
+    __syncthreads();
+    tile_z_transform<L, NT>(a, acc, Abuf, tw, T1, X0, Y0);
 }
 
 bool spread_z_supported(int L) { return L == 128 || L == 256; }
@@ -316,10 +386,20 @@ static void spread_z_launch(const SpreadZArgs &a, int batch, cudaStream_t s)
 {
     constexpr int NG = 128 / Plan<L>::TPL;
     const int tpa = L / 4;
+    if (a.box) {  // spread -> box, then the tile z transform
+        const size_t sm1 = (size_t)a.phi_n * 32 + (size_t)SZ_COLS * (L + 8) * 4;
+        cudaFuncSetAttribute(spread_z_kernel<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
+        spread_z_kernel<L, true><<<dim3(tpa * tpa, batch), 128, sm1, s>>>(a);
+        const size_t region = std::max((size_t)SZ_COLS * (L + 8) * 4, (size_t)SZ_LINES * (2 * a.K + 1) * 8);
+        const size_t sm2 = (size_t)L * 8 + (size_t)NG * line_stride(L) * 8 + region;
+        cudaFuncSetAttribute(pass_z_fast_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+        pass_z_fast_kernel<L><<<dim3(tpa * tpa, batch), 128, sm2, s>>>(a);
+        return;
+    }
     const size_t region = std::max((size_t)SZ_COLS * (L + 8) * 4, (size_t)SZ_LINES * (2 * a.K + 1) * 8);
     const size_t sm = (size_t)a.phi_n * 32 + (size_t)L * 8 + (size_t)NG * line_stride(L) * 8 + region;
-    cudaFuncSetAttribute(spread_z_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    spread_z_kernel<L><<<dim3(tpa * tpa, batch), 128, sm, s>>>(a);
+    cudaFuncSetAttribute(spread_z_kernel<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    spread_z_kernel<L, false><<<dim3(tpa * tpa, batch), 128, sm, s>>>(a);
 }
 
 int spread_z_bins(int L) { return (L / SZ_BIN) * (L / SZ_BIN); }
