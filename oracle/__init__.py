@@ -13,6 +13,8 @@ arrays of `synth/`.
                        knots times the ball transform (L276-L294 eq_fballhat,
                        eq_rhoPhat), the Fourier correlation (L398-L404 eq_ccghat)
                        and a direct inverse DFT onto the translation grid.
+* `complementarity.py` -- the shape-complementarity score G of eq_score (L447-L461)
+                       as the four real correlations of its expansion.
 """
 from .lens import (  # noqa: F401
     build_oracle,
@@ -27,3 +29,4 @@ from .bandlimited import (  # noqa: F401
     bandlimited_correlation,
     band_modes,
 )
+from .complementarity import sc_score_points  # noqa: F401
