@@ -163,6 +163,28 @@ def ncu_traffic(stage, rotations):
         return None
 
 
+def path_roofline(N, Np, K, complex_w, rot_per_s, peak):
+    """SURVEY §8(d)'s two whole-path numbers.  R2 (method efficiency): the method's
+    algorithmic bytes per rotation B_alg = 8 M_b 3 (write + read B's band spectrum, read A's)
+    + 8 N_pb 2 (folded product write + read) + s N^3 2 (f write + read), M_b / N_pb the band /
+    folded mode counts (halved for real weights), times rotations/s over the HBM peak.
+    R1: the DRAM bytes ncu measured per rotation over every kernel of the step
+    (profiles/r1/ncu_traffic.json) times rotations/s over the peak."""
+    half = 1 if complex_w else 2
+    M_b = (2 * K + 1) ** 3 / half
+    N_pb = Np ** 3 / half
+    s = 8 if complex_w else 4
+    b_alg = 8 * M_b * 3 + 8 * N_pb * 2 + s * N ** 3 * 2
+    out = {"B_alg_per_rot": b_alg, "R2_method_frac": b_alg * rot_per_s / 1e9 / peak}
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "r1", "ncu_traffic.json")))
+        dram = sum(d["dram_bytes_per_rotation"].values())
+        out.update({"dram_bytes_per_rot": dram, "R1_dram_frac": dram * rot_per_s / 1e9 / peak})
+    except Exception:
+        pass
+    return out
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -370,6 +392,8 @@ def run_ours(args, rank, world, local_rank):
         "e2e": {"value": e2e_value, "unit": METRIC, "h2d_bytes_per_step": int(R.size * 8),
                 "d2h_bytes_per_step": int(n_rot * 16)},
         "roofline": roof,
+        "path_roofline": path_roofline(w.N, kw["Np"], kw["K"], w.weights == "complex",
+                                       n_rot * args.steps / (ms_max / 1e3), peak),
         "cpu_baseline": cpu,
         "stages_ms_per_step": {k: v[0] for k, v in stages.items()},
         "profiled_step_ms": prof_ms,
