@@ -8,7 +8,7 @@ LIB := paper_1711_05075_b200/lib/libballcorr.so
 OBJDIR := build/obj
 OBJ := $(patsubst paper_1711_05075_b200/csrc/%.cu,$(OBJDIR)/%.o,$(SRC))
 
-all: $(LIB) oracle/liboracle.so
+all: $(LIB) oracle/liboracle.so examples/sweep_c
 
 $(OBJDIR)/%.o: paper_1711_05075_b200/csrc/%.cu $(HDR)
 	@mkdir -p $(OBJDIR)
@@ -21,7 +21,14 @@ $(LIB): $(OBJ)
 oracle/liboracle.so: oracle/lens_oracle.c
 	gcc -O2 -fopenmp -shared -fPIC -std=c99 -o $@ $< -lm
 
-clean:
-	rm -rf build $(LIB) oracle/liboracle.so
+# plain-C consumer of the ABI (no Python): links the library with an rpath to its in-tree place
+examples/sweep_c: examples/sweep_c.c include/ballcorr.h $(LIB)
+	gcc -O2 -std=gnu11 -Wall -Iinclude -o $@ $< -Lpaper_1711_05075_b200/lib -lballcorr \
+	    -Wl,-rpath,'$$ORIGIN/../paper_1711_05075_b200/lib' -lm
 
-.PHONY: all clean
+examples: examples/sweep_c
+
+clean:
+	rm -rf build $(LIB) oracle/liboracle.so examples/sweep_c
+
+.PHONY: all clean examples
