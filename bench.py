@@ -258,7 +258,11 @@ def run_ours(args, rank, world, local_rank):
     t = time.perf_counter()
     ctx.shape_upload(0, w.A_xyzr, w.A_w)
     ctx.shape_upload(1, w.B_xyzr, w.B_w)
-    ctx.spectrum_A(stream=stream)
+    if world > 1:  # rank 0 computes A's spectrum, NCCL broadcasts it (north_star)
+        from paper_1711_05075_b200.sharding import broadcast_spectrum_A
+        broadcast_spectrum_A(ctx, src=0)
+    else:
+        ctx.spectrum_A(stream=stream)
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t
 
@@ -386,7 +390,8 @@ def run_ours(args, rank, world, local_rank):
                    "rotations_per_rank_per_step": n_rot, "mode": kw["mode"], "Np": kw["Np"], "K": kw["K"],
                    "output": kind, "l2": "inputs larger than L2 (A spectrum %.0f MB)" % (
                        (2 * kw["K"] + 1) ** 2 * (kw["K"] + 1) * 8 / 1e6),
-                   "setup_s": setup_s},
+                   "setup_s": setup_s,
+                   "spectrum_A": "rank 0, NCCL broadcast" if world > 1 else "computed"},
         "clocks": clocks,
         "gpu_launches": launches,
         "e2e": {"value": e2e_value, "unit": METRIC, "h2d_bytes_per_step": int(R.size * 8),

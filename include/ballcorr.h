@@ -132,6 +132,27 @@ bc_status bc_shape_upload(bc_ctx *ctx, int which, const double *xyzr, const doub
 bc_status bc_spectrum_A(bc_ctx *ctx, void *stream);
 
 /*
+ * Distribution of A's spectrum over GPUs (north_star: "A's spectrum broadcast"; SURVEY
+ * §8(b)/(e)): rotations are sharded over ranks and every rank needs the same band spectrum
+ * of A (the factor rho_A_hat of the spectral product), so one rank
+ * computes it and the others receive it instead of recomputing it.
+ *
+ * bc_spectrum_A_buffer: the device buffer (on the context's device) that holds A's band
+ * spectrum, M*M*Kz complex64 values (M = 2K+1, Kz = K+1 for real and M for complex
+ * weights; layout private to the library, identical for identical bc_params).  Allocated on
+ * first use and owned by the context (freed by bc_destroy; valid until then).  After
+ * bc_spectrum_A it holds the spectrum.  Spectral mode only (BC_EUNSUPPORTED otherwise).
+ *
+ * bc_spectrum_A_import: declare the buffer's current contents to be A's spectrum, written
+ * by the caller (e.g. an NCCL broadcast from a context with identical bc_params that ran
+ * bc_spectrum_A on the same shape A).  The caller must have completed those writes (device
+ * synchronised).  Shape A must be uploaded (its extent enters the support check); BC_ESTATE
+ * otherwise.  Re-uploading A invalidates the import as it invalidates bc_spectrum_A.
+ */
+bc_status bc_spectrum_A_buffer(bc_ctx *ctx, void **dev_ptr, int64_t *bytes);
+bc_status bc_spectrum_A_import(bc_ctx *ctx);
+
+/*
  * Correlate A with R B for n_rot rotations.
  *   R:   host or device, n_rot row-major 3x3 doubles; R R^T = I within 1e-6
  *        and det R > 0, else BC_EINVAL.

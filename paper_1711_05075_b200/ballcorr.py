@@ -55,6 +55,10 @@ _lib.bc_shape_upload.argtypes = [_vp, ctypes.c_int, _vp, _vp, ctypes.c_int64]
 _lib.bc_shape_upload.restype = ctypes.c_int
 _lib.bc_spectrum_A.argtypes = [_vp, _vp]
 _lib.bc_spectrum_A.restype = ctypes.c_int
+_lib.bc_spectrum_A_buffer.argtypes = [_vp, ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_int64)]
+_lib.bc_spectrum_A_buffer.restype = ctypes.c_int
+_lib.bc_spectrum_A_import.argtypes = [_vp]
+_lib.bc_spectrum_A_import.restype = ctypes.c_int
 _lib.bc_correlate_rotations.argtypes = [_vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, _vp]
 _lib.bc_correlate_rotations.restype = ctypes.c_int
 _lib.bc_evaluate_points.argtypes = [_vp, _vp, _vp, ctypes.c_int64, _vp, _vp]
@@ -80,6 +84,8 @@ bc_create = _lib.bc_create
 bc_destroy = _lib.bc_destroy
 bc_shape_upload = _lib.bc_shape_upload
 bc_spectrum_A = _lib.bc_spectrum_A
+bc_spectrum_A_buffer = _lib.bc_spectrum_A_buffer
+bc_spectrum_A_import = _lib.bc_spectrum_A_import
 bc_correlate_rotations = _lib.bc_correlate_rotations
 bc_last_error = _lib.bc_last_error
 bc_status_string = _lib.bc_status_string
@@ -163,6 +169,7 @@ class Correlator:
         p.generic_only = int(bool(generic_only))
         p.concurrency = int(concurrency)
         self.params = p
+        self.device = int(device)
         self.N = p.N
         self.complex = p.weights == BC_WEIGHTS_COMPLEX
         self.f64 = p.precision == BC_FP64 and p.mode == BC_MODE_EXACT
@@ -198,6 +205,27 @@ class Correlator:
 
     def spectrum_A(self, stream=None):
         self._check(_lib.bc_spectrum_A(self._ctx, _stream_handle(stream)))
+
+    def spectrum_A_buffer(self):
+        """(device pointer, bytes) of the buffer holding A's band spectrum (owned by the context)."""
+        ptr, nbytes = _vp(), ctypes.c_int64()
+        self._check(_lib.bc_spectrum_A_buffer(self._ctx, ctypes.byref(ptr), ctypes.byref(nbytes)))
+        return int(ptr.value), int(nbytes.value)
+
+    def spectrum_A_tensor(self):
+        """The same buffer as a float32 torch tensor on the context's device (zero copy, via the
+        CUDA array interface) -- for a torch.distributed broadcast of A's spectrum."""
+        import torch
+        ptr, nbytes = self.spectrum_A_buffer()
+
+        class _Iface:
+            __cuda_array_interface__ = {"shape": (nbytes // 4,), "typestr": "<f4", "data": (ptr, False),
+                                        "version": 3, "strides": None}
+        return torch.as_tensor(_Iface(), device=torch.device("cuda", self.device))
+
+    def spectrum_A_import(self):
+        """Declare the buffer's contents (written by the caller) to be A's spectrum."""
+        self._check(_lib.bc_spectrum_A_import(self._ctx))
 
     def out_shape(self, n_rot, out_kind):
         kind = OUT_KINDS.get(out_kind, out_kind)

@@ -1216,7 +1216,7 @@ bc_status bc_spectrum_A(bc_ctx *ctx, void *stream)
     CU(ctx, cudaSetDevice(ctx->device));
     cudaStream_t s = (cudaStream_t)stream;
     const size_t nspec = (size_t)ctx->M * ctx->M * ctx->Kz;
-    TRY(dalloc(ctx, &ctx->d_Ahat, sizeof(float2) * nspec));
+    if (!ctx->d_Ahat) TRY(dalloc(ctx, &ctx->d_Ahat, sizeof(float2) * nspec));  // fixed size per context
     if (ctx->n[0] == 0) {
         CU(ctx, cudaMemsetAsync(ctx->d_Ahat, 0, sizeof(float2) * nspec, s));
         ctx->have_spec = true;
@@ -1239,6 +1239,30 @@ bc_status bc_spectrum_A(bc_ctx *ctx, void *stream)
     cudaFree(w2);
     if (st != BC_OK) return st;
     if (se != cudaSuccess) return fail(ctx, BC_ECUDA, "spectrum_A: %s", cudaGetErrorString(se));
+    ctx->have_spec = true;
+    return BC_OK;
+}
+
+bc_status bc_spectrum_A_buffer(bc_ctx *ctx, void **dev_ptr, int64_t *bytes)
+{
+    if (!ctx) return BC_EINVAL;
+    if (!dev_ptr || !bytes) return fail(ctx, BC_EINVAL, "NULL dev_ptr/bytes");
+    if (ctx->p.mode != BC_MODE_SPECTRAL) return fail(ctx, BC_EUNSUPPORTED, "exact mode has no spectrum of A");
+    CU(ctx, cudaSetDevice(ctx->device));
+    const size_t nspec = (size_t)ctx->M * ctx->M * ctx->Kz;
+    if (!ctx->d_Ahat) TRY(dalloc(ctx, &ctx->d_Ahat, sizeof(float2) * nspec));
+    *dev_ptr = ctx->d_Ahat;
+    *bytes = (int64_t)(sizeof(float2) * nspec);
+    return BC_OK;
+}
+
+bc_status bc_spectrum_A_import(bc_ctx *ctx)
+{
+    if (!ctx) return BC_EINVAL;
+    if (ctx->p.mode != BC_MODE_SPECTRAL) return fail(ctx, BC_EUNSUPPORTED, "exact mode has no spectrum of A");
+    if (!ctx->have[0]) return fail(ctx, BC_ESTATE, "shape A has not been uploaded");
+    if (!ctx->d_Ahat) return fail(ctx, BC_ESTATE, "bc_spectrum_A_buffer has not been called");
+    ctx->cm_ready = false;  // A'' (coset-major, B's multipliers) is rebuilt from the new contents
     ctx->have_spec = true;
     return BC_OK;
 }

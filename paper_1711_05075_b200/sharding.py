@@ -1,8 +1,10 @@
 """Rotation sharding across ranks (one process per GPU, torch.distributed).
 
 Rotations are independent units: a rank correlates its own block of
-rotations with no data-path collective; the only exchange is the gather of the tiny
-per-rotation results (NCCL all-gather over NVLink on the GPU box, gloo in the CPU tests).
+rotations with no data-path collective.  Two exchanges sit outside the per-rotation path:
+A's band spectrum, computed once by one rank and broadcast to the others (north_star "A's
+spectrum broadcast"), and the gather of the tiny per-rotation results (NCCL over NVLink on
+the GPU box, gloo in the CPU tests).
 """
 from __future__ import annotations
 
@@ -16,6 +18,24 @@ def rotation_block(n_rot: int, rank: int, world: int) -> tuple[int, int]:
     base, extra = divmod(n_rot, world)
     start = rank * base + min(rank, extra)
     return start, start + base + (1 if rank < extra else 0)
+
+
+def broadcast_spectrum_A(corr, src: int = 0, group=None):
+    """Rank `src` computes A's band spectrum (bc_spectrum_A); every rank receives it into its
+    context's spectrum buffer (in place, zero copy) and the others import it.  All ranks must
+    have uploaded the same shapes with identical parameters.  Collective over `group`."""
+    import torch
+    import torch.distributed as dist
+
+    if dist.get_rank(group) == src:
+        corr.spectrum_A()
+    buf = corr.spectrum_A_tensor()
+    dist.broadcast(buf, src=src, group=group)
+    if buf.is_cuda:
+        torch.cuda.synchronize(buf.device)
+    if dist.get_rank(group) != src:
+        corr.spectrum_A_import()
+    return buf.numel() * buf.element_size()
 
 
 def gather_extrema(local_val: np.ndarray, local_idx: np.ndarray, n_rot: int, group=None, device="cpu"):

@@ -1,12 +1,13 @@
 """Multi-rank host logic on CPU (gloo, world_size 2 and 3): rotation blocks and the
-all-gather of per-rotation results reproduce the single-rank global order exactly."""
+all-gather of per-rotation results reproduce the single-rank global order exactly; the
+broadcast of A's spectrum has one rank compute it and every other rank import the same bytes."""
 import os
 import socket
 
 import numpy as np
 import pytest
 
-from paper_1711_05075_b200.sharding import rotation_block, gather_extrema, global_best
+from paper_1711_05075_b200.sharding import rotation_block, gather_extrema, global_best, broadcast_spectrum_A
 
 
 def test_rotation_blocks_cover_exactly():
@@ -59,6 +60,56 @@ def test_gather_extrema_gloo(world, n_rot):
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, world, port, n_rot, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    res = dict(q.get(timeout=10) for _ in range(world))
+    assert all(res[r] for r in range(world)), res
+    assert all(p.exitcode == 0 for p in procs)
+
+
+class _FakeCorrelator:
+    """Stands in for ballcorr.Correlator on CPU: a host tensor as the spectrum buffer."""
+
+    def __init__(self, rank):
+        import torch
+        self.buf = torch.full((1000,), float(-1 - rank))  # garbage that differs per rank
+        self.computed = self.imported = 0
+
+    def spectrum_A(self):
+        import torch
+        self.buf.copy_(torch.arange(1000, dtype=torch.float32) * 0.5)
+        self.computed += 1
+
+    def spectrum_A_tensor(self):
+        return self.buf
+
+    def spectrum_A_import(self):
+        self.imported += 1
+
+
+def _bcast_worker(rank, world, port, src, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    c = _FakeCorrelator(rank)
+    nbytes = broadcast_spectrum_A(c, src=src)
+    ok = bool(torch.equal(c.buf, torch.arange(1000, dtype=torch.float32) * 0.5)) and nbytes == 4000
+    ok = ok and (c.computed, c.imported) == ((1, 0) if rank == src else (0, 1))
+    q.put((rank, ok))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,src", [(2, 0), (3, 2)])
+def test_broadcast_spectrum_gloo(world, src):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bcast_worker, args=(r, world, port, src, q)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
