@@ -41,13 +41,22 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--rot-per-rank", type=int, default=512)
+    ap.add_argument("--workload", default=WORKLOAD, choices=["tiny", "single", "torus", "sweep", "docking"],
+                    help="BASELINE.json config (the metric is quoted on the sweep; the others for reference)")
+    ap.add_argument("--rot-per-rank", type=int, default=0, help="0 = the config's rotation count")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-slabs", type=int, default=32, help="x-slabs of the 256^3 grid in the oracle sample")
+    ap.add_argument("--cpu-slabs", type=int, default=0, help="x-slabs of the grid in the oracle sample (0 = per config)")
     ap.add_argument("--max-batch", type=int, default=0, help="rotations per launch (0 = library default)")
     ap.add_argument("--concurrency", type=int, default=0, help="batches in flight (0 = library default)")
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.cpu_slabs <= 0:
+        args.cpu_slabs = CPU_SLABS[args.workload]
+    return args
+
+
+# oracle sample per config: ~10-30 s of fp64 CPU work on the box's cores
+CPU_SLABS = {"tiny": 32, "single": 64, "torus": 8, "sweep": 32, "docking": 2}
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -153,9 +162,11 @@ STAGE_KERNEL = {"fold_fast": "fold_fast_kernel", "spread_z_B": "spread_z_kernel"
                 "inv_y": "pass_kernel", "inv_z_reduce": "last_tma_kernel"}
 
 
-def ncu_traffic(stage, rotations):
-    """DRAM bytes per launch of `stage` from the committed ncu --set full capture
+def ncu_traffic(stage, rotations, workload="sweep"):
+    """DRAM bytes per launch of `stage` from the committed ncu --set full capture of the sweep
     (profiles/r1/ncu_traffic.json, per rotation), or None."""
+    if workload != "sweep":
+        return None
     try:
         d = json.load(open(os.path.join(ROOT, "profiles", "r1", "ncu_traffic.json")))
         return d["dram_bytes_per_rotation"][STAGE_KERNEL[stage]] * rotations
@@ -177,12 +188,24 @@ def path_roofline(N, Np, K, complex_w, rot_per_s, peak):
     b_alg = 8 * M_b * 3 + 8 * N_pb * 2 + s * N ** 3 * 2
     out = {"B_alg_per_rot": b_alg, "R2_method_frac": b_alg * rot_per_s / 1e9 / peak}
     try:
+        if (N, Np, K, complex_w) != (256, 256, 255, False):
+            raise ValueError("the committed ncu capture is the sweep's")
         d = json.load(open(os.path.join(ROOT, "profiles", "r1", "ncu_traffic.json")))
         dram = sum(d["dram_bytes_per_rotation"].values())
         out.update({"dram_bytes_per_rot": dram, "R1_dram_frac": dram * rot_per_s / 1e9 / peak})
     except Exception:
         pass
     return out
+
+
+def l2_note(w, kw):
+    """Flush-or-larger-than-L2 statement of the timing rules (L2 = 126 MB)."""
+    if kw["mode"] == "spectral":
+        kz = kw["K"] + 1 if w.weights == "real" else 2 * kw["K"] + 1
+        mb = (2 * kw["K"] + 1) ** 2 * kz * 8 / 1e6
+        return "inputs larger than L2 (A spectrum %.0f MB)" % mb if mb > 126 else \
+            "A spectrum %.0f MB fits L2 (re-read every rotation, no flush)" % mb
+    return "exact mode: inputs (ball lists) L2-resident, no flush"
 
 
 def measured_peaks():
@@ -201,36 +224,37 @@ def cpu_oracle_sample(w, R, slabs):
     import oracle
     oracle.build_oracle()
     N = w.N
+    slabs = min(slabs, N)
     lo = (N // 2 - slabs // 2, 0, 0)
     hi = (N // 2 - slabs // 2 + slabs, N, N)
     t = time.perf_counter()
-    oracle.correlate_grid(w.A_xyzr, w.A_w, w.B_xyzr, w.B_w, R, N, w.h, w.t0, lo, hi)
+    f = oracle.correlate_grid(w.A_xyzr, w.A_w, w.B_xyzr, w.B_w, R, N, w.h, w.t0, lo, hi)
     dt = time.perf_counter() - t
     n_t = slabs * N * N
     return {"value": n_t / dt, "unit": METRIC, "cores": oracle.oracle_threads(), "kind": "oracle",
             "sample": f"1 rotation x {slabs}x{N}x{N} translations (x-slabs {lo[0]}..{hi[0] - 1}) of the "
-                      f"{WORKLOAD} workload, fp64, {dt:.2f} s"}
+                      f"{w.name} workload, fp64, {dt:.2f} s"}, (f[lo[0]:hi[0]], lo[0], hi[0])
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    w = make_config(WORKLOAD, n_rot=max(args.steps + args.warmup, 1))
+    w = make_config(args.workload, n_rot=max(args.steps + args.warmup, 1))
     for i in range(args.warmup):
-        cpu_oracle_sample(w, w.R[i % w.n_rot], max(2, args.cpu_slabs // 4))
+        cpu_oracle_sample(w, w.R[i % w.n_rot], max(2, args.cpu_slabs // 4))[0]
     vals, tot = [], 0.0
     last = None
     for i in range(args.steps):
-        last = cpu_oracle_sample(w, w.R[(args.warmup + i) % w.n_rot], args.cpu_slabs)
+        last = cpu_oracle_sample(w, w.R[(args.warmup + i) % w.n_rot], args.cpu_slabs)[0]
         vals.append(last["value"])
     v = float(np.mean(vals))
-    per_step_translations = args.cpu_slabs * w.N * w.N
+    per_step_translations = min(args.cpu_slabs, w.N) * w.N * w.N
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": METRIC, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": per_step_translations / v * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "N": w.N, "n_A": len(w.A_xyzr), "n_B": len(w.B_xyzr),
+        "config": {"workload": w.name, "N": w.N, "n_A": len(w.A_xyzr), "n_B": len(w.B_xyzr),
                    "translations_per_step": per_step_translations, "rotations_per_step": 1},
         "cpu_baseline": {"value": v, "unit": METRIC, "cores": last["cores"], "kind": "oracle", "sample": last["sample"]},
         "e2e": {"value": v, "unit": METRIC, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -248,10 +272,10 @@ def run_ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    w = make_config(WORKLOAD, n_rot=args.rot_per_rank)
-    R = w.R if rank == 0 else random_rotations(np.random.default_rng((0, rank)), args.rot_per_rank)
+    w = make_config(args.workload, n_rot=args.rot_per_rank or None)
+    R = w.R if rank == 0 else random_rotations(np.random.default_rng((0, rank)), w.n_rot)
     n_rot = len(R)
-    kw = correlator_kwargs(WORKLOAD, w.N, w.h, w.t0, w.weights, max_batch=args.max_batch,
+    kw = correlator_kwargs(w.name, w.N, w.h, w.t0, w.weights, max_batch=args.max_batch,
                            concurrency=args.concurrency)
     ctx = ballcorr.Correlator(device=local_rank, **kw)
     stream = torch.cuda.current_stream(dev)
@@ -266,9 +290,11 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t
 
-    kind = "min_argmin"
+    kind = w.output  # sweep: min_argmin; docking: max_real; the others: the full field
+    _, oshape, odt = ctx.out_shape(n_rot, kind)
+    out_bytes = int(np.prod(oshape)) * np.dtype(odt).itemsize
     R_dev = torch.tensor(R, dtype=torch.float64, device=dev)
-    out = torch.empty(n_rot * 16, dtype=torch.uint8, device=dev)
+    out = torch.empty(out_bytes, dtype=torch.uint8, device=dev)
     for _ in range(args.warmup):
         ctx.correlate_rotations(R_dev, kind, out=out, stream=stream)
     torch.cuda.synchronize()
@@ -310,21 +336,21 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     ms_max = float(t_max.item())
-    res = np.frombuffer(out.cpu().numpy().tobytes(), dtype=ballcorr.EXTREMUM_DTYPE)
+    res = np.frombuffer(out.cpu().numpy().tobytes(), dtype=ballcorr.EXTREMUM_DTYPE) if kind != "full" else None
 
     units = n_rot * w.N ** 3 * args.steps * world
     value = units / (ms_max / 1e3)
 
     # gather the per-rotation (min, argmin) of all ranks (outside the timed region)
     best = None
-    if world > 1:
+    if world > 1 and res is not None:
         from paper_1711_05075_b200.sharding import gather_extrema, global_best
         vals, idxs = gather_extrema(res["val"], res["idx"], n_rot * world, device=dev)
-        best = global_best(vals, idxs, "min")
+        best = global_best(vals, idxs, "min" if kind == "min_argmin" else "max")
 
     # e2e through the public API with host buffers (pinned), copies inside the timed region
     R_host = torch.tensor(R, dtype=torch.float64).pin_memory()
-    out_host = torch.empty(n_rot * 16, dtype=torch.uint8).pin_memory()
+    out_host = torch.empty(out_bytes, dtype=torch.uint8).pin_memory()
     ctx.correlate_rotations(R_host, kind, out=out_host, stream=stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -346,11 +372,12 @@ def run_ours(args, rank, world, local_rank):
     # roofline of the dominant kernel (largest share of device time in the timed region):
     # HBM-bound if its algorithmic flop/byte is below the FP32 ridge, else ALU-bound
     q = ctx.query
-    work = stage_work(q, w.N, kw["Np"], kw["K"], w.weights == "complex")
+    spectral = kw["mode"] == "spectral"
+    work = stage_work(q, w.N, kw["Np"], kw["K"], w.weights == "complex") if spectral else {}
     peak, peak_kind = measured_peaks()
     alu_peak = alu_peak_tflops()
     ridge = alu_peak * 1e12 / (peak * 1e9)
-    batch = int(q("batch"))
+    batch = int(q("batch")) if spectral else 1
     per_stage = {}
     for name, (tot_ms, nl) in stages.items():
         if name not in work:
@@ -371,7 +398,7 @@ def run_ours(args, rank, world, local_rank):
         roof = {"bound": "alu" if alu else "hbm", "kernel": name,
                 "achieved": st["fp32_TFLOPs"] if alu else st["hbm_GBps"],
                 "peak": alu_peak if alu else peak, "unit": "TFLOP/s" if alu else "GB/s",
-                "frac": st["alu_frac"] if alu else st["hbm_frac"], "traffic": ncu_traffic(name, batch),
+                "frac": st["alu_frac"] if alu else st["hbm_frac"], "traffic": ncu_traffic(name, batch, w.name),
                 "traffic_source": "profiles/r1/ncu_traffic.json (ncu --set full, dram__bytes_read.sum + "
                                   "dram__bytes_write.sum per rotation x rotations per launch)",
                 "peak_source": ("derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz" if alu else peak_kind),
@@ -380,31 +407,41 @@ def run_ours(args, rank, world, local_rank):
                 "hbm_view": {"achieved_GBps": st["hbm_GBps"], "peak_GBps": peak, "frac": st["hbm_frac"]},
                 "ridge_flop_per_byte": ridge}
     cpu = None
+    rel_err = None
     if world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_oracle_sample(w, R[0], args.cpu_slabs)
+        cpu, (f_ref, x0, x1) = cpu_oracle_sample(w, R[0], args.cpu_slabs)
+        # the metric's third part (BASELINE.json: "rel max error"): this GPU run's full f of the
+        # same rotation (outside the timed region) against the oracle on the sampled slabs
+        f_gpu = ctx.correlate_rotations(R[:1], "full")[0][x0:x1]
+        if w.weights == "complex":
+            f_gpu = f_gpu[..., 0] + 1j * f_gpu[..., 1]
+        tol = 1e-9 if kw["precision"] == "f64" else 1e-4
+        rel_err = {"value": float(np.abs(f_gpu - f_ref).max() / np.abs(f_ref).max()), "tolerance": tol,
+                   "sample": "rotation 0, the cpu_baseline slabs (x %d..%d, %d translations), fp64 oracle"
+                             % (x0, x1 - 1, f_ref.size)}
     line = {
         "metric": METRIC, "value": value, "unit": METRIC, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "N": w.N, "n_A": len(w.A_xyzr), "n_B": len(w.B_xyzr),
+        "scaling": "weak", "vs_baseline": None, "dtype": kw["precision"], "data": "synthetic",
+        "config": {"workload": w.name, "N": w.N, "n_A": len(w.A_xyzr), "n_B": len(w.B_xyzr),
                    "rotations_per_rank_per_step": n_rot, "mode": kw["mode"], "Np": kw["Np"], "K": kw["K"],
-                   "output": kind, "l2": "inputs larger than L2 (A spectrum %.0f MB)" % (
-                       (2 * kw["K"] + 1) ** 2 * (kw["K"] + 1) * 8 / 1e6),
+                   "output": kind, "l2": l2_note(w, kw),
                    "setup_s": setup_s,
                    "spectrum_A": "rank 0, NCCL broadcast" if world > 1 else "computed"},
         "clocks": clocks,
         "gpu_launches": launches,
         "e2e": {"value": e2e_value, "unit": METRIC, "h2d_bytes_per_step": int(R.size * 8),
-                "d2h_bytes_per_step": int(n_rot * 16)},
+                "d2h_bytes_per_step": out_bytes},
         "roofline": roof,
         "path_roofline": path_roofline(w.N, kw["Np"], kw["K"], w.weights == "complex",
-                                       n_rot * args.steps / (ms_max / 1e3), peak),
+                                       n_rot * args.steps / (ms_max / 1e3), peak) if spectral else None,
         "cpu_baseline": cpu,
+        "rel_max_error": rel_err,
         "stages_ms_per_step": {k: v[0] for k, v in stages.items()},
         "profiled_step_ms": prof_ms,
         "stages": per_stage,
-        "result_sample": {"rot0_min": float(res[0]["val"]), "rot0_argmin": int(res[0]["idx"]),
-                          "global_best": best},
+        "result_sample": None if res is None else {"rot0_val": float(res[0]["val"]), "rot0_idx": int(res[0]["idx"]),
+                                                   "global_best": best},
     }
     print(json.dumps(line), flush=True)
 
