@@ -14,6 +14,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "ballcorr.h"
 #include "kernels.cuh"
 
@@ -229,6 +231,8 @@ cudaEvent_t take_event(bc_ctx *ctx)
     return e;
 }
 
+// One stage of the path: an NVTX range (header-only NVTX3; a no-op unless a tool such as ncu
+// --nvtx attaches) and, with bc_set_profiling, a pair of CUDA events on the stage's stream.
 struct StageScope {
     bc_ctx *ctx;
     cudaStream_t s;
@@ -236,6 +240,7 @@ struct StageScope {
     cudaEvent_t e0 = nullptr;
     StageScope(bc_ctx *c, cudaStream_t st, const char *nm) : ctx(c), s(st), name(nm)
     {
+        nvtxRangePushA(nm);
         if (ctx->prof) {
             e0 = take_event(ctx);
             cudaEventRecord(e0, s);
@@ -248,6 +253,7 @@ struct StageScope {
             cudaEventRecord(e1, s);
             ctx->pending.push_back({name, e0, e1});
         }
+        nvtxRangePop();
     }
 };
 
