@@ -174,3 +174,24 @@ def test_sweep_plan_ragged_grid(bc, oracle_mod):
     got = f.reshape(-1)[idx]
     assert np.abs(got - ref).max() <= TOL_F32 * np.abs(ref).max()
     assert mm[1]["val"] == float(f.max()) and mm[0]["val"] == float(f.min())
+
+
+def test_sweep_bench_call_late_rotations(bc, oracle_mod):
+    """The exact call bench.py times (512 rotations, min_argmin, default batching: 32 launches
+    of 16 and device buffers): the last batch's rotations agree with single-rotation full
+    outputs, and the oracle at the reported argmin is the minimum within tolerance."""
+    import torch
+    w = make_config("sweep", n_rot=512)
+    c = correlator(bc, w)
+    R_dev = torch.tensor(w.R, dtype=torch.float64, device="cuda")
+    out = torch.empty(512 * 16, dtype=torch.uint8, device="cuda")
+    c.correlate_rotations(R_dev, "min_argmin", out=out)
+    torch.cuda.synchronize()
+    red = bc.extremum_to_numpy(out.cpu().numpy())
+    for r in (497, 511):
+        f = c.correlate_rotations(w.R[r:r + 1], "full")[0]
+        assert red[r]["val"] == pytest.approx(float(f.min()), abs=1e-12)
+        assert f.reshape(-1)[red[r]["idx"]] == red[r]["val"]
+        idx = sample_indices(f, 30, 20, seed=r, extra=[int(red[r]["idx"])])
+        err, ref = sampled_parity(oracle_mod, w, w.R[r], f, idx)
+        assert err <= TOL_F32, (r, err)
