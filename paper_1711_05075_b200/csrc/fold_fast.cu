@@ -248,14 +248,14 @@ void launch_fold_fast(const FoldFastArgs &a_in, int batch, cudaStream_t s)
 // Block = one ix, 8 consecutive kz.  Rows iy outside B's support cylinder at this ix are
 // zero (spread_z writes them so) and are not loaded.  Per coset only the 128 in-band
 // outputs (q < 64 or q >= 192) are staged and stored.
-__global__ void __launch_bounds__(FF_NT, 5) pass_y_fast_kernel(PassYFastArgs a)
+__global__ void __launch_bounds__(FF_NT, 4) pass_y_fast_kernel(PassYFastArgs a)
 {
     constexpr int E = FF_L / FF_TPL;
     extern __shared__ float2 smf[];
     float2 *tw = smf;
     float2 *X = tw + FF_L;
-    float2 *Ab = X + FF_NL * FF_LS;
-    const float2 *__restrict__ ctw = a.ctw;  // through L1 (keeps shared memory to 5 blocks / SM)
+    float2 *Ab = X;  // the input lines live in registers once read, so the FFT buffer reuses X
+    const float2 *__restrict__ ctw = a.ctw;  // through L1
     const int line = threadIdx.x / FF_TPL, tl = threadIdx.x % FF_TPL;
     const int b = blockIdx.y;
     constexpr int ZT = FF_KZ / FF_NL;
@@ -293,15 +293,20 @@ __global__ void __launch_bounds__(FF_NT, 5) pass_y_fast_kernel(PassYFastArgs a)
         }
     }
     __syncthreads();
+    float2 xr[E];  // the line stays in registers across the cosets: one shared-memory read
+    //                (the kernel is L1/shared-bound; 4 blocks/SM at 121 registers)
+#pragma unroll
+    for (int m = 0; m < E; m++) xr[m] = X[line * FF_LS + pad(tl + FF_TPL * m)];
+    __syncthreads();  // X is overwritten by the first FFT exchange below
 #pragma unroll 1
     for (int p = 0; p < FF_C; p++) {  // runtime loop: one FFT copy in the instruction cache
         // coset twiddle e^{-2 pi i p (tl + 16 m) / 1024} = c1 * e^{-2 pi i p m / 64}: one L1 load
-        // per thread and a warp-uniform constant per element (the kernel is L1-bound)
+        // per thread and a warp-uniform constant per element
         const float2 c1 = __ldg(ctw + p * FF_L + tl);
         float2 y[E];
 #pragma unroll
         for (int m = 0; m < E; m++) {
-            const float2 v = X[line * FF_LS + pad(tl + FF_TPL * m)];
+            const float2 v = xr[m];
             const int e = (p * m) & 63;
             y[m] = p ? cmul(v, cmul(c1, make_float2(c_w64.re[e], c_w64.im[e]))) : v;
         }
@@ -337,7 +342,7 @@ bool pass_y_fast_supported(int L, int c, int G, int K, int complex_w)
 
 void launch_pass_y_fast(const PassYFastArgs &a, int batch, cudaStream_t s)
 {
-    const size_t sm = sizeof(float2) * ((size_t)FF_L + 2 * FF_NL * FF_LS);
+    const size_t sm = sizeof(float2) * ((size_t)FF_L + FF_NL * FF_LS);
     cudaFuncSetAttribute(pass_y_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     pass_y_fast_kernel<<<dim3((unsigned)(FF_L * (FF_KZ / FF_NL)), batch), FF_NT, sm, s>>>(a);
 }
