@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(128, BOX ? 8 : 4) spread_z_kernel(SpreadZArgs 
 
     for (int e = threadIdx.x; e < 2 * a.phi_n; e += NT) phi[e] = a.phi[e];
     if (!BOX) load_twiddles<L>(tw, a.tw, threadIdx.x, NT);
-    for (int e = threadIdx.x; e < SZ_COLS * CS; e += NT) acc[e] = 0.f;
+    for (int e = threadIdx.x; e < SZ_COLS * CS / 4; e += NT) reinterpret_cast<float4 *>(acc)[e] = make_float4(0.f, 0.f, 0.f, 0.f);
 
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int gi = lane >> 3, hl = lane & 7;
@@ -325,9 +325,10 @@ __global__ void __launch_bounds__(128, BOX ? 8 : 4) spread_z_kernel(SpreadZArgs 
 
     if (BOX) {  // the tile's 16 columns (1 KB each) to the box
         float *box = a.box + (long long)b * a.box_bstride;
-        for (int e = threadIdx.x; e < SZ_COLS * L; e += NT) {
-            const int cc = e / L, z = e % L;
-            box[((long long)(X0 + (cc >> 2)) * L + Y0 + (cc & 3)) * L + z] = acc[cc * CS + z];
+        for (int e = threadIdx.x; e < SZ_COLS * L / 4; e += NT) {  // 16-byte rows (CS, L multiples of 4)
+            const int cc = e / (L / 4), z4 = e % (L / 4);
+            *reinterpret_cast<float4 *>(box + ((long long)(X0 + (cc >> 2)) * L + Y0 + (cc & 3)) * L + 4 * z4) =
+                *reinterpret_cast<const float4 *>(acc + cc * CS + 4 * z4);
         }
     } else {
         tile_z_transform<L, NT>(a, acc, Abuf, tw, T1, X0, Y0);
