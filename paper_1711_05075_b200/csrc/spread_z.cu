@@ -190,15 +190,18 @@ __device__ __forceinline__ void tile_z_transform(const SpreadZArgs &a, float *ac
         __syncwarp();  // the next round's FFT rewrites this group's buffer
     }
     __syncthreads();  // zb complete
-    for (int e = threadIdx.x; e < SZ_LINES * Kz; e += NT) {
-        const int l = e / Kz, k = e % Kz;
-        const float2 Z = zb[l * M + K + k], Zm = zb[l * M + K - k];
-        const float2 mu = a.mult_z[k];
-        const float2 Xa = cmul(make_float2(0.5f * (Z.x + Zm.x), 0.5f * (Z.y - Zm.y)), mu);
-        const float2 Xb = cmul(make_float2(0.5f * (Z.y + Zm.y), -0.5f * (Z.x - Zm.x)), mu);
+#pragma unroll 1
+    for (int l = 0; l < SZ_LINES; l++) {  // line l = columns 2l (real part) and 2l + 1 (imaginary)
         const int ca = 2 * l, cb = 2 * l + 1;
-        T1[((long long)(X0 + (ca >> 2)) * L + Y0 + (ca & 3)) * Kz + k] = Xa;
-        T1[((long long)(X0 + (cb >> 2)) * L + Y0 + (cb & 3)) * Kz + k] = Xb;
+        float2 *Ta = T1 + ((long long)(X0 + (ca >> 2)) * L + Y0 + (ca & 3)) * Kz;
+        float2 *Tb = T1 + ((long long)(X0 + (cb >> 2)) * L + Y0 + (cb & 3)) * Kz;
+        const float2 *zl = zb + l * M + K;
+        for (int k = threadIdx.x; k < Kz; k += NT) {
+            const float2 Z = zl[k], Zm = zl[-k];
+            const float2 mu = a.mult_z[k];
+            Ta[k] = cmul(make_float2(0.5f * (Z.x + Zm.x), 0.5f * (Z.y - Zm.y)), mu);
+            Tb[k] = cmul(make_float2(0.5f * (Z.y + Zm.y), -0.5f * (Z.x - Zm.x)), mu);
+        }
     }
 }
 
@@ -369,12 +372,8 @@ __global__ void __launch_bounds__(128, 4) pass_z_fast_kernel(SpreadZArgs a)
     const float *box = a.box + (long long)b * a.box_bstride;
     for (int e = threadIdx.x; e < SZ_COLS * L / 4; e += NT) {
         const int cc = e / (L / 4), z4 = e % (L / 4);
-        const float4 v = *reinterpret_cast<const float4 *>(box + ((long long)(X0 + (cc >> 2)) * L + Y0 + (cc & 3)) * L + 4 * z4);
-        float *d = acc + cc * CS + 4 * z4;
-        d[0] = v.x;
-        d[1] = v.y;
-        d[2] = v.z;
-        d[3] = v.w;
+        *reinterpret_cast<float4 *>(acc + cc * CS + 4 * z4) =
+            *reinterpret_cast<const float4 *>(box + ((long long)(X0 + (cc >> 2)) * L + Y0 + (cc & 3)) * L + 4 * z4);
     }
     __syncthreads();
     tile_z_transform<L, NT>(a, acc, Abuf, tw, T1, X0, Y0);
