@@ -32,9 +32,12 @@ __device__ __forceinline__ int coset_kk(int q, int p, int c, int G, int klo, int
 // ============================================================================ generic axis pass
 // IN_MODE: 0 contiguous real rows, 1 contiguous complex rows, 2 strided in[b][O][L][I].
 // OUT_MODE: 0 rows out[b][row][nk] (row = line index), 1 strided out[b][O][nk][I].
+// SIGN > 0 (the inverse passes): one coset, no multipliers, outputs q < nk (every inverse
+// launch sets c = 1, klo = 0, unsigned k) -- compile-time here.
 template <int L, int SIGN, int IN_MODE, int OUT_MODE>
 __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TPL * Plan<L>::NL)) pass_kernel(PassArgs a)
 {
+    constexpr bool INV = SIGN > 0;
     constexpr int TPL = Plan<L>::TPL, NL = Plan<L>::NL, NT = TPL * NL;
     constexpr int LS = line_stride(L), E = L / TPL;
     extern __shared__ float2 sm[];
@@ -96,7 +99,8 @@ __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TP
     }
 
     float2 *outs = a.out + (long long)b * a.out_bstride;
-    for (int p = 0; p < a.c; p++) {
+    const int ncos = INV ? 1 : a.c;
+    for (int p = 0; p < ncos; p++) {
         float2 y[E];
 #pragma unroll
         for (int m = 0; m < E; m++) y[m] = p ? cmul(x[m], a.ctw[p * L + tl + TPL * m]) : x[m];
@@ -104,8 +108,8 @@ __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TP
         if (OUT_MODE == 0) {
 #pragma unroll
             for (int m = 0; m < E; m++) {
-                const int kk = coset_kk(tl + TPL * m, p, a.c, a.G, a.klo, a.signed_k);
-                if (kk >= 0 && kk < a.nk) OUT[line * a.nk + kk] = a.mult ? cmul(y[m], a.mult[kk]) : y[m];
+                const int kk = INV ? tl + TPL * m : coset_kk(tl + TPL * m, p, a.c, a.G, a.klo, a.signed_k);
+                if (kk >= 0 && kk < a.nk) OUT[line * a.nk + kk] = (!INV && a.mult) ? cmul(y[m], a.mult[kk]) : y[m];
             }
             __syncthreads();
         } else {
@@ -115,6 +119,12 @@ __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TP
             __syncthreads();
             const int pout = a.pitch_out ? a.pitch_out : a.I;
             float2 *out = outs + (long long)o * a.nk * pout;
+            if (INV) {  // rows q < nk of this block's NL columns: no per-element coset arithmetic
+                const int i = threadIdx.x % NL;
+                float2 *oc = out + i0 + i;
+                if (i0 + i < a.I)
+                    for (int q = threadIdx.x / NL; q < a.nk; q += NT / NL) oc[(long long)q * pout] = A[i * LS + pad(q)];
+            } else
             for (int e = threadIdx.x; e < L * NL; e += NT) {
                 const int q = e / NL, i = e % NL;
                 const int kk = coset_kk(q, p, a.c, a.G, a.klo, a.signed_k);
