@@ -548,7 +548,8 @@ __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TP
     constexpr int LS = line_stride(L), E = L / TPL;
     constexpr bool WS = warp_local<L>();
     extern __shared__ __align__(16) float2 sm[];
-    const int Fz = a.Fz, Pz = a.pitch ? a.pitch : a.Fz;  // stored modes, row pitch
+    constexpr int Fz = L / 2 + 1;  // Hermitian rows (launch_last takes this kernel only then)
+    const int Pz = a.pitch ? a.pitch : a.Fz;  // row pitch
     float2 *stage = sm;                          // [2][2 NL][Pz]
     float2 *tw = stage + 2 * 2 * NL * Pz;
     float2 *A = tw + L;
