@@ -111,23 +111,20 @@ __global__ void __launch_bounds__(FF_NT, 4) fold_fast_kernel(FoldFastArgs a)
         const int ky = slot_ky(tkyp, pass, al);  // this thread's line
         {
             // ---- T2 lines (ky, kz(i)) -> X (transposed through registers for coalescing)
+            // element m of this thread: row n = n0 + 16 m of line i (e = tid + 128 m, i = e % 8),
+            // so the line's validity and source column are per-thread constants
+            const int i = threadIdx.x % FF_NL, n0 = threadIdx.x / FF_NL;
+            const int kt = line_kz(i);
+            const int kyi = slot_ky(line_kyp(i), pass, al);
+            const bool ok = (pass == 0 ? (kt < FF_FZ) : (kt >= 1 && kt < FF_FZ)) && kyi >= -FF_K && kyi <= FF_K;
+            const float2 *src = T2 + (long long)(n0 * FF_M + kyi + FF_K) * FF_KZ + (pass == 0 ? kt : FF_NP - kt);
             float2 x[E];
 #pragma unroll
-            for (int m = 0; m < E; m++) {
-                const int e = threadIdx.x + FF_NT * m;
-                const int n = e / FF_NL, i = e % FF_NL;
-                const int kt = line_kz(i);
-                const int kyi = slot_ky(line_kyp(i), pass, al);
-                const bool ok = (pass == 0 ? (kt < FF_FZ) : (kt >= 1 && kt < FF_FZ)) && kyi >= -FF_K && kyi <= FF_K;
-                const int kz = pass == 0 ? kt : FF_NP - kt;
-                x[m] = ok ? T2[(n * FF_M + kyi + FF_K) * FF_KZ + kz] : make_float2(0.f, 0.f);
-            }
+            for (int m = 0; m < E; m++)
+                x[m] = ok ? src[(long long)(FF_NT / FF_NL) * m * FF_M * FF_KZ] : make_float2(0.f, 0.f);
             __syncthreads();  // previous group's last reads of X / Ab are done
 #pragma unroll
-            for (int m = 0; m < E; m++) {
-                const int e = threadIdx.x + FF_NT * m;
-                X[(e % FF_NL) * FF_LS + pad(e / FF_NL)] = x[m];
-            }
+            for (int m = 0; m < E; m++) X[i * FF_LS + pad(n0 + (FF_NT / FF_NL) * m)] = x[m];
             __syncthreads();
             const bool my_ok = (pass == 0 ? (tz < FF_FZ) : (tz >= 1 && tz < FF_FZ)) && ky >= -FF_K && ky <= FF_K;
             const int my_kz = pass == 0 ? tz : FF_NP - tz;
