@@ -320,10 +320,10 @@ __global__ void __launch_bounds__(FF_NT, 4) pass_y_fast_kernel(PassYFastArgs a)
             Ab[line * FF_LS + u] = cmul(y[m], mu);
         }
         __syncthreads();
+        const int io = threadIdx.x % FF_NL, u0 = threadIdx.x / FF_NL;  // e = tid + 128 r
 #pragma unroll
         for (int r = 0; r < 8; r++) {
-            const int e = threadIdx.x + FF_NT * r;
-            const int u = e / FF_NL, i = e % FF_NL;
+            const int u = u0 + (FF_NT / FF_NL) * r, i = io;
             const int q = u < 64 ? u : u + 128;
             const int ky = FF_C * q + p - (q >= 192 ? FF_G : 0);
             if (ky >= -FF_K) T2[(ky + FF_K) * FF_KZ + kz0 + i] = Ab[i * FF_LS + u];
