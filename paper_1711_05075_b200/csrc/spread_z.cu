@@ -166,9 +166,21 @@ __device__ __forceinline__ void tile_z_transform(const SpreadZArgs &a, float *ac
     for (int r = 0; r < rounds; r++) {
         const int p = g / SZ_LINES + (NG / SZ_LINES) * r;
         const bool active = p < c;
+        // coset twiddle e^{-2 pi i p n / G} at n = tl + TPL m: the lane's first value times the
+        // step e^{-2 pi i p TPL / G}, by recurrence (E steps, ~E ulp)
         float2 y[E];
+        if (active && p) {
+            float2 t = a.ctw[p * L + tl];
+            const float2 Wp = a.ctw[p * L + TPL];
 #pragma unroll
-        for (int m = 0; m < E; m++) y[m] = (active && p) ? cmul(x[m], a.ctw[p * L + tl + TPL * m]) : x[m];
+            for (int m = 0; m < E; m++) {
+                y[m] = cmul(x[m], t);
+                t = cmul(t, Wp);
+            }
+        } else {
+#pragma unroll
+            for (int m = 0; m < E; m++) y[m] = x[m];
+        }
         fft_regs<L, -1, true>(y, Abuf + g * LS, Abuf + g * LS, tw, tl);
         if (L == 256 && band4) {
             // plan L = 256, c = 4, K = 255: outputs m < 4 (k = 4q + p) and m >= 12
