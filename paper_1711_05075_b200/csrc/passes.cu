@@ -541,7 +541,7 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
                  : "memory");
 }
 
-template <int L>
+template <int L, bool NFULL>  // NFULL: N = L output rows (compile-time loop bounds)
 __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TPL * Plan<L>::NL)) last_tma_kernel(LastArgs a)
 {
     constexpr int TPL = Plan<L>::TPL, NL = Plan<L>::NL, NT = TPL * NL;
@@ -558,7 +558,8 @@ __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TP
     __shared__ unsigned long long red[2][NT / 32];
     const int line = threadIdx.x / TPL, tl = threadIdx.x % TPL;
     const int b = blockIdx.y;
-    const long long lines = (long long)a.N * a.N;
+    const int Nn = NFULL ? L : a.N;  // output rows
+    const long long lines = (long long)Nn * Nn;
     const long long ntiles = (lines + 2 * NL - 1) / (2 * NL);
     const bool reduce = a.out_kind != BC_OUT_F_FULL;
     const float2 *in = a.in + (long long)b * a.in_bstride;
@@ -617,13 +618,13 @@ __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TP
 #pragma unroll
             for (int m = 0; m < E; m++) {
                 const int q = tl + TPL * m;
-                if (q >= a.N) continue;
+                if (!NFULL && q >= Nn) continue;
                 const float2 v = cscale(x[m], a.scale);
-                const long long gidx = l0 * a.N + q;
+                const long long gidx = l0 * Nn + q;
                 if (!reduce) {
                     float *o = (float *)a.out_full + (long long)b * a.full_bstride + gidx;
                     o[0] = v.x;
-                    if (has1) o[a.N] = v.y;
+                    if (has1) o[Nn] = v.y;
                 } else {
                     const unsigned gi = (unsigned)gidx;
                     if (v.x < vmin) { vmin = v.x; imin = gi; }
@@ -634,9 +635,9 @@ __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TP
 #pragma unroll
                 for (int m = 0; m < E; m++) {
                     const int q = tl + TPL * m;
-                    if (q >= a.N) continue;
+                    if (!NFULL && q >= Nn) continue;
                     const float vy = x[m].y * a.scale;
-                    const unsigned gi = (unsigned)((l0 + 1) * a.N + q);
+                    const unsigned gi = (unsigned)((l0 + 1) * Nn + q);
                     if (vy < vmin) { vmin = vy; imin = gi; }
                     if (vy > vmax) { vmax = vy; imax = gi; }
                 }
@@ -788,8 +789,13 @@ void launch_last(const LastArgs &a, int batch, cudaStream_t s)
         const long long lines = (long long)a.N * a.N;
         const long long tiles = (lines + 2 * NL - 1) / (2 * NL);
         const long long cap = std::max(1LL, 4LL * 148 * 4 / std::max(batch, 1));
-        set_smem(last_tma_kernel<256>, sm);
-        last_tma_kernel<256><<<dim3((unsigned)std::min(tiles, cap), batch), Plan<256>::TPL * NL, sm, s>>>(a);
+        if (a.N == 256) {
+            set_smem(last_tma_kernel<256, true>, sm);
+            last_tma_kernel<256, true><<<dim3((unsigned)std::min(tiles, cap), batch), Plan<256>::TPL * NL, sm, s>>>(a);
+        } else {
+            set_smem(last_tma_kernel<256, false>, sm);
+            last_tma_kernel<256, false><<<dim3((unsigned)std::min(tiles, cap), batch), Plan<256>::TPL * NL, sm, s>>>(a);
+        }
         return;
     }
     switch (a.Np) {
