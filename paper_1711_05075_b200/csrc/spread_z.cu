@@ -142,14 +142,15 @@ __global__ void __launch_bounds__(256) szb_fill_kernel(SzBinArgs a)
 // g % 8 and cosets g / 8 + (NG / 8) r; the band of Z(k), |k| <= K, goes to zb[8][2K + 1]
 // (aliasing acc once the lines are in registers); A(k) = (Z(k) + conj Z(-k)) / 2,
 // B(k) = (Z(k) - conj Z(-k)) / 2i, times mult_z, are stored as T1 rows.
-template <int L, int NT>
+// B4: the sweep plan's band (c = 4, G = 1024, K = 255) as compile-time constants
+template <int L, int NT, bool B4 = false>
 __device__ __forceinline__ void tile_z_transform(const SpreadZArgs &a, float *acc, float2 *Abuf, const float2 *tw,
                                                  float2 *T1, int X0, int Y0)
 {
     constexpr int TPL = Plan<L>::TPL, E = L / TPL, NG = NT / TPL;
     constexpr int LS = line_stride(L);
     constexpr int CS = L + 8;
-    const int K = a.K, M = 2 * a.K + 1, Kz = a.K + 1;
+    const int K = B4 ? 255 : a.K, M = 2 * K + 1, Kz = K + 1;
     float2 *zb = (float2 *)acc;
     const int g = threadIdx.x / TPL, tl = threadIdx.x % TPL;
     const int line = g % SZ_LINES;
@@ -160,8 +161,8 @@ __device__ __forceinline__ void tile_z_transform(const SpreadZArgs &a, float *ac
         x[m] = make_float2(acc[(2 * line) * CS + n], acc[(2 * line + 1) * CS + n]);
     }
     __syncthreads();  // acc dead: zb may overwrite it
-    const int c = a.c, G = a.G;
-    const bool band4 = c == 4 && G == 1024 && K == 255;  // block-uniform
+    const int c = B4 ? 4 : a.c, G = B4 ? 1024 : a.G;
+    const bool band4 = B4 || (c == 4 && G == 1024 && K == 255);  // block-uniform
     const int rounds = (SZ_LINES * c + NG - 1) / NG;
     for (int r = 0; r < rounds; r++) {
         const int p = g / SZ_LINES + (NG / SZ_LINES) * r;
@@ -352,7 +353,7 @@ __global__ void __launch_bounds__(128, BOX ? 8 : 4) spread_z_kernel(SpreadZArgs 
 
 // z transform of the box written by spread_z_kernel<L, true>, tile by tile (4 x 4 columns):
 // the same FFT phase as the fused kernel, its input read from HBM (1 KB column rows).
-template <int L>
+template <int L, bool B4>
 __global__ void __launch_bounds__(128, 4) pass_z_fast_kernel(SpreadZArgs a)
 {
     constexpr int NT = 128;
@@ -388,7 +389,7 @@ __global__ void __launch_bounds__(128, 4) pass_z_fast_kernel(SpreadZArgs a)
             *reinterpret_cast<const float4 *>(box + ((long long)(X0 + (cc >> 2)) * L + Y0 + (cc & 3)) * L + 4 * z4);
     }
     __syncthreads();
-    tile_z_transform<L, NT>(a, acc, Abuf, tw, T1, X0, Y0);
+    tile_z_transform<L, NT, B4>(a, acc, Abuf, tw, T1, X0, Y0);
 }
 
 bool spread_z_supported(int L) { return L == 128 || L == 256; }
@@ -404,8 +405,13 @@ static void spread_z_launch(const SpreadZArgs &a, int batch, cudaStream_t s)
         spread_z_kernel<L, true><<<dim3(tpa * tpa, batch), 128, sm1, s>>>(a);
         const size_t region = std::max((size_t)SZ_COLS * (L + 8) * 4, (size_t)SZ_LINES * (2 * a.K + 1) * 8);
         const size_t sm2 = (size_t)L * 8 + (size_t)NG * line_stride(L) * 8 + region;
-        cudaFuncSetAttribute(pass_z_fast_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
-        pass_z_fast_kernel<L><<<dim3(tpa * tpa, batch), 128, sm2, s>>>(a);
+        if (L == 256 && a.c == 4 && a.G == 1024 && a.K == 255) {
+            cudaFuncSetAttribute(pass_z_fast_kernel<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+            pass_z_fast_kernel<L, true><<<dim3(tpa * tpa, batch), 128, sm2, s>>>(a);
+        } else {
+            cudaFuncSetAttribute(pass_z_fast_kernel<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+            pass_z_fast_kernel<L, false><<<dim3(tpa * tpa, batch), 128, sm2, s>>>(a);
+        }
         return;
     }
     const size_t region = std::max((size_t)SZ_COLS * (L + 8) * 4, (size_t)SZ_LINES * (2 * a.K + 1) * 8);
