@@ -845,7 +845,9 @@ bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, voi
         a.out = (float2 *)ws2;
         a.out_bstride = (long long)(s2_per / 8);
         StageScope sc(ctx, s, "spread_z_B");
-        launch_spread_z(a, nb, s);
+        if (!launch_spread_z(a, nb, s))
+            return fail(ctx, BC_EUNSUPPORTED, "spread_z: profile table (n = %d, U = %g) or box L = %d not compiled in",
+                        a.phi_n, (double)a.phi_U, a.L);
         ctx->launches += a.box ? 2 : 1;
     } else {
         SpreadArgs a{};

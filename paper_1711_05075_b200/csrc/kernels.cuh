@@ -76,7 +76,7 @@ struct SpreadZArgs {
     long long box_bstride;  // then a separate tile z transform (two kernels, see spread_z.cu)
 };
 bool spread_z_supported(int L);
-void launch_spread_z(const SpreadZArgs &a, int batch, cudaStream_t s);
+bool launch_spread_z(const SpreadZArgs &a, int batch, cudaStream_t s);  // false: unsupported plan/table
 
 // ----------------------------------------------------------------- coset-major band order
 // Band |k| <= K of an axis plan (L, c, G): coset p holds q in [0, qp] (k = c q + p >= 0) and

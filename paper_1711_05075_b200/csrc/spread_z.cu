@@ -30,6 +30,8 @@ namespace {
 constexpr int SZ_COLS = 16;    // columns per block (4 x 4)
 constexpr int SZ_LINES = 8;    // complex lines (column pairs)
 constexpr int SZ_BIN = 16;     // binning: 16 x 16 columns
+constexpr int SZ_PHI_N = 96;   // profile table pieces over [-W, W], W = 4 cells
+constexpr float SZ_PHI_U = 4.f;
 
 struct PhiVal {
     float p1, p2;
@@ -269,9 +271,11 @@ __global__ void __launch_bounds__(128, BOX ? 8 : 4) spread_z_kernel(SpreadZArgs 
     const float fx = (float)(X0 + wid), fy = (float)(Y0 + gi);
     const float fy0 = (float)Y0;
     float *accc = acc + col * CS;
-    const float U = a.phi_U, invD = a.phi_invD;
-    const float tmax = (float)a.phi_n - 1e-3f;
-    const int nphi = a.phi_n;
+    // the blob's profile table (pieces of W/48 over [-W, W], W = 4 cells: n = 96) as constants;
+    // launch_spread_z refuses a table of another shape
+    constexpr int nphi = SZ_PHI_N;
+    constexpr float U = SZ_PHI_U, invD = (float)SZ_PHI_N / (2.f * SZ_PHI_U);
+    constexpr float tmax = (float)SZ_PHI_N - 1e-3f;
     const int bin = (X0 / SZ_BIN) * (L / SZ_BIN) + Y0 / SZ_BIN;
     const int cnt = a.counts[b * a.nbins + bin];
     const int *lst = a.lists + (long long)b * a.list_stride + a.offs[b * a.nbins + bin];
@@ -431,11 +435,12 @@ void launch_spread_z_bin(const SzBinArgs &a, int batch, cudaStream_t s)
     szb_fill_kernel<<<dim3(a.nbins, batch), 256, 0, s>>>(a);
 }
 
-void launch_spread_z(const SpreadZArgs &a, int batch, cudaStream_t s)
+bool launch_spread_z(const SpreadZArgs &a, int batch, cudaStream_t s)
 {
+    if (a.phi_n != SZ_PHI_N || a.phi_U != SZ_PHI_U) return false;  // the table shape is compiled in
     switch (a.L) {
-    case 128: spread_z_launch<128>(a, batch, s); break;
-    case 256: spread_z_launch<256>(a, batch, s); break;
-    default: break;
+    case 128: spread_z_launch<128>(a, batch, s); return true;
+    case 256: spread_z_launch<256>(a, batch, s); return true;
+    default: return false;
     }
 }
