@@ -245,7 +245,7 @@ void launch_fold_fast(const FoldFastArgs &a_in, int batch, cudaStream_t s)
 // Block = one ix, 8 consecutive kz.  Rows iy outside B's support cylinder at this ix are
 // zero (spread_z writes them so) and are not loaded.  Per coset only the 128 in-band
 // outputs (q < 64 or q >= 192) are staged and stored.
-__global__ void __launch_bounds__(FF_NT, 4) pass_y_fast_kernel(PassYFastArgs a)
+__global__ void __launch_bounds__(FF_NT, 5) pass_y_fast_kernel(PassYFastArgs a)
 {
     constexpr int E = FF_L / FF_TPL;
     extern __shared__ float2 smf[];
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(FF_NT, 4) pass_y_fast_kernel(PassYFastArgs a)
     }
     __syncthreads();
     float2 xr[E];  // the line stays in registers across the cosets: one shared-memory read
-    //                (the kernel is L1/shared-bound; 4 blocks/SM at 121 registers)
+    //                (the kernel is L1/shared-bound; 5 blocks/SM at 96 registers)
 #pragma unroll
     for (int m = 0; m < E; m++) xr[m] = X[line * FF_LS + pad(tl + FF_TPL * m)];
     __syncthreads();  // X is overwritten by the first FFT exchange below
