@@ -1466,7 +1466,9 @@ bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, in
                 a.x1_pitch = zpitch;
                 a.N = (int)N;
                 StageScope sc(ctx, s, "fold_fast");
-                launch_fold_fast(a, b, s);
+                if (!launch_fold_fast(a, b, s))
+                    return fail(ctx, BC_EUNSUPPORTED, "fold_fast: strides (MS = %d, X1 pitch = %d) not the compiled plan's",
+                                a.MS, a.x1_pitch);
                 ctx->launches++;
             } else {
                 FoldXArgs a{};

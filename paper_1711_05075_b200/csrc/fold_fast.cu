@@ -30,6 +30,9 @@ constexpr int FF_L = 256, FF_C = 4, FF_TPL = 16, FF_NL = 8, FF_NT = FF_NL * FF_T
 constexpr int FF_G = FF_C * FF_L, FF_K = FF_G / 4 - 1, FF_M = 2 * FF_K + 1, FF_KZ = FF_K + 1;
 constexpr int FF_NP = FF_L, FF_FZ = FF_NP / 2 + 1;
 constexpr int FF_LS = line_stride(FF_L);
+// the plan's strides as compile-time constants (the launcher refuses others)
+constexpr int FF_MS = cm_row_stride(FF_L, FF_C, FF_G, FF_K);  // A'' row stride (coset-major)
+constexpr int FF_X1P = (FF_FZ + 7) & ~7;                     // X1 row pitch (api.cu's zpitch)
 static_assert(Plan<FF_L>::TPL == FF_TPL && Plan<FF_L>::n == 2, "fold_fast plan");
 
 }  // namespace
@@ -128,7 +131,7 @@ __global__ void __launch_bounds__(FF_NT, 4) fold_fast_kernel(FoldFastArgs a)
             __syncthreads();
             const bool my_ok = (pass == 0 ? (tz < FF_FZ) : (tz >= 1 && tz < FF_FZ)) && ky >= -FF_K && ky <= FF_K;
             const int my_kz = pass == 0 ? tz : FF_NP - tz;
-            const float2 *arow = a.Ahat + (long long)((ky + FF_K) * FF_KZ + (my_ok ? my_kz : 0)) * a.MS;
+            const float2 *arow = a.Ahat + (long long)((ky + FF_K) * FF_KZ + (my_ok ? my_kz : 0)) * FF_MS;
             // one copy of the FFT (runtime coset loop keeps the code in the instruction cache);
             // only the register-accumulator update is specialised per coset
 #pragma unroll 1
@@ -213,7 +216,7 @@ __global__ void __launch_bounds__(FF_NT, 4) fold_fast_kernel(FoldFastArgs a)
     float2 *X1 = a.X1 + (long long)b * a.x1_bstride;
     for (int e = threadIdx.x; e < FF_NL * a.N; e += FF_NT) {
         const int i = e % FF_NL, q = e / FF_NL;
-        X1[(q * FF_NP + line_kyp(i)) * a.x1_pitch + line_kz(i)] = X[i * FF_LS + pad(q)];
+        X1[(q * FF_NP + line_kyp(i)) * FF_X1P + line_kz(i)] = X[i * FF_LS + pad(q)];
     }
     __syncthreads();  // X is rewritten by the next item's first group
     }
@@ -224,8 +227,9 @@ bool fold_fast_supported(int L, int c, int G, int K, int Np, int complex_w)
     return L == FF_L && c == FF_C && G == FF_G && K == FF_K && Np == FF_NP && !complex_w;
 }
 
-void launch_fold_fast(const FoldFastArgs &a_in, int batch, cudaStream_t s)
+bool launch_fold_fast(const FoldFastArgs &a_in, int batch, cudaStream_t s)
 {
+    if (a_in.MS != FF_MS || a_in.x1_pitch != FF_X1P) return false;
     FoldFastArgs a = a_in;
     a.nb = batch;
     constexpr int ZT = (FF_FZ - 1) / FF_NL;
@@ -237,6 +241,7 @@ void launch_fold_fast(const FoldFastArgs &a_in, int batch, cudaStream_t s)
     const long long items = (long long)(FF_NP * ZT + FF_NP / FF_NL) * batch;
     const long long grid = std::min<long long>(items, (long long)sms * 4 * 4);  // 4 blocks / SM, 4 waves of items or more
     fold_fast_kernel<<<(unsigned)grid, FF_NT, sm, s>>>(a);
+    return true;
 }
 
 // ============================================================================ forward y pass

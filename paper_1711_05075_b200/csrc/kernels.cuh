@@ -85,7 +85,7 @@ bool launch_spread_z(const SpreadZArgs &a, int batch, cudaStream_t s);  // false
 struct CmSeg {
     int off, qn, cnt;  // segment start, first negative q, entries
 };
-__host__ __device__ inline CmSeg cm_segment(int p, int L, int c, int G, int K)
+__host__ __device__ constexpr CmSeg cm_segment(int p, int L, int c, int G, int K)
 {
     int off = 0;
     for (int pp = 0; pp <= p; pp++) {
@@ -97,7 +97,7 @@ __host__ __device__ inline CmSeg cm_segment(int p, int L, int c, int G, int K)
     }
     return CmSeg{0, 0, 0};
 }
-__host__ __device__ inline int cm_row_stride(int L, int c, int G, int K)
+__host__ __device__ constexpr int cm_row_stride(int L, int c, int G, int K)
 {
     const CmSeg s = cm_segment(c - 1, L, c, G, K);
     return s.off + ((s.cnt + 1) & ~1);
@@ -191,7 +191,7 @@ struct PassYFastArgs {
 };
 bool pass_y_fast_supported(int L, int c, int G, int K, int complex_w);
 void launch_pass_y_fast(const PassYFastArgs &a, int batch, cudaStream_t s);
-void launch_fold_fast(const FoldFastArgs &a, int batch, cudaStream_t s);
+bool launch_fold_fast(const FoldFastArgs &a, int batch, cudaStream_t s);  // false: strides not the compiled ones
 
 // contiguous inverse z pass + epilogue
 struct LastArgs {
