@@ -29,4 +29,4 @@ from .bandlimited import (  # noqa: F401
     bandlimited_correlation,
     band_modes,
 )
-from .complementarity import sc_score_points  # noqa: F401
+from .complementarity import sc_score_points, eq_score_points  # noqa: F401

@@ -21,6 +21,13 @@ real: interior-interior overlaps penalised by lambda^2, offset-interior overlaps
 rewarded, offset-offset overlaps penalised by 1, which is the sign pattern L458 states
 (DESIGN.md reading R-5).  This module only builds the ball sets and reads the real part;
 all arithmetic runs in libballcorr's kernels.
+
+Sign, stated explicitly: eq_score read literally, with the cross-correlation of L791
+conjugating its first argument (F_{RS2}), is G_eq = lambda^2 g - lambda g(S1 (+) B0, S2)
+- lambda g(S1, S2 (+) B0) + g(S1 (+) B0, S2 (+) B0) (the paper's algebra).
+The score returned here is G = -G_eq, so `best` returns max(-G_eq) = -min G_eq and its
+index is the argmin of the literal G_eq (pinned: oracle.eq_score_points against a
+conjugated voxel integral, tests/test_complementarity.py).
 """
 from __future__ import annotations
 
@@ -68,7 +75,8 @@ class Complementarity:
         return f[..., 0] if out is None else f
 
     def best(self, R, out=None, stream=None):
-        """Per rotation, the largest score and its flat grid index (lowest on ties)."""
+        """Per rotation, the largest score G = -G_eq and its flat grid index (lowest on ties):
+        val = max_t(-G_eq) = -min_t G_eq of the literal eq_score (see the module docstring)."""
         return self.corr.correlate_rotations(R, "max_real", out=out, stream=stream)
 
     def evaluate_points(self, R, t):

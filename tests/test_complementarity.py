@@ -56,6 +56,40 @@ def test_oracle_score_matches_voxel_definition(oracle_mod):
     assert (lam * np.abs(g_cross)).max() > 0.2 * np.abs(ref).max()
 
 
+def test_eq_score_verbatim_matches_conjugated_voxel_integral(oracle_mod):
+    """eq_score read literally: G_eq(t) = (F_{RS2} star F_{S1})(t) with star as defined at
+    PAPER.md L791, (f1 star f2)(t) = int conj(f1(x)) f2(x + t) dx.  Substituting y = x + t,
+    G_eq = int conj(F_{RS2}(y - t)) F_{S1}(y) dy: the brute-force voxel integral with the
+    moving shape's affinity CONJUGATED pins oracle.eq_score_points, and the score the
+    package maximises (sc_score_points, reading R-5) is exactly its negative."""
+    S1, S2, R = _shapes(6)
+    r0, lam = 0.05, 3.0
+    hv = 0.006
+    ax = (np.arange(-0.5, 0.5, hv) + hv / 2)
+    pts = np.stack(np.meshgrid(ax, ax, ax, indexing="ij"), axis=-1).reshape(-1, 3)
+    F1 = _affinity_on_lattice(S1, S1[:, :3], r0, lam, pts)
+    RB = S2[:, :3] @ R.T
+    N, h, t0 = 5, 0.1, (-0.2, -0.2, -0.2)
+    idx = np.array([0, 31, 62, 93, 124, 7, 112, 55, 68])
+    m = np.stack(np.unravel_index(idx, (N, N, N)), axis=1)
+    G_eq = oracle_mod.eq_score_points(S1, S2, r0, lam, R, N, h, t0, idx)
+    assert np.abs(G_eq.imag).max() <= 1e-13 * np.abs(G_eq).max()
+    G_eq = G_eq.real
+    for k, mm in enumerate(m):
+        t = np.asarray(t0) + h * mm
+        F2 = _affinity_on_lattice(S2, RB + t, r0, lam, pts)      # F_{RS2}(y - t)
+        G = (np.conj(F2) * F1).sum() * hv ** 3                    # L791: first argument conjugated
+        assert abs(G.imag) < 1e-12
+        assert G.real == pytest.approx(G_eq[k], abs=1e-2 * np.abs(G_eq).max()), (k, G, G_eq[k])
+    # the package's score is -G_eq (DESIGN.md R-5: the L458 narrative, not eq_score's algebra)
+    sc = oracle_mod.sc_score_points(S1, S2, r0, lam, R, N, h, t0, idx)
+    assert np.abs(sc + G_eq).max() <= 1e-13 * np.abs(G_eq).max()
+    # interior-interior collision dominates at lambda = 3: literal G_eq > 0 there (a PENALTY
+    # only under the sign flip of R-5)
+    deep = oracle_mod.eq_score_points(S1, S2, r0, lam, np.eye(3), 1, 1.0, (0.0, 0.0, 0.0), [0])
+    assert deep.real[0] > 0
+
+
 def test_zero_offset_reduces_to_scaled_correlation(oracle_mod):
     S1, S2, R = _shapes(4)
     lam = 3.0

@@ -269,3 +269,69 @@ def test_bandlimited_converges_to_lens(oracle_mod):
         errs.append(np.abs(fb - f).max() / np.abs(f).max())
     assert errs[0] > errs[1] > errs[2]
     assert errs[2] < 3e-3
+
+
+# ------------------------------------------------------------------ spherical band (K_sphere)
+# bandlimited_correlation(K_sphere=rho) keeps the modes |k_i| <= K with |k| <= rho (the
+# truncated Fourier sum of the single-configuration query orders its modes by |k|,
+# PAPER.md L432-L439 "spiral traversal ... starting from the dominant modes").
+
+def test_sphere_band_covering_the_cube_is_the_cube(oracle_mod):
+    """rho >= sqrt(3) K keeps every cube mode: the result is bitwise the cube band's."""
+    w = random_small_case(21, n_a=4, n_b=3, N=8)
+    args = (w.A_xyzr, w.A_w, w.B_xyzr, w.B_w, w.R[0], w.N, w.h, w.t0, 2.5, 5)
+    cube = oracle_mod.bandlimited_correlation(*args)
+    sph = oracle_mod.bandlimited_correlation(*args, K_sphere=math.sqrt(3) * 5 + 1e-9)
+    assert np.array_equal(cube, sph)
+    # and one just inside the corner drops the 8 corner modes: a different result
+    sph2 = oracle_mod.bandlimited_correlation(*args, K_sphere=math.sqrt(3) * 5 - 1e-6)
+    assert np.abs(sph2 - cube).max() > 1e-6 * np.abs(cube).max()
+
+
+def test_sphere_band_dc_and_seven_mode_closed_form(oracle_mod):
+    """rho < 1 keeps only k = 0: f~ = g_hat(0) / P^3 = (sum w vol_A)(sum v vol_B) / P^3.
+    rho = 1 keeps k = 0 and the six unit vectors +-e_i: for real weights
+    f~(t) = (1/P^3) [g_0 + 2 sum_i Re(g(e_i) exp(2 pi i t_i / P))] with
+    g(e_i) = fA(e_i) conj(fB(e_i)) of the NDFT (pinned above)."""
+    w = random_small_case(22, n_a=5, n_b=4, N=6)
+    P = 2.5
+    args = (w.A_xyzr, w.A_w, w.B_xyzr, w.B_w, w.R[1], w.N, w.h, w.t0, P, 3)
+    f0 = oracle_mod.bandlimited_correlation(*args, K_sphere=0.5)
+    ref0 = (w.A_w * vol(w.A_xyzr[:, 3])).sum() * (w.B_w * vol(w.B_xyzr[:, 3])).sum() / P ** 3
+    assert np.allclose(f0, ref0, rtol=1e-13, atol=0)
+    f1 = oracle_mod.bandlimited_correlation(*args, K_sphere=1.0)
+    RB = np.column_stack([w.B_xyzr[:, :3] @ w.R[1].T, w.B_xyzr[:, 3]])
+    fA = oracle_mod.ndft_density(w.A_xyzr, w.A_w, P, 1)
+    fB = oracle_mod.ndft_density(RB, w.B_w, P, 1)
+    e = [(2, 1, 1), (1, 2, 1), (1, 1, 2)]  # index k + K of +e_x, +e_y, +e_z
+    for m in [(0, 0, 0), (1, 4, 2), (5, 5, 5), (3, 0, 1)]:
+        t = np.asarray(w.t0) + w.h * np.asarray(m)
+        val = fA[1, 1, 1] * np.conj(fB[1, 1, 1])
+        for i, ix in enumerate(e):
+            val += 2 * (fA[ix] * np.conj(fB[ix]) * np.exp(2j * np.pi * t[i] / P)).real
+        assert f1[m] == pytest.approx(val.real / P ** 3, rel=1e-12)
+
+
+def test_sphere_band_parseval(oracle_mod):
+    """Parseval on the full period lattice (N = Np points spanning P, Np > 2K so the band
+    modes are orthogonal): sum_m |f~(t_m)|^2 h^3 = (1/P^3) sum_{|k_i|<=K, |k|<=rho} |g(k)|^2,
+    with g(k) = fA(k) fB(-k) of the NDFT.  A wrong mask (|k| < rho, rho^2 vs rho, a missing
+    octant) changes the right-hand side."""
+    w = random_small_case(23, n_a=4, n_b=4, N=8, complex_weights=True)
+    P, K, Np = 2.0, 6, 16
+    h = P / Np
+    RB = np.column_stack([w.B_xyzr[:, :3] @ w.R[0].T, w.B_xyzr[:, 3]])
+    fA = oracle_mod.ndft_density(w.A_xyzr, w.A_w, P, K)
+    fBn = oracle_mod.ndft_density(RB, w.B_w, P, K, sign=+1.0)   # fB(-k)
+    g2 = np.abs(fA * fBn) ** 2
+    k = np.arange(-K, K + 1)
+    kk = k[:, None, None] ** 2 + k[None, :, None] ** 2 + k[None, None, :] ** 2
+    for rho in (2.0, 3.5, 5.0, 7.9):
+        f = oracle_mod.bandlimited_correlation(w.A_xyzr, w.A_w, w.B_xyzr, w.B_w, w.R[0], Np, h,
+                                               (-1.0, -1.0, -1.0), P, K, K_sphere=rho)
+        lhs = (np.abs(f) ** 2).sum() * h ** 3
+        rhs = g2[kk <= rho * rho].sum() / P ** 3
+        assert lhs == pytest.approx(rhs, rel=1e-11), rho
+        # the retained mode count is the lattice-point count of the ball
+        n_brute = sum(1 for a in k for b in k for c in k if a * a + b * b + c * c <= rho * rho)
+        assert (kk <= rho * rho).sum() == n_brute
