@@ -102,6 +102,13 @@ typedef struct {
     int32_t concurrency;  /* spectral: rotation batches in flight on internal streams forked from
                              and joined to the caller's stream (0 or 1 = one batch at a time, on
                              the caller's stream; 2 = two) */
+    double tolerance;     /* spectral: > 0 enables the band-error guard: before the first
+                             correlation of a pair of uploaded shapes the library estimates the
+                             relative band error max|f_spec - f| / max|f| (two probe rotations,
+                             the spectral grid against the exact pair-lens f at ~3,800 sampled
+                             translations) and bc_correlate_rotations returns BC_ERANGE when it
+                             exceeds `tolerance` (raise K).  That first call is then synchronous.
+                             0 = off.  The estimate: bc_query("band_error"). */
 } bc_params;
 
 typedef struct bc_ctx bc_ctx;
@@ -123,12 +130,16 @@ bc_status bc_destroy(bc_ctx *ctx);
  * bound S = max_i |a_i,axis| + max_j |b_j| + max r + max s it requires
  * P >= max(S - t0, t0 + (N-1) h + S) on every axis (P = Np h), else
  * BC_ERANGE.  The box of each shape must also fit its spreading plan.
- * Synchronous with respect to the host.
+ * Synchronous with respect to the host; device xyzr / w are read after a device-wide
+ * synchronisation (they may come from any stream).
  */
 bc_status bc_shape_upload(bc_ctx *ctx, int which, const double *xyzr, const double *w, int64_t n);
 
-/* Compute and keep the spectrum of A on the band (spectral mode; a no-op in
- * exact mode).  Idempotent.  BC_ESTATE if A is missing.  Asynchronous on `stream`. */
+/* Compute and keep the spectrum of A on the band (PAPER.md L280-L294 eq_rhoPhat /
+ * eq_fballhat: knot transform times the ball transform; spectral mode, a no-op in exact
+ * mode).  Idempotent.  BC_ESTATE if A is missing.  Asynchronous on `stream`: runs in the
+ * context's workspaces, allocating them only on first use (no per-call allocation or
+ * synchronisation). */
 bc_status bc_spectrum_A(bc_ctx *ctx, void *stream);
 
 /*
@@ -153,12 +164,21 @@ bc_status bc_spectrum_A_buffer(bc_ctx *ctx, void **dev_ptr, int64_t *bytes);
 bc_status bc_spectrum_A_import(bc_ctx *ctx);
 
 /*
- * Correlate A with R B for n_rot rotations.
- *   R:   host or device, n_rot row-major 3x3 doubles; R R^T = I within 1e-6
- *        and det R > 0, else BC_EINVAL.
- *   out: host or device buffer laid out per bc_out_kind.
- * Device buffers: asynchronous on `stream`.  Host buffers: the call stages
- * them and returns after the result has reached `out`.
+ * Correlate A with R B for n_rot rotations (PAPER.md L316-L322 eq_relg; spectral route
+ * L398-L419 eq_ccghat, one inverse transform per rotation).
+ *   R:   host or device, n_rot row-major 3x3 doubles; every entry finite, |R R^T - I| <= 1e-5
+ *        (BC_FP32) or 1e-12 (BC_FP64) entrywise and det R > 0 (R in SO(3), L221-L233).
+ *        Host R: checked before any work, BC_EINVAL.  Device R: checked ON THE DEVICE by a
+ *        kernel on `stream` (no host round trip); a violation is reported as BC_EINVAL by the
+ *        next call on this context or by bc_sync (the outputs of the offending call are
+ *        undefined), like an asynchronous CUDA fault.
+ *   out: host or device buffer laid out per bc_out_kind, at least n_rot * (bytes per rotation)
+ *        bytes (BC_OUT_F_FULL: N^3 values of the result type; reductions: sizeof(bc_extremum),
+ *        twice for BC_OUT_MINMAX).  The library cannot check its size.
+ * Device R and out: asynchronous on `stream` -- no host synchronisation, no host copies
+ * (except the one-time band-error probe when bc_params.tolerance > 0).  Host buffers: the
+ * call stages them and returns after the result has reached `out`.  Calls on one context
+ * must be ordered by the caller (same stream, or synchronised): they share workspaces.
  * Spectral mode needs bc_spectrum_A first (BC_ESTATE otherwise).
  */
 bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, int out_kind,
@@ -170,13 +190,19 @@ bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, in
  * pair-lens sum of the combinatorial route (eq_ORP / eq_convgP) over the pairs
  * that overlap (uniform grid of A's centres); fp64, any mode.  The spectral grid of
  * bc_correlate_rotations approximates the same f within its band error.
- *   R:   host or device, n row-major 3x3 doubles (validated as for bc_correlate_rotations).
- *   t:   host or device, n x 3 doubles (finite).
+ *   R:   host or device, n row-major 3x3 doubles (validated as for bc_correlate_rotations:
+ *        host arrays at once, device arrays on the device with a deferred BC_EINVAL).
+ *   t:   host or device, n x 3 doubles (finite; same rule).
  *   out: host or device, n doubles (REAL weights) or 2n interleaved (COMPLEX: Re, Im).
- * Device out: asynchronous on `stream`; host out: returns after the values are written.
+ * Device R, t and out: asynchronous on `stream`; host out: returns after the values are
+ * written.
  */
 bc_status bc_evaluate_points(bc_ctx *ctx, const double *R, const double *t, int64_t n, double *out,
                              void *stream);
+
+/* Synchronise `stream` and report a deferred error of earlier calls on this context
+ * (BC_EINVAL from device-side validation of R / t, BC_ECUDA from a CUDA fault). */
+bc_status bc_sync(bc_ctx *ctx, void *stream);
 
 /* Last error message of the context (static string if ctx == NULL). */
 const char *bc_last_error(const bc_ctx *ctx);
@@ -185,7 +211,8 @@ const char *bc_status_string(int status);
 /*
  * Introspection (tests / bench): named double-valued properties of the plan.
  * Keys: "P", "K", "Np", "tau_A", "tau_B", "G_A", "G_B", "L_A", "L_B", "c_A", "c_B",
- * "cut_A", "cut_B", "band_modes", "batch", "bytes_workspace", "blob_B" (B smoothed with the
+ * "cut_A", "cut_B", "band_modes", "batch", "bytes_workspace", "band_error" (the band-error
+ * probe's estimate, -1 before it ran; see bc_params.tolerance), "blob_B" (B smoothed with the
  * KB blob window), "fused_spread_z", "fused_fold_inv", "fold_fast" (which fused kernels the
  * plan takes), "spread_cells_B" (sum of B's footprint volumes in fine cells), "live_tiles_B".
  * Unknown keys: BC_EINVAL.

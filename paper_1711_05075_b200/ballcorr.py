@@ -41,7 +41,8 @@ class bc_params(ctypes.Structure):
                 ("Np", ctypes.c_int32), ("K", ctypes.c_int32), ("precision", ctypes.c_int32),
                 ("mode", ctypes.c_int32), ("weights", ctypes.c_int32), ("max_batch", ctypes.c_int32),
                 ("spread_eps", ctypes.c_double), ("band_radius", ctypes.c_double),
-                ("generic_only", ctypes.c_int32), ("concurrency", ctypes.c_int32)]
+                ("generic_only", ctypes.c_int32), ("concurrency", ctypes.c_int32),
+                ("tolerance", ctypes.c_double)]
 
 
 EXTREMUM_DTYPE = np.dtype([("val", np.float64), ("idx", np.int64)])
@@ -63,6 +64,8 @@ _lib.bc_correlate_rotations.argtypes = [_vp, _vp, ctypes.c_int64, ctypes.c_int, 
 _lib.bc_correlate_rotations.restype = ctypes.c_int
 _lib.bc_evaluate_points.argtypes = [_vp, _vp, _vp, ctypes.c_int64, _vp, _vp]
 _lib.bc_evaluate_points.restype = ctypes.c_int
+_lib.bc_sync.argtypes = [_vp, _vp]
+_lib.bc_sync.restype = ctypes.c_int
 _lib.bc_last_error.argtypes = [_vp]
 _lib.bc_last_error.restype = ctypes.c_char_p
 _lib.bc_status_string.argtypes = [ctypes.c_int]
@@ -87,6 +90,7 @@ bc_spectrum_A = _lib.bc_spectrum_A
 bc_spectrum_A_buffer = _lib.bc_spectrum_A_buffer
 bc_spectrum_A_import = _lib.bc_spectrum_A_import
 bc_correlate_rotations = _lib.bc_correlate_rotations
+bc_sync = _lib.bc_sync
 bc_last_error = _lib.bc_last_error
 bc_status_string = _lib.bc_status_string
 bc_query = _lib.bc_query
@@ -112,6 +116,33 @@ def _ptr(a):
         return a.data_ptr(), a
     a = np.ascontiguousarray(a)
     return a.ctypes.data, a
+
+
+def _out_ptr(out, nbytes, dtype, what="out"):
+    """Address of a caller-provided output buffer after checking it can hold `nbytes`: a
+    C-contiguous numpy array or torch tensor (host or cuda) of the result dtype (`dtype`) or
+    of raw bytes (uint8).  Never copies: the library writes into `out` itself."""
+    if hasattr(out, "data_ptr"):  # torch tensor
+        import torch
+        if not out.is_contiguous():
+            raise ValueError(f"{what} must be contiguous")
+        size = out.numel() * out.element_size()
+        ok_dt = out.dtype == torch.uint8 or (out.element_size() == np.dtype(dtype).itemsize and
+                                              out.dtype.is_floating_point == (np.dtype(dtype).kind == "f"))
+        ptr = out.data_ptr()
+    else:
+        if not isinstance(out, np.ndarray):
+            raise ValueError(f"{what} must be a numpy array or a torch tensor")
+        if not out.flags.c_contiguous or not out.flags.writeable:
+            raise ValueError(f"{what} must be C-contiguous and writeable")
+        size = out.nbytes
+        ok_dt = out.dtype == np.uint8 or out.dtype == np.dtype(dtype)
+        ptr = out.ctypes.data
+    if not ok_dt:
+        raise ValueError(f"{what} has dtype {out.dtype}; expected {np.dtype(dtype)} or uint8 bytes")
+    if size < nbytes:
+        raise ValueError(f"{what} holds {size} bytes; the call writes {nbytes}")
+    return ptr
 
 
 def _as_f64(a, cols=None):
@@ -152,7 +183,8 @@ class Correlator:
     """One libballcorr context on one device."""
 
     def __init__(self, N, h, t0, Np=0, K=0, mode="spectral", precision="f32", weights="real",
-                 max_batch=0, spread_eps=0.0, band_radius=0.0, generic_only=False, concurrency=0, device=0):
+                 max_batch=0, spread_eps=0.0, band_radius=0.0, generic_only=False, concurrency=0, tolerance=0.0,
+                 device=0):
         p = bc_params()
         p.N = int(N)
         p.h = float(h)
@@ -168,6 +200,7 @@ class Correlator:
         p.band_radius = float(band_radius)
         p.generic_only = int(bool(generic_only))
         p.concurrency = int(concurrency)
+        p.tolerance = float(tolerance)
         self.params = p
         self.device = int(device)
         self.N = p.N
@@ -239,12 +272,14 @@ class Correlator:
         numpy array or torch tensor (host or cuda) of the right byte size.  Returns `out`
         (numpy structured array for reductions when allocated here)."""
         Rv = _as_f64(R)
+        if tuple(Rv.shape[1:]) != (3, 3) and not (Rv.ndim == 2 and Rv.shape[1] == 9):
+            raise ValueError("R must have shape (n_rot, 3, 3)")
         n_rot = int(Rv.shape[0])
         kind, shp, dt = self.out_shape(n_rot, out_kind)
         if out is None:
             out = np.empty(shp, dtype=dt)
+        po = _out_ptr(out, int(np.prod(shp)) * np.dtype(dt).itemsize, dt)
         pr, kr = _ptr(Rv)
-        po, ko = _ptr(out)
         self._check(_lib.bc_correlate_rotations(self._ctx, pr, n_rot, kind, po, _stream_handle(stream)))
         return out
 
@@ -260,9 +295,9 @@ class Correlator:
         ret_complex = out is None and self.complex
         if out is None:
             out = np.empty((n, 2) if self.complex else (n,), dtype=np.float64)
+        po = _out_ptr(out, n * (2 if self.complex else 1) * 8, np.float64)
         pr, kr = _ptr(Rv)
         pt, kt = _ptr(tv)
-        po, ko = _ptr(out)
         self._check(_lib.bc_evaluate_points(self._ctx, pr, pt, n, po, _stream_handle(stream)))
         return out[:, 0] + 1j * out[:, 1] if ret_complex else out
 
@@ -271,6 +306,11 @@ class Correlator:
         v = ctypes.c_double()
         self._check(_lib.bc_query(self._ctx, key.encode(), ctypes.byref(v)))
         return v.value
+
+    def sync(self, stream=None):
+        """bc_sync: wait for `stream` and raise a deferred error of earlier calls (BC_EINVAL from
+        on-device validation of device-resident R / t)."""
+        self._check(_lib.bc_sync(self._ctx, _stream_handle(stream)))
 
     def launch_count(self):
         return int(_lib.bc_launch_count(self._ctx))

@@ -1,7 +1,8 @@
 // api.cu -- the C ABI of libballcorr: contexts, validation, plans, orchestration.
 //
-// Every compute step runs in the kernels of spectral.cu / exact.cu; this file
-// only validates, plans, allocates and launches.  There is no CPU fallback.
+// Every compute step runs in the kernels of spread*.cu / passes.cu / fold_fast.cu /
+// exact.cu / query.cu / validate.cu; this file only validates, plans, allocates and
+// launches.  There is no CPU fallback.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -103,6 +104,7 @@ struct bc_ctx {
     int64_t live_tiles_B = 0;      // 4x4 column tiles of B's box inside its support cylinder
     float2 *d_Ahat = nullptr;      // A' = A_hat * origin phase, [ky][kz][kx] natural order
     float2 *d_Ahat_cm = nullptr;   // same, x axis in the coset-major order of B's plan
+    size_t Ahat_cm_bytes = 0;
     bool cm_ready = false;
     int MS = 0;                    // row stride of d_Ahat_cm
     int *d_xtab = nullptr;         // fused-fold extraction table of B's x plan
@@ -131,6 +133,12 @@ struct bc_ctx {
     double qg0[3] = {0, 0, 0}, qcs = 0;
     double *d_qR = nullptr, *d_qt = nullptr, *d_qpart = nullptr, *d_qout = nullptr;
     int64_t q_cap = 0;
+
+    // deferred validation of device-resident inputs (validate.cu): mapped pinned status words
+    unsigned *h_status = nullptr, *d_status = nullptr;
+    // band-error probe (bc_params.tolerance): estimate for the current shapes, -1 = not run
+    bool probe_done = false;
+    double probe_err = -1.0;
 
     int64_t launches = 0;
     bool prof = false;
@@ -187,13 +195,17 @@ bool is_device_ptr(const void *ptr)
     return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
+// Host copy of a caller array for the synchronous setup call bc_shape_upload.  A device array
+// may have been produced on any of the caller's streams (including non-blocking ones that
+// the legacy default stream does not order against), so the device is synchronised first.
 bc_status fetch_host(bc_ctx *ctx, const double *src, size_t count, std::vector<double> &dst)
 {
     dst.resize(count);
     if (count == 0) return BC_OK;
-    if (is_device_ptr(src))
+    if (is_device_ptr(src)) {
+        CU(ctx, cudaDeviceSynchronize());
         CU(ctx, cudaMemcpy(dst.data(), src, count * sizeof(double), cudaMemcpyDeviceToHost));
-    else
+    } else
         memcpy(dst.data(), src, count * sizeof(double));
     return BC_OK;
 }
@@ -979,8 +991,28 @@ bc_status upload_shape_device(bc_ctx *ctx, int which)
     return BC_OK;
 }
 
-bc_status validate_rotations(bc_ctx *ctx, const std::vector<double> &R, int64_t n_rot)
+// Tolerance on |R R^T - I| entries: 1e-5 for the fp32 path, 1e-12 for fp64.
+double rot_tol(const bc_ctx *ctx) { return ctx->p.precision == BC_FP64 ? 1e-12 : 1e-5; }
+
+// A violation recorded on the device by validate.cu (deferred BC_EINVAL); resets the words.
+bc_status check_deferred(bc_ctx *ctx)
 {
+    if (!ctx->h_status) return BC_OK;
+    volatile unsigned *st = ctx->h_status;
+    const unsigned flags = st[0];
+    if (!flags) return BC_OK;
+    const unsigned idx = st[1];
+    st[0] = 0;
+    st[1] = 0xffffffffu;
+    return fail(ctx, BC_EINVAL, "deferred (device-resident input of an earlier call): entry %u: %s%s%s%s", idx,
+                (flags & BC_DEFER_NONFINITE_R) ? "non-finite R " : "",
+                (flags & BC_DEFER_NOT_ORTHONORMAL) ? "R R^T deviates from I " : "",
+                (flags & BC_DEFER_DET) ? "det R <= 0 " : "", (flags & BC_DEFER_NONFINITE_T) ? "non-finite t" : "");
+}
+
+bc_status validate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot)
+{
+    const double tol = rot_tol(ctx);
     for (int64_t r = 0; r < n_rot; r++) {
         const double *m = &R[9 * r];
         for (int q = 0; q < 9; q++)
@@ -989,7 +1021,7 @@ bc_status validate_rotations(bc_ctx *ctx, const std::vector<double> &R, int64_t 
             for (int j = 0; j < 3; j++) {
                 double d = 0;
                 for (int k = 0; k < 3; k++) d += m[3 * i + k] * m[3 * j + k];
-                if (std::fabs(d - (i == j ? 1.0 : 0.0)) > 1e-6)
+                if (std::fabs(d - (i == j ? 1.0 : 0.0)) > tol)
                     return fail(ctx, BC_EINVAL, "rotation %lld: R R^T deviates from I by %.3g", (long long)r,
                                 std::fabs(d - (i == j ? 1.0 : 0.0)));
             }
@@ -1000,337 +1032,104 @@ bc_status validate_rotations(bc_ctx *ctx, const std::vector<double> &R, int64_t 
     return BC_OK;
 }
 
-size_t out_elem_bytes(const bc_ctx *ctx, int kind)
+bc_status ensure_deferred_status(bc_ctx *ctx)
 {
-    const bool cplx = ctx->p.weights == BC_WEIGHTS_COMPLEX;
-    const bool f64 = ctx->p.precision == BC_FP64 && ctx->p.mode == BC_MODE_EXACT;
-    if (kind == BC_OUT_F_FULL) {
-        const size_t N3 = (size_t)ctx->p.N * ctx->p.N * ctx->p.N;
-        return N3 * (f64 ? 8 : 4) * (cplx ? 2 : 1);
-    }
-    return sizeof(bc_extremum) * (kind == BC_OUT_MINMAX ? 2 : 1);
-}
-
-}  // namespace
-
-// ============================================================================ public API
-
-extern "C" {
-
-const char *bc_status_string(int st)
-{
-    switch (st) {
-    case BC_OK: return "BC_OK";
-    case BC_EINVAL: return "BC_EINVAL";
-    case BC_ERANGE: return "BC_ERANGE";
-    case BC_ENOMEM: return "BC_ENOMEM";
-    case BC_ESTATE: return "BC_ESTATE";
-    case BC_EUNSUPPORTED: return "BC_EUNSUPPORTED";
-    case BC_ECUDA: return "BC_ECUDA";
-    default: return "BC_UNKNOWN";
-    }
-}
-
-const char *bc_last_error(const bc_ctx *ctx)
-{
-    if (!ctx) return "no context";
-    return ctx->err.c_str();
-}
-
-bc_status bc_create(int device, const bc_params *p, bc_ctx **out)
-{
-    if (!p || !out) return BC_EINVAL;
-    *out = nullptr;
-    if (p->N < 1 || !(p->h > 0) || !std::isfinite(p->h)) return BC_EINVAL;
-    for (int a = 0; a < 3; a++)
-        if (!std::isfinite(p->t0[a])) return BC_EINVAL;
-    if (p->mode != BC_MODE_SPECTRAL && p->mode != BC_MODE_EXACT) return BC_EINVAL;
-    if (p->precision != BC_FP32 && p->precision != BC_FP64) return BC_EINVAL;
-    if (p->weights != BC_WEIGHTS_REAL && p->weights != BC_WEIGHTS_COMPLEX) return BC_EINVAL;
-    if (p->max_batch < 0) return BC_EINVAL;
-    if (p->concurrency < 0 || p->concurrency > 2) return BC_EINVAL;
-    if (p->mode == BC_MODE_SPECTRAL) {
-        if (p->precision != BC_FP32) return BC_EUNSUPPORTED;
-        if (p->Np < p->N || p->Np < 2 || (p->Np % 2) != 0 || !friendly(p->Np) || p->Np > 1024) return BC_EINVAL;
-        if (p->K < 1 || p->K > 2047) return BC_EINVAL;
-        if (!(p->band_radius >= 0) || !std::isfinite(p->band_radius)) return BC_EINVAL;
-        if (!fft_size_supported(p->Np)) return BC_EUNSUPPORTED;
-        if (p->N > 1625) return BC_EUNSUPPORTED;
-    }
-    int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
-        cudaGetLastError();
-        return BC_ECUDA;
-    }
-    if (cudaSetDevice(device) != cudaSuccess) return BC_ECUDA;
-    bc_ctx *ctx = new bc_ctx();
-    ctx->device = device;
-    ctx->p = *p;
-    if (p->mode == BC_MODE_SPECTRAL) {
-        const bool cplx = p->weights == BC_WEIGHTS_COMPLEX;
-        ctx->P = p->Np * p->h;
-        ctx->K = p->K;
-        ctx->M = 2 * p->K + 1;
-        ctx->Kz = cplx ? ctx->M : p->K + 1;
-        ctx->Fz = cplx ? p->Np : p->Np / 2 + 1;
-        if (ensure_twiddles(ctx, p->Np) != BC_OK) {
-            bc_destroy(ctx);
-            return BC_ENOMEM;
-        }
-    }
-    *out = ctx;
-    return BC_OK;
-}
-
-bc_status bc_destroy(bc_ctx *ctx)
-{
-    if (!ctx) return BC_OK;
-    cudaSetDevice(ctx->device);
-    for (int w = 0; w < 2; w++) {
-        dfree(ctx->d_balls[w]);
-        dfree(ctx->d_wre[w]);
-        dfree(ctx->d_wim[w]);
-        dfree(ctx->d_balls64[w]);
-        dfree(ctx->d_w64[w]);
-        for (int a = 0; a < 3; a++) dfree(ctx->plan[w].d_mult[a]);
-        dfree(ctx->plan[w].d_ctw);
-    }
-    for (auto &kv : ctx->d_tw) cudaFree(kv.second);
-    dfree(ctx->d_csr_off);
-    dfree(ctx->d_csr_idx);
-    dfree(ctx->d_prof);
-    dfree(ctx->d_prof_off);
-    dfree(ctx->d_bcells);
-    dfree(ctx->d_g02);
-    dfree(ctx->d_phi);
-    dfree(ctx->d_dec);
-    dfree(ctx->d_recB);
-    for (Slot &sl : ctx->slot) {
-        if (sl.ws1) cudaFree(sl.ws1);
-        if (sl.ws2) cudaFree(sl.ws2);
-        dfree(sl.keys);
-        dfree(sl.recA);
-        dfree(sl.szcnt);
-        dfree(sl.szoff);
-        dfree(sl.szlist);
-        if (sl.stream) cudaStreamDestroy(sl.stream);
-        if (sl.done) cudaEventDestroy(sl.done);
-    }
-    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
-    dfree(ctx->d_qstart);
-    dfree(ctx->d_qidx);
-    dfree(ctx->d_qR);
-    dfree(ctx->d_qt);
-    dfree(ctx->d_qpart);
-    dfree(ctx->d_qout);
-    dfree(ctx->d_Ahat);
-    dfree(ctx->d_Ahat_cm);
-    dfree(ctx->d_xtab);
-    dfree(ctx->d_segs);
-
-    dfree(ctx->d_rot);
-    dfree(ctx->d_rot64);
-    if (ctx->d_out_stage) cudaFree(ctx->d_out_stage);
-    dfree(ctx->d_acc);
-    dfree(ctx->d_part);
-    dfree(ctx->d_part_idx);
-    for (auto &pe : ctx->pending) {
-        cudaEventDestroy(pe.e0);
-        cudaEventDestroy(pe.e1);
-    }
-    for (auto e : ctx->event_pool) cudaEventDestroy(e);
-    delete ctx;
-    return BC_OK;
-}
-
-bc_status bc_shape_upload(bc_ctx *ctx, int which, const double *xyzr, const double *w, int64_t n)
-{
-    if (!ctx) return BC_EINVAL;
-    if (which != 0 && which != 1) return fail(ctx, BC_EINVAL, "which must be 0 (A) or 1 (B)");
-    if (n < 0 || (n > 0 && !xyzr)) return fail(ctx, BC_EINVAL, "bad shape size or NULL xyzr");
-    if (n > (1ll << 30)) return fail(ctx, BC_EINVAL, "too many balls");
-    CU(ctx, cudaSetDevice(ctx->device));
-    const bool cplx = ctx->p.weights == BC_WEIGHTS_COMPLEX;
-    std::vector<double> x, wv;
-    TRY(fetch_host(ctx, xyzr, (size_t)n * 4, x));
-    if (w) TRY(fetch_host(ctx, w, (size_t)n * (cplx ? 2 : 1), wv));
-    for (int64_t i = 0; i < n; i++) {
-        for (int q = 0; q < 4; q++)
-            if (!std::isfinite(x[4 * i + q])) return fail(ctx, BC_EINVAL, "ball %lld has a non-finite entry", (long long)i);
-        if (!(x[4 * i + 3] > 0)) return fail(ctx, BC_EINVAL, "ball %lld has radius <= 0", (long long)i);
-    }
-    for (double v : wv)
-        if (!std::isfinite(v)) return fail(ctx, BC_EINVAL, "non-finite weight");
-    ctx->hxyzr[which] = x;
-    ctx->hw[which].assign((size_t)n * 2, 0.0);
-    for (int64_t i = 0; i < n; i++) {
-        if (!w) {
-            ctx->hw[which][2 * i] = 1.0;
-        } else if (cplx) {
-            ctx->hw[which][2 * i] = wv[2 * i];
-            ctx->hw[which][2 * i + 1] = wv[2 * i + 1];
-        } else {
-            ctx->hw[which][2 * i] = wv[i];
-        }
-    }
-    ctx->n[which] = n;
-    ctx->have[which] = true;
-    ctx->qgrid_ready = false;
-    if (which == 0) ctx->have_spec = false;
-    ctx->cm_ready = false;
-    TRY(upload_shape_device(ctx, which));
-    if (ctx->p.mode == BC_MODE_SPECTRAL && n > 0) {
-        double lo[3], hi[3], rmax, rho;
-        shape_bounds(ctx, which, lo, hi, rmax, rho);
-        if (which == 1)
-            for (int a = 0; a < 3; a++) {  // any rotation keeps B inside the ball of radius max|b_j|
-                lo[a] = -rho;
-                hi[a] = rho;
-            }
-        TRY(plan_shape(ctx, which, lo, hi, rmax));
-        if (which == 0) TRY(build_csr_A(ctx));
-        if (which == 1 && !ctx->plan[1].blob) TRY(build_profiles_B(ctx));
-        if (which == 1) {
-            const ShapePlan &pb = ctx->plan[1];
-            ctx->live_r = (rho + rmax + pb.cut) / pb.hf + 2.0;
-            ctx->spread_cells_B = 0;
-            for (int64_t j = 0; j < n; j++) {
-                const double rc = (ctx->hxyzr[1][4 * j + 3] + pb.cut) / pb.hf;
-                ctx->spread_cells_B += 4.0 / 3.0 * kPi * rc * rc * rc;
-            }
-            ctx->live_tiles_B = 0;  // same test as spread_z_kernel's zero-tile exit
-            for (int X0 = 0; X0 < pb.L; X0 += 4)
-                for (int Y0 = 0; Y0 < pb.L; Y0 += 4) {
-                    const double cx = -pb.o[0], cy = -pb.o[1];
-                    const double dx = std::max(std::max(X0 - cx, cx - (X0 + 3)), 0.0);
-                    const double dy = std::max(std::max(Y0 - cy, cy - (Y0 + 3)), 0.0);
-                    if (dx * dx + dy * dy <= (ctx->live_r + 1) * (ctx->live_r + 1)) ctx->live_tiles_B++;
-                }
-            if (ctx->plan[1].blob) TRY(build_spread_z_tables(ctx));
-        }
-    }
-    TRY(check_support(ctx));
-    return BC_OK;
-}
-
-bc_status bc_spectrum_A(bc_ctx *ctx, void *stream)
-{
-    if (!ctx) return BC_EINVAL;
-    if (!ctx->have[0]) return fail(ctx, BC_ESTATE, "shape A has not been uploaded");
-    if (ctx->p.mode != BC_MODE_SPECTRAL || ctx->have_spec) {
-        ctx->have_spec = true;
-        return BC_OK;
-    }
-    CU(ctx, cudaSetDevice(ctx->device));
-    cudaStream_t s = (cudaStream_t)stream;
-    const size_t nspec = (size_t)ctx->M * ctx->M * ctx->Kz;
-    if (!ctx->d_Ahat) TRY(dalloc(ctx, &ctx->d_Ahat, sizeof(float2) * nspec));  // fixed size per context
-    if (ctx->n[0] == 0) {
-        CU(ctx, cudaMemsetAsync(ctx->d_Ahat, 0, sizeof(float2) * nspec, s));
-        ctx->have_spec = true;
-        return BC_OK;
-    }
-    size_t s1, s2;
-    spectral_ws_sizes(ctx, 0, s1, s2);
-    void *w1 = nullptr, *w2 = nullptr;
-    CU(ctx, cudaMalloc(&w1, s1));
-    cudaError_t e = cudaMalloc(&w2, s2);
+    if (ctx->h_status) return BC_OK;
+    unsigned *h = nullptr;
+    CU(ctx, cudaHostAlloc((void **)&h, 2 * sizeof(unsigned), cudaHostAllocMapped));
+    h[0] = 0;
+    h[1] = 0xffffffffu;
+    unsigned *d = nullptr;
+    cudaError_t e = cudaHostGetDevicePointer((void **)&d, h, 0);
     if (e != cudaSuccess) {
-        cudaFree(w1);
-        return fail(ctx, BC_ENOMEM, "spectrum_A workspace: %s", cudaGetErrorString(e));
+        cudaFreeHost(h);
+        return fail(ctx, BC_ECUDA, "cudaHostGetDevicePointer: %s", cudaGetErrorString(e));
     }
-    ctx->cm_ready = false;
-    bc_status st = shape_spectrum(ctx, 0, nullptr, 1, w1, w2, s1, s2, s, ctx->slot[0]);
-    cudaError_t se = cudaStreamSynchronize(s);
-    collect_profile(ctx);
-    cudaFree(w1);
-    cudaFree(w2);
-    if (st != BC_OK) return st;
-    if (se != cudaSuccess) return fail(ctx, BC_ECUDA, "spectrum_A: %s", cudaGetErrorString(se));
-    ctx->have_spec = true;
+    ctx->h_status = h;
+    ctx->d_status = d;
     return BC_OK;
 }
 
-bc_status bc_spectrum_A_buffer(bc_ctx *ctx, void **dev_ptr, int64_t *bytes)
+// Rotations of the call into ctx->d_rot (fp32, spectral path) and ctx->d_rot64 (fp64, exact
+// mode), on `s`.  Host R was validated by the caller and is copied; device R is validated
+// and converted by validate.cu with no host round trip (violations: deferred BC_EINVAL).
+bc_status prepare_rotations(bc_ctx *ctx, const double *R, bool dev_R, int64_t n_rot, cudaStream_t s)
 {
-    if (!ctx) return BC_EINVAL;
-    if (!dev_ptr || !bytes) return fail(ctx, BC_EINVAL, "NULL dev_ptr/bytes");
-    if (ctx->p.mode != BC_MODE_SPECTRAL) return fail(ctx, BC_EUNSUPPORTED, "exact mode has no spectrum of A");
-    CU(ctx, cudaSetDevice(ctx->device));
-    const size_t nspec = (size_t)ctx->M * ctx->M * ctx->Kz;
-    if (!ctx->d_Ahat) TRY(dalloc(ctx, &ctx->d_Ahat, sizeof(float2) * nspec));
-    *dev_ptr = ctx->d_Ahat;
-    *bytes = (int64_t)(sizeof(float2) * nspec);
-    return BC_OK;
-}
-
-bc_status bc_spectrum_A_import(bc_ctx *ctx)
-{
-    if (!ctx) return BC_EINVAL;
-    if (ctx->p.mode != BC_MODE_SPECTRAL) return fail(ctx, BC_EUNSUPPORTED, "exact mode has no spectrum of A");
-    if (!ctx->have[0]) return fail(ctx, BC_ESTATE, "shape A has not been uploaded");
-    if (!ctx->d_Ahat) return fail(ctx, BC_ESTATE, "bc_spectrum_A_buffer has not been called");
-    ctx->cm_ready = false;  // A'' (coset-major, B's multipliers) is rebuilt from the new contents
-    ctx->have_spec = true;
-    return BC_OK;
-}
-
-bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, int out_kind, void *out, void *stream)
-{
-    if (!ctx) return BC_EINVAL;
-    if (!R || !out || n_rot < 1) return fail(ctx, BC_EINVAL, "NULL R/out or n_rot < 1");
-    if (out_kind < BC_OUT_F_FULL || out_kind > BC_OUT_MAX_REAL) return fail(ctx, BC_EINVAL, "bad out_kind");
-    const bool cplx = ctx->p.weights == BC_WEIGHTS_COMPLEX;
-    if (cplx && out_kind != BC_OUT_F_FULL && out_kind != BC_OUT_MAX_REAL)
-        return fail(ctx, BC_EINVAL, "complex weights support F_FULL and MAX_REAL only");
-    if (!ctx->have[0] || !ctx->have[1]) return fail(ctx, BC_ESTATE, "upload both shapes first");
-    if (ctx->p.mode == BC_MODE_SPECTRAL && !ctx->have_spec && ctx->n[0] > 0 && ctx->n[1] > 0)
-        return fail(ctx, BC_ESTATE, "call bc_spectrum_A first");
-    CU(ctx, cudaSetDevice(ctx->device));
-    cudaStream_t s = (cudaStream_t)stream;
-
-    std::vector<double> hR;
-    TRY(fetch_host(ctx, R, (size_t)n_rot * 9, hR));
-    TRY(validate_rotations(ctx, hR, n_rot));
-
-    const size_t out_per = out_elem_bytes(ctx, out_kind);
-    const bool host_out = !is_device_ptr(out);
-    char *dout = (char *)out;
-    if (host_out) {
-        TRY(ensure_ws(ctx, &ctx->d_out_stage, ctx->out_stage_bytes, out_per * n_rot));
-        dout = (char *)ctx->d_out_stage;
-    }
-
-    // empty shape: f == 0 identically
-    if (ctx->n[0] == 0 || ctx->n[1] == 0) {
-        if (out_kind == BC_OUT_F_FULL) {
-            CU(ctx, cudaMemsetAsync(dout, 0, out_per * n_rot, s));
-        } else {
-            std::vector<bc_extremum> z((size_t)n_rot * (out_kind == BC_OUT_MINMAX ? 2 : 1));
-            for (auto &e : z) {
-                e.val = 0.0;
-                e.idx = 0;
-            }
-            CU(ctx, cudaMemcpyAsync(dout, z.data(), z.size() * sizeof(bc_extremum), cudaMemcpyHostToDevice, s));
-            CU(ctx, cudaStreamSynchronize(s));
-        }
-        if (host_out) {
-            CU(ctx, cudaMemcpyAsync(out, dout, out_per * n_rot, cudaMemcpyDeviceToHost, s));
-            CU(ctx, cudaStreamSynchronize(s));
-        }
-        return BC_OK;
-    }
-
-    // rotations to the device (fp32 for the spectral path, fp64 for exact mode)
+    TRY(ensure_deferred_status(ctx));
     if (n_rot > ctx->rot_cap) {
         TRY(dalloc(ctx, &ctx->d_rot, sizeof(float) * 9 * n_rot));
         TRY(dalloc(ctx, &ctx->d_rot64, sizeof(double) * 9 * n_rot));
         ctx->rot_cap = n_rot;
     }
-    std::vector<float> fR(hR.begin(), hR.end());
-    CU(ctx, cudaMemcpyAsync(ctx->d_rot, fR.data(), sizeof(float) * 9 * n_rot, cudaMemcpyHostToDevice, s));
-    CU(ctx, cudaMemcpyAsync(ctx->d_rot64, hR.data(), sizeof(double) * 9 * n_rot, cudaMemcpyHostToDevice, s));
+    RotPrepArgs a{};
+    a.n = n_rot;
+    a.tol = rot_tol(ctx);
+    a.r32 = ctx->d_rot;
+    a.status = ctx->d_status;
+    if (dev_R) {
+        a.R = R;
+        a.r64 = ctx->d_rot64;
+    } else {
+        CU(ctx, cudaMemcpyAsync(ctx->d_rot64, R, sizeof(double) * 9 * n_rot, cudaMemcpyHostToDevice, s));
+        a.R = ctx->d_rot64;
+    }
+    launch_rot_prep(a, s);
+    ctx->launches++;
+    CU(ctx, cudaGetLastError());
+    return BC_OK;
+}
 
+bc_status ensure_query_ws(bc_ctx *ctx, int64_t chunk)
+{
+    if (ctx->q_cap >= chunk) return BC_OK;
+    const int nblk = query_blocks((int)ctx->n[1]);
+    TRY(dalloc(ctx, &ctx->d_qR, sizeof(double) * 9 * chunk));
+    TRY(dalloc(ctx, &ctx->d_qt, sizeof(double) * 3 * chunk));
+    TRY(dalloc(ctx, &ctx->d_qpart, sizeof(double) * 2 * nblk * chunk));
+    TRY(dalloc(ctx, &ctx->d_qout, sizeof(double) * 2 * chunk));
+    ctx->q_cap = chunk;
+    return BC_OK;
+}
+
+// Exact pair-lens query of the nq configurations in ctx->d_qR / ctx->d_qt (query.cu).
+bc_status run_query(bc_ctx *ctx, int nq, double *dst, cudaStream_t s)
+{
+    const bool cplx = ctx->p.weights == BC_WEIGHTS_COMPLEX;
+    QueryArgs qa{};
+    qa.nq = nq;
+    qa.nB = (int)ctx->n[1];
+    qa.R = ctx->d_qR;
+    qa.t = ctx->d_qt;
+    qa.A = ctx->d_balls64[0];
+    qa.B = ctx->d_balls64[1];
+    qa.wA = ctx->d_w64[0];
+    qa.wB = ctx->d_w64[1];
+    qa.start = ctx->d_qstart;
+    qa.idx = ctx->d_qidx;
+    qa.nx = ctx->qn[0];
+    qa.ny = ctx->qn[1];
+    qa.nz = ctx->qn[2];
+    qa.gx0 = ctx->qg0[0];
+    qa.gy0 = ctx->qg0[1];
+    qa.gz0 = ctx->qg0[2];
+    qa.inv_cs = 1.0 / ctx->qcs;
+    qa.partial = ctx->d_qpart;
+    qa.out = dst;
+    qa.complex_w = cplx;
+    {
+        StageScope sc(ctx, s, "evaluate_points");
+        launch_query(qa, s);
+        ctx->launches += 2;
+    }
+    CU(ctx, cudaGetLastError());
+    return BC_OK;
+}
+
+// The per-rotation path for n_rot rotations already prepared in ctx->d_rot (fp32) and
+// ctx->d_rot64 (fp64), written to the device buffer dout (out_per bytes per rotation).
+bc_status run_rotations(bc_ctx *ctx, int64_t n_rot, int out_kind, char *dout, size_t out_per, cudaStream_t s)
+{
+    const bool cplx = ctx->p.weights == BC_WEIGHTS_COMPLEX;
     const long long N = ctx->p.N, N3 = N * N * N;
     if (ctx->p.mode == BC_MODE_EXACT) {
         int nb = ctx->p.max_batch > 0 ? ctx->p.max_batch : 8;
@@ -1426,7 +1225,11 @@ bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, in
             const ShapePlan &pb = ctx->plan[1];
             ctx->MS = cm_row_stride(pb.L, pb.c, pb.G, ctx->K);
             const size_t nspec = (size_t)ctx->MS * ctx->M * ctx->Kz;
-            TRY(dalloc(ctx, &ctx->d_Ahat_cm, sizeof(float2) * nspec));
+            // grown only (a cudaFree would synchronise the device: the call stays asynchronous)
+            if (ctx->Ahat_cm_bytes < sizeof(float2) * nspec) {
+                TRY(dalloc(ctx, &ctx->d_Ahat_cm, sizeof(float2) * nspec));
+                ctx->Ahat_cm_bytes = sizeof(float2) * nspec;
+            }
             launch_permute_cm(ctx->d_Ahat, pb.d_mult[0], ctx->d_Ahat_cm, (long long)ctx->M * ctx->Kz, ctx->K, pb.L, pb.c,
                               pb.G, cplx, ctx->MS, ctx->Kz, ctx->p.band_radius, pb.blob ? ctx->d_dec : nullptr, s);
             ctx->launches++;
@@ -1574,9 +1377,436 @@ bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, in
             }
         }
     }
+    return BC_OK;
+}
+
+size_t out_elem_bytes(const bc_ctx *ctx, int kind)
+{
+    const bool cplx = ctx->p.weights == BC_WEIGHTS_COMPLEX;
+    const bool f64 = ctx->p.precision == BC_FP64 && ctx->p.mode == BC_MODE_EXACT;
+    if (kind == BC_OUT_F_FULL) {
+        const size_t N3 = (size_t)ctx->p.N * ctx->p.N * ctx->p.N;
+        return N3 * (f64 ? 8 : 4) * (cplx ? 2 : 1);
+    }
+    return sizeof(bc_extremum) * (kind == BC_OUT_MINMAX ? 2 : 1);
+}
+
+// Band-error guard (bc_params.tolerance > 0, spectral mode).  The spectral result is the
+// band-limited f (include/ballcorr.h); how far it is from the exact f depends on the shapes
+// (few or small balls need a wider band).  Once per pair of uploaded shapes,
+// before the first correlation, the library correlates two probe rotations (the identity
+// and a fixed generic one) on the full grid, evaluates the EXACT f (query.cu, fp64
+// pair-lens sum) at a 12^3 block of translations around each probe's max|f| and at 2,048
+// pseudo-random translations, and estimates the relative error max|f_spec - f_exact| /
+// max|f_exact| over those samples.  Above the tolerance: BC_ERANGE (raise K).  The estimate
+// is a sampled lower bound of the true grid maximum, kept by bc_query("band_error").
+// Synchronous (setup-time work).
+bc_status band_probe(bc_ctx *ctx, cudaStream_t s)
+{
+    if (ctx->p.mode != BC_MODE_SPECTRAL || !(ctx->p.tolerance > 0) || ctx->probe_done) return BC_OK;
+    if (ctx->n[0] == 0 || ctx->n[1] == 0) {
+        ctx->probe_done = true;
+        ctx->probe_err = 0.0;
+        return BC_OK;
+    }
+    const bool cplx = ctx->p.weights == BC_WEIGHTS_COMPLEX;
+    const int64_t N = ctx->p.N, N3 = N * N * N;
+    double Rp[18] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+    {  // unit quaternion (w, x, y, z) ~ (0.8, 0.2, -0.4, 0.4), normalised
+        double q[4] = {0.8, 0.2, -0.4, 0.4}, nq = 0;
+        for (double v : q) nq += v * v;
+        nq = std::sqrt(nq);
+        for (double &v : q) v /= nq;
+        const double w = q[0], x = q[1], y = q[2], z = q[3];
+        const double m[9] = {1 - 2 * (y * y + z * z), 2 * (x * y - z * w), 2 * (x * z + y * w),
+                             2 * (x * y + z * w), 1 - 2 * (x * x + z * z), 2 * (y * z - x * w),
+                             2 * (x * z - y * w), 2 * (y * z + x * w), 1 - 2 * (x * x + y * y)};
+        for (int i = 0; i < 9; i++) Rp[9 + i] = m[i];
+    }
+    TRY(prepare_rotations(ctx, Rp, false, 2, s));
+    const size_t out_per = out_elem_bytes(ctx, BC_OUT_F_FULL);
+    void *d = nullptr;
+    CU(ctx, cudaMalloc(&d, out_per * 2));
+    bc_status st = run_rotations(ctx, 2, BC_OUT_F_FULL, (char *)d, out_per, s);
+    std::vector<float> f(out_per * 2 / sizeof(float));
+    if (st == BC_OK) {
+        cudaError_t e = cudaMemcpyAsync(f.data(), d, out_per * 2, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) st = fail(ctx, BC_ECUDA, "band probe: %s", cudaGetErrorString(e));
+    }
+    cudaFree(d);
+    if (st != BC_OK) return st;
+    if (!ctx->qgrid_ready) TRY(build_query_grid(ctx));
+    const int cw = cplx ? 2 : 1;
+    double err = 0.0, scale = 0.0;
+    for (int r = 0; r < 2; r++) {
+        const float *fr = f.data() + (size_t)r * N3 * cw;
+        int64_t am = 0;
+        double best = -1;
+        for (int64_t i = 0; i < N3; i++) {
+            const double v = cplx ? std::hypot((double)fr[2 * i], (double)fr[2 * i + 1]) : std::fabs((double)fr[i]);
+            if (v > best) {
+                best = v;
+                am = i;
+            }
+        }
+        std::vector<int64_t> idx;
+        const int64_t ax = am / (N * N), ay = (am / N) % N, az = am % N;
+        const int64_t B = std::min<int64_t>(12, N);
+        auto lo = [&](int64_t c) { return std::min(std::max<int64_t>(c - B / 2, 0), N - B); };
+        for (int64_t i = lo(ax); i < lo(ax) + B; i++)
+            for (int64_t j = lo(ay); j < lo(ay) + B; j++)
+                for (int64_t k = lo(az); k < lo(az) + B; k++) idx.push_back((i * N + j) * N + k);
+        uint64_t x = 0x9e3779b97f4a7c15ull + (uint64_t)r;
+        for (int q = 0; q < 2048; q++) {  // splitmix64
+            x += 0x9e3779b97f4a7c15ull;
+            uint64_t z = x;
+            z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+            z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+            z ^= z >> 31;
+            idx.push_back((int64_t)(z % (uint64_t)N3));
+        }
+        const int64_t nq = (int64_t)idx.size();
+        TRY(ensure_query_ws(ctx, nq));
+        std::vector<double> hR((size_t)9 * nq), ht((size_t)3 * nq), ex((size_t)2 * nq);
+        for (int64_t q = 0; q < nq; q++) {
+            for (int i = 0; i < 9; i++) hR[9 * q + i] = Rp[9 * r + i];
+            const int64_t m[3] = {idx[q] / (N * N), (idx[q] / N) % N, idx[q] % N};
+            for (int a = 0; a < 3; a++) ht[3 * q + a] = ctx->p.t0[a] + (double)m[a] * ctx->p.h;
+        }
+        CU(ctx, cudaMemcpyAsync(ctx->d_qR, hR.data(), sizeof(double) * hR.size(), cudaMemcpyHostToDevice, s));
+        CU(ctx, cudaMemcpyAsync(ctx->d_qt, ht.data(), sizeof(double) * ht.size(), cudaMemcpyHostToDevice, s));
+        TRY(run_query(ctx, (int)nq, ctx->d_qout, s));
+        CU(ctx, cudaMemcpyAsync(ex.data(), ctx->d_qout, sizeof(double) * cw * nq, cudaMemcpyDeviceToHost, s));
+        CU(ctx, cudaStreamSynchronize(s));
+        for (int64_t q = 0; q < nq; q++) {
+            const int64_t i = idx[q];
+            double dv, sv;
+            if (cplx) {
+                dv = std::hypot((double)fr[2 * i] - ex[2 * q], (double)fr[2 * i + 1] - ex[2 * q + 1]);
+                sv = std::hypot(ex[2 * q], ex[2 * q + 1]);
+            } else {
+                dv = std::fabs((double)fr[i] - ex[q]);
+                sv = std::fabs(ex[q]);
+            }
+            err = std::max(err, dv);
+            scale = std::max(scale, sv);
+        }
+    }
+    ctx->probe_done = true;
+    ctx->probe_err = scale > 0 ? err / scale : 0.0;
+    if (ctx->probe_err > ctx->p.tolerance)
+        return fail(ctx, BC_ERANGE,
+                    "band K=%d too narrow for these shapes: estimated max relative error %.3g > tolerance %.3g "
+                    "(probe rotations vs the exact pair-lens sum; raise K)",
+                    ctx->K, ctx->probe_err, ctx->p.tolerance);
+    return BC_OK;
+}
+
+
+}  // namespace
+
+// ============================================================================ public API
+
+extern "C" {
+
+const char *bc_status_string(int st)
+{
+    switch (st) {
+    case BC_OK: return "BC_OK";
+    case BC_EINVAL: return "BC_EINVAL";
+    case BC_ERANGE: return "BC_ERANGE";
+    case BC_ENOMEM: return "BC_ENOMEM";
+    case BC_ESTATE: return "BC_ESTATE";
+    case BC_EUNSUPPORTED: return "BC_EUNSUPPORTED";
+    case BC_ECUDA: return "BC_ECUDA";
+    default: return "BC_UNKNOWN";
+    }
+}
+
+const char *bc_last_error(const bc_ctx *ctx)
+{
+    if (!ctx) return "no context";
+    return ctx->err.c_str();
+}
+
+bc_status bc_create(int device, const bc_params *p, bc_ctx **out)
+{
+    if (!p || !out) return BC_EINVAL;
+    *out = nullptr;
+    if (p->N < 1 || !(p->h > 0) || !std::isfinite(p->h)) return BC_EINVAL;
+    for (int a = 0; a < 3; a++)
+        if (!std::isfinite(p->t0[a])) return BC_EINVAL;
+    if (p->mode != BC_MODE_SPECTRAL && p->mode != BC_MODE_EXACT) return BC_EINVAL;
+    if (p->precision != BC_FP32 && p->precision != BC_FP64) return BC_EINVAL;
+    if (p->weights != BC_WEIGHTS_REAL && p->weights != BC_WEIGHTS_COMPLEX) return BC_EINVAL;
+    if (p->max_batch < 0) return BC_EINVAL;
+    if (p->concurrency < 0 || p->concurrency > 2) return BC_EINVAL;
+    if (!(p->tolerance >= 0) || !std::isfinite(p->tolerance)) return BC_EINVAL;
+    if (p->mode == BC_MODE_SPECTRAL) {
+        if (p->precision != BC_FP32) return BC_EUNSUPPORTED;
+        if (p->Np < p->N || p->Np < 2 || (p->Np % 2) != 0 || !friendly(p->Np) || p->Np > 1024) return BC_EINVAL;
+        if (p->K < 1 || p->K > 2047) return BC_EINVAL;
+        if (!(p->band_radius >= 0) || !std::isfinite(p->band_radius)) return BC_EINVAL;
+        if (!fft_size_supported(p->Np)) return BC_EUNSUPPORTED;
+        if (p->N > 1625) return BC_EUNSUPPORTED;
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+        cudaGetLastError();
+        return BC_ECUDA;
+    }
+    if (cudaSetDevice(device) != cudaSuccess) return BC_ECUDA;
+    bc_ctx *ctx = new bc_ctx();
+    ctx->device = device;
+    ctx->p = *p;
+    if (p->mode == BC_MODE_SPECTRAL) {
+        const bool cplx = p->weights == BC_WEIGHTS_COMPLEX;
+        ctx->P = p->Np * p->h;
+        ctx->K = p->K;
+        ctx->M = 2 * p->K + 1;
+        ctx->Kz = cplx ? ctx->M : p->K + 1;
+        ctx->Fz = cplx ? p->Np : p->Np / 2 + 1;
+        if (ensure_twiddles(ctx, p->Np) != BC_OK) {
+            bc_destroy(ctx);
+            return BC_ENOMEM;
+        }
+    }
+    *out = ctx;
+    return BC_OK;
+}
+
+bc_status bc_destroy(bc_ctx *ctx)
+{
+    if (!ctx) return BC_OK;
+    cudaSetDevice(ctx->device);
+    for (int w = 0; w < 2; w++) {
+        dfree(ctx->d_balls[w]);
+        dfree(ctx->d_wre[w]);
+        dfree(ctx->d_wim[w]);
+        dfree(ctx->d_balls64[w]);
+        dfree(ctx->d_w64[w]);
+        for (int a = 0; a < 3; a++) dfree(ctx->plan[w].d_mult[a]);
+        dfree(ctx->plan[w].d_ctw);
+    }
+    for (auto &kv : ctx->d_tw) cudaFree(kv.second);
+    dfree(ctx->d_csr_off);
+    dfree(ctx->d_csr_idx);
+    dfree(ctx->d_prof);
+    dfree(ctx->d_prof_off);
+    dfree(ctx->d_bcells);
+    dfree(ctx->d_g02);
+    dfree(ctx->d_phi);
+    dfree(ctx->d_dec);
+    dfree(ctx->d_recB);
+    for (Slot &sl : ctx->slot) {
+        if (sl.ws1) cudaFree(sl.ws1);
+        if (sl.ws2) cudaFree(sl.ws2);
+        dfree(sl.keys);
+        dfree(sl.recA);
+        dfree(sl.szcnt);
+        dfree(sl.szoff);
+        dfree(sl.szlist);
+        if (sl.stream) cudaStreamDestroy(sl.stream);
+        if (sl.done) cudaEventDestroy(sl.done);
+    }
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    dfree(ctx->d_qstart);
+    dfree(ctx->d_qidx);
+    dfree(ctx->d_qR);
+    dfree(ctx->d_qt);
+    dfree(ctx->d_qpart);
+    dfree(ctx->d_qout);
+    dfree(ctx->d_Ahat);
+    dfree(ctx->d_Ahat_cm);
+    dfree(ctx->d_xtab);
+    dfree(ctx->d_segs);
+
+    dfree(ctx->d_rot);
+    dfree(ctx->d_rot64);
+    if (ctx->d_out_stage) cudaFree(ctx->d_out_stage);
+    dfree(ctx->d_acc);
+    dfree(ctx->d_part);
+    dfree(ctx->d_part_idx);
+    for (auto &pe : ctx->pending) {
+        cudaEventDestroy(pe.e0);
+        cudaEventDestroy(pe.e1);
+    }
+    for (auto e : ctx->event_pool) cudaEventDestroy(e);
+    if (ctx->h_status) cudaFreeHost(ctx->h_status);
+    delete ctx;
+    return BC_OK;
+}
+
+bc_status bc_shape_upload(bc_ctx *ctx, int which, const double *xyzr, const double *w, int64_t n)
+{
+    if (!ctx) return BC_EINVAL;
+    TRY(check_deferred(ctx));
+    if (which != 0 && which != 1) return fail(ctx, BC_EINVAL, "which must be 0 (A) or 1 (B)");
+    if (n < 0 || (n > 0 && !xyzr)) return fail(ctx, BC_EINVAL, "bad shape size or NULL xyzr");
+    if (n > (1ll << 30)) return fail(ctx, BC_EINVAL, "too many balls");
+    CU(ctx, cudaSetDevice(ctx->device));
+    const bool cplx = ctx->p.weights == BC_WEIGHTS_COMPLEX;
+    std::vector<double> x, wv;
+    TRY(fetch_host(ctx, xyzr, (size_t)n * 4, x));
+    if (w) TRY(fetch_host(ctx, w, (size_t)n * (cplx ? 2 : 1), wv));
+    for (int64_t i = 0; i < n; i++) {
+        for (int q = 0; q < 4; q++)
+            if (!std::isfinite(x[4 * i + q])) return fail(ctx, BC_EINVAL, "ball %lld has a non-finite entry", (long long)i);
+        if (!(x[4 * i + 3] > 0)) return fail(ctx, BC_EINVAL, "ball %lld has radius <= 0", (long long)i);
+    }
+    for (double v : wv)
+        if (!std::isfinite(v)) return fail(ctx, BC_EINVAL, "non-finite weight");
+    ctx->hxyzr[which] = x;
+    ctx->hw[which].assign((size_t)n * 2, 0.0);
+    for (int64_t i = 0; i < n; i++) {
+        if (!w) {
+            ctx->hw[which][2 * i] = 1.0;
+        } else if (cplx) {
+            ctx->hw[which][2 * i] = wv[2 * i];
+            ctx->hw[which][2 * i + 1] = wv[2 * i + 1];
+        } else {
+            ctx->hw[which][2 * i] = wv[i];
+        }
+    }
+    ctx->n[which] = n;
+    ctx->have[which] = true;
+    ctx->qgrid_ready = false;
+    ctx->probe_done = false;
+    ctx->probe_err = -1.0;
+    if (which == 0) ctx->have_spec = false;
+    ctx->cm_ready = false;
+    TRY(upload_shape_device(ctx, which));
+    if (ctx->p.mode == BC_MODE_SPECTRAL && n > 0) {
+        double lo[3], hi[3], rmax, rho;
+        shape_bounds(ctx, which, lo, hi, rmax, rho);
+        if (which == 1)
+            for (int a = 0; a < 3; a++) {  // any rotation keeps B inside the ball of radius max|b_j|
+                lo[a] = -rho;
+                hi[a] = rho;
+            }
+        TRY(plan_shape(ctx, which, lo, hi, rmax));
+        if (which == 0) TRY(build_csr_A(ctx));
+        if (which == 1 && !ctx->plan[1].blob) TRY(build_profiles_B(ctx));
+        if (which == 1) {
+            const ShapePlan &pb = ctx->plan[1];
+            ctx->live_r = (rho + rmax + pb.cut) / pb.hf + 2.0;
+            ctx->spread_cells_B = 0;
+            for (int64_t j = 0; j < n; j++) {
+                const double rc = (ctx->hxyzr[1][4 * j + 3] + pb.cut) / pb.hf;
+                ctx->spread_cells_B += 4.0 / 3.0 * kPi * rc * rc * rc;
+            }
+            ctx->live_tiles_B = 0;  // same test as spread_z_kernel's zero-tile exit
+            for (int X0 = 0; X0 < pb.L; X0 += 4)
+                for (int Y0 = 0; Y0 < pb.L; Y0 += 4) {
+                    const double cx = -pb.o[0], cy = -pb.o[1];
+                    const double dx = std::max(std::max(X0 - cx, cx - (X0 + 3)), 0.0);
+                    const double dy = std::max(std::max(Y0 - cy, cy - (Y0 + 3)), 0.0);
+                    if (dx * dx + dy * dy <= (ctx->live_r + 1) * (ctx->live_r + 1)) ctx->live_tiles_B++;
+                }
+            if (ctx->plan[1].blob) TRY(build_spread_z_tables(ctx));
+        }
+    }
+    TRY(check_support(ctx));
+    return BC_OK;
+}
+
+bc_status bc_spectrum_A(bc_ctx *ctx, void *stream)
+{
+    if (!ctx) return BC_EINVAL;
+    TRY(check_deferred(ctx));
+    if (!ctx->have[0]) return fail(ctx, BC_ESTATE, "shape A has not been uploaded");
+    if (ctx->p.mode != BC_MODE_SPECTRAL || ctx->have_spec) {
+        ctx->have_spec = true;
+        return BC_OK;
+    }
+    CU(ctx, cudaSetDevice(ctx->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t nspec = (size_t)ctx->M * ctx->M * ctx->Kz;
+    if (!ctx->d_Ahat) TRY(dalloc(ctx, &ctx->d_Ahat, sizeof(float2) * nspec));  // fixed size per context
+    ctx->cm_ready = false;
+    ctx->probe_done = false;
+    if (ctx->n[0] == 0) {
+        CU(ctx, cudaMemsetAsync(ctx->d_Ahat, 0, sizeof(float2) * nspec, s));
+        ctx->have_spec = true;
+        return BC_OK;
+    }
+    // A's spread / z / y passes run in the context's batch workspaces (slot 0; kept, grown
+    // when A's plan needs more): no allocation and no synchronisation per call
+    size_t s1, s2;
+    spectral_ws_sizes(ctx, 0, s1, s2);
+    Slot &sl = ctx->slot[0];
+    TRY(ensure_ws(ctx, &sl.ws1, sl.ws1_bytes, s1));
+    TRY(ensure_ws(ctx, &sl.ws2, sl.ws2_bytes, s2));
+    TRY(shape_spectrum(ctx, 0, nullptr, 1, sl.ws1, sl.ws2, s1, s2, s, sl));
+    if (ctx->prof) collect_profile(ctx);
+    ctx->have_spec = true;
+    return BC_OK;
+}
+
+bc_status bc_spectrum_A_buffer(bc_ctx *ctx, void **dev_ptr, int64_t *bytes)
+{
+    if (!ctx) return BC_EINVAL;
+    if (!dev_ptr || !bytes) return fail(ctx, BC_EINVAL, "NULL dev_ptr/bytes");
+    if (ctx->p.mode != BC_MODE_SPECTRAL) return fail(ctx, BC_EUNSUPPORTED, "exact mode has no spectrum of A");
+    CU(ctx, cudaSetDevice(ctx->device));
+    const size_t nspec = (size_t)ctx->M * ctx->M * ctx->Kz;
+    if (!ctx->d_Ahat) TRY(dalloc(ctx, &ctx->d_Ahat, sizeof(float2) * nspec));
+    *dev_ptr = ctx->d_Ahat;
+    *bytes = (int64_t)(sizeof(float2) * nspec);
+    return BC_OK;
+}
+
+bc_status bc_spectrum_A_import(bc_ctx *ctx)
+{
+    if (!ctx) return BC_EINVAL;
+    if (ctx->p.mode != BC_MODE_SPECTRAL) return fail(ctx, BC_EUNSUPPORTED, "exact mode has no spectrum of A");
+    if (!ctx->have[0]) return fail(ctx, BC_ESTATE, "shape A has not been uploaded");
+    if (!ctx->d_Ahat) return fail(ctx, BC_ESTATE, "bc_spectrum_A_buffer has not been called");
+    ctx->cm_ready = false;  // A'' (coset-major, B's multipliers) is rebuilt from the new contents
+    ctx->probe_done = false;
+    ctx->have_spec = true;
+    return BC_OK;
+}
+
+bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, int out_kind, void *out, void *stream)
+{
+    if (!ctx) return BC_EINVAL;
+    TRY(check_deferred(ctx));
+    if (!R || !out || n_rot < 1) return fail(ctx, BC_EINVAL, "NULL R/out or n_rot < 1");
+    if (out_kind < BC_OUT_F_FULL || out_kind > BC_OUT_MAX_REAL) return fail(ctx, BC_EINVAL, "bad out_kind");
+    const bool cplx = ctx->p.weights == BC_WEIGHTS_COMPLEX;
+    if (cplx && out_kind != BC_OUT_F_FULL && out_kind != BC_OUT_MAX_REAL)
+        return fail(ctx, BC_EINVAL, "complex weights support F_FULL and MAX_REAL only");
+    if (!ctx->have[0] || !ctx->have[1]) return fail(ctx, BC_ESTATE, "upload both shapes first");
+    if (ctx->p.mode == BC_MODE_SPECTRAL && !ctx->have_spec && ctx->n[0] > 0 && ctx->n[1] > 0)
+        return fail(ctx, BC_ESTATE, "call bc_spectrum_A first");
+    CU(ctx, cudaSetDevice(ctx->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool dev_R = is_device_ptr(R);
+    if (!dev_R) TRY(validate_rotations(ctx, R, n_rot));  // host R: immediate BC_EINVAL
+    // band-error guard (bc_params.tolerance): once per pair of uploaded shapes
+    TRY(band_probe(ctx, s));
+
+    const size_t out_per = out_elem_bytes(ctx, out_kind);
+    const bool host_out = !is_device_ptr(out);
+    char *dout = (char *)out;
+    if (host_out) {
+        TRY(ensure_ws(ctx, &ctx->d_out_stage, ctx->out_stage_bytes, out_per * n_rot));
+        dout = (char *)ctx->d_out_stage;
+    }
+    TRY(prepare_rotations(ctx, R, dev_R, n_rot, s));
+
+    if (ctx->n[0] == 0 || ctx->n[1] == 0) {
+        // empty shape: f == 0 identically; a bc_extremum {0.0, 0} is all-zero bytes too
+        CU(ctx, cudaMemsetAsync(dout, 0, out_per * n_rot, s));
+    } else {
+        TRY(run_rotations(ctx, n_rot, out_kind, dout, out_per, s));
+    }
     if (host_out) {
         CU(ctx, cudaMemcpyAsync(out, dout, out_per * n_rot, cudaMemcpyDeviceToHost, s));
         CU(ctx, cudaStreamSynchronize(s));
+        TRY(check_deferred(ctx));
     }
     if (ctx->prof) collect_profile(ctx);
     return BC_OK;
@@ -1585,17 +1815,18 @@ bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, in
 bc_status bc_evaluate_points(bc_ctx *ctx, const double *R, const double *t, int64_t n, double *out, void *stream)
 {
     if (!ctx) return BC_EINVAL;
+    TRY(check_deferred(ctx));
     if (!R || !t || !out || n < 1) return fail(ctx, BC_EINVAL, "NULL R/t/out or n < 1");
     if (!ctx->have[0] || !ctx->have[1]) return fail(ctx, BC_ESTATE, "upload both shapes first");
     CU(ctx, cudaSetDevice(ctx->device));
     cudaStream_t s = (cudaStream_t)stream;
     const bool cplx = ctx->p.weights == BC_WEIGHTS_COMPLEX;
-    std::vector<double> hR, ht;
-    TRY(fetch_host(ctx, R, (size_t)n * 9, hR));
-    TRY(fetch_host(ctx, t, (size_t)n * 3, ht));
-    TRY(validate_rotations(ctx, hR, n));
-    for (double v : ht)
-        if (!std::isfinite(v)) return fail(ctx, BC_EINVAL, "non-finite translation");
+    const bool dev_R = is_device_ptr(R), dev_t = is_device_ptr(t);
+    if (!dev_R) TRY(validate_rotations(ctx, R, n));
+    if (!dev_t)
+        for (int64_t q = 0; q < 3 * n; q++)
+            if (!std::isfinite(t[q])) return fail(ctx, BC_EINVAL, "non-finite translation");
+    TRY(ensure_deferred_status(ctx));
     const size_t out_per = cplx ? 2 : 1;
     const bool host_out = !is_device_ptr(out);
     if (ctx->n[0] == 0 || ctx->n[1] == 0) {
@@ -1607,50 +1838,43 @@ bc_status bc_evaluate_points(bc_ctx *ctx, const double *R, const double *t, int6
     }
     if (!ctx->qgrid_ready) TRY(build_query_grid(ctx));
     const int64_t chunk = std::min<int64_t>(n, 65535);
-    const int nblk = query_blocks((int)ctx->n[1]);
-    if (ctx->q_cap < chunk) {
-        TRY(dalloc(ctx, &ctx->d_qR, sizeof(double) * 9 * chunk));
-        TRY(dalloc(ctx, &ctx->d_qt, sizeof(double) * 3 * chunk));
-        TRY(dalloc(ctx, &ctx->d_qpart, sizeof(double) * 2 * nblk * chunk));
-        TRY(dalloc(ctx, &ctx->d_qout, sizeof(double) * 2 * chunk));
-        ctx->q_cap = chunk;
-    }
+    TRY(ensure_query_ws(ctx, chunk));
     for (int64_t q0 = 0; q0 < n; q0 += chunk) {
         const int nq = (int)std::min<int64_t>(chunk, n - q0);
-        CU(ctx, cudaMemcpyAsync(ctx->d_qR, hR.data() + 9 * q0, sizeof(double) * 9 * nq, cudaMemcpyHostToDevice, s));
-        CU(ctx, cudaMemcpyAsync(ctx->d_qt, ht.data() + 3 * q0, sizeof(double) * 3 * nq, cudaMemcpyHostToDevice, s));
-        QueryArgs qa{};
-        qa.nq = nq;
-        qa.nB = (int)ctx->n[1];
-        qa.R = ctx->d_qR;
-        qa.t = ctx->d_qt;
-        qa.A = ctx->d_balls64[0];
-        qa.B = ctx->d_balls64[1];
-        qa.wA = ctx->d_w64[0];
-        qa.wB = ctx->d_w64[1];
-        qa.start = ctx->d_qstart;
-        qa.idx = ctx->d_qidx;
-        qa.nx = ctx->qn[0];
-        qa.ny = ctx->qn[1];
-        qa.nz = ctx->qn[2];
-        qa.gx0 = ctx->qg0[0];
-        qa.gy0 = ctx->qg0[1];
-        qa.gz0 = ctx->qg0[2];
-        qa.inv_cs = 1.0 / ctx->qcs;
-        qa.partial = ctx->d_qpart;
-        qa.out = host_out ? ctx->d_qout : out + out_per * q0;
-        qa.complex_w = cplx;
-        {
-            StageScope sc(ctx, s, "evaluate_points");
-            launch_query(qa, s);
-            ctx->launches += 2;
+        // R and t into the query buffers: host arrays are copied (validated above), device
+        // arrays are validated and copied on the device (deferred BC_EINVAL, no host round trip)
+        RotPrepArgs ra{};
+        ra.R = dev_R ? R + 9 * q0 : ctx->d_qR;
+        ra.t = dev_t ? t + 3 * q0 : nullptr;
+        ra.n = nq;
+        ra.index_base = q0;
+        ra.tol = rot_tol(ctx);
+        ra.r64 = dev_R ? ctx->d_qR : nullptr;
+        ra.t64 = dev_t ? ctx->d_qt : nullptr;
+        ra.status = ctx->d_status;
+        if (!dev_R) CU(ctx, cudaMemcpyAsync(ctx->d_qR, R + 9 * q0, sizeof(double) * 9 * nq, cudaMemcpyHostToDevice, s));
+        if (!dev_t) CU(ctx, cudaMemcpyAsync(ctx->d_qt, t + 3 * q0, sizeof(double) * 3 * nq, cudaMemcpyHostToDevice, s));
+        if (dev_R || dev_t) {
+            launch_rot_prep(ra, s);
+            ctx->launches++;
         }
-        CU(ctx, cudaGetLastError());
+        double *dst = host_out ? ctx->d_qout : out + out_per * q0;
+        TRY(run_query(ctx, nq, dst, s));
         if (host_out) {
             CU(ctx, cudaMemcpyAsync(out + out_per * q0, ctx->d_qout, sizeof(double) * out_per * nq, cudaMemcpyDeviceToHost, s));
             CU(ctx, cudaStreamSynchronize(s));
         }
     }
+    if (host_out) TRY(check_deferred(ctx));
+    return BC_OK;
+}
+
+bc_status bc_sync(bc_ctx *ctx, void *stream)
+{
+    if (!ctx) return BC_EINVAL;
+    CU(ctx, cudaSetDevice(ctx->device));
+    CU(ctx, cudaStreamSynchronize((cudaStream_t)stream));
+    TRY(check_deferred(ctx));
     return BC_OK;
 }
 
@@ -1679,6 +1903,7 @@ bc_status bc_query(const bc_ctx *ctx, const char *key, double *value)
     else if (k == "spread_cells_B") *value = ctx->spread_cells_B;
     else if (k == "live_tiles_B") *value = (double)ctx->live_tiles_B;
     else if (k == "K") *value = ctx->K;
+    else if (k == "band_error") *value = ctx->probe_done ? ctx->probe_err : -1.0;
     else if (k == "Np") *value = ctx->p.Np;
     else if (k == "fused_fold_inv") *value = (!ctx->p.generic_only && fold_fuses_inverse(B.L, ctx->p.Np)) ? 1 : 0;
     else if (k == "fold_fast")

@@ -264,3 +264,23 @@ struct QueryArgs {
 };
 int query_blocks(int nB);
 void launch_query(const QueryArgs &a, cudaStream_t s);
+
+// ----------------------------------------------------------------- device-side validation (validate.cu)
+enum : unsigned {
+    BC_DEFER_NONFINITE_R = 1u,
+    BC_DEFER_NOT_ORTHONORMAL = 2u,
+    BC_DEFER_DET = 4u,
+    BC_DEFER_NONFINITE_T = 8u,
+};
+struct RotPrepArgs {
+    const double *R;     // [n][9] caller array (device)
+    const double *t;     // [n][3] caller translations (device) or nullptr
+    long long n;
+    long long index_base;  // index of R[0] in the caller's array (chunked calls)
+    double tol;          // max |R R^T - I| entry
+    float *r32;          // [n][9] fp32 copy or nullptr
+    double *r64;         // [n][9] fp64 copy or nullptr
+    double *t64;         // [n][3] fp64 copy of t or nullptr
+    unsigned *status;    // [2] (mapped host memory): OR of BC_DEFER_* flags, lowest bad index
+};
+void launch_rot_prep(const RotPrepArgs &a, cudaStream_t s);

@@ -781,8 +781,10 @@ void launch_last(const LastArgs &a, int batch, cudaStream_t s)
 {
     // TMA-fed C2R path: the tile rows must be 16-byte aligned (the stage offsets and
     // the row blocks are multiples of 2 NL rows; Fz * 8 bytes per row)
+    // every row (not only every full tile): a ragged last tile of an odd number of rows must
+    // still copy a multiple of 16 bytes (cp.async.bulk size rule and the expect_tx count)
     if (a.hermitian && a.Np == 256 && ((uintptr_t)a.in % 16) == 0 && (a.in_bstride * 8) % 16 == 0 &&
-        ((a.pitch ? a.pitch : a.Fz) * 8 * 2 * Plan<256>::NL) % 16 == 0) {
+        ((a.pitch ? a.pitch : a.Fz) * 8) % 16 == 0) {
         constexpr int NL = Plan<256>::NL;
         const size_t sm = sizeof(float2) * (2 * 2 * NL * (size_t)(a.pitch ? a.pitch : a.Fz) + 256 +
                                             (Plan<256>::n >= 3 ? 2 : 1) * (size_t)NL * line_stride(256));

@@ -27,4 +27,42 @@ def correlator_kwargs(name: str, N: int, h: float, t0, weights: str, **overrides
     p.update(overrides)
     return dict(N=N, h=h, t0=t0, Np=p["Np"], K=p["K"], mode=p["mode"], precision=p["precision"],
                 weights=weights, max_batch=p.get("max_batch", 0), spread_eps=p.get("spread_eps", 0.0),
-                generic_only=p.get("generic_only", False), concurrency=p.get("concurrency", 0))
+                generic_only=p.get("generic_only", False), concurrency=p.get("concurrency", 0),
+                tolerance=p.get("tolerance", 0.0))
+
+
+def choose_band(name: str, N: int, h: float, t0, weights: str, A, wA, B, wB, tol: float = 5e-5,
+                K_max: int = 2047, growth: float = 1.25, device: int = 0, **overrides) -> dict:
+    """(Correlator kwargs, band-error estimate): a band K meeting a requested tolerance for
+    THESE shapes.
+
+    Starts at the preset's K and widens it by `growth` until the library's band-error guard
+    (bc_params.tolerance: two probe rotations of the spectral grid against the exact pair-lens
+    f at sampled translations) accepts it; raises BallCorrError(BC_ERANGE) past K_max.  Exact
+    mode needs no band and is returned unchanged.  The default 5e-5 keeps a 2x margin under the
+    north_star 1e-4 for the translations and rotations the probe did not sample."""
+    from .ballcorr import Correlator, BallCorrError, BC_ERANGE
+    kw = correlator_kwargs(name, N, h, t0, weights, **overrides)
+    if kw["mode"] != "spectral":
+        return kw, 0.0
+    K = kw["K"]
+    last = None
+    while K <= K_max:
+        kw.update(K=K, tolerance=tol)
+        c = Correlator(device=device, **kw)
+        try:
+            c.shape_upload(0, A, wA)  # errors here (support wrap, no box) are not band errors
+            c.shape_upload(1, B, wB)
+            c.spectrum_A()
+            try:
+                c.correlate_rotations([[[1.0, 0, 0], [0, 1.0, 0], [0, 0, 1.0]]],
+                                      "full" if weights == "complex" else "max_argmax")
+                return kw, c.query("band_error")
+            except BallCorrError as e:
+                if e.status != BC_ERANGE:
+                    raise
+                last = e
+        finally:
+            c.close()
+        K = int(K * growth) + 1
+    raise last

@@ -85,3 +85,31 @@ def test_null_context_is_safe(bc):
     assert bc.bc_destroy(None) == 0
     assert bc.bc_last_error(None) == b"no context"
     assert bc.bc_launch_count(None) == 0
+
+
+def test_out_buffers_are_checked_not_copied(bc):
+    """ballcorr._out_ptr: a caller's `out` must hold the bytes the call writes, be
+    C-contiguous, and have the result dtype or raw bytes; it is never silently replaced by a
+    contiguous copy (the library would write into a temporary)."""
+    import numpy as np
+    import torch
+    f32 = np.float32
+    assert bc._out_ptr(np.empty((2, 4, 4, 4), f32), 2 * 64 * 4, f32) > 0
+    assert bc._out_ptr(np.empty(512, np.uint8), 512, f32) > 0
+    assert bc._out_ptr(torch.empty(512, dtype=torch.uint8), 512, f32) > 0
+    assert bc._out_ptr(torch.empty((2, 64), dtype=torch.float32), 512, f32) > 0
+    bad = [
+        (np.empty((2, 4, 4, 3), f32), 2 * 64 * 4, f32),            # too small
+        (np.empty((4, 4, 8), f32)[:, :, ::2], 64 * 4, f32),        # not contiguous
+        (np.empty(128, np.float64), 512, f32),                      # wrong dtype
+        (torch.empty((8, 16), dtype=torch.float32).t(), 512, f32),  # non-contiguous tensor
+        (torch.empty(100, dtype=torch.uint8), 512, f32),           # too small tensor
+        ([0.0] * 128, 512, f32),                                    # not an array
+    ]
+    for out, nbytes, dt in bad:
+        with pytest.raises(ValueError):
+            bc._out_ptr(out, nbytes, dt)
+    ext = np.empty(3, bc.EXTREMUM_DTYPE)
+    assert bc._out_ptr(ext, 3 * 16, bc.EXTREMUM_DTYPE) > 0
+    with pytest.raises(ValueError):
+        bc._out_ptr(np.empty(2, bc.EXTREMUM_DTYPE), 3 * 16, bc.EXTREMUM_DTYPE)

@@ -1,0 +1,215 @@
+"""The C ABI's promises (include/ballcorr.h), exercised on the GPU.
+
+* Device-resident R / t are validated ON THE DEVICE: an invalid rotation in a device buffer
+  does not stall the call; BC_EINVAL surfaces at bc_sync / the next call (deferred).
+* Per-precision rotation tolerance: 1e-5 (fp32), 1e-12 (fp64).
+* Asynchrony: with device buffers neither bc_spectrum_A nor bc_correlate_rotations waits
+  for the stream (a pending sleep kernel is still running when they return).
+* The band-error guard (bc_params.tolerance) rejects a B the preset band is too narrow for
+  and accepts the workload's own B; presets.choose_band widens K until it passes.
+* Options without other coverage: concurrency = 2, complex weights in fp32 exact mode, an
+  odd output size on the Np = 256 generic plan (ragged TMA tile).
+"""
+import numpy as np
+import pytest
+
+from synth import make_config, random_small_case
+from gpu_helpers import rel_max_err, as_complex
+
+pytestmark = pytest.mark.gpu
+
+TOL_F32 = 1e-4
+EDGE_B = np.array([[0.0, 0.0, 0.0, 0.02], [0.2, 0.0, 0.0, 0.02], [0.0, -0.2, 0.0, 0.005],
+                   [0.0, 0.0, 0.2, 0.01], [-0.1155, 0.1155, -0.1155, 0.02]])
+
+
+@pytest.fixture(scope="module")
+def bc():
+    import torch
+    assert torch.cuda.is_available()
+    from paper_1711_05075_b200 import ballcorr
+    return ballcorr
+
+
+def small(bc, seed=60, **kw):
+    w = random_small_case(seed, n_a=8, n_b=6, n_rot=3, N=16)
+    c = bc.Correlator(N=w.N, h=w.h, t0=w.t0, Np=20, K=19, **kw)
+    c.shape_upload(0, w.A_xyzr, w.A_w)
+    c.shape_upload(1, w.B_xyzr, w.B_w)
+    c.spectrum_A()
+    return w, c
+
+
+def test_device_R_is_validated_on_device_deferred(bc):
+    import torch
+    w, c = small(bc)
+    bad = torch.tensor(w.R, device="cuda")
+    bad[1] *= 1.01                                    # not orthonormal
+    out = torch.empty((3, 16, 16, 16), dtype=torch.float32, device="cuda")
+    c.correlate_rotations(bad, "full", out=out)       # returns: no host round trip to check R
+    with pytest.raises(bc.BallCorrError) as e:
+        c.sync()
+    assert e.value.status == bc.BC_EINVAL and "entry 1" in str(e.value)
+    c.sync()                                          # reported once
+    # the next call after an invalid device R (without bc_sync) reports it too
+    bad2 = torch.tensor(w.R, device="cuda")
+    bad2[2, 0, 0] = float("nan")
+    c.correlate_rotations(bad2, "full", out=out)
+    torch.cuda.synchronize()
+    with pytest.raises(bc.BallCorrError) as e:
+        c.correlate_rotations(torch.tensor(w.R, device="cuda"), "full", out=out)
+    assert e.value.status == bc.BC_EINVAL and "entry 2" in str(e.value)
+    # valid device R: identical to the host path
+    c.correlate_rotations(torch.tensor(w.R, device="cuda"), "full", out=out)
+    c.sync()
+    assert np.array_equal(out.cpu().numpy(), c.correlate_rotations(w.R, "full"))
+
+
+def test_device_t_is_validated_on_device_deferred(bc):
+    import torch
+    w, c = small(bc, seed=61)
+    t = torch.zeros((4, 3), dtype=torch.float64, device="cuda")
+    t[3, 1] = float("inf")
+    R = torch.tensor(np.repeat(w.R[:1], 4, axis=0), device="cuda")
+    out = torch.empty(4, dtype=torch.float64, device="cuda")
+    c.evaluate_points(R, t, out=out)
+    with pytest.raises(bc.BallCorrError) as e:
+        c.sync()
+    assert e.value.status == bc.BC_EINVAL and "entry 3" in str(e.value)
+    t[3, 1] = 0.0
+    c.evaluate_points(R, t, out=out)
+    c.sync()
+    assert np.allclose(out.cpu().numpy(), c.evaluate_points(w.R[[0, 0, 0, 0]], np.zeros((4, 3))), rtol=0, atol=0)
+
+
+def test_rotation_tolerance_per_precision(bc):
+    w = random_small_case(62, n_a=5, n_b=4, n_rot=1, N=8)
+    R = w.R.copy()
+    R[0] *= 1.0 + 3e-6                                # |R R^T - I| ~ 6e-6
+    f32 = bc.Correlator(N=w.N, h=w.h, t0=w.t0, mode="exact", precision="f32")
+    f64 = bc.Correlator(N=w.N, h=w.h, t0=w.t0, mode="exact", precision="f64")
+    for c in (f32, f64):
+        c.shape_upload(0, w.A_xyzr, w.A_w)
+        c.shape_upload(1, w.B_xyzr, w.B_w)
+    f32.correlate_rotations(R, "full")                # within 1e-5
+    with pytest.raises(bc.BallCorrError) as e:
+        f64.correlate_rotations(R, "full")            # beyond 1e-12
+    assert e.value.status == bc.BC_EINVAL
+    R2 = w.R.copy()
+    R2[0] *= 1.0 + 2e-5                               # beyond 1e-5
+    with pytest.raises(bc.BallCorrError):
+        f32.correlate_rotations(R2, "full")
+
+
+def test_device_calls_do_not_wait_for_the_stream(bc):
+    import torch
+    w = make_config("sweep", n_rot=4)
+    from paper_1711_05075_b200.presets import correlator_kwargs
+    c = bc.Correlator(**correlator_kwargs("sweep", w.N, w.h, w.t0, "real"))
+    c.shape_upload(0, w.A_xyzr, w.A_w)
+    c.shape_upload(1, w.B_xyzr, w.B_w)
+    s = torch.cuda.Stream()
+    R = torch.tensor(w.R, device="cuda")
+    out = torch.empty(4 * 16, dtype=torch.uint8, device="cuda")
+    c.spectrum_A(stream=s)                            # first call allocates the workspaces
+    c.correlate_rotations(R, "min_argmin", out=out, stream=s)
+    s.synchronize()
+    ref = bc.extremum_to_numpy(out.cpu().numpy())
+    # a fresh A spectrum and a correlation behind a ~0.5 s sleep on the same stream
+    c.shape_upload(0, w.A_xyzr, w.A_w)
+    with torch.cuda.stream(s):
+        torch.cuda._sleep(1_000_000_000)
+    c.spectrum_A(stream=s)
+    c.correlate_rotations(R, "min_argmin", out=out, stream=s)
+    assert not s.query(), "a call waited for the stream"
+    c.sync(stream=s)
+    assert np.array_equal(bc.extremum_to_numpy(out.cpu().numpy()), ref)
+
+
+def test_band_guard_rejects_then_choose_band_widens(bc, oracle_mod):
+    from paper_1711_05075_b200.presets import correlator_kwargs, choose_band
+    w = make_config("sweep", n_rot=2)
+    # the workload's own B passes the guard at the preset band
+    c = bc.Correlator(**correlator_kwargs("sweep", w.N, w.h, w.t0, "real", tolerance=1e-4))
+    c.shape_upload(0, w.A_xyzr, w.A_w)
+    c.shape_upload(1, w.B_xyzr, w.B_w)
+    c.spectrum_A()
+    c.correlate_rotations(w.R, "min_argmin")
+    assert 0 < c.query("band_error") < 1e-4
+    # five edge balls: band error ~2.5e-4 at K = 255 -> BC_ERANGE instead of a silent miss
+    e5 = bc.Correlator(**correlator_kwargs("sweep", w.N, w.h, w.t0, "real", tolerance=1e-4))
+    e5.shape_upload(0, w.A_xyzr, w.A_w)
+    e5.shape_upload(1, EDGE_B)
+    e5.spectrum_A()
+    with pytest.raises(bc.BallCorrError) as e:
+        e5.correlate_rotations(w.R, "min_argmin")
+    assert e.value.status == bc.BC_ERANGE
+    assert e5.query("band_error") > 1e-4
+    # choose_band: widen K until the guard accepts.  These balls (r = 0.005 is below the
+    # band's resolution 2/K) converge slowly (probe 7.6e-4 at K = 255, 2.4e-4 at K = 499,
+    # tools/band_guard_probe.py), so the demonstration asks for 3e-4; the oracle agrees
+    kw, est = choose_band("sweep", w.N, w.h, w.t0, "real", w.A_xyzr, w.A_w, EDGE_B, None, tol=3e-4)
+    assert kw["K"] > 255 and est <= 3e-4
+    c2 = bc.Correlator(**kw)
+    c2.shape_upload(0, w.A_xyzr, w.A_w)
+    c2.shape_upload(1, EDGE_B)
+    c2.spectrum_A()
+    f = c2.correlate_rotations(w.R[1:2], "full")[0]
+    rng = np.random.default_rng(5)
+    flat = f.reshape(-1)
+    idx = np.unique(np.concatenate([rng.choice(flat.size, 200, replace=False),
+                                    np.argpartition(np.abs(flat), -100)[-100:]]))
+    ref = oracle_mod.correlate_points(w.A_xyzr, w.A_w, EDGE_B, None, w.R[1], w.N, w.h, w.t0, idx)
+    assert np.abs(flat[idx] - ref).max() <= 3e-4 * np.abs(ref).max()
+
+
+def test_concurrency_two_is_bitwise_identical(bc):
+    from paper_1711_05075_b200.presets import correlator_kwargs
+    w = make_config("sweep", n_rot=40)
+    res = []
+    for conc in (0, 2):
+        c = bc.Correlator(**correlator_kwargs("sweep", w.N, w.h, w.t0, "real", concurrency=conc, max_batch=8))
+        c.shape_upload(0, w.A_xyzr, w.A_w)
+        c.shape_upload(1, w.B_xyzr, w.B_w)
+        c.spectrum_A()
+        res.append((c.correlate_rotations(w.R, "minmax"), c.correlate_rotations(w.R[[3, 17, 39]], "full")))
+        c.close()
+    assert np.array_equal(res[0][0], res[1][0])
+    assert np.array_equal(res[0][1], res[1][1])
+
+
+def test_complex_weights_exact_fp32(bc, oracle_mod):
+    w = random_small_case(63, n_a=12, n_b=9, n_rot=2, N=20, complex_weights=True)
+    c = bc.Correlator(N=w.N, h=w.h, t0=w.t0, mode="exact", precision="f32", weights="complex")
+    c.shape_upload(0, w.A_xyzr, w.A_w)
+    c.shape_upload(1, w.B_xyzr, w.B_w)
+    f = as_complex(c.correlate_rotations(w.R, "full"))
+    best = c.correlate_rotations(w.R, "max_real")
+    for r in range(w.n_rot):
+        ref = oracle_mod.correlate_grid(w.A_xyzr, w.A_w, w.B_xyzr, w.B_w, w.R[r], w.N, w.h, w.t0)
+        assert rel_max_err(f[r], ref) <= 1e-5
+        assert best[r]["val"] == pytest.approx(float(f[r].real.max()), abs=1e-6 * np.abs(ref).max())
+
+
+def test_odd_N_on_the_np256_generic_plan(bc, oracle_mod):
+    """N = 255 with Np = 256 on the generic plan (unpadded Hermitian rows of 129 modes): the
+    inverse z pass's ragged last tile holds an odd row count; the grid is the first 255^3
+    points of the N = 256 grid with the same t0, h."""
+    from paper_1711_05075_b200.presets import correlator_kwargs
+    w = make_config("sweep", n_rot=1)
+    fs = []
+    for N, generic in ((255, True), (256, False)):
+        c = bc.Correlator(**correlator_kwargs("sweep", N, w.h, w.t0, "real", generic_only=generic))
+        c.shape_upload(0, w.A_xyzr, w.A_w)
+        c.shape_upload(1, w.B_xyzr, w.B_w)
+        c.spectrum_A()
+        fs.append((c.correlate_rotations(w.R, "full")[0], c.correlate_rotations(w.R, "minmax")[0]))
+        c.close()
+    (f255, mm255), (f256, _) = fs
+    assert f255.shape == (255, 255, 255)
+    assert rel_max_err(f255, f256[:255, :255, :255]) <= 2e-5
+    assert mm255[1]["val"] == float(f255.max()) and mm255[0]["val"] == float(f255.min())
+    rng = np.random.default_rng(8)
+    idx = np.unique(np.concatenate([rng.choice(255 ** 3, 60, replace=False), [int(mm255[1]["idx"]), 255 ** 3 - 1]]))
+    ref = oracle_mod.correlate_points(w.A_xyzr, w.A_w, w.B_xyzr, w.B_w, w.R[0], 255, w.h, w.t0, idx)
+    assert np.abs(f255.reshape(-1)[idx] - ref).max() <= TOL_F32 * np.abs(ref).max()

@@ -15,8 +15,9 @@ from gpu_helpers import rel_max_err, as_complex, check_extremum
 pytestmark = pytest.mark.gpu
 
 # fp32 pipeline vs fp64 band-limited reference: spreading eps 1e-7 with the
-# Gaussian deconvolution gain and fp32 FFT rounding -> a few 1e-6 of max|f|.
-IMPL_TOL = 2e-5
+# Gaussian deconvolution gain, the blob window's alias level (<= 6e-6 of the band) and fp32
+# FFT rounding -> a few 1e-6 of max|f|; the SURVEY.md §8(c) fp32 bar is 1e-5.
+IMPL_TOL = 1e-5
 
 
 @pytest.fixture(scope="module")
