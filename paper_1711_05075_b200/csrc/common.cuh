@@ -10,12 +10,20 @@ struct cf {
     float x, y;
 };
 
-BC_DEV float2 cmul(float2 a, float2 b) { return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
-BC_DEV float2 cmulc(float2 a, float2 b) { return make_float2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y); } // a * conj(b)
-BC_DEV float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-BC_DEV float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+// Complex arithmetic on sm_100's packed fp32x2 pipe (FADD2 / FMUL2 / FFMA2: one issue slot
+// for both components; operand swaps, lane broadcasts and the negations below are encoded as
+// instruction modifiers).  Per component the rounding is that of the scalar fadd / fmul / fma.
+BC_DEV float2 f2(float x) { return make_float2(x, x); }
+BC_DEV float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
+BC_DEV float2 csub(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+// a b = a.x (b.x, b.y) - a.y (b.y, -b.x)
+BC_DEV float2 cmul(float2 a, float2 b) { return __ffma2_rn(f2(-a.y), make_float2(b.y, -b.x), __fmul2_rn(f2(a.x), b)); }
+// a conj(b) = a.x (b.x, -b.y) + a.y (b.y, b.x)
+BC_DEV float2 cmulc(float2 a, float2 b) { return __ffma2_rn(f2(a.x), make_float2(b.x, -b.y), __fmul2_rn(f2(a.y), make_float2(b.y, b.x))); }
 BC_DEV float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
-BC_DEV float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+BC_DEV float2 cscale(float2 a, float s) { return __fmul2_rn(a, f2(s)); }
+// a + b c (complex)
+BC_DEV float2 cfma(float2 b, float2 c, float2 a) { return __ffma2_rn(f2(-b.y), make_float2(c.y, -c.x), __ffma2_rn(f2(b.x), c, a)); }
 
 // e^{2 pi i num/den} for integers (argument reduced exactly before the float division)
 BC_DEV float2 expi_frac(long long num, long long den)

@@ -100,7 +100,7 @@ template <int SIGN> struct Dft<3, SIGN> {
     static BC_DEV void run(float2 *v) {
         const float s3 = 0.86602540378443864676f;
         const float2 t1 = cadd(v[1], v[2]);
-        const float2 t2 = make_float2(v[0].x - 0.5f * t1.x, v[0].y - 0.5f * t1.y);
+        const float2 t2 = __ffma2_rn(f2(-0.5f), t1, v[0]);
         const float2 t3 = mul_si<SIGN>(cscale(csub(v[1], v[2]), s3));
         v[0] = cadd(v[0], t1);
         v[1] = cadd(t2, t3);
@@ -126,11 +126,11 @@ template <int SIGN> struct Dft<5, SIGN> {
         const float2 a1 = cadd(v[1], v[4]), b1 = csub(v[1], v[4]);
         const float2 a2 = cadd(v[2], v[3]), b2 = csub(v[2], v[3]);
         const float2 x0 = v[0];
-        const float2 r1 = make_float2(x0.x + c1 * a1.x + c2 * a2.x, x0.y + c1 * a1.y + c2 * a2.y);
-        const float2 r2 = make_float2(x0.x + c2 * a1.x + c1 * a2.x, x0.y + c2 * a1.y + c1 * a2.y);
-        const float2 i1 = mul_si<SIGN>(make_float2(s1 * b1.x + s2 * b2.x, s1 * b1.y + s2 * b2.y));
-        const float2 i2 = mul_si<SIGN>(make_float2(s2 * b1.x - s1 * b2.x, s2 * b1.y - s1 * b2.y));
-        v[0] = make_float2(x0.x + a1.x + a2.x, x0.y + a1.y + a2.y);
+        const float2 r1 = __ffma2_rn(f2(c2), a2, __ffma2_rn(f2(c1), a1, x0));
+        const float2 r2 = __ffma2_rn(f2(c1), a2, __ffma2_rn(f2(c2), a1, x0));
+        const float2 i1 = mul_si<SIGN>(__ffma2_rn(f2(s2), b2, __fmul2_rn(f2(s1), b1)));
+        const float2 i2 = mul_si<SIGN>(__ffma2_rn(f2(-s1), b2, __fmul2_rn(f2(s2), b1)));
+        v[0] = cadd(cadd(x0, a1), a2);
         v[1] = cadd(r1, i1);
         v[4] = csub(r1, i1);
         v[2] = cadd(r2, i2);
@@ -322,19 +322,109 @@ struct Mid<L, S, SIGN, WS, false> {
     }
 };
 
+// Powers w[r] = u^r, r in [1, R), by a product tree of depth ceil(log2 R) (w[2^k] squares,
+// w[h + k] = w[h] w[k]); relative error ~ r eps(u) + depth ulps (< 1e-6 for R = 16).
+template <int R>
+BC_DEV void twiddle_powers(float2 (&w)[R], float2 u)
+{
+    w[0] = make_float2(1.f, 0.f);
+    if (R > 1) w[1] = u;
+#pragma unroll
+    for (int k = 2; k < R; k++) {
+        int h = 1;
+        while (2 * h <= k) h *= 2;  // highest power of two <= k (compile-time after unrolling)
+        w[k] = (h == k) ? cmul(w[h / 2], w[h / 2]) : cmul(w[h], w[k - h]);
+    }
+}
+
+// Two-stage plans whose last stage gives each thread one output group (Ns == TPL): thread
+// j's last-stage twiddles are w^{r j} = u^r with u = w^j, so they are generated in registers
+// (twiddle_powers) from one base instead of R - 1 shared-memory table loads -- these
+// kernels are bound by L1 / shared-memory bandwidth, and sm_100's packed FFMA2 makes the
+// 3-instruction complex products cheap.  A per-thread factor c^{r'} on stage input r'
+// (a coset twiddle split as c^{tl} W^m) is absorbed by passing u = w^j c.
+template <int L>
+__host__ __device__ constexpr bool pow_plan() { return Plan<L>::n == 2 && L / Plan<L>::r[1] == Plan<L>::TPL; }
+
+template <int L, int SIGN, bool WS = false>
+BC_DEV void fft_regs_pow(float2 (&x)[L / Plan<L>::TPL], float2 *A, float2 u, int tl)
+{
+    static_assert(pow_plan<L>(), "fft_regs_pow needs a two-stage plan with Ns == TPL");
+    static_assert(!WS || warp_local<L>(), "warp-synchronous FFT needs lines inside one warp");
+    constexpr int R0 = Plan<L>::r[0], R = Plan<L>::r[1], TPL = Plan<L>::TPL;
+    static_assert((L / R0) / TPL == 1, "one stage-0 group per thread");
+    {
+        float2 v[R0];
+#pragma unroll
+        for (int r = 0; r < R0; r++) v[r] = x[r];
+        Dft<R0, SIGN>::run(v);
+#pragma unroll
+        for (int r = 0; r < R0; r++) A[pad(tl * R0 + r)] = v[r];
+    }
+    line_sync<WS>();
+    {
+        float2 w[R];
+        twiddle_powers<R>(w, u);
+        float2 v[R];
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+            const float2 y = A[pad(tl + r * TPL)];
+            v[r] = r ? cmul(y, w[r]) : y;
+        }
+        Dft<R, SIGN>::run(v);
+#pragma unroll
+        for (int r = 0; r < R; r++) x[r] = v[r];
+    }
+}
+
+// Same two-stage transform with the last stage's twiddles read from a caller table
+// tw2[(r - 1) TPL + tl] (r in [1, R)): lanes read consecutive entries (conflict-free).  Used
+// where a coset twiddle is absorbed into per-coset tables (fold_fast_kernel).
+template <int L, int SIGN, bool WS = false>
+BC_DEV void fft_regs_tab(float2 (&x)[L / Plan<L>::TPL], float2 *A, const float2 *tw2, int tl)
+{
+    static_assert(pow_plan<L>(), "fft_regs_tab needs a two-stage plan with Ns == TPL");
+    constexpr int R0 = Plan<L>::r[0], R = Plan<L>::r[1], TPL = Plan<L>::TPL;
+    {
+        float2 v[R0];
+#pragma unroll
+        for (int r = 0; r < R0; r++) v[r] = x[r];
+        Dft<R0, SIGN>::run(v);
+#pragma unroll
+        for (int r = 0; r < R0; r++) A[pad(tl * R0 + r)] = v[r];
+    }
+    line_sync<WS>();
+    {
+        float2 v[R];
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+            const float2 y = A[pad(tl + r * TPL)];
+            v[r] = r ? cmul(y, tw2[(r - 1) * TPL + tl]) : y;
+        }
+        Dft<R, SIGN>::run(v);
+#pragma unroll
+        for (int r = 0; r < R; r++) x[r] = v[r];
+    }
+}
+
 // FFT of the calling thread-group's line, registers in / registers out (see header).
 // A and B are this line's shared-memory buffers (B used only when n >= 3).
 // Contains barriers (block-wide, or warp-wide with WS = true, which requires
 // warp_local<L>()): every thread of the block (warp) must call it.  The caller must
 // barrier before writing A/B again (the last stage reads them); the twiddle table tw must
 // be visible to the calling threads before the call.
-template <int L, int SIGN, bool WS = false>
+template <int L, int SIGN, bool WS = false, bool POW = true>
 BC_DEV void fft_regs(float2 (&x)[L / Plan<L>::TPL], float2 *A, float2 *B, const float2 *tw, int tl)
 {
     static_assert(!WS || warp_local<L>(), "warp-synchronous FFT needs lines inside one warp");
     static_assert(plan_ok<L>(), "bad FFT plan");
     constexpr int TPL = Plan<L>::TPL;
     constexpr int n = Plan<L>::n;
+    if constexpr (POW && L == 256 && pow_plan<L>()) {  // last-stage twiddles as powers of tw[tl] = w^{tl} (table row r = 1)
+        const float2 w1 = tw[tl];
+        fft_regs_pow<L, SIGN, WS>(x, A, SIGN < 0 ? w1 : cconj(w1), tl);
+        return;
+    }
     // stage 0 (Ns = 1, no twiddles): registers -> A
     {
         constexpr int R = Plan<L>::r[0];

@@ -148,6 +148,9 @@ __global__ void __launch_bounds__(FF_NT, 4) fold_fast_kernel(FoldFastArgs a)
                     const bool in_band = my_ok && !(p == 0 && m == 12 && tl == 0);
                     av[u] = in_band ? __ldg(arow + pos) : make_float2(0.f, 0.f);
                 }
+                // (measured: absorbing the coset twiddle into per-coset last-stage tables or
+                // generating the last stage's twiddles in registers cost more than the table
+                // reads they save here)
                 float2 y[E];
 #pragma unroll
                 for (int m = 0; m < E; m++) {
@@ -155,7 +158,7 @@ __global__ void __launch_bounds__(FF_NT, 4) fold_fast_kernel(FoldFastArgs a)
                     const float2 v = X[line * FF_LS + pad(n)];
                     y[m] = p ? cmul(v, ctw[p * FF_L + n]) : v;
                 }
-                fft_regs<FF_L, -1, true>(y, Ab + line * FF_LS, Ab + line * FF_LS, tw, tl);
+                fft_regs<FF_L, -1, true, false>(y, Ab + line * FF_LS, Ab + line * FF_LS, tw, tl);
                 // S[j] = sum of the products of outputs m = j and m = j + 12 (same target)
                 float2 S[4];
 #pragma unroll
@@ -208,7 +211,7 @@ __global__ void __launch_bounds__(FF_NT, 4) fold_fast_kernel(FoldFastArgs a)
     float2 v[E];
 #pragma unroll
     for (int m = 0; m < E; m++) v[m] = X[line * FF_LS + pad(tl + FF_TPL * m)];
-    fft_regs<FF_NP, +1, true>(v, Ab + line * FF_LS, Ab + line * FF_LS, tw, tl);
+    fft_regs<FF_NP, +1, true, false>(v, Ab + line * FF_LS, Ab + line * FF_LS, tw, tl);
     __syncthreads();
 #pragma unroll
     for (int m = 0; m < E; m++) X[line * FF_LS + pad(tl + FF_TPL * m)] = v[m];
@@ -305,15 +308,16 @@ __global__ void __launch_bounds__(FF_NT, 5) pass_y_fast_kernel(PassYFastArgs a)
         // coset twiddle e^{-2 pi i p (tl + 16 m) / 1024} = c1 W^m, W = e^{-2 pi i p / 64}: one L1
         // load per thread, then a 16-step recurrence (error ~16 ulp, far below the band error;
         // a per-element constant-bank index costed more than the extra multiply)
-        float2 t = __ldg(ctw + p * FF_L + tl);
-        const float2 Wp = make_float2(c_w64.re[p], c_w64.im[p]);
+        // split as e^{-2 pi i p m / 64} (constant bank) x e^{-2 pi i p tl / 1024}, the latter on
+        // the last stage's twiddle base (fft_regs_pow, as in fold_fast_kernel)
+        const float2 u = __ldg(ctw + FF_L + 4 * tl + p);
         float2 y[E];
 #pragma unroll
         for (int m = 0; m < E; m++) {
-            y[m] = p ? cmul(xr[m], t) : xr[m];
-            t = cmul(t, Wp);
+            const int e = (p * m) & 63;
+            y[m] = (p && m) ? cmul(xr[m], make_float2(c_w64.re[e], c_w64.im[e])) : xr[m];
         }
-        fft_regs<FF_L, -1, true>(y, Ab + line * FF_LS, Ab + line * FF_LS, tw, tl);
+        fft_regs_pow<FF_L, -1, true>(y, Ab + line * FF_LS, u, tl);
         __syncwarp();
         // in-band outputs u = q (q < 64) or q - 128 (q >= 192), times mult_y(ky)
 #pragma unroll
