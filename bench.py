@@ -5,10 +5,15 @@ config the north_star metric is quoted on), per-rotation (min, argmin).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-One process per GPU (torchrun for N > 1, NCCL).  A step = one pass of the whole
-path (spread -> box DFT -> spectral product/fold -> inverse FFT -> reduction) over
-the rank's batch of rotations; each rank owns its own batch (weak scaling, no
-data-path collective).  Rank 0 prints one JSON line.
+One process per GPU (torchrun for N > 1, NCCL; `--gpus N` without a torchrun
+environment re-launches itself under torch.distributed.run).  A step = one pass of
+the whole path (spread -> box DFT -> spectral product/fold -> inverse FFT ->
+reduction) over the config's 512 rotations, sharded over the ranks in contiguous
+blocks (sharding.rotation_block; strong scaling), followed by the
+all-gather of the per-rotation (min, argmin) records -- T includes it (SURVEY.md
+§8(d)).  `--scaling weak` keeps the rank's block at the full rotation count instead.
+Rank 0 prints one JSON line.  `--dry-run` runs the same launcher and protocol on CPU
+(gloo, a stand-in correlator; tests/test_bench_launcher.py).
 
 `--impl reference` times the fp64 CPU oracle (oracle/, the only other place
 this script executes it) on a bounded sample of the same workload.
@@ -33,6 +38,8 @@ from synth import make_config, random_rotations  # noqa: E402
 
 WORKLOAD = "sweep"
 METRIC = "translations*rotations/s"
+# bc_extremum (include/ballcorr.h): {double val; int64 idx}
+REC_DTYPE = np.dtype([("val", np.float64), ("idx", np.int64)])
 
 
 def parse():
@@ -49,6 +56,11 @@ def parse():
     ap.add_argument("--cpu-slabs", type=int, default=0, help="x-slabs of the grid in the oracle sample (0 = per config)")
     ap.add_argument("--max-batch", type=int, default=0, help="rotations per launch (0 = library default)")
     ap.add_argument("--concurrency", type=int, default=0, help="batches in flight (0 = library default)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: the config's rotations sharded over the ranks (headline); weak: every rank "
+                         "correlates its own full rotation set")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU-only launcher/protocol check: gloo, stand-in correlator, no CUDA")
     args = ap.parse_args()
     if args.cpu_slabs <= 0:
         args.cpu_slabs = CPU_SLABS[args.workload]
@@ -116,13 +128,21 @@ class ClockSampler:
 # ----------------------------------------------------------------------------- algorithmic bytes
 
 def stage_work(q, N, Np, K, complex_w):
-    """Algorithmic work per rotation of each kernel of the spectral path:
-    compulsory bytes (input read once + output written once) and FP32 flops
-    (5 n log2 n per complex n-point FFT, 6 per complex multiply, 2 per complex add,
-    30 per window-profile evaluation of a spread cell)."""
+    """Algorithmic work per rotation of each kernel of the spectral path.
+
+    Bytes: SURVEY.md §8(d)'s per-unit figures wherever the kernel carries a §8(d) step --
+    the fold (a5: spectral product + fold) moves A's band spectrum (read once per rotation,
+    8 M_b bytes, M_b = M^3 / 2 modes for real weights) and writes the folded product
+    (8 N_pb, N_pb = Np^3 / 2); the last pass (a6 + a7) reads the folded/inverse-transformed
+    rows and writes f or nothing (reductions).  Multi-pass FFT intermediates (T1, T2, X1, Y1)
+    are implementation traffic, excluded by §8(d); they are listed separately as
+    `impl_bytes` (compulsory read + write of each kernel's own input and output).
+    Flops (FP32 view): 5 n log2 n per complex n-point FFT, 6 per complex multiply, 2 per
+    complex add, 30 per window-profile evaluation of a spread cell."""
     M = 2 * K + 1
     Kz = M if complex_w else K + 1
     Fz = Np if complex_w else Np // 2 + 1
+    half = 1 if complex_w else 2
     L, c = int(q("L_B")), int(q("c_B"))
     lg = math.log2
     fft = lambda n: 5.0 * n * lg(n)
@@ -133,22 +153,24 @@ def stage_work(q, N, Np, K, complex_w):
     F = Np * Np * Fz * 8
     X1 = N * Np * Fz * 8
     Y1 = N * N * Fz * 8
+    a5 = 8 * M ** 3 / half + 8 * Np ** 3 / half       # §8(d): A band read + folded product write
     axis = lambda lines: lines * c * (fft(L) + 6 * L)       # c coset transforms + coset twiddles
     tiles = q("live_tiles_B")
     spread_z_flops = 30 * q("spread_cells_B") + tiles * 8 * axis(1) + tiles * 16 * Kz * 8
     fold_flops = axis(M * Kz) + 8.0 * M * M * Kz + Np * Fz * fft(Np)
+    # name: (§8(d) algorithmic bytes or None, implementation bytes, flops)
     return {
-        "spread_z_B": (T1, spread_z_flops),            # fused spread + z transform: write T1
-        "pass_y_fast": (T1 + T2, axis(L * Kz) + 6.0 * L * M * Kz),
-        "fold_fast": (T2 + Bh + X1, fold_flops),       # read T2 and A's band, write X1
-        "fold_x_inv": (T2 + Bh + X1, fold_flops),
-        "spread_B": (box, 30 * q("spread_cells_B")),
-        "pass_z_B": (box + T1, axis(L * L)),
-        "pass_y_B": (T1 + T2, axis(L * Kz) + 6.0 * L * M * Kz),
-        "fold_x": (T2 + Bh + F, axis(M * Kz) + 8.0 * M * M * Kz),
-        "inv_x": (F + X1, Np * Fz * fft(Np)),
-        "inv_y": (X1 + Y1, N * Fz * fft(Np)),
-        "inv_z_reduce": (Y1, (N * N / 2) * fft(Np) + N ** 3),
+        "spread_z_B": (None, T1, spread_z_flops),          # fused spread + z transform: write T1
+        "pass_y_fast": (None, T1 + T2, axis(L * Kz) + 6.0 * L * M * Kz),
+        "fold_fast": (a5, T2 + Bh + X1, fold_flops),       # read T2 and A's band, write X1
+        "fold_x_inv": (a5, T2 + Bh + X1, fold_flops),
+        "spread_B": (None, box, 30 * q("spread_cells_B")),
+        "pass_z_B": (None, box + T1, axis(L * L)),
+        "pass_y_B": (None, T1 + T2, axis(L * Kz) + 6.0 * L * M * Kz),
+        "fold_x": (a5, T2 + Bh + F, axis(M * Kz) + 8.0 * M * M * Kz),
+        "inv_x": (None, F + X1, Np * Fz * fft(Np)),
+        "inv_y": (None, X1 + Y1, N * Fz * fft(Np)),
+        "inv_z_reduce": (None, Y1, (N * N / 2) * fft(Np) + N ** 3),
     }
 
 
@@ -162,13 +184,25 @@ STAGE_KERNEL = {"fold_fast": "fold_fast_kernel", "spread_z_B": "spread_z_kernel"
                 "inv_y": "pass_kernel", "inv_z_reduce": "last_tma_kernel"}
 
 
+TRAFFIC_FILES = ("profiles/r2/ncu_traffic.json", "profiles/r1/ncu_traffic.json")
+
+
+def _traffic_file():
+    for rel in TRAFFIC_FILES:
+        path = os.path.join(ROOT, rel)
+        if os.path.exists(path):
+            return rel, json.load(open(path))
+    return None, None
+
+
 def ncu_traffic(stage, rotations, workload="sweep"):
-    """DRAM bytes per launch of `stage` from the committed ncu --set full capture of the sweep
-    (profiles/r1/ncu_traffic.json, per rotation), or None."""
+    """DRAM bytes per launch of `stage` (dram__bytes_read.sum + dram__bytes_write.sum) from the
+    committed ncu --set full capture of the sweep at the bench's own rotations per launch
+    (profiles/r2/ncu_traffic.json; per rotation x rotations per launch), or None."""
     if workload != "sweep":
         return None
+    rel, d = _traffic_file()
     try:
-        d = json.load(open(os.path.join(ROOT, "profiles", "r1", "ncu_traffic.json")))
         return d["dram_bytes_per_rotation"][STAGE_KERNEL[stage]] * rotations
     except Exception:
         return None
@@ -190,9 +224,9 @@ def path_roofline(N, Np, K, complex_w, rot_per_s, peak):
     try:
         if (N, Np, K, complex_w) != (256, 256, 255, False):
             raise ValueError("the committed ncu capture is the sweep's")
-        d = json.load(open(os.path.join(ROOT, "profiles", "r1", "ncu_traffic.json")))
+        rel, d = _traffic_file()
         dram = sum(d["dram_bytes_per_rotation"].values())
-        out.update({"dram_bytes_per_rot": dram, "R1_dram_frac": dram * rot_per_s / 1e9 / peak})
+        out.update({"dram_bytes_per_rot": dram, "R1_dram_frac": dram * rot_per_s / 1e9 / peak, "dram_source": rel})
     except Exception:
         pass
     return out
@@ -264,63 +298,175 @@ def run_reference(args, rank, world):
 
 # ----------------------------------------------------------------------------- our path
 
+class _DryCorrelator:
+    """--dry-run stand-in for ballcorr.Correlator (CPU, no CUDA): deterministic per-rotation
+    extremum records (a function of the rotation matrix only), so that any sharding of the
+    rotations must reproduce the single-rank records exactly."""
+
+    def __init__(self):
+        self._launches = 0
+
+    def correlate_rotations(self, R, kind, out=None, stream=None):
+        R = np.asarray(R.cpu() if hasattr(R, "cpu") else R, dtype=np.float64).reshape(-1, 9)
+        rec = np.zeros(len(R), dtype=REC_DTYPE)
+        rec["val"] = (R * np.arange(1, 10)).sum(axis=1)
+        rec["idx"] = (np.abs(R[:, 0]) * 1e6).astype(np.int64)
+        self._launches += 1
+        buf = np.frombuffer(rec.tobytes(), dtype=np.uint8)
+        out[: buf.size].copy_(__import__("torch").from_numpy(buf.copy()))
+        return out
+
+    def launch_count(self):
+        return self._launches
+
+
+def gather_records(out_local, n_local, cap, world, dev):
+    """All-gather of the ranks' per-rotation records (16-byte bc_extremum each, padded to
+    `cap` rotations per rank) into one [world * cap * 16] byte tensor on `dev` (NCCL over
+    NVLink on the GPU box, gloo on CPU); rank r's block sits at [r * cap, r * cap + n_r)."""
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return out_local
+    send = out_local if n_local == cap else torch.cat(
+        [out_local, torch.zeros((cap - n_local) * 16, dtype=torch.uint8, device=dev)])
+    recv = torch.empty(world * cap * 16, dtype=torch.uint8, device=dev)
+    dist.all_gather(list(recv.chunk(world)), send)
+    return recv
+
+
+def unpack_global(recv, n_rot, world):
+    """Global rotation-order records from gather_records' buffer."""
+    from paper_1711_05075_b200.sharding import rotation_block
+    raw = np.frombuffer(recv.cpu().numpy().tobytes(), dtype=REC_DTYPE)
+    if world == 1:
+        return raw[:n_rot]
+    cap = -(-n_rot // world)
+    out = np.empty(n_rot, dtype=REC_DTYPE)
+    for r in range(world):
+        s0, e0 = rotation_block(n_rot, r, world)
+        out[s0:e0] = raw[r * cap: r * cap + (e0 - s0)]
+    return out
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
-    from paper_1711_05075_b200 import ballcorr
     from paper_1711_05075_b200.presets import correlator_kwargs
+    from paper_1711_05075_b200.sharding import rotation_block, global_best
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    dry = args.dry_run
+    if not dry:
+        from paper_1711_05075_b200 import ballcorr
+    dev = torch.device("cpu") if dry else torch.device("cuda", local_rank)
+    if not dry:
+        torch.cuda.set_device(local_rank)
     w = make_config(args.workload, n_rot=args.rot_per_rank or None)
-    R = w.R if rank == 0 else random_rotations(np.random.default_rng((0, rank)), w.n_rot)
+    n_all = w.n_rot
+    if args.scaling == "strong":
+        s0, e0 = rotation_block(n_all, rank, world)
+        R = w.R[s0:e0]
+        units_per_step = n_all            # the whole job: the config's rotations once
+    else:
+        R = w.R if rank == 0 else random_rotations(np.random.default_rng((0, rank)), n_all)
+        s0, e0 = 0, n_all
+        units_per_step = n_all * world
     n_rot = len(R)
+    cap = -(-n_all // world) if args.scaling == "strong" else n_all
     kw = correlator_kwargs(w.name, w.N, w.h, w.t0, w.weights, max_batch=args.max_batch,
                            concurrency=args.concurrency)
-    ctx = ballcorr.Correlator(device=local_rank, **kw)
-    stream = torch.cuda.current_stream(dev)
     t = time.perf_counter()
-    ctx.shape_upload(0, w.A_xyzr, w.A_w)
-    ctx.shape_upload(1, w.B_xyzr, w.B_w)
-    if world > 1:  # rank 0 computes A's spectrum, NCCL broadcasts it (north_star)
-        from paper_1711_05075_b200.sharding import broadcast_spectrum_A
-        broadcast_spectrum_A(ctx, src=0)
+    if dry:
+        ctx = _DryCorrelator()
+        stream = None
     else:
-        ctx.spectrum_A(stream=stream)
-    torch.cuda.synchronize()
+        ctx = ballcorr.Correlator(device=local_rank, **kw)
+        stream = torch.cuda.current_stream(dev)
+        ctx.shape_upload(0, w.A_xyzr, w.A_w)
+        ctx.shape_upload(1, w.B_xyzr, w.B_w)
+        if world > 1:  # rank 0 computes A's spectrum, NCCL broadcasts it (north_star)
+            from paper_1711_05075_b200.sharding import broadcast_spectrum_A
+            broadcast_spectrum_A(ctx, src=0)
+        else:
+            ctx.spectrum_A(stream=stream)
+        torch.cuda.synchronize()
     setup_s = time.perf_counter() - t
 
     kind = w.output  # sweep: min_argmin; docking: max_real; the others: the full field
-    _, oshape, odt = ctx.out_shape(n_rot, kind)
-    out_bytes = int(np.prod(oshape)) * np.dtype(odt).itemsize
+    reduced = kind != "full"
+    if dry:
+        out_bytes = n_rot * 16
+    else:
+        _, oshape, odt = ctx.out_shape(n_rot, kind)
+        out_bytes = int(np.prod(oshape)) * np.dtype(odt).itemsize
     R_dev = torch.tensor(R, dtype=torch.float64, device=dev)
-    out = torch.empty(out_bytes, dtype=torch.uint8, device=dev)
-    for _ in range(args.warmup):
-        ctx.correlate_rotations(R_dev, kind, out=out, stream=stream)
-    torch.cuda.synchronize()
+    out = torch.empty(max(out_bytes, 16), dtype=torch.uint8, device=dev)
 
-    sampler = ClockSampler(local_rank)
-    sampler.start()
-    time.sleep(0.3)
-    l0 = ctx.launch_count()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    e0.record(stream)
-    for _ in range(args.steps):
+    def step():
         ctx.correlate_rotations(R_dev, kind, out=out, stream=stream)
-    e1.record(stream)
-    torch.cuda.synchronize()
+        if reduced:  # the per-rotation results of every rank, in global order, on every rank
+            return gather_records(out[:out_bytes], n_rot, cap, world if args.scaling == "strong" else 1, dev)
+        return out
+
+    def sync():
+        if not dry:
+            torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    sync()
+
+    sampler = None if dry else ClockSampler(local_rank)
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    l0 = ctx.launch_count()
     if world > 1:
         dist.barrier()
-    ms = e0.elapsed_time(e1)
+    sync()
+    if dry:
+        t0 = time.perf_counter()
+    else:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+    for _ in range(args.steps):
+        glob = step()
+    if dry:
+        ms = (time.perf_counter() - t0) * 1e3
+    else:
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+    if world > 1:
+        dist.barrier()
     launches = ctx.launch_count() - l0
-    clocks = sampler.stop()
+    clocks = sampler.stop() if sampler else None
+    t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    ms_max = float(t_max.item())
+    value = units_per_step * w.N ** 3 * args.steps / (ms_max / 1e3)
+    best = None
+    if reduced and args.scaling == "strong":
+        recs = unpack_global(glob, n_all, world)
+        best = global_best(recs["val"], recs["idx"], "min" if kind == "min_argmin" else "max")
+        best = {"rotation": best[0], "value": best[1], "translation_index": best[2],
+                "records_sha1": __import__("hashlib").sha1(recs.tobytes()).hexdigest()}
+
+    if dry:
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "value": value, "unit": METRIC, "n_gpus": world, "steps": args.steps,
+                              "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                              "scaling": args.scaling, "dry_run": True, "gpu_launches": 0,
+                              "config": {"workload": w.name, "rotations_per_step": n_all,
+                                         "rotations_per_rank": [rotation_block(n_all, r, world)
+                                                                for r in range(world)]},
+                              "result_sample": {"global_best": best}}), flush=True)
+        return
+
     # per-stage device times: one more (untimed) step with the library's per-launch CUDA
-    # events on; profiling serialises the batches (no concurrent slots), so shares refer to
-    # this profiled step
+    # events on (profiling serialises the batches), so shares refer to this profiled step
     ctx.set_profiling(True)
     ctx.reset_stage_times()
     p0 = torch.cuda.Event(enable_timing=True)
@@ -332,23 +478,9 @@ def run_ours(args, rank, world, local_rank):
     prof_ms = p0.elapsed_time(p1)
     stages = ctx.stage_times()
     ctx.set_profiling(False)
-    t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    ms_max = float(t_max.item())
-    res = np.frombuffer(out.cpu().numpy().tobytes(), dtype=ballcorr.EXTREMUM_DTYPE) if kind != "full" else None
 
-    units = n_rot * w.N ** 3 * args.steps * world
-    value = units / (ms_max / 1e3)
-
-    # gather the per-rotation (min, argmin) of all ranks (outside the timed region)
-    best = None
-    if world > 1 and res is not None:
-        from paper_1711_05075_b200.sharding import gather_extrema, global_best
-        vals, idxs = gather_extrema(res["val"], res["idx"], n_rot * world, device=dev)
-        best = global_best(vals, idxs, "min" if kind == "min_argmin" else "max")
-
-    # e2e through the public API with host buffers (pinned), copies inside the timed region
+    # e2e through the public API with host buffers (pinned): the H2D copy of the rank's R block
+    # and the D2H read of its results happen inside the call, inside the timed region
     R_host = torch.tensor(R, dtype=torch.float64).pin_memory()
     out_host = torch.empty(out_bytes, dtype=torch.uint8).pin_memory()
     ctx.correlate_rotations(R_host, kind, out=out_host, stream=stream)
@@ -365,54 +497,56 @@ def run_ours(args, rank, world, local_rank):
     e2e_ms = torch.tensor([h0.elapsed_time(h1)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
-    e2e_value = n_rot * w.N ** 3 * args.e2e_steps * world / (float(e2e_ms.item()) / 1e3)
+    e2e_value = units_per_step * w.N ** 3 * args.e2e_steps / (float(e2e_ms.item()) / 1e3)
 
     if rank != 0:
         return
-    # roofline of the dominant kernel (largest share of device time in the timed region):
-    # HBM-bound if its algorithmic flop/byte is below the FP32 ridge, else ALU-bound
     q = ctx.query
     spectral = kw["mode"] == "spectral"
     work = stage_work(q, w.N, kw["Np"], kw["K"], w.weights == "complex") if spectral else {}
     peak, peak_kind = measured_peaks()
     alu_peak = alu_peak_tflops()
-    ridge = alu_peak * 1e12 / (peak * 1e9)
     batch = int(q("batch")) if spectral else 1
     per_stage = {}
     for name, (tot_ms, nl) in stages.items():
         if name not in work:
             continue
-        by, fl = work[name]
+        alg, impl, fl = work[name]
         avg_s = tot_ms / nl / 1e3
         per_stage[name] = {"ms_per_rot": tot_ms / n_rot, "share": tot_ms / prof_ms,
-                           "hbm_GBps": by * batch / avg_s / 1e9, "hbm_frac": by * batch / avg_s / 1e9 / peak,
-                           "fp32_TFLOPs": fl * batch / avg_s / 1e12, "alu_frac": fl * batch / avg_s / 1e12 / alu_peak,
-                           "flop_per_byte": fl / by}
+                           "alg_bytes_per_rot": alg,
+                           "hbm_frac_alg": None if alg is None else alg * batch / avg_s / 1e9 / peak,
+                           "impl_GBps": impl * batch / avg_s / 1e9, "hbm_frac_impl": impl * batch / avg_s / 1e9 / peak,
+                           "fp32_TFLOPs": fl * batch / avg_s / 1e12, "alu_frac": fl * batch / avg_s / 1e12 / alu_peak}
     roof = None
     if per_stage:
         name = max(per_stage, key=lambda k: per_stage[k]["share"])
         st = per_stage[name]
         tot_ms, nl = stages[name]
-        by, fl = work[name]
-        alu = fl / by > ridge
-        roof = {"bound": "alu" if alu else "hbm", "kernel": name,
-                "achieved": st["fp32_TFLOPs"] if alu else st["hbm_GBps"],
-                "peak": alu_peak if alu else peak, "unit": "TFLOP/s" if alu else "GB/s",
-                "frac": st["alu_frac"] if alu else st["hbm_frac"], "traffic": ncu_traffic(name, batch, w.name),
-                "traffic_source": "profiles/r1/ncu_traffic.json (ncu --set full, dram__bytes_read.sum + "
-                                  "dram__bytes_write.sum per rotation x rotations per launch)",
-                "peak_source": ("derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz" if alu else peak_kind),
-                "alg_bytes_per_launch": by * batch, "alg_flops_per_launch": fl * batch,
+        alg, impl, fl = work[name]
+        by = alg if alg is not None else impl
+        achieved = by * batch / (tot_ms / nl / 1e3) / 1e9
+        traffic = ncu_traffic(name, batch, w.name)
+        roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "bytes_basis": ("SURVEY.md §8(d) a5: A band read 8*M^3/2 + folded product write 8*Np^3/2 per "
+                                "rotation x rotations per launch" if alg is not None else "kernel input + output"),
+                "alg_bytes_per_launch": by * batch, "rotations_per_launch": batch,
                 "avg_launch_ms": tot_ms / nl, "share_of_step": st["share"],
-                "hbm_view": {"achieved_GBps": st["hbm_GBps"], "peak_GBps": peak, "frac": st["hbm_frac"]},
-                "ridge_flop_per_byte": ridge}
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (%s)" % peak_kind,
+                "traffic_source": (_traffic_file()[0] or "none") + " (ncu --set full, dram__bytes_read.sum + "
+                                  "dram__bytes_write.sum per rotation x rotations per launch)",
+                "impl_view": {"bytes_per_launch": impl * batch, "GBps": st["impl_GBps"], "frac": st["hbm_frac_impl"],
+                              "note": "compulsory read+write of the kernel's own input/output incl. FFT intermediates"},
+                "alu_view": {"fp32_TFLOPs": st["fp32_TFLOPs"], "peak_TFLOPs": alu_peak, "frac": st["alu_frac"],
+                             "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz"}}
     cpu = None
     rel_err = None
     if world == 1 and not args.no_cpu_baseline:
-        cpu, (f_ref, x0, x1) = cpu_oracle_sample(w, R[0], args.cpu_slabs)
+        cpu, (f_ref, x0, x1) = cpu_oracle_sample(w, w.R[0], args.cpu_slabs)
         # the metric's third part (BASELINE.json: "rel max error"): this GPU run's full f of the
         # same rotation (outside the timed region) against the oracle on the sampled slabs
-        f_gpu = ctx.correlate_rotations(R[:1], "full")[0][x0:x1]
+        f_gpu = ctx.correlate_rotations(w.R[:1], "full")[0][x0:x1]
         if w.weights == "complex":
             f_gpu = f_gpu[..., 0] + 1j * f_gpu[..., 1]
         tol = 1e-9 if kw["precision"] == "f64" else 1e-4
@@ -422,32 +556,50 @@ def run_ours(args, rank, world, local_rank):
     line = {
         "metric": METRIC, "value": value, "unit": METRIC, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": kw["precision"], "data": "synthetic",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": kw["precision"], "data": "synthetic",
         "config": {"workload": w.name, "N": w.N, "n_A": len(w.A_xyzr), "n_B": len(w.B_xyzr),
-                   "rotations_per_rank_per_step": n_rot, "mode": kw["mode"], "Np": kw["Np"], "K": kw["K"],
-                   "output": kind, "l2": l2_note(w, kw),
+                   "rotations_per_step": units_per_step, "rotations_per_rank": n_rot,
+                   "mode": kw["mode"], "Np": kw["Np"], "K": kw["K"], "output": kind, "l2": l2_note(w, kw),
+                   "timed": ("per step: every rank correlates its rotation block, then the NCCL all-gather of "
+                             "the per-rotation records (strong scaling, SURVEY.md §8(d)-(e))"
+                             if args.scaling == "strong" else "per step: every rank its own full rotation set"),
                    "setup_s": setup_s,
                    "spectrum_A": "rank 0, NCCL broadcast" if world > 1 else "computed"},
         "clocks": clocks,
         "gpu_launches": launches,
         "e2e": {"value": e2e_value, "unit": METRIC, "h2d_bytes_per_step": int(R.size * 8),
-                "d2h_bytes_per_step": out_bytes},
+                "d2h_bytes_per_step": out_bytes,
+                "note": "bc_correlate_rotations with pinned host R and host out (copies inside the call); "
+                        "per rank, max over ranks, without the all-gather"},
         "roofline": roof,
         "path_roofline": path_roofline(w.N, kw["Np"], kw["K"], w.weights == "complex",
-                                       n_rot * args.steps / (ms_max / 1e3), peak) if spectral else None,
+                                       units_per_step * args.steps / (ms_max / 1e3) / world, peak) if spectral else None,
         "cpu_baseline": cpu,
         "rel_max_error": rel_err,
         "stages_ms_per_step": {k: v[0] for k, v in stages.items()},
         "profiled_step_ms": prof_ms,
         "stages": per_stage,
-        "result_sample": None if res is None else {"rot0_val": float(res[0]["val"]), "rot0_idx": int(res[0]["idx"]),
-                                                   "global_best": best},
+        "result_sample": {"global_best": best},
     }
     print(json.dumps(line), flush=True)
 
 
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N` outside torchrun: one process per GPU under torch.distributed.run
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -457,8 +609,9 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl")
+        if not args.dry_run:
+            torch.cuda.set_device(local_rank)
+        dist.init_process_group("gloo" if args.dry_run else "nccl")
     try:
         run_ours(args, rank, world, local_rank)
     finally:
