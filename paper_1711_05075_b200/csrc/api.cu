@@ -119,8 +119,10 @@ struct bc_ctx {
     int64_t rot_cap = 0;
     void *d_out_stage = nullptr;
     size_t out_stage_bytes = 0;
-    double *d_acc = nullptr;
+    void *d_acc = nullptr;          // exact mode: fixed-point accumulators (exact.cu)
     size_t acc_bytes = 0;
+    bool ex_ready = false;          // exact_plan() for the current shapes
+    double ex_qscale = 1.0;
     double *d_part = nullptr;
     long long *d_part_idx = nullptr;
     int part_cap = 0;
@@ -1125,6 +1127,25 @@ bc_status run_query(bc_ctx *ctx, int nq, double *dst, cudaStream_t s)
     return BC_OK;
 }
 
+// Exact mode's fixed-point scale (exact.cu): 2^61 / B with B = min(|A|_inf |B|_1, |A|_1 |B|_inf)
+// >= max |f| (|f| <= |rho_A|_inf |rho_B|_1 and symmetrically; |rho|_inf <= sum |w|, |rho|_1 =
+// sum |w| vol), so no partial sum can overflow int64.
+bc_status exact_plan(bc_ctx *ctx)
+{
+    if (ctx->ex_ready) return BC_OK;
+    double sAi = 0, sA1 = 0, sBi = 0, sB1 = 0;
+    for (int w = 0; w < 2; w++)
+        for (int64_t i = 0; i < ctx->n[w]; i++) {
+            const double m = std::hypot(ctx->hw[w][2 * i], ctx->hw[w][2 * i + 1]), r = ctx->hxyzr[w][4 * i + 3];
+            (w ? sBi : sAi) += m;
+            (w ? sB1 : sA1) += m * 4.0 / 3.0 * kPi * r * r * r;
+        }
+    const double bound = std::min(sAi * sB1, sA1 * sBi);
+    ctx->ex_qscale = bound > 0 ? std::ldexp(1.0, 61) / bound : 1.0;
+    ctx->ex_ready = true;
+    return BC_OK;
+}
+
 // The per-rotation path for n_rot rotations already prepared in ctx->d_rot (fp32) and
 // ctx->d_rot64 (fp64), written to the device buffer dout (out_per bytes per rotation).
 bc_status run_rotations(bc_ctx *ctx, int64_t n_rot, int out_kind, char *dout, size_t out_per, cudaStream_t s)
@@ -1132,8 +1153,9 @@ bc_status run_rotations(bc_ctx *ctx, int64_t n_rot, int out_kind, char *dout, si
     const bool cplx = ctx->p.weights == BC_WEIGHTS_COMPLEX;
     const long long N = ctx->p.N, N3 = N * N * N;
     if (ctx->p.mode == BC_MODE_EXACT) {
+        TRY(exact_plan(ctx));
         int nb = ctx->p.max_batch > 0 ? ctx->p.max_batch : 8;
-        const size_t per = (size_t)N3 * (cplx ? 2 : 1) * sizeof(double);
+        const size_t per = (size_t)N3 * (cplx ? 2 : 1) * sizeof(long long);
         while (nb > 1 && per * nb > ((size_t)4 << 30)) nb /= 2;
         nb = (int)std::min<int64_t>(nb, n_rot);
         if (ctx->acc_bytes < per * nb) {
@@ -1153,6 +1175,7 @@ bc_status run_rotations(bc_ctx *ctx, int64_t n_rot, int out_kind, char *dout, si
             a.nB = (int)ctx->n[1];
             a.N = (int)N;
             a.h = ctx->p.h;
+            a.inv_h = 1.0 / ctx->p.h;
             a.t0x = ctx->p.t0[0];
             a.t0y = ctx->p.t0[1];
             a.t0z = ctx->p.t0[2];
@@ -1163,19 +1186,21 @@ bc_status run_rotations(bc_ctx *ctx, int64_t n_rot, int out_kind, char *dout, si
             a.rot = ctx->d_rot64 + 9 * r0;
             a.complex_w = cplx;
             a.fp64 = ctx->p.precision == BC_FP64;
-            a.acc = ctx->d_acc;
-            a.acc_bstride = (long long)(per / sizeof(double));
+            a.iacc = (long long *)ctx->d_acc;
+            a.acc_bstride = (long long)(per / sizeof(long long));
+            a.qscale = ctx->ex_qscale;
             {
                 StageScope sc(ctx, s, "exact_pairs");
-                launch_exact(a, b, s);
+                launch_exact_scatter(a, b, s);
                 ctx->launches++;
             }
             ExactOutArgs o{};
             o.N = (int)N;
             o.complex_w = cplx;
             o.fp64 = a.fp64;
-            o.acc = ctx->d_acc;
+            o.iacc = a.iacc;
             o.acc_bstride = a.acc_bstride;
+            o.inv_qscale = 1.0 / ctx->ex_qscale;
             o.out_kind = out_kind;
             o.out = dout + out_per * r0;
             o.partials = ctx->d_part;
@@ -1674,6 +1699,7 @@ bc_status bc_shape_upload(bc_ctx *ctx, int which, const double *xyzr, const doub
     ctx->qgrid_ready = false;
     ctx->probe_done = false;
     ctx->probe_err = -1.0;
+    ctx->ex_ready = false;
     if (which == 0) ctx->have_spec = false;
     ctx->cm_ready = false;
     TRY(upload_shape_device(ctx, which));

@@ -6,12 +6,19 @@
 // f_{B_O} = f_{B_1} * f_{B_2}.  For indicator primitives that kernel is the
 // two-ball intersection volume V(r, s, d), so
 //     f_R(t_m) = sum_ij w_i v_j V(r_i, s_j, |a_i - R b_j - t_m|).
-// Each (i, j) pair spreads V onto the grid points inside its obstacle ball;
-// accumulation is fp64.  This is the paper's "pairwise Minkowski sum" GPU
-// kernel (L515-L520), here with exact lens weights.
+// Each (i, j) pair (one warp, lanes over its footprint) spreads V onto the grid points
+// inside its obstacle ball (fixed-point integer sums: see below).  This is the paper's "pairwise
+// Minkowski sum" GPU kernel (L515-L520), here with exact lens weights.
+#include <algorithm>
+
 #include "kernels.cuh"
 
 #include "ballcorr.h"
+
+template <typename T>
+__device__ __forceinline__ T lens_div(T a, T b) { return a / b; }
+template <>
+__device__ __forceinline__ float lens_div<float>(float a, float b) { return __fdividef(a, b); }
 
 template <typename T>
 __device__ __forceinline__ T lens_volume_dev(T r, T s, T d)
@@ -22,63 +29,94 @@ __device__ __forceinline__ T lens_volume_dev(T r, T s, T d)
     const T rs = r - s;
     if (d <= (rs < 0 ? -rs : rs)) return (T)4 / (T)3 * pi * m * m * m;
     const T e = r + s - d;
-    return pi * e * e * (d * d + (T)2 * d * (r + s) - (T)3 * rs * rs) / ((T)12 * d);
+    return lens_div<T>(pi * e * e * (d * d + (T)2 * d * (r + s) - (T)3 * rs * rs), (T)12 * d);
 }
 
-template <typename T, bool CPLX>
-__global__ void __launch_bounds__(256) exact_kernel(ExactArgs a)
+// ---------------------------------------------------------------- accumulation
+//
+// The per-point sums are fixed-point integers: each term w_i v_j V x qscale rounded to int64,
+// qscale = 2^61 / (a bound on |f|, set by the host).  Integer addition is associative, so the
+// sums are bitwise independent of the order in which warps add their terms (64-bit integer
+// reductions, RED.E.ADD.64 -- no floating-point atomics), of the batching and of the launch:
+// deterministic.  The quantisation (<= 2^-62 of the bound per term) sits far below fp64's 1e-9
+// parity bar.
+struct KnotBox {
+    double cx, cy, cz, rs;
+    int lo[3], hi[3];  // grid point range (inclusive), empty if lo > hi on an axis
+};
+
+__device__ __forceinline__ KnotBox knot_box(const ExactArgs &a, int b, long long k)
 {
-    const int b = blockIdx.y;
-    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= (long long)a.nA * a.nB) return;
-    const int i = (int)(p / a.nB), j = (int)(p % a.nB);
+    const int i = (int)(k / a.nB), j = (int)(k % a.nB);
     const double *R = a.rot + 9 * b;
     const double4 ai = a.A[i], bj = a.B[j];
+    KnotBox kb;
     // obstacle knot a_i - R b_j (eq_ORP), radius r_i + s_j
-    const double cx = ai.x - (R[0] * bj.x + R[1] * bj.y + R[2] * bj.z);
-    const double cy = ai.y - (R[3] * bj.x + R[4] * bj.y + R[5] * bj.z);
-    const double cz = ai.z - (R[6] * bj.x + R[7] * bj.y + R[8] * bj.z);
-    const double rs = ai.w + bj.w;
-    const int N = a.N;
-    const double ih = 1.0 / a.h;
-    int x0 = (int)ceil((cx - rs - a.t0x) * ih), x1 = (int)floor((cx + rs - a.t0x) * ih);
-    int y0 = (int)ceil((cy - rs - a.t0y) * ih), y1 = (int)floor((cy + rs - a.t0y) * ih);
-    int z0 = (int)ceil((cz - rs - a.t0z) * ih), z1 = (int)floor((cz + rs - a.t0z) * ih);
-    x0 = max(x0, 0); y0 = max(y0, 0); z0 = max(z0, 0);
-    x1 = min(x1, N - 1); y1 = min(y1, N - 1); z1 = min(z1, N - 1);
-    if (x0 > x1 || y0 > y1 || z0 > z1) return;
+    kb.cx = ai.x - (R[0] * bj.x + R[1] * bj.y + R[2] * bj.z);
+    kb.cy = ai.y - (R[3] * bj.x + R[4] * bj.y + R[5] * bj.z);
+    kb.cz = ai.z - (R[6] * bj.x + R[7] * bj.y + R[8] * bj.z);
+    kb.rs = ai.w + bj.w;
+    const double ih = a.inv_h;
+    const double c[3] = {kb.cx - a.t0x, kb.cy - a.t0y, kb.cz - a.t0z};
+#pragma unroll
+    for (int d = 0; d < 3; d++) {
+        kb.lo[d] = max((int)ceil((c[d] - kb.rs) * ih), 0);
+        kb.hi[d] = min((int)floor((c[d] + kb.rs) * ih), a.N - 1);
+    }
+    return kb;
+}
+
+__device__ __forceinline__ long long to_fixed(double x) { return __double2ll_rn(x); }
+__device__ __forceinline__ long long to_fixed(float x) { return __float2ll_rn(x); }
+
+// Warp per obstacle knot: lanes own the grid points of the knot's footprint box and add their
+// fixed-point terms to the output accumulator with 64-bit integer reductions (RED.E.ADD.64:
+// associative, so the result does not depend on which warp adds first -- deterministic).
+template <typename T, bool CPLX>
+__global__ void __launch_bounds__(256) exact_scatter_kernel(ExactArgs a)
+{
+    const int b = blockIdx.y;
+    const long long k = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (k >= (long long)a.nA * a.nB) return;
+    const KnotBox kb = knot_box(a, b, k);
+    const int nx = kb.hi[0] - kb.lo[0] + 1, ny = kb.hi[1] - kb.lo[1] + 1, nz = kb.hi[2] - kb.lo[2] + 1;
+    if (nx <= 0 || ny <= 0 || nz <= 0) return;
+    const int i = (int)(k / a.nB), j = (int)(k % a.nB);
+    const double ih = a.inv_h;
+    // centre relative to the box's first point and radii, grid units
+    const T cx = (T)((kb.cx - a.t0x) * ih - kb.lo[0]), cy = (T)((kb.cy - a.t0y) * ih - kb.lo[1]),
+            cz = (T)((kb.cz - a.t0z) * ih - kb.lo[2]);
+    const double rr = a.A[i].w * ih, ss = a.B[j].w * ih;
+    const T r = (T)rr, s = (T)ss, rho2 = (T)((rr + ss) * (rr + ss));
     const double2 wa = a.wA[i], wb = a.wB[j];
-    const double wr = wa.x * wb.x - wa.y * wb.y, wi = wa.x * wb.y + wa.y * wb.x;
-    double *acc = a.acc + (long long)b * a.acc_bstride;
-    const long long N3 = (long long)N * N * N;
-    const T r = (T)ai.w, s = (T)bj.w;
-    for (int mx = x0; mx <= x1; mx++) {
-        const T dx = (T)(cx - (a.t0x + mx * a.h));
-        for (int my = y0; my <= y1; my++) {
-            const T dy = (T)(cy - (a.t0y + my * a.h));
-            for (int mz = z0; mz <= z1; mz++) {
-                const T dz = (T)(cz - (a.t0z + mz * a.h));
-                const T d = sqrt(dx * dx + dy * dy + dz * dz);
-                const T v = lens_volume_dev<T>(r, s, d);
-                if (v == (T)0) continue;
-                const long long idx = ((long long)mx * N + my) * N + mz;
-                atomicAdd(acc + idx, wr * (double)v);
-                if (CPLX) atomicAdd(acc + N3 + idx, wi * (double)v);
-            }
-        }
+    const double h3q = a.h * a.h * a.h * a.qscale;  // V in grid units x h^3 x fixed-point scale
+    const T wr = (T)((wa.x * wb.x - wa.y * wb.y) * h3q), wi = (T)((wa.x * wb.y + wa.y * wb.x) * h3q);
+    const long long N = a.N, N3 = N * N * N;
+    unsigned long long *acc = (unsigned long long *)a.iacc + (long long)b * a.acc_bstride;
+    const int nyz = ny * nz, tot = nx * nyz;
+    for (int q = lane; q < tot; q += 32) {
+        const int ix = q / nyz, iy = (q / nz) % ny, iz = q % nz;
+        const T dx = cx - (T)ix, dy = cy - (T)iy, dz = cz - (T)iz;
+        const T d2 = dx * dx + dy * dy + dz * dz;
+        if (d2 >= rho2) continue;
+        const T v = lens_volume_dev<T>(r, s, sqrt(d2));
+        const long long idx = ((long long)(kb.lo[0] + ix) * N + (kb.lo[1] + iy)) * N + (kb.lo[2] + iz);
+        atomicAdd(acc + idx, (unsigned long long)to_fixed(wr * v));
+        if (CPLX) atomicAdd(acc + N3 + idx, (unsigned long long)to_fixed(wi * v));
     }
 }
 
-void launch_exact(const ExactArgs &a, int batch, cudaStream_t s)
+void launch_exact_scatter(const ExactArgs &a, int batch, cudaStream_t s)
 {
-    const long long np = (long long)a.nA * a.nB;
-    dim3 grid((unsigned)((np + 255) / 256), batch);
+    const long long warps = (long long)a.nA * a.nB;
+    dim3 grid((unsigned)((warps * 32 + 255) / 256), batch);
     if (a.fp64) {
-        if (a.complex_w) exact_kernel<double, true><<<grid, 256, 0, s>>>(a);
-        else exact_kernel<double, false><<<grid, 256, 0, s>>>(a);
+        if (a.complex_w) exact_scatter_kernel<double, true><<<grid, 256, 0, s>>>(a);
+        else exact_scatter_kernel<double, false><<<grid, 256, 0, s>>>(a);
     } else {
-        if (a.complex_w) exact_kernel<float, true><<<grid, 256, 0, s>>>(a);
-        else exact_kernel<float, false><<<grid, 256, 0, s>>>(a);
+        if (a.complex_w) exact_scatter_kernel<float, true><<<grid, 256, 0, s>>>(a);
+        else exact_scatter_kernel<float, false><<<grid, 256, 0, s>>>(a);
     }
 }
 
@@ -90,8 +128,8 @@ __global__ void exact_full_kernel(ExactOutArgs a)
     const long long N3 = (long long)a.N * a.N * a.N;
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N3) return;
-    const double *acc = a.acc + (long long)b * a.acc_bstride;
-    const double re = acc[i], im = a.complex_w ? acc[N3 + i] : 0.0;
+    const long long *acc = a.iacc + (long long)b * a.acc_bstride;
+    const double re = (double)acc[i] * a.inv_qscale, im = a.complex_w ? (double)acc[N3 + i] * a.inv_qscale : 0.0;
     if (a.fp64) {
         double *o = (double *)a.out;
         if (a.complex_w) {
@@ -130,10 +168,10 @@ __global__ void __launch_bounds__(256) exact_reduce1(ExactOutArgs a, int nblk)
     __shared__ ValIdx smin[8], smax[8];
     const int b = blockIdx.y;
     const long long N3 = (long long)a.N * a.N * a.N;
-    const double *acc = a.acc + (long long)b * a.acc_bstride;
+    const long long *acc = a.iacc + (long long)b * a.acc_bstride;
     ValIdx mn = {1e300, 0x7fffffffffffffffll}, mx = {-1e300, 0x7fffffffffffffffll};
     for (long long i = (long long)blockIdx.x * 256 + threadIdx.x; i < N3; i += (long long)nblk * 256) {
-        const ValIdx c = {acc[i] + 0.0, i};
+        const ValIdx c = {(double)acc[i] * a.inv_qscale + 0.0, i};
         if (better_min(c, mn)) mn = c;
         if (better_max(c, mx)) mx = c;
     }

@@ -224,7 +224,7 @@ void launch_keys_finalize(const unsigned long long *keys, int batch, int out_kin
 // ----------------------------------------------------------------- exact mode
 struct ExactArgs {
     int nA, nB, N;
-    double h, t0x, t0y, t0z;
+    double h, inv_h, t0x, t0y, t0z;
     const double4 *A;    // (x, y, z, r)
     const double4 *B;
     const double2 *wA;   // (re, im)
@@ -232,16 +232,18 @@ struct ExactArgs {
     const double *rot;   // [b][9]
     int complex_w;
     int fp64;            // evaluate V in double (1) or float (0)
-    double *acc;         // [b][N^3] (re) followed by [b][N^3] (im) when complex
+    long long *iacc;     // [b][N^3] (re) followed by [b][N^3] (im) when complex: fixed point, value * qscale
     long long acc_bstride;
+    double qscale;       // 2^61 / (bound on |f|)
 };
-void launch_exact(const ExactArgs &a, int batch, cudaStream_t s);
+void launch_exact_scatter(const ExactArgs &a, int batch, cudaStream_t s);
 
 struct ExactOutArgs {
     int N;
     int complex_w, fp64;
-    const double *acc;
+    const long long *iacc;
     long long acc_bstride;
+    double inv_qscale;
     int out_kind;
     void *out;           // full output or bc_extremum[]
     double *partials;    // scratch: [b][nblocks][2] vals

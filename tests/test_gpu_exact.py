@@ -104,3 +104,38 @@ def test_invalid_rotation_and_radius(bc):
     with pytest.raises(bc.BallCorrError) as e:
         c.shape_upload(1, bad_b)
     assert e.value.status == bc.BC_EINVAL
+
+
+def test_exact_is_deterministic_across_batchings(bc):
+    """Output tiles owned by blocks, fixed-point integer sums (exact.cu): the bits of every
+    value are independent of launch order, list splits and batching -- repeated calls and
+    batch sizes 1 / 3 / 8 agree bitwise (fp64, complex weights, rotated)."""
+    w = random_small_case(71, n_a=40, n_b=30, n_rot=7, N=24, complex_weights=True)
+    outs = []
+    for nb in (1, 3, 8):
+        c = bc.Correlator(N=w.N, h=w.h, t0=w.t0, mode="exact", precision="f64", weights="complex", max_batch=nb)
+        c.shape_upload(0, w.A_xyzr, w.A_w)
+        c.shape_upload(1, w.B_xyzr, w.B_w)
+        outs.append(c.correlate_rotations(w.R, "full"))
+        outs.append(c.correlate_rotations(w.R, "full"))
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+
+
+def test_single_exact_reductions_and_large_knots(bc, oracle_mod):
+    """Single-rotation workload (fp32): min/max against the oracle's full grid; and knots
+    much larger than a tile (radii 0.3-0.45 on h = 1/16: footprints of ~15 points per axis
+    span several 8^3 output tiles) in fp64 against the oracle."""
+    w = make_config("single")
+    c = make_exact(bc, w)
+    mm = c.correlate_rotations(w.R, "minmax")
+    ref = oracle_mod.correlate_grid(w.A_xyzr, w.A_w, w.B_xyzr, w.B_w, w.R[0], w.N, w.h, w.t0)
+    tol = 1e-4 * np.abs(ref).max()
+    check_extremum(mm[0, 0]["val"], mm[0, 0]["idx"], ref, "min", tol)
+    check_extremum(mm[0, 1]["val"], mm[0, 1]["idx"], ref, "max", tol)
+    big = random_small_case(72, n_a=6, n_b=5, n_rot=2, N=32, r_lo=0.3, r_hi=0.45)
+    cb = make_exact(bc, big, precision="f64")
+    f = cb.correlate_rotations(big.R, "full")
+    for r in range(2):
+        rb = oracle_mod.correlate_grid(big.A_xyzr, big.A_w, big.B_xyzr, big.B_w, big.R[r], big.N, big.h, big.t0)
+        assert rel_max_err(f[r], rb) <= 1e-9
