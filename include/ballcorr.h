@@ -200,6 +200,27 @@ bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, in
 bc_status bc_evaluate_points(bc_ctx *ctx, const double *R, const double *t, int64_t n, double *out,
                              void *stream);
 
+/*
+ * The paper's time-critical single-configuration query (PAPER.md L432-L439 eq_single, "a
+ * spiral traversal of the frequency grid starting from the dominant modes"; accuracy vs
+ * time L539-L546): by Parseval, f_R(t) evaluated in the frequency domain over a truncated
+ * set of m' modes,
+ *     f_m'(t) = (1/P^3) sum_{k in S_m'} A_hat(k) B_hat_R(-k) e^{2 pi i k . t / P},
+ * with A_hat the band spectrum of bc_spectrum_A and B_hat_R the direct NDFT of the rotated
+ * knots times the ball transform (eq_rhoPhat / eq_fballhat).  S_m' = the first m' band modes
+ * (|k_i| <= K) in radial-shell order (|k|^2, then kx, ky, kz), a mode and its mirror -k kept
+ * together for real weights (so m' counts them both).  Cost linear in m' x n_B per query.
+ * With m' = all modes of |k| <= rho it equals the band-limited f of the spherical band; with
+ * m' = (2K + 1)^3 it equals the spectral grid of bc_correlate_rotations at grid points.
+ *   R, t, out: as bc_evaluate_points (host or device; device R / t validated on the device).
+ *   m_prime:   1 <= m' <= min((2K + 1)^3, 2^22), else BC_ERANGE.
+ * Spectral mode only (BC_EUNSUPPORTED); needs bc_spectrum_A (BC_ESTATE).  The first call for
+ * a larger m' (or after an upload / a new spectrum) builds the mode list on the host and
+ * synchronises `stream` once; later calls are asynchronous for device buffers.
+ */
+bc_status bc_evaluate_points_spectral(bc_ctx *ctx, const double *R, const double *t, int64_t n, int64_t m_prime,
+                                      double *out, void *stream);
+
 /* Synchronise `stream` and report a deferred error of earlier calls on this context
  * (BC_EINVAL from device-side validation of R / t, BC_ECUDA from a CUDA fault). */
 bc_status bc_sync(bc_ctx *ctx, void *stream);
@@ -212,7 +233,8 @@ const char *bc_status_string(int status);
  * Introspection (tests / bench): named double-valued properties of the plan.
  * Keys: "P", "K", "Np", "tau_A", "tau_B", "G_A", "G_B", "L_A", "L_B", "c_A", "c_B",
  * "cut_A", "cut_B", "band_modes", "batch", "bytes_workspace", "band_error" (the band-error
- * probe's estimate, -1 before it ran; see bc_params.tolerance), "blob_B" (B smoothed with the
+ * probe's estimate, -1 before it ran; see bc_params.tolerance), "query_modes" (m' the spectral
+ * query's tables serve), "blob_B" (B smoothed with the
  * KB blob window), "fused_spread_z", "fused_fold_inv", "fold_fast" (which fused kernels the
  * plan takes), "spread_cells_B" (sum of B's footprint volumes in fine cells), "live_tiles_B".
  * Unknown keys: BC_EINVAL.

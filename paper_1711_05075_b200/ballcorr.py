@@ -64,6 +64,8 @@ _lib.bc_correlate_rotations.argtypes = [_vp, _vp, ctypes.c_int64, ctypes.c_int, 
 _lib.bc_correlate_rotations.restype = ctypes.c_int
 _lib.bc_evaluate_points.argtypes = [_vp, _vp, _vp, ctypes.c_int64, _vp, _vp]
 _lib.bc_evaluate_points.restype = ctypes.c_int
+_lib.bc_evaluate_points_spectral.argtypes = [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64, _vp, _vp]
+_lib.bc_evaluate_points_spectral.restype = ctypes.c_int
 _lib.bc_sync.argtypes = [_vp, _vp]
 _lib.bc_sync.restype = ctypes.c_int
 _lib.bc_last_error.argtypes = [_vp]
@@ -90,6 +92,7 @@ bc_spectrum_A = _lib.bc_spectrum_A
 bc_spectrum_A_buffer = _lib.bc_spectrum_A_buffer
 bc_spectrum_A_import = _lib.bc_spectrum_A_import
 bc_correlate_rotations = _lib.bc_correlate_rotations
+bc_evaluate_points_spectral = _lib.bc_evaluate_points_spectral
 bc_sync = _lib.bc_sync
 bc_last_error = _lib.bc_last_error
 bc_status_string = _lib.bc_status_string
@@ -299,6 +302,24 @@ class Correlator:
         pr, kr = _ptr(Rv)
         pt, kt = _ptr(tv)
         self._check(_lib.bc_evaluate_points(self._ctx, pr, pt, n, po, _stream_handle(stream)))
+        return out[:, 0] + 1j * out[:, 1] if ret_complex else out
+
+    def evaluate_points_spectral(self, R, t, m_prime, out=None, stream=None):
+        """The paper's truncated-Parseval query: f_R(t) over the first
+        m_prime band modes in radial-shell order.  Same arguments and results as
+        evaluate_points."""
+        Rv = _as_f64(R)
+        tv = _as_f64(t)
+        n = int(Rv.shape[0])
+        if tuple(tv.shape) != (n, 3):
+            raise ValueError("t must have shape (n, 3)")
+        ret_complex = out is None and self.complex
+        if out is None:
+            out = np.empty((n, 2) if self.complex else (n,), dtype=np.float64)
+        po = _out_ptr(out, n * (2 if self.complex else 1) * 8, np.float64)
+        pr, kr = _ptr(Rv)
+        pt, kt = _ptr(tv)
+        self._check(_lib.bc_evaluate_points_spectral(self._ctx, pr, pt, n, int(m_prime), po, _stream_handle(stream)))
         return out[:, 0] + 1j * out[:, 1] if ret_complex else out
 
     # -- introspection / profiling

@@ -142,6 +142,18 @@ struct bc_ctx {
     bool probe_done = false;
     double probe_err = -1.0;
 
+    // spectral single-configuration query (query_spectral.cu): retained modes in radial-shell
+    // order, their A', the shell table of B; rebuilt when m' grows or the shapes / spectrum change
+    bool qs_ready = false;
+    int64_t qs_m = 0;              // m' the current tables serve (modes counted with multiplicity)
+    int qs_nm = 0, qs_nsh = 0;
+    int4 *d_qs_modes = nullptr;
+    int *d_qs_k2 = nullptr;
+    float *d_qs_mult = nullptr;
+    float2 *d_qs_Aq = nullptr, *d_qs_bv = nullptr, *d_qs_part = nullptr;
+    double *d_qs_mpart = nullptr;
+    size_t qs_part_bytes = 0, qs_mpart_bytes = 0;
+
     int64_t launches = 0;
     bool prof = false;
     std::vector<PendingEvent> pending;
@@ -1146,6 +1158,92 @@ bc_status exact_plan(bc_ctx *ctx)
     return BC_OK;
 }
 
+// Retained modes of the spectral query for m' (query_spectral.cu): the band's modes |k_i| <= K
+// sorted by (|k|^2, kx, ky, kz) -- the radial-shell ("spiral") order of PAPER.md L436 -- with a
+// mode and its mirror kept together for real weights (half space kz > 0 | kz = 0, ky > 0 |
+// kz = ky = 0, kx > 0, counted twice; k = 0 once).  The first modes whose multiplicities add up
+// to at most m' are retained.  Built on the host once per (shapes, spectrum, larger m').
+bc_status qs_prepare(bc_ctx *ctx, int64_t m_prime, cudaStream_t s)
+{
+    if (ctx->qs_ready && m_prime <= ctx->qs_m) return BC_OK;
+    const bool cplx = ctx->p.weights == BC_WEIGHTS_COMPLEX;
+    const int K = ctx->K;
+    // enumerate a ball |k| <= Rk (grown until it holds m' modes or the whole cube band)
+    struct Mode {
+        int k2, x, y, z;
+    };
+    std::vector<Mode> modes;
+    double Rk = std::cbrt(3.0 * (double)m_prime / (4 * kPi)) + 2;
+    for (;;) {
+        modes.clear();
+        const int lim = std::min(K, (int)std::ceil(Rk));
+        const long long R2 = (long long)(Rk * Rk);
+        for (int x = -lim; x <= lim; x++)
+            for (int y = -lim; y <= lim; y++)
+                for (int z = cplx ? -lim : 0; z <= lim; z++) {
+                    const long long k2 = (long long)x * x + (long long)y * y + (long long)z * z;
+                    if (k2 > R2) continue;
+                    if (!cplx && (z == 0 && (y < 0 || (y == 0 && x < 0)))) continue;  // the mirror half
+                    modes.push_back({(int)k2, x, y, z});
+                }
+        int64_t cnt = 0;
+        for (const Mode &m : modes) cnt += (cplx || m.k2 == 0) ? 1 : 2;
+        if (cnt >= m_prime || R2 >= 3LL * K * K) break;  // enough modes, or the whole cube band
+        Rk *= 1.25;
+    }
+    std::sort(modes.begin(), modes.end(), [](const Mode &a, const Mode &b) {
+        if (a.k2 != b.k2) return a.k2 < b.k2;
+        if (a.x != b.x) return a.x < b.x;
+        if (a.y != b.y) return a.y < b.y;
+        return a.z < b.z;
+    });
+    std::vector<int4> hm;
+    std::vector<float> hmult;
+    std::vector<int> k2s;
+    int64_t cnt = 0;
+    for (const Mode &m : modes) {
+        const int mu = (cplx || m.k2 == 0) ? 1 : 2;
+        if (cnt + mu > m_prime) break;
+        cnt += mu;
+        if (k2s.empty() || k2s.back() != m.k2) k2s.push_back(m.k2);
+        hm.push_back(make_int4(m.x, m.y, m.z, (int)k2s.size() - 1));
+        hmult.push_back((float)mu);
+    }
+    ctx->qs_nm = (int)hm.size();
+    ctx->qs_nsh = (int)k2s.size();
+    ctx->qs_m = m_prime;  // serves every m' <= this (a real-weight pair may leave cnt = m' - 1)
+    const int nB = (int)ctx->n[1];
+    TRY(dalloc(ctx, &ctx->d_qs_modes, sizeof(int4) * hm.size()));
+    TRY(dalloc(ctx, &ctx->d_qs_mult, sizeof(float) * hm.size()));
+    TRY(dalloc(ctx, &ctx->d_qs_k2, sizeof(int) * k2s.size()));
+    TRY(dalloc(ctx, &ctx->d_qs_Aq, sizeof(float2) * hm.size()));
+    TRY(dalloc(ctx, &ctx->d_qs_bv, sizeof(float2) * (size_t)std::max(nB, 1) * k2s.size()));
+    CU(ctx, cudaMemcpyAsync(ctx->d_qs_modes, hm.data(), sizeof(int4) * hm.size(), cudaMemcpyHostToDevice, s));
+    CU(ctx, cudaMemcpyAsync(ctx->d_qs_mult, hmult.data(), sizeof(float) * hmult.size(), cudaMemcpyHostToDevice, s));
+    CU(ctx, cudaMemcpyAsync(ctx->d_qs_k2, k2s.data(), sizeof(int) * k2s.size(), cudaMemcpyHostToDevice, s));
+    QsTableArgs t{};
+    t.B = ctx->d_balls64[1];
+    t.wB = ctx->d_w64[1];
+    t.nB = nB;
+    t.k2 = ctx->d_qs_k2;
+    t.nsh = ctx->qs_nsh;
+    t.P = ctx->P;
+    t.complex_w = cplx;
+    t.bv = ctx->d_qs_bv;
+    t.Ahat = ctx->d_Ahat;
+    t.modes = ctx->d_qs_modes;
+    t.nm = ctx->qs_nm;
+    t.K = K;
+    t.Kz = ctx->Kz;
+    t.Aq = ctx->d_qs_Aq;
+    launch_qs_tables(t, s);
+    ctx->launches += 2;
+    CU(ctx, cudaStreamSynchronize(s));  // host vectors above go out of scope (pageable copies)
+    CU(ctx, cudaGetLastError());
+    ctx->qs_ready = true;
+    return BC_OK;
+}
+
 // The per-rotation path for n_rot rotations already prepared in ctx->d_rot (fp32) and
 // ctx->d_rot64 (fp64), written to the device buffer dout (out_per bytes per rotation).
 bc_status run_rotations(bc_ctx *ctx, int64_t n_rot, int out_kind, char *dout, size_t out_per, cudaStream_t s)
@@ -1636,6 +1734,13 @@ bc_status bc_destroy(bc_ctx *ctx)
         if (sl.done) cudaEventDestroy(sl.done);
     }
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    dfree(ctx->d_qs_modes);
+    dfree(ctx->d_qs_k2);
+    dfree(ctx->d_qs_mult);
+    dfree(ctx->d_qs_Aq);
+    dfree(ctx->d_qs_bv);
+    dfree(ctx->d_qs_part);
+    dfree(ctx->d_qs_mpart);
     dfree(ctx->d_qstart);
     dfree(ctx->d_qidx);
     dfree(ctx->d_qR);
@@ -1700,6 +1805,7 @@ bc_status bc_shape_upload(bc_ctx *ctx, int which, const double *xyzr, const doub
     ctx->probe_done = false;
     ctx->probe_err = -1.0;
     ctx->ex_ready = false;
+    ctx->qs_ready = false;
     if (which == 0) ctx->have_spec = false;
     ctx->cm_ready = false;
     TRY(upload_shape_device(ctx, which));
@@ -1752,6 +1858,7 @@ bc_status bc_spectrum_A(bc_ctx *ctx, void *stream)
     if (!ctx->d_Ahat) TRY(dalloc(ctx, &ctx->d_Ahat, sizeof(float2) * nspec));  // fixed size per context
     ctx->cm_ready = false;
     ctx->probe_done = false;
+    ctx->qs_ready = false;
     if (ctx->n[0] == 0) {
         CU(ctx, cudaMemsetAsync(ctx->d_Ahat, 0, sizeof(float2) * nspec, s));
         ctx->have_spec = true;
@@ -1791,6 +1898,7 @@ bc_status bc_spectrum_A_import(bc_ctx *ctx)
     if (!ctx->d_Ahat) return fail(ctx, BC_ESTATE, "bc_spectrum_A_buffer has not been called");
     ctx->cm_ready = false;  // A'' (coset-major, B's multipliers) is rebuilt from the new contents
     ctx->probe_done = false;
+    ctx->qs_ready = false;
     ctx->have_spec = true;
     return BC_OK;
 }
@@ -1895,6 +2003,109 @@ bc_status bc_evaluate_points(bc_ctx *ctx, const double *R, const double *t, int6
     return BC_OK;
 }
 
+bc_status bc_evaluate_points_spectral(bc_ctx *ctx, const double *R, const double *t, int64_t n, int64_t m_prime,
+                                      double *out, void *stream)
+{
+    if (!ctx) return BC_EINVAL;
+    TRY(check_deferred(ctx));
+    if (!R || !t || !out || n < 1) return fail(ctx, BC_EINVAL, "NULL R/t/out or n < 1");
+    if (ctx->p.mode != BC_MODE_SPECTRAL) return fail(ctx, BC_EUNSUPPORTED, "the spectral query needs spectral mode");
+    if (!ctx->have[0] || !ctx->have[1]) return fail(ctx, BC_ESTATE, "upload both shapes first");
+    if (!ctx->have_spec) return fail(ctx, BC_ESTATE, "call bc_spectrum_A first");
+    const int64_t band = (int64_t)ctx->M * ctx->M * ctx->M;
+    if (m_prime < 1 || m_prime > std::min<int64_t>(band, (int64_t)1 << 22))
+        return fail(ctx, BC_ERANGE, "m' = %lld outside [1, min(band modes %lld, 2^22)]", (long long)m_prime,
+                    (long long)band);
+    CU(ctx, cudaSetDevice(ctx->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool cplx = ctx->p.weights == BC_WEIGHTS_COMPLEX;
+    const bool dev_R = is_device_ptr(R), dev_t = is_device_ptr(t);
+    if (!dev_R) TRY(validate_rotations(ctx, R, n));
+    if (!dev_t)
+        for (int64_t q = 0; q < 3 * n; q++)
+            if (!std::isfinite(t[q])) return fail(ctx, BC_EINVAL, "non-finite translation");
+    TRY(ensure_deferred_status(ctx));
+    const size_t out_per = cplx ? 2 : 1;
+    const bool host_out = !is_device_ptr(out);
+    if (ctx->n[0] == 0 || ctx->n[1] == 0) {
+        if (host_out)
+            std::fill(out, out + out_per * n, 0.0);
+        else
+            CU(ctx, cudaMemsetAsync(out, 0, sizeof(double) * out_per * n, s));
+        return BC_OK;
+    }
+    TRY(qs_prepare(ctx, m_prime, s));
+    // the retained modes for THIS m' (a prefix of the prepared list)
+    QsArgs a{};
+    a.nB = (int)ctx->n[1];
+    {
+        // prefix length: modes whose multiplicities add up to <= m'
+        int64_t cnt = 0;
+        int nm = 0;
+        // the list is sorted; k = 0 first, multiplicity 1, the rest 2 (real) or 1 (complex)
+        for (; nm < ctx->qs_nm; nm++) {
+            const int mu = (cplx || nm == 0) ? 1 : 2;
+            if (cnt + mu > m_prime) break;
+            cnt += mu;
+        }
+        a.nm = nm;
+    }
+    a.nsh = ctx->qs_nsh;
+    a.B = ctx->d_balls64[1];
+    a.t0x = ctx->p.t0[0];
+    a.t0y = ctx->p.t0[1];
+    a.t0z = ctx->p.t0[2];
+    a.invP = 1.0 / ctx->P;
+    a.modes = ctx->d_qs_modes;
+    a.bv = ctx->d_qs_bv;
+    a.Aq = ctx->d_qs_Aq;
+    a.mult = ctx->d_qs_mult;
+    a.scale = 1.0 / (ctx->P * ctx->P * ctx->P);
+    a.complex_w = cplx;
+    const int nbc = qs_ball_chunks(a.nB), nmb = qs_mode_blocks(a.nm);
+    const size_t per_q = (size_t)nbc * a.nm * sizeof(float2);
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>({n, 65535, (int64_t)((size_t)512 << 20) / (int64_t)per_q}));
+    TRY(ensure_query_ws(ctx, chunk));
+    TRY(ensure_ws(ctx, (void **)&ctx->d_qs_part, ctx->qs_part_bytes, per_q * chunk));
+    TRY(ensure_ws(ctx, (void **)&ctx->d_qs_mpart, ctx->qs_mpart_bytes, sizeof(double) * 2 * nmb * chunk));
+    a.part = ctx->d_qs_part;
+    a.mpart = ctx->d_qs_mpart;
+    for (int64_t q0 = 0; q0 < n; q0 += chunk) {
+        const int nq = (int)std::min<int64_t>(chunk, n - q0);
+        RotPrepArgs ra{};
+        ra.R = dev_R ? R + 9 * q0 : ctx->d_qR;
+        ra.t = dev_t ? t + 3 * q0 : nullptr;
+        ra.n = nq;
+        ra.index_base = q0;
+        ra.tol = rot_tol(ctx);
+        ra.r64 = dev_R ? ctx->d_qR : nullptr;
+        ra.t64 = dev_t ? ctx->d_qt : nullptr;
+        ra.status = ctx->d_status;
+        if (!dev_R) CU(ctx, cudaMemcpyAsync(ctx->d_qR, R + 9 * q0, sizeof(double) * 9 * nq, cudaMemcpyHostToDevice, s));
+        if (!dev_t) CU(ctx, cudaMemcpyAsync(ctx->d_qt, t + 3 * q0, sizeof(double) * 3 * nq, cudaMemcpyHostToDevice, s));
+        if (dev_R || dev_t) {
+            launch_rot_prep(ra, s);
+            ctx->launches++;
+        }
+        a.nq = nq;
+        a.R = ctx->d_qR;
+        a.t = ctx->d_qt;
+        a.out = host_out ? ctx->d_qout : out + out_per * q0;
+        {
+            StageScope sc(ctx, s, "evaluate_points_spectral");
+            launch_qs(a, s);
+            ctx->launches += 3;
+        }
+        CU(ctx, cudaGetLastError());
+        if (host_out) {
+            CU(ctx, cudaMemcpyAsync(out + out_per * q0, ctx->d_qout, sizeof(double) * out_per * nq, cudaMemcpyDeviceToHost, s));
+            CU(ctx, cudaStreamSynchronize(s));
+        }
+    }
+    if (host_out) TRY(check_deferred(ctx));
+    return BC_OK;
+}
+
 bc_status bc_sync(bc_ctx *ctx, void *stream)
 {
     if (!ctx) return BC_EINVAL;
@@ -1930,6 +2141,7 @@ bc_status bc_query(const bc_ctx *ctx, const char *key, double *value)
     else if (k == "live_tiles_B") *value = (double)ctx->live_tiles_B;
     else if (k == "K") *value = ctx->K;
     else if (k == "band_error") *value = ctx->probe_done ? ctx->probe_err : -1.0;
+    else if (k == "query_modes") *value = (double)ctx->qs_m;
     else if (k == "Np") *value = ctx->p.Np;
     else if (k == "fused_fold_inv") *value = (!ctx->p.generic_only && fold_fuses_inverse(B.L, ctx->p.Np)) ? 1 : 0;
     else if (k == "fold_fast")

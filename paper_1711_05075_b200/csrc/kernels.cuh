@@ -286,3 +286,38 @@ struct RotPrepArgs {
     unsigned *status;    // [2] (mapped host memory): OR of BC_DEFER_* flags, lowest bad index
 };
 void launch_rot_prep(const RotPrepArgs &a, cudaStream_t s);
+
+// ----------------------------------------------------------------- spectral single-configuration query (query_spectral.cu)
+struct QsArgs {
+    int nq, nB, nm, nsh;
+    const double *R, *t;     // [nq][9], [nq][3]
+    const double4 *B;        // B's balls (x, y, z, s)
+    double t0x, t0y, t0z, invP;
+    const int4 *modes;       // [nm] (kx, ky, kz, shell index)
+    const float2 *bv;        // [nB][nsh] v_j beta_hat(s_j, |k_shell| / P)
+    const float2 *Aq;        // [nm] A'(k) of the retained modes
+    const float *mult;       // [nm] 1 (k = 0, or complex weights) or 2 (a +-k pair, real weights)
+    float2 *part;            // [nq][ball chunks][nm]
+    double *mpart;           // [nq][mode blocks][2]
+    double *out;             // [nq] or [nq][2]
+    double scale;            // 1 / P^3
+    int complex_w;
+};
+struct QsTableArgs {
+    const double4 *B;
+    const double2 *wB;
+    int nB;
+    const int *k2;           // [nsh] |k|^2 of each shell
+    int nsh;
+    double P;
+    int complex_w;
+    float2 *bv;              // [nB][nsh]
+    const float2 *Ahat;      // band spectrum [ky][kz][kx]
+    const int4 *modes;
+    int nm, K, Kz;
+    float2 *Aq;              // [nm]
+};
+int qs_ball_chunks(int nB);
+int qs_mode_blocks(int nm);
+void launch_qs_tables(const QsTableArgs &t, cudaStream_t s);
+void launch_qs(const QsArgs &a, cudaStream_t s);
