@@ -59,6 +59,10 @@ def parse():
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="strong: the config's rotations sharded over the ranks (headline); weak: every rank "
                          "correlates its own full rotation set")
+    ap.add_argument("--collectives", default="nccl", choices=["nccl", "p2p"],
+                    help="strong scaling: nccl = NCCL broadcast of A's spectrum + all-gather of the records per "
+                         "step; p2p = A's spectrum sharded by balls and reduced over peer memory inside the A'' "
+                         "build, records stored into every rank's buffer by the reduction epilogue (no gather)")
     ap.add_argument("--dry-run", action="store_true",
                     help="CPU-only launcher/protocol check: gloo, stand-in correlator, no CUDA")
     args = ap.parse_args()
@@ -384,7 +388,13 @@ def run_ours(args, rank, world, local_rank):
         stream = torch.cuda.current_stream(dev)
         ctx.shape_upload(0, w.A_xyzr, w.A_w)
         ctx.shape_upload(1, w.B_xyzr, w.B_w)
-        if world > 1:  # rank 0 computes A's spectrum, NCCL broadcasts it (north_star)
+        p2p = args.collectives == "p2p" and args.scaling == "strong"
+        if p2p:
+            if world == 1:
+                dist.init_process_group("gloo", init_method="tcp://127.0.0.1:%d" % _free_port(), rank=0, world_size=1)
+            from paper_1711_05075_b200.sharding import allreduce_spectrum_A_p2p
+            allreduce_spectrum_A_p2p(ctx, len(w.A_xyzr))
+        elif world > 1:  # rank 0 computes A's spectrum, NCCL broadcasts it (north_star)
             from paper_1711_05075_b200.sharding import broadcast_spectrum_A
             broadcast_spectrum_A(ctx, src=0)
         else:
@@ -402,8 +412,16 @@ def run_ours(args, rank, world, local_rank):
     R_dev = torch.tensor(R, dtype=torch.float64, device=dev)
     out = torch.empty(max(out_bytes, 16), dtype=torch.uint8, device=dev)
 
+    p2p = (not dry) and args.collectives == "p2p" and args.scaling == "strong" and reduced
+    if p2p:  # the job's records, stored into every rank's buffer by the reduction epilogue
+        from paper_1711_05075_b200.sharding import result_peers_p2p
+        glob_p2p = torch.zeros(n_all * 16, dtype=torch.uint8, device=dev)
+        _, mapped = result_peers_p2p(ctx, glob_p2p.data_ptr(), n_all)
+
     def step():
         ctx.correlate_rotations(R_dev, kind, out=out, stream=stream)
+        if p2p:  # nothing to launch: the epilogue stored the records in every rank's buffer
+            return glob_p2p
         if reduced:  # the per-rotation results of every rank, in global order, on every rank
             return gather_records(out[:out_bytes], n_rot, cap, world if args.scaling == "strong" else 1, dev)
         return out
@@ -449,7 +467,8 @@ def run_ours(args, rank, world, local_rank):
     value = units_per_step * w.N ** 3 * args.steps / (ms_max / 1e3)
     best = None
     if reduced and args.scaling == "strong":
-        recs = unpack_global(glob, n_all, world)
+        recs = (np.frombuffer(glob.cpu().numpy().tobytes(), dtype=REC_DTYPE) if p2p
+                else unpack_global(glob, n_all, world))
         best = global_best(recs["val"], recs["idx"], "min" if kind == "min_argmin" else "max")
         best = {"rotation": best[0], "value": best[1], "translation_index": best[2],
                 "records_sha1": __import__("hashlib").sha1(recs.tobytes()).hexdigest()}
@@ -465,6 +484,10 @@ def run_ours(args, rank, world, local_rank):
                               "result_sample": {"global_best": best}}), flush=True)
         return
 
+    if p2p:
+        ctx.set_result_peers([])  # the untimed legs below write no peer buffers
+        for ptr in mapped:
+            ctx.ipc_close(ptr)
     # per-stage device times: one more (untimed) step with the library's per-launch CUDA
     # events on (profiling serialises the batches), so shares refer to this profiled step
     ctx.set_profiling(True)
@@ -560,11 +583,16 @@ def run_ours(args, rank, world, local_rank):
         "config": {"workload": w.name, "N": w.N, "n_A": len(w.A_xyzr), "n_B": len(w.B_xyzr),
                    "rotations_per_step": units_per_step, "rotations_per_rank": n_rot,
                    "mode": kw["mode"], "Np": kw["Np"], "K": kw["K"], "output": kind, "l2": l2_note(w, kw),
-                   "timed": ("per step: every rank correlates its rotation block, then the NCCL all-gather of "
+                   "timed": ("per step: every rank correlates its rotation block; its reduction epilogue stores "
+                             "the records into every rank's job-wide buffer over peer memory (no gather launch)"
+                             if p2p else
+                             "per step: every rank correlates its rotation block, then the NCCL all-gather of "
                              "the per-rotation records (strong scaling, SURVEY.md §8(d)-(e))"
                              if args.scaling == "strong" else "per step: every rank its own full rotation set"),
+                   "collectives": args.collectives,
                    "setup_s": setup_s,
-                   "spectrum_A": "rank 0, NCCL broadcast" if world > 1 else "computed"},
+                   "spectrum_A": ("sharded by balls, partials reduced over peer memory in the A'' build" if p2p
+                                  else "rank 0, NCCL broadcast" if world > 1 else "computed")},
         "clocks": clocks,
         "gpu_launches": launches,
         "e2e": {"value": e2e_value, "unit": METRIC, "h2d_bytes_per_step": int(R.size * 8),

@@ -221,6 +221,44 @@ bc_status bc_evaluate_points(bc_ctx *ctx, const double *R, const double *t, int6
 bc_status bc_evaluate_points_spectral(bc_ctx *ctx, const double *R, const double *t, int64_t n, int64_t m_prime,
                                       double *out, void *stream);
 
+/*
+ * Fused exchanges over peer memory for rotation-sharded multi-GPU runs (one process per GPU
+ * of an NVLink / NVSwitch box).  The caller moves 64-byte IPC handles
+ * between its processes (e.g. torch.distributed all_gather_object) and orders the steps with
+ * its own barriers; the library does the data movement inside its kernels.
+ *
+ * bc_ipc_handle / bc_ipc_open / bc_ipc_close: cudaIpcGetMemHandle / cudaIpcOpenMemHandle
+ *   (peer access enabled lazily) / cudaIpcCloseMemHandle of a device allocation of the
+ *   calling process (handle: BC_IPC_HANDLE_BYTES bytes).
+ *
+ * A's spectrum sharded by balls (rho_hat_A is linear in the knots):
+ *   bc_spectrum_A_partial(ctx, lo, hi, stream): the band spectrum of A's balls [lo, hi) (A is
+ *     uploaded whole on every rank) into the context's PARTIAL buffer
+ *     (bc_spectrum_A_partial_buffer: device pointer and bytes, owned by the context).
+ *     Synchronises `stream` once (the slice's candidate lists are built on the host).
+ *   bc_spectrum_A_reduce(ctx, partials, n, stream): partials[0..n) are the partial buffers of
+ *     all n ranks in rank order (this rank's own and peers' mapped ones, n <= BC_MAX_PEERS);
+ *     one kernel reads them all over NVLink, sums them in that order (every rank gets the same
+ *     bits) and writes this rank's A spectrum and the A'' layout the fold consumes -- the
+ *     all-reduce fused into the A'' build.  Needs both shapes uploaded.  Asynchronous on
+ *     `stream`; the caller keeps every partial intact until all ranks' reduce kernels are done.
+ *
+ * bc_set_result_peers(ctx, buffers, n, base): from now on the reduction outputs of
+ *   bc_correlate_rotations (spectral mode) are also stored by the epilogue kernel into each of
+ *   buffers[0..n) (bc_extremum arrays of the whole job's rotations, e.g. peers' mapped
+ *   buffers), at global rotation index base + (index within the call) -- the all-gather of
+ *   the per-rotation results fused into a7.  n = 0 turns it off.
+ */
+#define BC_IPC_HANDLE_BYTES 64
+#define BC_MAX_PEERS 8
+bc_status bc_ipc_handle(bc_ctx *ctx, const void *dev_ptr, void *handle);
+bc_status bc_ipc_open(bc_ctx *ctx, const void *handle, void **dev_ptr);
+bc_status bc_ipc_close(bc_ctx *ctx, void *dev_ptr);
+bc_status bc_spectrum_A_partial(bc_ctx *ctx, int64_t lo, int64_t hi, void *stream);
+bc_status bc_spectrum_A_partial_buffer(bc_ctx *ctx, void **dev_ptr, int64_t *bytes);
+bc_status bc_spectrum_A_reduce(bc_ctx *ctx, const void *const *partials, int n, void *stream);
+bc_status bc_set_result_peers(bc_ctx *ctx, void *const *buffers, int n, int64_t base);
+
 /* Synchronise `stream` and report a deferred error of earlier calls on this context
  * (BC_EINVAL from device-side validation of R / t, BC_ECUDA from a CUDA fault). */
 bc_status bc_sync(bc_ctx *ctx, void *stream);

@@ -66,6 +66,20 @@ _lib.bc_evaluate_points.argtypes = [_vp, _vp, _vp, ctypes.c_int64, _vp, _vp]
 _lib.bc_evaluate_points.restype = ctypes.c_int
 _lib.bc_evaluate_points_spectral.argtypes = [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64, _vp, _vp]
 _lib.bc_evaluate_points_spectral.restype = ctypes.c_int
+_lib.bc_ipc_handle.argtypes = [_vp, _vp, _vp]
+_lib.bc_ipc_handle.restype = ctypes.c_int
+_lib.bc_ipc_open.argtypes = [_vp, _vp, ctypes.POINTER(_vp)]
+_lib.bc_ipc_open.restype = ctypes.c_int
+_lib.bc_ipc_close.argtypes = [_vp, _vp]
+_lib.bc_ipc_close.restype = ctypes.c_int
+_lib.bc_spectrum_A_partial.argtypes = [_vp, ctypes.c_int64, ctypes.c_int64, _vp]
+_lib.bc_spectrum_A_partial.restype = ctypes.c_int
+_lib.bc_spectrum_A_partial_buffer.argtypes = [_vp, ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_int64)]
+_lib.bc_spectrum_A_partial_buffer.restype = ctypes.c_int
+_lib.bc_spectrum_A_reduce.argtypes = [_vp, ctypes.POINTER(_vp), ctypes.c_int, _vp]
+_lib.bc_spectrum_A_reduce.restype = ctypes.c_int
+_lib.bc_set_result_peers.argtypes = [_vp, ctypes.POINTER(_vp), ctypes.c_int, ctypes.c_int64]
+_lib.bc_set_result_peers.restype = ctypes.c_int
 _lib.bc_sync.argtypes = [_vp, _vp]
 _lib.bc_sync.restype = ctypes.c_int
 _lib.bc_last_error.argtypes = [_vp]
@@ -94,6 +108,15 @@ bc_spectrum_A_import = _lib.bc_spectrum_A_import
 bc_correlate_rotations = _lib.bc_correlate_rotations
 bc_evaluate_points_spectral = _lib.bc_evaluate_points_spectral
 bc_sync = _lib.bc_sync
+bc_ipc_handle = _lib.bc_ipc_handle
+bc_ipc_open = _lib.bc_ipc_open
+bc_ipc_close = _lib.bc_ipc_close
+bc_spectrum_A_partial = _lib.bc_spectrum_A_partial
+bc_spectrum_A_partial_buffer = _lib.bc_spectrum_A_partial_buffer
+bc_spectrum_A_reduce = _lib.bc_spectrum_A_reduce
+bc_set_result_peers = _lib.bc_set_result_peers
+IPC_HANDLE_BYTES = 64
+MAX_PEERS = 8
 bc_last_error = _lib.bc_last_error
 bc_status_string = _lib.bc_status_string
 bc_query = _lib.bc_query
@@ -262,6 +285,44 @@ class Correlator:
     def spectrum_A_import(self):
         """Declare the buffer's contents (written by the caller) to be A's spectrum."""
         self._check(_lib.bc_spectrum_A_import(self._ctx))
+
+    # -- fused exchanges over peer memory (include/ballcorr.h; sharding.py drives them)
+    def ipc_handle(self, dev_ptr):
+        """64-byte cudaIpc handle (bytes) of a device allocation of this process."""
+        buf = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+        self._check(_lib.bc_ipc_handle(self._ctx, dev_ptr, buf))
+        return buf.raw
+
+    def ipc_open(self, handle):
+        """Map a peer's allocation; returns its device pointer in this process."""
+        ptr = _vp()
+        buf = ctypes.create_string_buffer(bytes(handle), IPC_HANDLE_BYTES)
+        self._check(_lib.bc_ipc_open(self._ctx, buf, ctypes.byref(ptr)))
+        return int(ptr.value)
+
+    def ipc_close(self, dev_ptr):
+        self._check(_lib.bc_ipc_close(self._ctx, dev_ptr))
+
+    def spectrum_A_partial(self, lo, hi, stream=None):
+        """Band spectrum of A's balls [lo, hi) into the context's partial buffer."""
+        self._check(_lib.bc_spectrum_A_partial(self._ctx, int(lo), int(hi), _stream_handle(stream)))
+
+    def spectrum_A_partial_buffer(self):
+        ptr, nbytes = _vp(), ctypes.c_int64()
+        self._check(_lib.bc_spectrum_A_partial_buffer(self._ctx, ctypes.byref(ptr), ctypes.byref(nbytes)))
+        return int(ptr.value), int(nbytes.value)
+
+    def spectrum_A_reduce(self, partial_ptrs, stream=None):
+        """A's spectrum = the sum of the ranks' partial spectra (device pointers, rank order),
+        read over peer memory by one kernel fused with the A'' build."""
+        arr = (_vp * len(partial_ptrs))(*[int(p) for p in partial_ptrs])
+        self._check(_lib.bc_spectrum_A_reduce(self._ctx, arr, len(partial_ptrs), _stream_handle(stream)))
+
+    def set_result_peers(self, buffers, base=0):
+        """Reduction records of later correlate calls also go to these device buffers at global
+        rotation index base + i (the fused result exchange); [] turns it off."""
+        arr = (_vp * max(len(buffers), 1))(*[int(p) for p in buffers])
+        self._check(_lib.bc_set_result_peers(self._ctx, arr, len(buffers), int(base)))
 
     def out_shape(self, n_rot, out_kind):
         kind = OUT_KINDS.get(out_kind, out_kind)

@@ -85,6 +85,9 @@ struct bc_ctx {
     ShapePlan plan[2];
     std::map<int, float2 *> d_tw;  // exp(-2 pi i m / L) per FFT length
     int *d_csr_off = nullptr, *d_csr_idx = nullptr;
+    int64_t csr_lo = 0, csr_hi = -1;  // A's balls the per-tile candidate lists cover (hi < 0: all)
+    float2 *d_Ahat_part = nullptr;    // partial band spectrum of a slice of A (bc_spectrum_A_partial)
+    ResultPeers res_peers{};          // fused result exchange (bc_set_result_peers)
     float4 *d_prof = nullptr;     // per-ball radial profile tables of B (cubic Hermite pieces)
     int *d_prof_off = nullptr;
     double dprof = 0;
@@ -739,14 +742,17 @@ bc_status build_query_grid(bc_ctx *ctx)
     return BC_OK;
 }
 
-bc_status build_csr_A(bc_ctx *ctx)
+bc_status build_csr_A(bc_ctx *ctx, int64_t lo = 0, int64_t hi = -1)
 {
+    if (hi < 0) hi = ctx->n[0];
+    ctx->csr_lo = lo;
+    ctx->csr_hi = hi == ctx->n[0] ? -1 : hi;
     const ShapePlan &pl = ctx->plan[0];
     const int tpa = (pl.L + 15) / 16;
     const int ntiles = tpa * tpa * tpa;
     std::vector<std::vector<int>> lists(ntiles);
     const std::vector<double> &x = ctx->hxyzr[0];
-    for (int64_t i = 0; i < ctx->n[0]; i++) {
+    for (int64_t i = lo; i < hi; i++) {
         double u[3];
         int t0[3], t1[3];
         const double rc = (x[4 * i + 3] + pl.cut) / pl.hf;
@@ -1488,7 +1494,9 @@ bc_status run_rotations(bc_ctx *ctx, int64_t n_rot, int out_kind, char *dout, si
             }
             if (out_kind != BC_OUT_F_FULL) {
                 StageScope sc(ctx, s, "finalize");
-                launch_keys_finalize(keys, b, out_kind, dout + out_per * r0, s);
+                ResultPeers rp = ctx->res_peers;
+                rp.base += r0;
+                launch_keys_finalize(keys, b, out_kind, dout + out_per * r0, rp, s);
                 ctx->launches++;
             }
             CU(ctx, cudaGetLastError());
@@ -1749,6 +1757,7 @@ bc_status bc_destroy(bc_ctx *ctx)
     dfree(ctx->d_qout);
     dfree(ctx->d_Ahat);
     dfree(ctx->d_Ahat_cm);
+    dfree(ctx->d_Ahat_part);
     dfree(ctx->d_xtab);
     dfree(ctx->d_segs);
 
@@ -1864,6 +1873,7 @@ bc_status bc_spectrum_A(bc_ctx *ctx, void *stream)
         ctx->have_spec = true;
         return BC_OK;
     }
+    if (ctx->csr_lo != 0 || ctx->csr_hi >= 0) TRY(build_csr_A(ctx));  // after a partial spectrum
     // A's spread / z / y passes run in the context's batch workspaces (slot 0; kept, grown
     // when A's plan needs more): no allocation and no synchronisation per call
     size_t s1, s2;
@@ -2103,6 +2113,150 @@ bc_status bc_evaluate_points_spectral(bc_ctx *ctx, const double *R, const double
         }
     }
     if (host_out) TRY(check_deferred(ctx));
+    return BC_OK;
+}
+
+// ------------------------------------------------------------------ fused exchanges (collectives.cu)
+
+bc_status bc_ipc_handle(bc_ctx *ctx, const void *dev_ptr, void *handle)
+{
+    if (!ctx) return BC_EINVAL;
+    if (!dev_ptr || !handle) return fail(ctx, BC_EINVAL, "NULL dev_ptr/handle");
+    CU(ctx, cudaSetDevice(ctx->device));
+    cudaIpcMemHandle_t h;
+    CU(ctx, cudaIpcGetMemHandle(&h, (void *)dev_ptr));
+    static_assert(sizeof(h) == BC_IPC_HANDLE_BYTES, "IPC handle size");
+    memcpy(handle, &h, sizeof(h));
+    return BC_OK;
+}
+
+bc_status bc_ipc_open(bc_ctx *ctx, const void *handle, void **dev_ptr)
+{
+    if (!ctx) return BC_EINVAL;
+    if (!dev_ptr || !handle) return fail(ctx, BC_EINVAL, "NULL dev_ptr/handle");
+    CU(ctx, cudaSetDevice(ctx->device));
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    CU(ctx, cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return BC_OK;
+}
+
+bc_status bc_ipc_close(bc_ctx *ctx, void *dev_ptr)
+{
+    if (!ctx) return BC_EINVAL;
+    CU(ctx, cudaSetDevice(ctx->device));
+    CU(ctx, cudaIpcCloseMemHandle(dev_ptr));
+    return BC_OK;
+}
+
+bc_status bc_spectrum_A_partial_buffer(bc_ctx *ctx, void **dev_ptr, int64_t *bytes)
+{
+    if (!ctx) return BC_EINVAL;
+    if (!dev_ptr || !bytes) return fail(ctx, BC_EINVAL, "NULL dev_ptr/bytes");
+    if (ctx->p.mode != BC_MODE_SPECTRAL) return fail(ctx, BC_EUNSUPPORTED, "exact mode has no spectrum of A");
+    CU(ctx, cudaSetDevice(ctx->device));
+    const size_t nspec = (size_t)ctx->M * ctx->M * ctx->Kz;
+    if (!ctx->d_Ahat_part) TRY(dalloc(ctx, &ctx->d_Ahat_part, sizeof(float2) * nspec));
+    *dev_ptr = ctx->d_Ahat_part;
+    *bytes = (int64_t)(sizeof(float2) * nspec);
+    return BC_OK;
+}
+
+bc_status bc_spectrum_A_partial(bc_ctx *ctx, int64_t lo, int64_t hi, void *stream)
+{
+    if (!ctx) return BC_EINVAL;
+    TRY(check_deferred(ctx));
+    if (!ctx->have[0]) return fail(ctx, BC_ESTATE, "shape A has not been uploaded");
+    if (ctx->p.mode != BC_MODE_SPECTRAL) return fail(ctx, BC_EUNSUPPORTED, "exact mode has no spectrum of A");
+    if (lo < 0 || hi < lo || hi > ctx->n[0]) return fail(ctx, BC_EINVAL, "ball slice [%lld, %lld) outside [0, %lld)",
+                                                         (long long)lo, (long long)hi, (long long)ctx->n[0]);
+    CU(ctx, cudaSetDevice(ctx->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    void *part = nullptr;
+    int64_t bytes = 0;
+    TRY(bc_spectrum_A_partial_buffer(ctx, &part, &bytes));
+    if (hi == lo) {
+        CU(ctx, cudaMemsetAsync(part, 0, (size_t)bytes, s));
+        return BC_OK;
+    }
+    CU(ctx, cudaStreamSynchronize(s));  // the candidate lists below are rebuilt on the host
+    TRY(build_csr_A(ctx, lo, hi));
+    size_t s1, s2;
+    spectral_ws_sizes(ctx, 0, s1, s2);
+    Slot &sl = ctx->slot[0];
+    TRY(ensure_ws(ctx, &sl.ws1, sl.ws1_bytes, s1));
+    TRY(ensure_ws(ctx, &sl.ws2, sl.ws2_bytes, s2));
+    float2 *full = ctx->d_Ahat;
+    ctx->d_Ahat = (float2 *)part;  // shape_spectrum's x pass writes d_Ahat
+    const bc_status st = shape_spectrum(ctx, 0, nullptr, 1, sl.ws1, sl.ws2, s1, s2, s, sl);
+    ctx->d_Ahat = full;
+    TRY(st);
+    if (ctx->prof) collect_profile(ctx);
+    return BC_OK;
+}
+
+bc_status bc_spectrum_A_reduce(bc_ctx *ctx, const void *const *partials, int n, void *stream)
+{
+    if (!ctx) return BC_EINVAL;
+    TRY(check_deferred(ctx));
+    if (!partials || n < 1 || n > BC_MAX_PEERS) return fail(ctx, BC_EINVAL, "need 1..%d partial spectra", BC_MAX_PEERS);
+    for (int r = 0; r < n; r++)
+        if (!partials[r]) return fail(ctx, BC_EINVAL, "partial spectrum %d is NULL", r);
+    if (ctx->p.mode != BC_MODE_SPECTRAL) return fail(ctx, BC_EUNSUPPORTED, "exact mode has no spectrum of A");
+    if (!ctx->have[0] || !ctx->have[1]) return fail(ctx, BC_ESTATE, "upload both shapes first (A'' needs B's plan)");
+    if (!ctx->plan[1].ok) return fail(ctx, BC_ESTATE, "shape B has no spectral plan (empty B)");
+    CU(ctx, cudaSetDevice(ctx->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t nspec = (size_t)ctx->M * ctx->M * ctx->Kz;
+    if (!ctx->d_Ahat) TRY(dalloc(ctx, &ctx->d_Ahat, sizeof(float2) * nspec));
+    const bool cplx = ctx->p.weights == BC_WEIGHTS_COMPLEX;
+    const ShapePlan &pb = ctx->plan[1];
+    ctx->MS = cm_row_stride(pb.L, pb.c, pb.G, ctx->K);
+    const size_t ncm = (size_t)ctx->MS * ctx->M * ctx->Kz;
+    if (ctx->Ahat_cm_bytes < sizeof(float2) * ncm) {
+        TRY(dalloc(ctx, &ctx->d_Ahat_cm, sizeof(float2) * ncm));
+        ctx->Ahat_cm_bytes = sizeof(float2) * ncm;
+    }
+    ReducePermuteArgs a{};
+    for (int r = 0; r < n; r++) a.parts[r] = (const float2 *)partials[r];
+    a.n_parts = n;
+    a.Ahat = ctx->d_Ahat;
+    a.mult = pb.d_mult[0];
+    a.out = ctx->d_Ahat_cm;
+    a.rows = (long long)ctx->M * ctx->Kz;
+    a.K = ctx->K;
+    a.L = pb.L;
+    a.c = pb.c;
+    a.G = pb.G;
+    a.neg = cplx;
+    a.MS = ctx->MS;
+    a.Kz = ctx->Kz;
+    a.R2 = ctx->p.band_radius > 0 ? ctx->p.band_radius * ctx->p.band_radius : 0.0;
+    a.dec = pb.blob ? ctx->d_dec : nullptr;
+    {
+        StageScope sc(ctx, s, "reduce_permute");
+        launch_reduce_permute(a, s);
+        ctx->launches++;
+    }
+    CU(ctx, cudaGetLastError());
+    ctx->cm_ready = true;
+    ctx->have_spec = true;
+    ctx->probe_done = false;
+    ctx->qs_ready = false;
+    return BC_OK;
+}
+
+bc_status bc_set_result_peers(bc_ctx *ctx, void *const *buffers, int n, int64_t base)
+{
+    if (!ctx) return BC_EINVAL;
+    if (n < 0 || n > BC_MAX_PEERS || (n > 0 && !buffers) || base < 0)
+        return fail(ctx, BC_EINVAL, "need 0..%d result buffers and base >= 0", BC_MAX_PEERS);
+    for (int r = 0; r < n; r++)
+        if (!buffers[r]) return fail(ctx, BC_EINVAL, "result buffer %d is NULL", r);
+    ctx->res_peers = ResultPeers{};
+    for (int r = 0; r < n; r++) ctx->res_peers.buf[r] = buffers[r];
+    ctx->res_peers.n = n;
+    ctx->res_peers.base = base;
     return BC_OK;
 }
 

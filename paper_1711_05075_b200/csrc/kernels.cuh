@@ -3,6 +3,8 @@
 
 #include "common.cuh"
 
+#include "ballcorr.h"  // BC_MAX_PEERS: ranks of one NVLink / NVSwitch domain (one box)
+
 // ----------------------------------------------------------------- spreading
 // Gaussian-smoothed ball density on a box of the fine lattice (spacing hf):
 //   rho_s(x_n) = sum_j v_j (1_{B(c_j, s_j)} * G_tau)(x_n),  x_n = (o + n) hf,  n in [0, L)^3
@@ -219,7 +221,29 @@ void launch_last(const LastArgs &a, int batch, cudaStream_t s);
 void launch_permute_cm(const float2 *in, const float2 *mult, float2 *out, long long rows, int K, int L, int c, int G,
                        int neg, int MS, int Kz, double band_radius, const float *dec, cudaStream_t s);
 void launch_keys_init(unsigned long long *keys, int n, cudaStream_t s);
-void launch_keys_finalize(const unsigned long long *keys, int batch, int out_kind, void *out, cudaStream_t s);
+// peers: result buffers (bc_extremum[], device pointers, possibly mapped from other GPUs) that
+// receive the same records at global rotation index peer_base + r (nullptr / 0: none)
+struct ResultPeers {
+    void *buf[BC_MAX_PEERS];
+    int n;
+    long long base;
+};
+void launch_keys_finalize(const unsigned long long *keys, int batch, int out_kind, void *out, const ResultPeers &peers,
+                          cudaStream_t s);
+
+// collectives.cu: all-reduce of partial spectra (peer reads) fused into the A'' build
+struct ReducePermuteArgs {
+    const float2 *parts[BC_MAX_PEERS];  // partial band spectra [ky][kz][kx], one per rank, rank order
+    int n_parts;
+    float2 *Ahat;                       // reduced spectrum (this rank)
+    const float2 *mult;                 // B's x multipliers
+    float2 *out;                        // A'' (coset-major rows, stride MS)
+    long long rows;
+    int K, L, c, G, neg, MS, Kz;
+    double R2;
+    const float *dec;
+};
+void launch_reduce_permute(const ReducePermuteArgs &a, cudaStream_t s);
 
 // ----------------------------------------------------------------- exact mode
 struct ExactArgs {

@@ -838,7 +838,8 @@ void launch_keys_init(unsigned long long *keys, int n, cudaStream_t s)
     keys_init_kernel<<<(n + 255) / 256, 256, 0, s>>>(keys, n);
 }
 
-__global__ void keys_finalize_kernel(const unsigned long long *keys, int batch, int kind, bc_extremum *out)
+__global__ void keys_finalize_kernel(const unsigned long long *keys, int batch, int kind, bc_extremum *out,
+                                     ResultPeers peers)
 {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= batch) return;
@@ -848,16 +849,22 @@ __global__ void keys_finalize_kernel(const unsigned long long *keys, int batch, 
     emin.idx = (int64_t)(kmin & 0xffffffffull);
     emax.val = (double)float_from_order_bits((uint32_t)(kmax >> 32));
     emax.idx = (int64_t)(0xffffffffull - (kmax & 0xffffffffull));
-    if (kind == BC_OUT_MIN_ARGMIN)
-        out[r] = emin;
-    else if (kind == BC_OUT_MINMAX) {
-        out[2 * r] = emin;
-        out[2 * r + 1] = emax;
-    } else
-        out[r] = emax;
+    const int per = kind == BC_OUT_MINMAX ? 2 : 1;
+    const bc_extremum e0 = kind == BC_OUT_MAX_ARGMAX || kind == BC_OUT_MAX_REAL ? emax : emin;
+    out[per * r] = e0;
+    if (per == 2) out[2 * r + 1] = emax;
+    // fused result exchange (collectives.cu): the same records into every peer's buffer at the
+    // rotation's global index -- NVLink stores instead of an all-gather after the step
+    for (int p = 0; p < peers.n; p++) {
+        bc_extremum *o = (bc_extremum *)peers.buf[p] + per * (peers.base + r);
+        o[0] = e0;
+        if (per == 2) o[1] = emax;
+    }
+    if (peers.n) __threadfence_system();
 }
 
-void launch_keys_finalize(const unsigned long long *keys, int batch, int out_kind, void *out, cudaStream_t s)
+void launch_keys_finalize(const unsigned long long *keys, int batch, int out_kind, void *out, const ResultPeers &peers,
+                          cudaStream_t s)
 {
-    keys_finalize_kernel<<<(batch + 127) / 128, 128, 0, s>>>(keys, batch, out_kind, (bc_extremum *)out);
+    keys_finalize_kernel<<<(batch + 127) / 128, 128, 0, s>>>(keys, batch, out_kind, (bc_extremum *)out, peers);
 }

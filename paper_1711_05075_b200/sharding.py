@@ -67,3 +67,58 @@ def global_best(vals: np.ndarray, idxs: np.ndarray, kind: str = "min"):
     """(rotation, value, translation index) of the best rotation; ties -> lowest rotation."""
     r = int(np.argmin(vals)) if kind == "min" else int(np.argmax(vals))
     return r, float(vals[r]), int(idxs[r])
+
+
+# ----------------------------------------------------------------------------- fused exchanges
+# (SURVEY §8(f) N4; include/ballcorr.h "Fused exchanges over peer memory").  The library does
+# the data movement inside its kernels over NVLink; these helpers only move the 64-byte IPC
+# handles between the processes and order the steps with barriers.
+
+def _exchange_handles(corr, ptr, group=None):
+    """Every rank's device pointer for `ptr`'s peer allocation, in rank order (own pointer as
+    is, the others mapped through cudaIpc)."""
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    handles = [None] * world
+    dist.all_gather_object(handles, corr.ipc_handle(ptr), group=group)
+    return [ptr if r == rank else corr.ipc_open(handles[r]) for r in range(world)]
+
+
+def allreduce_spectrum_A_p2p(corr, n_A: int, group=None, sync=None):
+    """A's spectrum sharded by balls: rank g computes the partial spectrum of its contiguous
+    block of A's balls, then one kernel per rank reads every rank's partial over peer memory,
+    sums them in rank order and builds A'' (bc_spectrum_A_reduce).  Every rank ends with the
+    same spectrum bits.  `sync()` waits for the device (torch.cuda.synchronize by default)."""
+    import torch.distributed as dist
+    if sync is None:
+        import torch
+        sync = torch.cuda.synchronize
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    lo, hi = rotation_block(n_A, rank, world)
+    corr.spectrum_A_partial(lo, hi)
+    own, _ = corr.spectrum_A_partial_buffer()
+    ptrs = _exchange_handles(corr, own, group)
+    sync()
+    dist.barrier(group=group)          # every partial is complete
+    corr.spectrum_A_reduce(ptrs)
+    sync()
+    dist.barrier(group=group)          # every rank has read every partial
+    for r, p in enumerate(ptrs):
+        if r != rank:
+            corr.ipc_close(p)
+    return lo, hi
+
+
+def result_peers_p2p(corr, global_buf_ptr, n_rot: int, group=None):
+    """Fused result exchange: every rank allocates the WHOLE job's record buffer
+    (`global_buf_ptr`, n_rot bc_extremum records); the reduction epilogue of each rank then
+    stores its rotations' records into every rank's buffer at their global indices
+    (bc_set_result_peers), so no all-gather follows the step -- a barrier after the step is
+    all the caller needs before reading.  Returns (this rank's rotation block, mapped pointers
+    to close at the end)."""
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    start, stop = rotation_block(n_rot, rank, world)
+    ptrs = _exchange_handles(corr, global_buf_ptr, group)
+    corr.set_result_peers(ptrs, base=start)
+    return (start, stop), [p for r, p in enumerate(ptrs) if r != rank]

@@ -117,3 +117,80 @@ def test_broadcast_spectrum_gloo(world, src):
     res = dict(q.get(timeout=10) for _ in range(world))
     assert all(res[r] for r in range(world)), res
     assert all(p.exitcode == 0 for p in procs)
+
+
+class _FakePeerCorrelator:
+    """CPU stand-in for the fused-exchange API: 'device pointers' are (rank, name) tokens and
+    IPC handles encode them, so the protocol's pointer lists can be checked across ranks."""
+
+    def __init__(self, rank):
+        self.rank = rank
+        self.calls = []
+        self.opened, self.closed = [], []
+
+    def spectrum_A_partial(self, lo, hi):
+        self.calls.append(("partial", lo, hi))
+
+    def spectrum_A_partial_buffer(self):
+        return ("part", self.rank), 0
+
+    def ipc_handle(self, ptr):
+        return repr(ptr).encode()
+
+    def ipc_open(self, handle):
+        p = ("mapped",) + eval(handle.decode())
+        self.opened.append(p)
+        return p
+
+    def ipc_close(self, p):
+        self.closed.append(p)
+
+    def spectrum_A_reduce(self, ptrs):
+        self.calls.append(("reduce", list(ptrs)))
+
+    def set_result_peers(self, ptrs, base=0):
+        self.calls.append(("peers", list(ptrs), base))
+
+
+def _p2p_worker(rank, world, port, n_A, n_rot, q):
+    import torch.distributed as dist
+    from paper_1711_05075_b200.sharding import allreduce_spectrum_A_p2p, result_peers_p2p
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    c = _FakePeerCorrelator(rank)
+    lo, hi = allreduce_spectrum_A_p2p(c, n_A, sync=lambda: None)
+    (s, e), to_close = result_peers_p2p(c, ("glob", rank), n_rot)
+    q.put((rank, lo, hi, s, e, c.calls, c.opened, c.closed, to_close))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_fused_exchange_protocol_gloo(world):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    n_A, n_rot = 50000, 512
+    procs = [ctx.Process(target=_p2p_worker, args=(r, world, port, n_A, n_rot, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    res = {r[0]: r for r in (q.get(timeout=10) for _ in range(world))}
+    assert all(p.exitcode == 0 for p in procs)
+    # A's balls and the rotations are covered by contiguous blocks in rank order
+    assert [res[r][1] for r in range(world)][0] == 0 and res[world - 1][2] == n_A
+    assert all(res[r][2] == res[r + 1][1] for r in range(world - 1))
+    assert all(res[r][4] == res[r + 1][3] for r in range(world - 1)) and res[world - 1][4] == n_rot
+    for r in range(world):
+        calls = res[r][5]
+        assert calls[0] == ("partial", res[r][1], res[r][2])
+        # the reduce reads every rank's partial in rank order: own pointer, peers mapped
+        expect = [("part", g) if g == r else ("mapped", "part", g) for g in range(world)]
+        assert calls[1] == ("reduce", expect)
+        # mapped partials are closed after the reduce; the result buffers stay mapped
+        assert sorted(res[r][7]) == sorted(p for p in expect if p[0] == "mapped")
+        expect_glob = [("glob", g) if g == r else ("mapped", "glob", g) for g in range(world)]
+        assert calls[2] == ("peers", expect_glob, res[r][3])
+        assert sorted(res[r][8]) == sorted(p for p in expect_glob if p[0] == "mapped")
