@@ -161,3 +161,20 @@ def test_blob_fused_path_vs_bandlimited(bc, oracle_mod, seed):
     assert g.query("blob_B") == 0
     fg = g.correlate_rotations(w.R, "full")
     assert rel_max_err(f, fg) <= IMPL_TOL
+
+
+@pytest.mark.parametrize("rho", [9.5, 17.0])
+def test_band_radius_is_the_spherical_band(bc, oracle_mod, rho):
+    """bc_params.band_radius > 0 restricts the cube band |k_i| <= K to |k| <= band_radius (A's
+    band spectrum is zeroed outside the sphere when the fold's A'' layout is built): the
+    result is the band-limited f of the spherical band -- the oracle's K_sphere (pinned in
+    tests/test_oracle.py)."""
+    w = random_small_case(53, n_a=10, n_b=8, n_rot=2, N=16)
+    Np, K = 24, 20
+    P = Np * w.h
+    c = spectral(bc, w, Np, K, band_radius=rho)
+    f = c.correlate_rotations(w.R, "full")
+    for r in range(w.n_rot):
+        ref = oracle_mod.bandlimited_correlation(w.A_xyzr, w.A_w, w.B_xyzr, w.B_w, w.R[r], w.N, w.h, w.t0, P, K,
+                                                 K_sphere=rho)
+        assert rel_max_err(f[r], ref) <= IMPL_TOL, (rho, r, rel_max_err(f[r], ref))
