@@ -126,6 +126,8 @@ struct bc_ctx {
     size_t acc_bytes = 0;
     bool ex_ready = false;          // exact_plan() for the current shapes
     double ex_qscale = 1.0;
+    bool ex_thread_per_knot = false;
+    int *d_permB = nullptr;         // B's balls by radius (exact mode, thread-per-knot kernel)
     double *d_part = nullptr;
     long long *d_part_idx = nullptr;
     int part_cap = 0;
@@ -1160,6 +1162,23 @@ bc_status exact_plan(bc_ctx *ctx)
         }
     const double bound = std::min(sAi * sB1, sA1 * sBi);
     ctx->ex_qscale = bound > 0 ? std::ldexp(1.0, 61) / bound : 1.0;
+    // kernel choice (measured, Tiny / Single): a thread per knot walking its ball (B by radius)
+    // when there are enough knots to fill the GPU (>= 2^18) and footprints are small (mean box
+    // <= 1000 points): Single 0.60 -> 0.45 ms; else a warp per knot (Tiny: 1,024 knots, 0.034 ms
+    // vs 0.20 ms with a thread per knot)
+    double mr = 0, ms = 0;
+    for (int64_t i = 0; i < ctx->n[0]; i++) mr += ctx->hxyzr[0][4 * i + 3];
+    for (int64_t j = 0; j < ctx->n[1]; j++) ms += ctx->hxyzr[1][4 * j + 3];
+    mr /= std::max<int64_t>(ctx->n[0], 1);
+    ms /= std::max<int64_t>(ctx->n[1], 1);
+    const double side = 2 * (mr + ms) / ctx->p.h + 1;
+    ctx->ex_thread_per_knot = side * side * side <= 1000.0 && (double)ctx->n[0] * ctx->n[1] >= 262144.0;
+    std::vector<int> perm((size_t)std::max<int64_t>(ctx->n[1], 1), 0);
+    for (int64_t j = 0; j < ctx->n[1]; j++) perm[j] = (int)j;
+    std::stable_sort(perm.begin(), perm.begin() + ctx->n[1],
+                     [&](int x, int y) { return ctx->hxyzr[1][4 * x + 3] < ctx->hxyzr[1][4 * y + 3]; });
+    TRY(dalloc(ctx, &ctx->d_permB, sizeof(int) * perm.size()));
+    CU(ctx, cudaMemcpy(ctx->d_permB, perm.data(), sizeof(int) * perm.size(), cudaMemcpyHostToDevice));
     ctx->ex_ready = true;
     return BC_OK;
 }
@@ -1293,6 +1312,8 @@ bc_status run_rotations(bc_ctx *ctx, int64_t n_rot, int out_kind, char *dout, si
             a.iacc = (long long *)ctx->d_acc;
             a.acc_bstride = (long long)(per / sizeof(long long));
             a.qscale = ctx->ex_qscale;
+            a.thread_per_knot = ctx->ex_thread_per_knot ? 1 : 0;
+            a.permB = ctx->d_permB;
             {
                 StageScope sc(ctx, s, "exact_pairs");
                 launch_exact_scatter(a, b, s);
@@ -1765,6 +1786,7 @@ bc_status bc_destroy(bc_ctx *ctx)
     dfree(ctx->d_rot64);
     if (ctx->d_out_stage) cudaFree(ctx->d_out_stage);
     dfree(ctx->d_acc);
+    dfree(ctx->d_permB);
     dfree(ctx->d_part);
     dfree(ctx->d_part_idx);
     for (auto &pe : ctx->pending) {

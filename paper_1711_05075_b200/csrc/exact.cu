@@ -45,9 +45,8 @@ struct KnotBox {
     int lo[3], hi[3];  // grid point range (inclusive), empty if lo > hi on an axis
 };
 
-__device__ __forceinline__ KnotBox knot_box(const ExactArgs &a, int b, long long k)
+__device__ __forceinline__ KnotBox knot_box(const ExactArgs &a, int b, int i, int j)
 {
-    const int i = (int)(k / a.nB), j = (int)(k % a.nB);
     const double *R = a.rot + 9 * b;
     const double4 ai = a.A[i], bj = a.B[j];
     KnotBox kb;
@@ -69,20 +68,20 @@ __device__ __forceinline__ KnotBox knot_box(const ExactArgs &a, int b, long long
 __device__ __forceinline__ long long to_fixed(double x) { return __double2ll_rn(x); }
 __device__ __forceinline__ long long to_fixed(float x) { return __float2ll_rn(x); }
 
-// Warp per obstacle knot: lanes own the grid points of the knot's footprint box and add their
+// Warp per obstacle knot: lanes own (y, z) columns of the knot's footprint box, walk x, and add their
 // fixed-point terms to the output accumulator with 64-bit integer reductions (RED.E.ADD.64:
 // associative, so the result does not depend on which warp adds first -- deterministic).
 template <typename T, bool CPLX>
 __global__ void __launch_bounds__(256) exact_scatter_kernel(ExactArgs a)
 {
-    const int b = blockIdx.y;
-    const long long k = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    // grid (ceil(nB / 8), A chunk, rotation): warp w of the block = knot (i, j), no division
+    const int b = blockIdx.z;
+    const int i = a.i0 + blockIdx.y, j = blockIdx.x * 8 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
-    if (k >= (long long)a.nA * a.nB) return;
-    const KnotBox kb = knot_box(a, b, k);
+    if (j >= a.nB) return;
+    const KnotBox kb = knot_box(a, b, i, j);
     const int nx = kb.hi[0] - kb.lo[0] + 1, ny = kb.hi[1] - kb.lo[1] + 1, nz = kb.hi[2] - kb.lo[2] + 1;
     if (nx <= 0 || ny <= 0 || nz <= 0) return;
-    const int i = (int)(k / a.nB), j = (int)(k % a.nB);
     const double ih = a.inv_h;
     // centre relative to the box's first point and radii, grid units
     const T cx = (T)((kb.cx - a.t0x) * ih - kb.lo[0]), cy = (T)((kb.cy - a.t0y) * ih - kb.lo[1]),
@@ -94,29 +93,96 @@ __global__ void __launch_bounds__(256) exact_scatter_kernel(ExactArgs a)
     const T wr = (T)((wa.x * wb.x - wa.y * wb.y) * h3q), wi = (T)((wa.x * wb.y + wa.y * wb.x) * h3q);
     const long long N = a.N, N3 = N * N * N;
     unsigned long long *acc = (unsigned long long *)a.iacc + (long long)b * a.acc_bstride;
-    const int nyz = ny * nz, tot = nx * nyz;
-    for (int q = lane; q < tot; q += 32) {
-        const int ix = q / nyz, iy = (q / nz) % ny, iz = q % nz;
-        const T dx = cx - (T)ix, dy = cy - (T)iy, dz = cz - (T)iz;
-        const T d2 = dx * dx + dy * dy + dz * dz;
-        if (d2 >= rho2) continue;
-        const T v = lens_volume_dev<T>(r, s, sqrt(d2));
-        const long long idx = ((long long)(kb.lo[0] + ix) * N + (kb.lo[1] + iy)) * N + (kb.lo[2] + iz);
-        atomicAdd(acc + idx, (unsigned long long)to_fixed(wr * v));
-        if (CPLX) atomicAdd(acc + N3 + idx, (unsigned long long)to_fixed(wi * v));
+    // lanes own (y, z) columns of the footprint box (one division per column) and walk x
+    const int nyz = ny * nz;
+    for (int q = lane; q < nyz; q += 32) {
+        const int iy = q / nz, iz = q - (q / nz) * nz;
+        const T dy = cy - (T)iy, dz = cz - (T)iz;
+        const T dyz2 = dy * dy + dz * dz;
+        if (dyz2 >= rho2) continue;
+        const long long row = ((long long)kb.lo[0] * N + (kb.lo[1] + iy)) * N + (kb.lo[2] + iz);
+        for (int ix = 0; ix < nx; ix++) {
+            const T dx = cx - (T)ix;
+            const T d2 = dx * dx + dyz2;
+            if (d2 >= rho2) continue;
+            const T v = lens_volume_dev<T>(r, s, sqrt(d2));
+            const long long idx = row + (long long)ix * N * N;
+            atomicAdd(acc + idx, (unsigned long long)to_fixed(wr * v));
+            if (CPLX) atomicAdd(acc + N3 + idx, (unsigned long long)to_fixed(wi * v));
+        }
     }
 }
 
-void launch_exact_scatter(const ExactArgs &a, int batch, cudaStream_t s)
+// Thread per obstacle knot (for small footprints, where a warp per knot idles most lanes):
+// the thread walks the grid points INSIDE the obstacle ball (per (x, y) row its z range from
+// the chord), B's balls taken in order of radius (a.permB) so a warp's 32 knots have similar
+// footprints; the same fixed-point integer reductions as above.
+template <typename T, bool CPLX>
+__global__ void __launch_bounds__(256) exact_knot_kernel(ExactArgs a)
 {
-    const long long warps = (long long)a.nA * a.nB;
-    dim3 grid((unsigned)((warps * 32 + 255) / 256), batch);
-    if (a.fp64) {
-        if (a.complex_w) exact_scatter_kernel<double, true><<<grid, 256, 0, s>>>(a);
-        else exact_scatter_kernel<double, false><<<grid, 256, 0, s>>>(a);
-    } else {
-        if (a.complex_w) exact_scatter_kernel<float, true><<<grid, 256, 0, s>>>(a);
-        else exact_scatter_kernel<float, false><<<grid, 256, 0, s>>>(a);
+    const int b = blockIdx.z;
+    const int i = a.i0 + blockIdx.y, jj = blockIdx.x * 256 + threadIdx.x;
+    if (jj >= a.nB) return;
+    const int j = a.permB[jj];
+    const KnotBox kb = knot_box(a, b, i, j);
+    const int nx = kb.hi[0] - kb.lo[0] + 1, ny = kb.hi[1] - kb.lo[1] + 1, nz = kb.hi[2] - kb.lo[2] + 1;
+    if (nx <= 0 || ny <= 0 || nz <= 0) return;
+    const double ih = a.inv_h;
+    const T cx = (T)((kb.cx - a.t0x) * ih - kb.lo[0]), cy = (T)((kb.cy - a.t0y) * ih - kb.lo[1]),
+            cz = (T)((kb.cz - a.t0z) * ih - kb.lo[2]);
+    const double rr = a.A[i].w * ih, ss = a.B[j].w * ih;
+    const T r = (T)rr, s = (T)ss, rho2 = (T)((rr + ss) * (rr + ss));
+    const double2 wa = a.wA[i], wb = a.wB[j];
+    const double h3q = a.h * a.h * a.h * a.qscale;
+    const T wr = (T)((wa.x * wb.x - wa.y * wb.y) * h3q), wi = (T)((wa.x * wb.y + wa.y * wb.x) * h3q);
+    const long long N = a.N, N3 = N * N * N;
+    unsigned long long *acc = (unsigned long long *)a.iacc + (long long)b * a.acc_bstride;
+    for (int ix = 0; ix < nx; ix++) {
+        const T dx = cx - (T)ix;
+        for (int iy = 0; iy < ny; iy++) {
+            const T dy = cy - (T)iy;
+            const T dxy2 = dx * dx + dy * dy;
+            if (dxy2 >= rho2) continue;
+            const T hz = sqrt(rho2 - dxy2);
+            const int z0 = max(0, (int)ceil(cz - hz)), z1 = min(nz - 1, (int)floor(cz + hz));
+            const long long row = ((long long)(kb.lo[0] + ix) * N + (kb.lo[1] + iy)) * N + kb.lo[2];
+            for (int iz = z0; iz <= z1; iz++) {
+                const T dz = cz - (T)iz;
+                const T d2 = dxy2 + dz * dz;
+                if (d2 >= rho2) continue;
+                const T v = lens_volume_dev<T>(r, s, sqrt(d2));
+                atomicAdd(acc + row + iz, (unsigned long long)to_fixed(wr * v));
+                if (CPLX) atomicAdd(acc + N3 + row + iz, (unsigned long long)to_fixed(wi * v));
+            }
+        }
+    }
+}
+
+void launch_exact_scatter(const ExactArgs &a_in, int batch, cudaStream_t s)
+{
+    ExactArgs a = a_in;
+    for (int i0 = 0; i0 < a_in.nA; i0 += 65535) {  // grid.y limit: A in chunks
+        a.i0 = i0;
+        const unsigned ny = (unsigned)std::min(65535, a_in.nA - i0);
+        if (a.thread_per_knot) {
+            dim3 grid((unsigned)((a.nB + 255) / 256), ny, batch);
+            if (a.fp64) {
+                if (a.complex_w) exact_knot_kernel<double, true><<<grid, 256, 0, s>>>(a);
+                else exact_knot_kernel<double, false><<<grid, 256, 0, s>>>(a);
+            } else {
+                if (a.complex_w) exact_knot_kernel<float, true><<<grid, 256, 0, s>>>(a);
+                else exact_knot_kernel<float, false><<<grid, 256, 0, s>>>(a);
+            }
+        } else {
+            dim3 grid((unsigned)((a.nB + 7) / 8), ny, batch);
+            if (a.fp64) {
+                if (a.complex_w) exact_scatter_kernel<double, true><<<grid, 256, 0, s>>>(a);
+                else exact_scatter_kernel<double, false><<<grid, 256, 0, s>>>(a);
+            } else {
+                if (a.complex_w) exact_scatter_kernel<float, true><<<grid, 256, 0, s>>>(a);
+                else exact_scatter_kernel<float, false><<<grid, 256, 0, s>>>(a);
+            }
+        }
     }
 }
 

@@ -259,6 +259,9 @@ struct ExactArgs {
     long long *iacc;     // [b][N^3] (re) followed by [b][N^3] (im) when complex: fixed point, value * qscale
     long long acc_bstride;
     double qscale;       // 2^61 / (bound on |f|)
+    int i0;              // first A ball of the launch (set by launch_exact_scatter)
+    int thread_per_knot; // 1: thread per knot (small footprints), 0: warp per knot
+    const int *permB;    // B's balls in order of radius (thread-per-knot kernel)
 };
 void launch_exact_scatter(const ExactArgs &a, int batch, cudaStream_t s);
 

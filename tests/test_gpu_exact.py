@@ -120,6 +120,18 @@ def test_exact_is_deterministic_across_batchings(bc):
         outs.append(c.correlate_rotations(w.R, "full"))
     for o in outs[1:]:
         assert np.array_equal(o, outs[0])
+    # the thread-per-knot kernel (>= 2^18 small knots: the Single workload, 3 rotations)
+    ws = make_config("single")
+    R3 = random_rotations(np.random.default_rng(3), 3)
+    fs = []
+    for nb in (1, 3):
+        c = bc.Correlator(N=ws.N, h=ws.h, t0=ws.t0, mode="exact", precision="f32", max_batch=nb)
+        c.shape_upload(0, ws.A_xyzr, ws.A_w)
+        c.shape_upload(1, ws.B_xyzr, ws.B_w)
+        fs.append(c.correlate_rotations(R3, "full"))
+        fs.append(c.correlate_rotations(R3, "full"))
+    for o in fs[1:]:
+        assert np.array_equal(o, fs[0])
 
 
 def test_single_exact_reductions_and_large_knots(bc, oracle_mod):
