@@ -90,7 +90,10 @@ typedef struct {
     double t0[3];         /* grid origin */
     int32_t Np;           /* FFT period in grid cells: P = Np*h; Np >= N; factors in {2,3,5} (spectral) */
     int32_t K;            /* band half-width: modes |k_i| <= K, K < 4096 (spectral) */
-    int32_t precision;    /* bc_precision; SPECTRAL supports BC_FP32 only */
+    int32_t precision;    /* bc_precision; SPECTRAL with BC_FP64 is a parity mode: the same plan and
+                             method with direct fp64 sums instead of the fp32 FFT kernels (K <= 64,
+                             Np <= 256, box <= 160 cells, BC_OUT_F_FULL only; no tolerance probe,
+                             spectral query or spectrum exchange) */
     int32_t mode;         /* bc_mode */
     int32_t weights;      /* bc_weight_kind */
     int32_t max_batch;    /* rotations processed per launch; 0 = library default */

@@ -231,7 +231,7 @@ class Correlator:
         self.device = int(device)
         self.N = p.N
         self.complex = p.weights == BC_WEIGHTS_COMPLEX
-        self.f64 = p.precision == BC_FP64 and p.mode == BC_MODE_EXACT
+        self.f64 = p.precision == BC_FP64
         self._ctx = _vp()
         st = _lib.bc_create(int(device), ctypes.byref(p), ctypes.byref(self._ctx))
         if st != BC_OK:

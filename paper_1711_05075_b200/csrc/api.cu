@@ -159,6 +159,13 @@ struct bc_ctx {
     double *d_qs_mpart = nullptr;
     size_t qs_part_bytes = 0, qs_mpart_bytes = 0;
 
+    // spectral fp64 parity mode (spectral64.cu)
+    bool sp64 = false;
+    double2 *d_A64 = nullptr, *d_B64 = nullptr, *d_G64 = nullptr;
+    double2 *d_sp64_w1 = nullptr, *d_sp64_w2 = nullptr;
+    size_t sp64_ws_bytes = 0;
+    std::map<long long, double2 *> d_tw64;  // e^{-2 pi i r / G} per period G
+
     int64_t launches = 0;
     bool prof = false;
     std::vector<PendingEvent> pending;
@@ -336,7 +343,7 @@ bc_status plan_shape(bc_ctx *ctx, int which, const double lo[3], const double hi
 {
     const double P = ctx->P;
     const int K = ctx->K;
-    const double eps = ctx->p.spread_eps > 0 ? ctx->p.spread_eps : 1e-7;
+    const double eps = ctx->p.spread_eps > 0 ? ctx->p.spread_eps : (ctx->sp64 ? 1e-15 : 1e-7);
     const double lg = std::log(1.0 / eps);
     const int Gmin = 4 * (K + 1);
     double extent = 0;
@@ -347,7 +354,7 @@ bc_status plan_shape(bc_ctx *ctx, int which, const double lo[3], const double hi
     double best_cost = 1e300;
     // B with real weights: the fused spread + z kernel with the KB blob when a box size it
     // supports fits (G >= 4 (K + 1) as for the Gaussian: band |nu_i| <= 1/4 of the fine grid)
-    if (which == 1 && ctx->p.weights == BC_WEIGHTS_REAL && !ctx->p.generic_only) {
+    if (which == 1 && ctx->p.weights == BC_WEIGHTS_REAL && !ctx->p.generic_only && !ctx->sp64) {
         for (int c = 1; c <= 8; c++)
             for (int L : {128, 256}) {
                 if (!spread_z_supported(L) || c * L < Gmin) continue;
@@ -1269,10 +1276,171 @@ bc_status qs_prepare(bc_ctx *ctx, int64_t m_prime, cudaStream_t s)
     return BC_OK;
 }
 
+// ------------------------------------------------------------------ spectral fp64 parity mode
+
+bc_status sp64_twiddles(bc_ctx *ctx, long long G, double2 **out)
+{
+    auto it = ctx->d_tw64.find(G);
+    if (it != ctx->d_tw64.end()) {
+        *out = it->second;
+        return BC_OK;
+    }
+    std::vector<double2> t((size_t)G);
+    for (long long r = 0; r < G; r++) {
+        const double ang = -2 * kPi * (double)r / (double)G;
+        t[r] = make_double2(std::cos(ang), std::sin(ang));
+    }
+    double2 *d = nullptr;
+    CU(ctx, cudaMalloc(&d, sizeof(double2) * G));
+    CU(ctx, cudaMemcpy(d, t.data(), sizeof(double2) * G, cudaMemcpyHostToDevice));
+    ctx->d_tw64[G] = d;
+    *out = d;
+    return BC_OK;
+}
+
+// The band spectrum of shape `which` (rotated by the device matrix `rot` for B) into `band`
+// [kx][ky][kz] (full band, each axis k in [-K, K]): spread, then z, y, x axis DFTs.
+bc_status sp64_shape_spectrum(bc_ctx *ctx, int which, const double *rot, double2 *band, cudaStream_t s)
+{
+    const ShapePlan &pl = ctx->plan[which];
+    const int L = pl.L, M = ctx->M, K = ctx->K;
+    if (L > 160 || M > 129)
+        return fail(ctx, BC_EUNSUPPORTED, "spectral fp64 is a parity mode: box L = %d (<= 160), band M = %d (<= 129)", L,
+                    M);
+    const size_t N = ctx->p.N;
+    const size_t need = sizeof(double2) * std::max({(size_t)L * L * L, (size_t)L * L * M, N * M * M, N * N * M,
+                                                    N * N * N});
+    if (ctx->sp64_ws_bytes < need) {
+        TRY(dalloc(ctx, &ctx->d_sp64_w1, need));
+        TRY(dalloc(ctx, &ctx->d_sp64_w2, need));
+        ctx->sp64_ws_bytes = need;
+    }
+    double2 *tw = nullptr;
+    TRY(sp64_twiddles(ctx, pl.G, &tw));
+    Sp64SpreadArgs sa{};
+    sa.L = L;
+    for (int a = 0; a < 3; a++) sa.o[a] = pl.o[a];
+    sa.hf = pl.hf;
+    sa.tau = pl.tau;
+    sa.cut = pl.cut;
+    sa.balls = ctx->d_balls64[which];
+    sa.w = ctx->d_w64[which];
+    sa.n = (int)ctx->n[which];
+    sa.rot = rot;
+    sa.out = ctx->d_sp64_w1;
+    {
+        StageScope sc(ctx, s, which ? "sp64_spread_B" : "sp64_spread_A");
+        launch_sp64_spread(sa, s);
+        ctx->launches++;
+    }
+    Sp64DftArgs d{};
+    d.qlo = -K;
+    d.nlo = 0;
+    d.G = pl.G;
+    d.sign = -1;
+    d.tw = tw;
+    d.mult = 1;
+    d.hf = pl.hf;
+    d.tau = pl.tau;
+    d.P = ctx->P;
+    d.origin = which == 0;
+    d.nq = M;
+    d.Lin = L;
+    // z: box [ix][iy][iz] -> [ix][iy][kz]
+    d.in = ctx->d_sp64_w1;
+    d.out = ctx->d_sp64_w2;
+    d.O = L * L;
+    d.I = 1;
+    d.off = pl.o[2];
+    d.t0 = ctx->p.t0[2];
+    launch_sp64_dft(d, s);
+    // y: [ix][iy][kz] -> [ix][ky][kz]
+    d.in = ctx->d_sp64_w2;
+    d.out = ctx->d_sp64_w1;
+    d.O = L;
+    d.I = M;
+    d.off = pl.o[1];
+    d.t0 = ctx->p.t0[1];
+    launch_sp64_dft(d, s);
+    // x: [ix][ky][kz] -> band [kx][ky][kz]
+    d.in = ctx->d_sp64_w1;
+    d.out = band;
+    d.O = 1;
+    d.I = M * M;
+    d.off = pl.o[0];
+    d.t0 = ctx->p.t0[0];
+    launch_sp64_dft(d, s);
+    ctx->launches += 3;
+    CU(ctx, cudaGetLastError());
+    return BC_OK;
+}
+
+bc_status sp64_spectrum_A(bc_ctx *ctx, cudaStream_t s)
+{
+    const size_t M3 = (size_t)ctx->M * ctx->M * ctx->M;
+    if (!ctx->d_A64) TRY(dalloc(ctx, &ctx->d_A64, sizeof(double2) * M3));
+    if (ctx->n[0] == 0) {
+        CU(ctx, cudaMemsetAsync(ctx->d_A64, 0, sizeof(double2) * M3, s));
+        return BC_OK;
+    }
+    return sp64_shape_spectrum(ctx, 0, nullptr, ctx->d_A64, s);
+}
+
+// f for n_rot rotations (ctx->d_rot64), F_FULL only: B's band, G = A' B(-k), inverse x, y, z.
+bc_status sp64_run_rotations(bc_ctx *ctx, int64_t n_rot, int out_kind, char *dout, size_t out_per, cudaStream_t s)
+{
+    if (out_kind != BC_OUT_F_FULL)
+        return fail(ctx, BC_EUNSUPPORTED, "spectral fp64 (parity mode) returns the full field only");
+    const int M = ctx->M, K = ctx->K, N = ctx->p.N, Np = ctx->p.Np;
+    const size_t M3 = (size_t)M * M * M;
+    if (!ctx->d_B64) TRY(dalloc(ctx, &ctx->d_B64, sizeof(double2) * M3));
+    if (!ctx->d_G64) TRY(dalloc(ctx, &ctx->d_G64, sizeof(double2) * M3));
+    double2 *twN = nullptr;
+    TRY(sp64_twiddles(ctx, Np, &twN));
+    const bool cplx = ctx->p.weights == BC_WEIGHTS_COMPLEX;
+    for (int64_t r = 0; r < n_rot; r++) {
+        TRY(sp64_shape_spectrum(ctx, 1, ctx->d_rot64 + 9 * r, ctx->d_B64, s));
+        launch_sp64_product(ctx->d_A64, ctx->d_B64, ctx->d_G64, M, s);
+        Sp64DftArgs d{};
+        d.qlo = 0;
+        d.nlo = -K;
+        d.G = Np;
+        d.sign = +1;
+        d.tw = twN;
+        d.mult = 0;
+        d.nq = N;
+        d.Lin = M;
+        // inverse x: [kx][ky][kz] -> [mx][ky][kz]   (workspaces hold N M M <= L L M doubles)
+        d.in = ctx->d_G64;
+        d.out = ctx->d_sp64_w1;
+        d.O = 1;
+        d.I = M * M;
+        launch_sp64_dft(d, s);
+        // inverse y: [mx][ky][kz] -> [mx][my][kz]
+        d.in = ctx->d_sp64_w1;
+        d.out = ctx->d_sp64_w2;
+        d.O = N;
+        d.I = M;
+        launch_sp64_dft(d, s);
+        // inverse z: [mx][my][kz] -> [mx][my][mz]
+        d.in = ctx->d_sp64_w2;
+        d.out = ctx->d_sp64_w1;
+        d.O = N * N;
+        d.I = 1;
+        launch_sp64_dft(d, s);
+        launch_sp64_output(ctx->d_sp64_w1, (long long)N * N * N, 1.0 / (ctx->P * ctx->P * ctx->P), cplx,
+                           (double *)(dout + out_per * r), s);
+        ctx->launches += 5;
+        CU(ctx, cudaGetLastError());
+    }
+    return BC_OK;
+}
+
 // The per-rotation path for n_rot rotations already prepared in ctx->d_rot (fp32) and
 // ctx->d_rot64 (fp64), written to the device buffer dout (out_per bytes per rotation).
 bc_status run_rotations(bc_ctx *ctx, int64_t n_rot, int out_kind, char *dout, size_t out_per, cudaStream_t s)
 {
+    if (ctx->sp64) return sp64_run_rotations(ctx, n_rot, out_kind, dout, out_per, s);
     const bool cplx = ctx->p.weights == BC_WEIGHTS_COMPLEX;
     const long long N = ctx->p.N, N3 = N * N * N;
     if (ctx->p.mode == BC_MODE_EXACT) {
@@ -1535,7 +1703,7 @@ bc_status run_rotations(bc_ctx *ctx, int64_t n_rot, int out_kind, char *dout, si
 size_t out_elem_bytes(const bc_ctx *ctx, int kind)
 {
     const bool cplx = ctx->p.weights == BC_WEIGHTS_COMPLEX;
-    const bool f64 = ctx->p.precision == BC_FP64 && ctx->p.mode == BC_MODE_EXACT;
+    const bool f64 = ctx->p.precision == BC_FP64;
     if (kind == BC_OUT_F_FULL) {
         const size_t N3 = (size_t)ctx->p.N * ctx->p.N * ctx->p.N;
         return N3 * (f64 ? 8 : 4) * (cplx ? 2 : 1);
@@ -1695,12 +1863,14 @@ bc_status bc_create(int device, const bc_params *p, bc_ctx **out)
     if (p->max_batch < 0) return BC_EINVAL;
     if (p->concurrency < 0 || p->concurrency > 2) return BC_EINVAL;
     if (!(p->tolerance >= 0) || !std::isfinite(p->tolerance)) return BC_EINVAL;
+    if (p->mode == BC_MODE_SPECTRAL && p->precision == BC_FP64 && p->tolerance > 0) return BC_EUNSUPPORTED;
     if (p->mode == BC_MODE_SPECTRAL) {
-        if (p->precision != BC_FP32) return BC_EUNSUPPORTED;
+        // fp64: the parity mode of spectral64.cu (small problems, F_FULL output)
+        if (p->precision == BC_FP64 && (p->K > 64 || p->Np > 256)) return BC_EUNSUPPORTED;
         if (p->Np < p->N || p->Np < 2 || (p->Np % 2) != 0 || !friendly(p->Np) || p->Np > 1024) return BC_EINVAL;
         if (p->K < 1 || p->K > 2047) return BC_EINVAL;
         if (!(p->band_radius >= 0) || !std::isfinite(p->band_radius)) return BC_EINVAL;
-        if (!fft_size_supported(p->Np)) return BC_EUNSUPPORTED;
+        if (p->precision != BC_FP64 && !fft_size_supported(p->Np)) return BC_EUNSUPPORTED;  // fp64: direct DFTs
         if (p->N > 1625) return BC_EUNSUPPORTED;
     }
     int ndev = 0;
@@ -1719,6 +1889,7 @@ bc_status bc_create(int device, const bc_params *p, bc_ctx **out)
         ctx->M = 2 * p->K + 1;
         ctx->Kz = cplx ? ctx->M : p->K + 1;
         ctx->Fz = cplx ? p->Np : p->Np / 2 + 1;
+        ctx->sp64 = p->precision == BC_FP64;
         if (ensure_twiddles(ctx, p->Np) != BC_OK) {
             bc_destroy(ctx);
             return BC_ENOMEM;
@@ -1763,6 +1934,12 @@ bc_status bc_destroy(bc_ctx *ctx)
         if (sl.done) cudaEventDestroy(sl.done);
     }
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    dfree(ctx->d_A64);
+    dfree(ctx->d_B64);
+    dfree(ctx->d_G64);
+    dfree(ctx->d_sp64_w1);
+    dfree(ctx->d_sp64_w2);
+    for (auto &kv : ctx->d_tw64) cudaFree(kv.second);
     dfree(ctx->d_qs_modes);
     dfree(ctx->d_qs_k2);
     dfree(ctx->d_qs_mult);
@@ -1895,6 +2072,11 @@ bc_status bc_spectrum_A(bc_ctx *ctx, void *stream)
         ctx->have_spec = true;
         return BC_OK;
     }
+    if (ctx->sp64) {
+        TRY(sp64_spectrum_A(ctx, s));
+        ctx->have_spec = true;
+        return BC_OK;
+    }
     if (ctx->csr_lo != 0 || ctx->csr_hi >= 0) TRY(build_csr_A(ctx));  // after a partial spectrum
     // A's spread / z / y passes run in the context's batch workspaces (slot 0; kept, grown
     // when A's plan needs more): no allocation and no synchronisation per call
@@ -1912,6 +2094,7 @@ bc_status bc_spectrum_A(bc_ctx *ctx, void *stream)
 bc_status bc_spectrum_A_buffer(bc_ctx *ctx, void **dev_ptr, int64_t *bytes)
 {
     if (!ctx) return BC_EINVAL;
+    if (ctx->sp64) return fail(ctx, BC_EUNSUPPORTED, "the fp64 spectral parity mode keeps its spectrum private");
     if (!dev_ptr || !bytes) return fail(ctx, BC_EINVAL, "NULL dev_ptr/bytes");
     if (ctx->p.mode != BC_MODE_SPECTRAL) return fail(ctx, BC_EUNSUPPORTED, "exact mode has no spectrum of A");
     CU(ctx, cudaSetDevice(ctx->device));
@@ -1925,6 +2108,7 @@ bc_status bc_spectrum_A_buffer(bc_ctx *ctx, void **dev_ptr, int64_t *bytes)
 bc_status bc_spectrum_A_import(bc_ctx *ctx)
 {
     if (!ctx) return BC_EINVAL;
+    if (ctx->sp64) return fail(ctx, BC_EUNSUPPORTED, "the fp64 spectral parity mode keeps its spectrum private");
     if (ctx->p.mode != BC_MODE_SPECTRAL) return fail(ctx, BC_EUNSUPPORTED, "exact mode has no spectrum of A");
     if (!ctx->have[0]) return fail(ctx, BC_ESTATE, "shape A has not been uploaded");
     if (!ctx->d_Ahat) return fail(ctx, BC_ESTATE, "bc_spectrum_A_buffer has not been called");
@@ -2041,7 +2225,8 @@ bc_status bc_evaluate_points_spectral(bc_ctx *ctx, const double *R, const double
     if (!ctx) return BC_EINVAL;
     TRY(check_deferred(ctx));
     if (!R || !t || !out || n < 1) return fail(ctx, BC_EINVAL, "NULL R/t/out or n < 1");
-    if (ctx->p.mode != BC_MODE_SPECTRAL) return fail(ctx, BC_EUNSUPPORTED, "the spectral query needs spectral mode");
+    if (ctx->p.mode != BC_MODE_SPECTRAL || ctx->sp64)
+        return fail(ctx, BC_EUNSUPPORTED, "the spectral query needs spectral mode in fp32");
     if (!ctx->have[0] || !ctx->have[1]) return fail(ctx, BC_ESTATE, "upload both shapes first");
     if (!ctx->have_spec) return fail(ctx, BC_ESTATE, "call bc_spectrum_A first");
     const int64_t band = (int64_t)ctx->M * ctx->M * ctx->M;
@@ -2174,6 +2359,7 @@ bc_status bc_ipc_close(bc_ctx *ctx, void *dev_ptr)
 bc_status bc_spectrum_A_partial_buffer(bc_ctx *ctx, void **dev_ptr, int64_t *bytes)
 {
     if (!ctx) return BC_EINVAL;
+    if (ctx->sp64) return fail(ctx, BC_EUNSUPPORTED, "the fp64 spectral parity mode keeps its spectrum private");
     if (!dev_ptr || !bytes) return fail(ctx, BC_EINVAL, "NULL dev_ptr/bytes");
     if (ctx->p.mode != BC_MODE_SPECTRAL) return fail(ctx, BC_EUNSUPPORTED, "exact mode has no spectrum of A");
     CU(ctx, cudaSetDevice(ctx->device));
@@ -2220,6 +2406,7 @@ bc_status bc_spectrum_A_partial(bc_ctx *ctx, int64_t lo, int64_t hi, void *strea
 bc_status bc_spectrum_A_reduce(bc_ctx *ctx, const void *const *partials, int n, void *stream)
 {
     if (!ctx) return BC_EINVAL;
+    if (ctx->sp64) return fail(ctx, BC_EUNSUPPORTED, "the fp64 spectral parity mode keeps its spectrum private");
     TRY(check_deferred(ctx));
     if (!partials || n < 1 || n > BC_MAX_PEERS) return fail(ctx, BC_EINVAL, "need 1..%d partial spectra", BC_MAX_PEERS);
     for (int r = 0; r < n; r++)

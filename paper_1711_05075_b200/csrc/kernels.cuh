@@ -348,3 +348,32 @@ int qs_ball_chunks(int nB);
 int qs_mode_blocks(int nm);
 void launch_qs_tables(const QsTableArgs &t, cudaStream_t s);
 void launch_qs(const QsArgs &a, cudaStream_t s);
+
+// ----------------------------------------------------------------- spectral fp64 parity mode (spectral64.cu)
+struct Sp64SpreadArgs {
+    int L;                  // box edge (cells)
+    double o[3];            // box origin (cells)
+    double hf, tau, cut;    // fine spacing, Gaussian sigma, footprint beyond the radius (length)
+    const double4 *balls;   // (x, y, z, r)
+    const double2 *w;       // weights (re, im)
+    int n;
+    const double *rot;      // 9 doubles (row-major R) or nullptr (identity)
+    double2 *out;           // box [L][L][L]
+};
+struct Sp64DftArgs {
+    const double2 *in;      // [O][Lin][I]
+    double2 *out;           // [O][nq][I]
+    int O, Lin, I, nq;
+    long long qlo, nlo;     // output index q <-> qlo + q, input n <-> nlo + n
+    long long G;            // period of the phase (fine grid G forward, Np inverse)
+    int sign;               // -1 forward, +1 inverse
+    const double2 *tw;      // e^{-2 pi i r / G}, r in [0, G)
+    int mult;               // forward multipliers (below) or none
+    long long off;          // box origin on this axis (cells)
+    double hf, tau, P, t0;
+    int origin;             // A: times the origin phase e^{2 pi i k t0 / P}
+};
+void launch_sp64_spread(const Sp64SpreadArgs &a, cudaStream_t s);
+void launch_sp64_dft(const Sp64DftArgs &a, cudaStream_t s);
+void launch_sp64_product(const double2 *A, const double2 *B, double2 *Gk, int M, cudaStream_t s);
+void launch_sp64_output(const double2 *f, long long n, double scale, int complex_w, double *out, cudaStream_t s);

@@ -75,10 +75,13 @@ def test_create_rejects_bad_params_without_gpu(bc, kw):
     assert e.value.status == bc.BC_EINVAL
 
 
-def test_spectral_fp64_unsupported(bc):
-    with pytest.raises(bc.BallCorrError) as e:
-        bc.Correlator(N=8, h=0.1, t0=(0, 0, 0), Np=8, K=4, precision="f64")
-    assert e.value.status == bc.BC_EUNSUPPORTED
+def test_spectral_fp64_limits(bc):
+    """Spectral fp64 is a small-problem parity mode (include/ballcorr.h): a band beyond K = 64,
+    or the fp32-only band-error probe, is refused before any device work."""
+    for kw in (dict(K=65), dict(K=4, tolerance=1e-4)):
+        with pytest.raises(bc.BallCorrError) as e:
+            bc.Correlator(N=8, h=0.1, t0=(0, 0, 0), Np=8, precision="f64", **kw)
+        assert e.value.status == bc.BC_EUNSUPPORTED
 
 
 def test_null_context_is_safe(bc):
