@@ -704,6 +704,30 @@ bc_status build_spread_z_tables(bc_ctx *ctx)
     return BC_OK;
 }
 
+// Generic (Gaussian) plan of B: cell-unit balls and the footprint radius for the per-rotation
+// 16 x 16-column binning (the spread_z binning kernels), so that each 16^3 spread tile scans
+// only the balls listed in its column bin instead of all of B (boxes of 16-multiple edge).
+bool generic_bins_B(const bc_ctx *ctx) { return !ctx->plan[1].blob && ctx->plan[1].L % 16 == 0 && !ctx->sp64; }
+
+bc_status build_generic_bins_B(bc_ctx *ctx)
+{
+    if (!generic_bins_B(ctx)) return BC_OK;
+    const ShapePlan &pl = ctx->plan[1];
+    const int64_t nb = ctx->n[1];
+    const size_t cnt = (size_t)std::max<int64_t>(nb, 1);
+    std::vector<float4> bc(cnt, make_float4(0, 0, 0, 1));
+    ctx->rc_max_B = 0;
+    for (int64_t j = 0; j < nb; j++) {
+        const double *x = &ctx->hxyzr[1][4 * j];
+        bc[j] = make_float4((float)(x[0] / pl.hf), (float)(x[1] / pl.hf), (float)(x[2] / pl.hf), (float)(x[3] / pl.hf));
+        ctx->rc_max_B = std::max(ctx->rc_max_B, (x[3] + pl.cut) / pl.hf);
+    }
+    TRY(dalloc(ctx, &ctx->d_bcells, sizeof(float4) * cnt));
+    CU(ctx, cudaMemcpy(ctx->d_bcells, bc.data(), sizeof(float4) * cnt, cudaMemcpyHostToDevice));
+    ctx->slot[0].sz_cap = ctx->slot[1].sz_cap = 0;  // binning workspace resized at the next correlate
+    return BC_OK;
+}
+
 bool use_spread_z(const bc_ctx *ctx) { return ctx->plan[1].ok && ctx->plan[1].blob; }
 
 // Uniform grid of A's centres for bc_evaluate_points: cell size cs >= max r_A + max s_B, so
@@ -892,6 +916,42 @@ bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, voi
         ctx->launches += a.box ? 2 : 1;
     } else {
         SpreadArgs a{};
+        if (which == 1 && generic_bins_B(ctx)) {  // per-rotation column bins (spread_z.cu kernels)
+            const int n = (int)ctx->n[1];
+            const int nbins = spread_z_bins(L);
+            const long long lstride = (long long)n * spread_z_bins_per_ball((float)ctx->rc_max_B);
+            if (sl.sz_cap < nb) {
+                TRY(dalloc(ctx, &sl.recA, sizeof(float4) * (size_t)n * nb));
+                TRY(dalloc(ctx, &sl.szcnt, sizeof(int) * (size_t)nbins * nb));
+                TRY(dalloc(ctx, &sl.szoff, sizeof(int) * (size_t)nbins * nb));
+                TRY(dalloc(ctx, &sl.szlist, sizeof(int) * (size_t)lstride * nb));
+                sl.sz_cap = nb;
+            }
+            SzBinArgs bn{};
+            bn.n = n;
+            bn.balls = ctx->d_bcells;
+            bn.rot = d_rot;
+            bn.ox = (float)pl.o[0];
+            bn.oy = (float)pl.o[1];
+            bn.oz = (float)pl.o[2];
+            bn.cut = (float)(pl.cut / pl.hf);
+            bn.recA = sl.recA;
+            bn.bpa = spread_z_bins_per_axis(L);
+            bn.nbins = nbins;
+            bn.counts = sl.szcnt;
+            bn.offs = sl.szoff;
+            bn.lists = sl.szlist;
+            bn.list_stride = lstride;
+            StageScope sc(ctx, s, "bin_B");
+            launch_spread_z_bin(bn, nb, s);
+            ctx->launches += 3;
+            a.bin_counts = sl.szcnt;
+            a.bin_offs = sl.szoff;
+            a.bin_lists = sl.szlist;
+            a.bin_stride = lstride;
+            a.nbins = nbins;
+            a.bpa = bn.bpa;
+        }
         a.L = L;
         a.ox = pl.o[0];
         a.oy = pl.o[1];
@@ -2045,6 +2105,7 @@ bc_status bc_shape_upload(bc_ctx *ctx, int which, const double *xyzr, const doub
                     if (dx * dx + dy * dy <= (ctx->live_r + 1) * (ctx->live_r + 1)) ctx->live_tiles_B++;
                 }
             if (ctx->plan[1].blob) TRY(build_spread_z_tables(ctx));
+            else TRY(build_generic_bins_B(ctx));
         }
     }
     TRY(check_support(ctx));

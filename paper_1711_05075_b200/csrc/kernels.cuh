@@ -34,6 +34,11 @@ struct SpreadArgs {
     const float4 *prof;
     const int *prof_off;
     float inv_dprof;
+    // optional per-rotation candidate lists of B (16 x 16-column bins of spread_z.cu's binning):
+    // tile (tx, ty, tz) scans bin tx * bpa + ty of its rotation
+    const int *bin_counts, *bin_offs, *bin_lists;
+    long long bin_stride;
+    int nbins, bpa;
 };
 
 // fused spreading + z transform of R B (spread_z.cu), real weights.  Cell units throughout:

@@ -82,9 +82,14 @@ __global__ void __launch_bounds__(256) spread_kernel(SpreadArgs a)
     }
 
     int c0 = 0, ncand = a.n_balls;
+    const int *cidx = a.csr_idx;
     if (a.csr_off) {
         c0 = a.csr_off[tile];
         ncand = a.csr_off[tile + 1] - c0;
+    } else if (a.bin_counts) {  // B: this rotation's column bin (ball order)
+        const int bin = tx * a.bpa + ty;
+        ncand = a.bin_counts[b * a.nbins + bin];
+        cidx = a.bin_lists + (long long)b * a.bin_stride + a.bin_offs[b * a.nbins + bin];
     }
     const float fx0 = (float)X0, fy0 = (float)Y0, fz0 = (float)Z0, fe = (float)(SP_T - 1);
     const float tau = a.tau;
@@ -101,7 +106,7 @@ __global__ void __launch_bounds__(256) spread_kernel(SpreadArgs a)
             bool ok = false;
             float4 u = make_float4(0, 0, 0, 0), wv = make_float4(0, 0, 0, 0);
             if (q < ncand) {
-                const int j = a.csr_idx ? a.csr_idx[c0 + q] : q;
+                const int j = cidx ? cidx[c0 + q] : q;
                 const float4 bl = a.balls[j];
                 float cx = bl.x, cy = bl.y, cz = bl.z;
                 if (a.rot) {  // eq_Mink0 (L235): a rigid motion relocates the centre only
