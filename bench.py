@@ -389,9 +389,7 @@ def run_ours(args, rank, world, local_rank):
         ctx.shape_upload(0, w.A_xyzr, w.A_w)
         ctx.shape_upload(1, w.B_xyzr, w.B_w)
         p2p = args.collectives == "p2p" and args.scaling == "strong"
-        if p2p:
-            if world == 1:
-                dist.init_process_group("gloo", init_method="tcp://127.0.0.1:%d" % _free_port(), rank=0, world_size=1)
+        if p2p:  # (a world of one needs no process group: the helpers skip the exchanges)
             from paper_1711_05075_b200.sharding import allreduce_spectrum_A_p2p
             allreduce_spectrum_A_p2p(ctx, len(w.A_xyzr))
         elif world > 1:  # rank 0 computes A's spectrum, NCCL broadcasts it (north_star)
@@ -415,8 +413,8 @@ def run_ours(args, rank, world, local_rank):
     p2p = (not dry) and args.collectives == "p2p" and args.scaling == "strong" and reduced
     if p2p:  # the job's records, stored into every rank's buffer by the reduction epilogue
         from paper_1711_05075_b200.sharding import result_peers_p2p
-        glob_p2p = torch.zeros(n_all * 16, dtype=torch.uint8, device=dev)
-        _, mapped = result_peers_p2p(ctx, glob_p2p.data_ptr(), n_all)
+        glob_ptr, glob_p2p = ctx.result_buffer(n_all * 16)  # an allocation base (IPC-exportable)
+        _, mapped = result_peers_p2p(ctx, glob_ptr, n_all)
 
     def step():
         ctx.correlate_rotations(R_dev, kind, out=out, stream=stream)

@@ -232,7 +232,12 @@ bc_status bc_evaluate_points_spectral(bc_ctx *ctx, const double *R, const double
  *
  * bc_ipc_handle / bc_ipc_open / bc_ipc_close: cudaIpcGetMemHandle / cudaIpcOpenMemHandle
  *   (peer access enabled lazily) / cudaIpcCloseMemHandle of a device allocation of the
- *   calling process (handle: BC_IPC_HANDLE_BYTES bytes).
+ *   calling process (handle: BC_IPC_HANDLE_BYTES bytes).  dev_ptr must be the BASE of its
+ *   allocation (a handle maps the whole allocation): BC_EINVAL otherwise -- pass the
+ *   context's own buffers (bc_spectrum_A_partial_buffer, bc_result_buffer).
+ *
+ * bc_result_buffer(ctx, bytes, dev_ptr): a context-owned device buffer of at least `bytes`
+ *   (zeroed when first allocated or grown), for the job-wide records of bc_set_result_peers.
  *
  * A's spectrum sharded by balls (rho_hat_A is linear in the knots):
  *   bc_spectrum_A_partial(ctx, lo, hi, stream): the band spectrum of A's balls [lo, hi) (A is
@@ -260,6 +265,7 @@ bc_status bc_ipc_close(bc_ctx *ctx, void *dev_ptr);
 bc_status bc_spectrum_A_partial(bc_ctx *ctx, int64_t lo, int64_t hi, void *stream);
 bc_status bc_spectrum_A_partial_buffer(bc_ctx *ctx, void **dev_ptr, int64_t *bytes);
 bc_status bc_spectrum_A_reduce(bc_ctx *ctx, const void *const *partials, int n, void *stream);
+bc_status bc_result_buffer(bc_ctx *ctx, int64_t bytes, void **dev_ptr);
 bc_status bc_set_result_peers(bc_ctx *ctx, void *const *buffers, int n, int64_t base);
 
 /* Synchronise `stream` and report a deferred error of earlier calls on this context

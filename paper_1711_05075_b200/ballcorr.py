@@ -78,6 +78,8 @@ _lib.bc_spectrum_A_partial_buffer.argtypes = [_vp, ctypes.POINTER(_vp), ctypes.P
 _lib.bc_spectrum_A_partial_buffer.restype = ctypes.c_int
 _lib.bc_spectrum_A_reduce.argtypes = [_vp, ctypes.POINTER(_vp), ctypes.c_int, _vp]
 _lib.bc_spectrum_A_reduce.restype = ctypes.c_int
+_lib.bc_result_buffer.argtypes = [_vp, ctypes.c_int64, ctypes.POINTER(_vp)]
+_lib.bc_result_buffer.restype = ctypes.c_int
 _lib.bc_set_result_peers.argtypes = [_vp, ctypes.POINTER(_vp), ctypes.c_int, ctypes.c_int64]
 _lib.bc_set_result_peers.restype = ctypes.c_int
 _lib.bc_sync.argtypes = [_vp, _vp]
@@ -115,6 +117,7 @@ bc_spectrum_A_partial = _lib.bc_spectrum_A_partial
 bc_spectrum_A_partial_buffer = _lib.bc_spectrum_A_partial_buffer
 bc_spectrum_A_reduce = _lib.bc_spectrum_A_reduce
 bc_set_result_peers = _lib.bc_set_result_peers
+bc_result_buffer = _lib.bc_result_buffer
 IPC_HANDLE_BYTES = 64
 MAX_PEERS = 8
 bc_last_error = _lib.bc_last_error
@@ -317,6 +320,18 @@ class Correlator:
         read over peer memory by one kernel fused with the A'' build."""
         arr = (_vp * len(partial_ptrs))(*[int(p) for p in partial_ptrs])
         self._check(_lib.bc_spectrum_A_reduce(self._ctx, arr, len(partial_ptrs), _stream_handle(stream)))
+
+    def result_buffer(self, nbytes):
+        """(device pointer, torch uint8 tensor view) of the context-owned job-wide record buffer
+        (an allocation base, so it can be exported with ipc_handle)."""
+        import torch
+        ptr = _vp()
+        self._check(_lib.bc_result_buffer(self._ctx, int(nbytes), ctypes.byref(ptr)))
+
+        class _Iface:
+            __cuda_array_interface__ = {"shape": (int(nbytes),), "typestr": "|u1", "data": (int(ptr.value), False),
+                                        "version": 3, "strides": None}
+        return int(ptr.value), torch.as_tensor(_Iface(), device=torch.device("cuda", self.device))
 
     def set_result_peers(self, buffers, base=0):
         """Reduction records of later correlate calls also go to these device buffers at global

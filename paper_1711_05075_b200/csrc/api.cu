@@ -88,6 +88,8 @@ struct bc_ctx {
     int64_t csr_lo = 0, csr_hi = -1;  // A's balls the per-tile candidate lists cover (hi < 0: all)
     float2 *d_Ahat_part = nullptr;    // partial band spectrum of a slice of A (bc_spectrum_A_partial)
     ResultPeers res_peers{};          // fused result exchange (bc_set_result_peers)
+    void *d_res = nullptr;            // job-wide record buffer (bc_result_buffer)
+    size_t res_bytes = 0;
     float4 *d_prof = nullptr;     // per-ball radial profile tables of B (cubic Hermite pieces)
     int *d_prof_off = nullptr;
     double dprof = 0;
@@ -2016,6 +2018,7 @@ bc_status bc_destroy(bc_ctx *ctx)
     dfree(ctx->d_Ahat);
     dfree(ctx->d_Ahat_cm);
     dfree(ctx->d_Ahat_part);
+    dfree(ctx->d_res);
     dfree(ctx->d_xtab);
     dfree(ctx->d_segs);
 
@@ -2391,6 +2394,23 @@ bc_status bc_ipc_handle(bc_ctx *ctx, const void *dev_ptr, void *handle)
     if (!ctx) return BC_EINVAL;
     if (!dev_ptr || !handle) return fail(ctx, BC_EINVAL, "NULL dev_ptr/handle");
     CU(ctx, cudaSetDevice(ctx->device));
+    {
+        // a handle maps the whole allocation: a pointer inside a larger one (e.g. a caching
+        // allocator's sub-block) would open at the allocation's base on the peer
+        typedef int (*range_fn)(unsigned long long *, size_t *, unsigned long long);
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) == cudaSuccess && fn &&
+            q == cudaDriverEntryPointSuccess) {
+            unsigned long long base = 0;
+            size_t size = 0;
+            if (((range_fn)fn)(&base, &size, (unsigned long long)(uintptr_t)dev_ptr) == 0 &&
+                base != (unsigned long long)(uintptr_t)dev_ptr)
+                return fail(ctx, BC_EINVAL, "dev_ptr is not the base of its allocation (offset %llu)",
+                            (unsigned long long)(uintptr_t)dev_ptr - base);
+        }
+        cudaGetLastError();
+    }
     cudaIpcMemHandle_t h;
     CU(ctx, cudaIpcGetMemHandle(&h, (void *)dev_ptr));
     static_assert(sizeof(h) == BC_IPC_HANDLE_BYTES, "IPC handle size");
@@ -2513,6 +2533,20 @@ bc_status bc_spectrum_A_reduce(bc_ctx *ctx, const void *const *partials, int n, 
     ctx->have_spec = true;
     ctx->probe_done = false;
     ctx->qs_ready = false;
+    return BC_OK;
+}
+
+bc_status bc_result_buffer(bc_ctx *ctx, int64_t bytes, void **dev_ptr)
+{
+    if (!ctx) return BC_EINVAL;
+    if (!dev_ptr || bytes < 1) return fail(ctx, BC_EINVAL, "NULL dev_ptr or bytes < 1");
+    CU(ctx, cudaSetDevice(ctx->device));
+    if (ctx->res_bytes < (size_t)bytes) {
+        TRY(dalloc(ctx, &ctx->d_res, (size_t)bytes));
+        ctx->res_bytes = (size_t)bytes;
+        CU(ctx, cudaMemset(ctx->d_res, 0, (size_t)bytes));
+    }
+    *dev_ptr = ctx->d_res;
     return BC_OK;
 }
 

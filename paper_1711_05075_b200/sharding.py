@@ -74,11 +74,27 @@ def global_best(vals: np.ndarray, idxs: np.ndarray, kind: str = "min"):
 # the data movement inside its kernels over NVLink; these helpers only move the 64-byte IPC
 # handles between the processes and order the steps with barriers.
 
+def _world(group=None):
+    """(world size, rank); a process without a process group is a world of one."""
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return 1, 0
+    return dist.get_world_size(group), dist.get_rank(group)
+
+
+def _barrier(group=None):
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        dist.barrier(group=group)
+
+
 def _exchange_handles(corr, ptr, group=None):
     """Every rank's device pointer for `ptr`'s peer allocation, in rank order (own pointer as
     is, the others mapped through cudaIpc)."""
     import torch.distributed as dist
-    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    world, rank = _world(group)
+    if world == 1:
+        return [ptr]
     handles = [None] * world
     dist.all_gather_object(handles, corr.ipc_handle(ptr), group=group)
     return [ptr if r == rank else corr.ipc_open(handles[r]) for r in range(world)]
@@ -89,20 +105,19 @@ def allreduce_spectrum_A_p2p(corr, n_A: int, group=None, sync=None):
     block of A's balls, then one kernel per rank reads every rank's partial over peer memory,
     sums them in rank order and builds A'' (bc_spectrum_A_reduce).  Every rank ends with the
     same spectrum bits.  `sync()` waits for the device (torch.cuda.synchronize by default)."""
-    import torch.distributed as dist
     if sync is None:
         import torch
         sync = torch.cuda.synchronize
-    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    world, rank = _world(group)
     lo, hi = rotation_block(n_A, rank, world)
     corr.spectrum_A_partial(lo, hi)
     own, _ = corr.spectrum_A_partial_buffer()
     ptrs = _exchange_handles(corr, own, group)
     sync()
-    dist.barrier(group=group)          # every partial is complete
+    _barrier(group)                    # every partial is complete
     corr.spectrum_A_reduce(ptrs)
     sync()
-    dist.barrier(group=group)          # every rank has read every partial
+    _barrier(group)                    # every rank has read every partial
     for r, p in enumerate(ptrs):
         if r != rank:
             corr.ipc_close(p)
@@ -116,8 +131,7 @@ def result_peers_p2p(corr, global_buf_ptr, n_rot: int, group=None):
     (bc_set_result_peers), so no all-gather follows the step -- a barrier after the step is
     all the caller needs before reading.  Returns (this rank's rotation block, mapped pointers
     to close at the end)."""
-    import torch.distributed as dist
-    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    world, rank = _world(group)
     start, stop = rotation_block(n_rot, rank, world)
     ptrs = _exchange_handles(corr, global_buf_ptr, group)
     corr.set_result_peers(ptrs, base=start)

@@ -109,9 +109,14 @@ def test_results_stored_into_peers_by_the_epilogue(bc, sweep, kind):
 def test_ipc_handle_of_a_device_buffer(bc, sweep):
     import torch
     c = ctx_for(bc, sweep)
-    buf = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
-    h = c.ipc_handle(buf.data_ptr())
+    ptr, view = c.result_buffer(1 << 20)
+    assert view.numel() == 1 << 20 and int(view.sum().item()) == 0
+    h = c.ipc_handle(ptr)
     assert isinstance(h, bytes) and len(h) == bc.IPC_HANDLE_BYTES
+    # a pointer inside an allocation would map the allocation's base on the peer: refused
+    with pytest.raises(bc.BallCorrError) as e:
+        c.ipc_handle(ptr + 256)
+    assert e.value.status == bc.BC_EINVAL
     with pytest.raises(bc.BallCorrError):
         c.set_result_peers([0])
     with pytest.raises(bc.BallCorrError):
