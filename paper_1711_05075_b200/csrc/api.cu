@@ -98,6 +98,7 @@ struct bc_ctx {
     float4 *d_bcells = nullptr;
     float2 *d_g02 = nullptr;
     float4 *d_recB = nullptr;      // (s, w, g0, g2) per ball of B (cells)
+    float *d_recWi = nullptr;      // imaginary part of B's weights (complex weights)
     double rc_max_B = 0;           // max (s + W) / hf over B
 
     float4 *d_phi = nullptr;
@@ -356,10 +357,12 @@ bc_status plan_shape(bc_ctx *ctx, int which, const double lo[3], const double hi
     double best_cost = 1e300;
     // B with real weights: the fused spread + z kernel with the KB blob when a box size it
     // supports fits (G >= 4 (K + 1) as for the Gaussian: band |nu_i| <= 1/4 of the fine grid)
-    if (which == 1 && ctx->p.weights == BC_WEIGHTS_REAL && !ctx->p.generic_only && !ctx->sp64) {
+    // (complex weights: the blob spread to a complex box, then the generic complex-row z pass)
+    const bool cplx_w = ctx->p.weights == BC_WEIGHTS_COMPLEX;
+    if (which == 1 && !ctx->p.generic_only && !ctx->sp64) {
         for (int c = 1; c <= 8; c++)
-            for (int L : {128, 256}) {
-                if (!spread_z_supported(L) || c * L < Gmin) continue;
+            for (int L : {128, 256, 384}) {
+                if (!spread_z_supported(L, cplx_w) || c * L < Gmin) continue;
                 const int G = c * L;
                 const double hf = P / G;
                 if (L * hf < extent + 2 * kBlobW * hf + 4 * hf) continue;
@@ -691,6 +694,10 @@ bc_status build_spread_z_tables(bc_ctx *ctx)
     }
     TRY(dalloc(ctx, &ctx->d_recB, sizeof(float4) * cnt));
     CU(ctx, cudaMemcpy(ctx->d_recB, rb.data(), sizeof(float4) * cnt, cudaMemcpyHostToDevice));
+    std::vector<float> wi(cnt, 0.f);
+    for (int64_t j = 0; j < nb; j++) wi[j] = (float)ctx->hw[1][2 * j + 1];
+    TRY(dalloc(ctx, &ctx->d_recWi, sizeof(float) * cnt));
+    CU(ctx, cudaMemcpy(ctx->d_recWi, wi.data(), sizeof(float) * cnt, cudaMemcpyHostToDevice));
     ctx->slot[0].sz_cap = ctx->slot[1].sz_cap = 0;  // binning workspace resized at the next correlate
     TRY(dalloc(ctx, &ctx->d_phi, sizeof(float4) * tab.size()));
     TRY(dalloc(ctx, &ctx->d_bcells, sizeof(float4) * cnt));
@@ -886,6 +893,8 @@ bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, voi
         a.n_balls = n;
         a.recA = sl.recA;
         a.recB = ctx->d_recB;
+        a.recWi = ctx->d_recWi;
+        a.cplx = cplx ? 1 : 0;
         a.counts = sl.szcnt;
         a.offs = sl.szoff;
         a.lists = sl.szlist;
@@ -899,7 +908,8 @@ bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, voi
         a.cy = (float)(-pl.o[1]);
         a.live_r2 = (float)(ctx->live_r * ctx->live_r);
         a.zero_r2 = (float)((ctx->live_r + 1) * (ctx->live_r + 1));
-        a.skip_zero = pass_y_fast_supported(L, pl.c, pl.G, ctx->K, cplx) ? 1 : 0;
+        // complex weights: the complex box, its unwritten zero tiles skipped by the z pass below
+        a.skip_zero = (cplx || pass_y_fast_supported(L, pl.c, pl.G, ctx->K, cplx)) ? 1 : 0;
         // the sweep's plan: spread to the box (ws1, free until the y pass writes T2 there) and
         // transform it in a second kernel -- the spread alone runs at twice the occupancy
         if (a.skip_zero) {
@@ -915,7 +925,7 @@ bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, voi
         if (!launch_spread_z(a, nb, s))
             return fail(ctx, BC_EUNSUPPORTED, "spread_z: profile table (n = %d, U = %g) or box L = %d not compiled in",
                         a.phi_n, (double)a.phi_U, a.L);
-        ctx->launches += a.box ? 2 : 1;
+        ctx->launches += (a.box && !cplx) ? 2 : 1;
     } else {
         SpreadArgs a{};
         if (which == 1 && generic_bins_B(ctx)) {  // per-rotation column bins (spread_z.cu kernels)
@@ -989,7 +999,7 @@ bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, voi
     base.signed_k = 1;
     base.tw = tw;
     base.ctw = pl.d_ctw;
-    if (!(which == 1 && use_spread_z(ctx))) {
+    if (!(which == 1 && use_spread_z(ctx)) || (which == 1 && cplx)) {
         PassArgs a = base;
         a.klo = cplx ? -ctx->K : 0;
         a.nk = ctx->Kz;
@@ -1000,6 +1010,12 @@ bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, voi
         a.in_bstride = (long long)(s1_per / (cplx ? 8 : 4));
         a.out = (float2 *)ws2;
         a.out_bstride = (long long)(s2_per / 8);
+        if (which == 1 && use_spread_z(ctx)) {  // the complex box of spread_z: skip its zero tiles
+            a.zskip = 2;                          // (the y pass below reads only live rows)
+            a.zcx = (float)(-pl.o[0]);
+            a.zcy = (float)(-pl.o[1]);
+            a.zero_r2 = (float)((ctx->live_r + 1) * (ctx->live_r + 1));
+        }
         StageScope sc(ctx, s, which ? "pass_z_B" : "pass_z_A");
         launch_pass(a, 0, nb, s);
         ctx->launches++;
@@ -1030,6 +1046,12 @@ bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, voi
         a.in_bstride = (long long)(s2_per / 8);
         a.out = (float2 *)ws1;
         a.out_bstride = (long long)(s1_per / 8);
+        if (which == 1 && use_spread_z(ctx)) {  // T1 of the complex box: live rows only
+            a.ylive = 1;
+            a.zcx = (float)(-pl.o[0]);
+            a.zcy = (float)(-pl.o[1]);
+            a.live_r2 = (float)(ctx->live_r * ctx->live_r);
+        }
         StageScope sc(ctx, s, which ? "pass_y_B" : "pass_y_A");
         launch_pass(a, 1, nb, s);
         ctx->launches++;
@@ -1984,6 +2006,7 @@ bc_status bc_destroy(bc_ctx *ctx)
     dfree(ctx->d_phi);
     dfree(ctx->d_dec);
     dfree(ctx->d_recB);
+    dfree(ctx->d_recWi);
     for (Slot &sl : ctx->slot) {
         if (sl.ws1) cudaFree(sl.ws1);
         if (sl.ws2) cudaFree(sl.ws2);

@@ -64,7 +64,9 @@ struct SpreadZArgs {
     int L, K, c, G;
     int n_balls;
     const float4 *recA;     // [b][n] rotated balls (SzBinArgs)
-    const float4 *recB;     // [n] (s, w, g0, g2): radius (cells), weight, d -> 0 series g0 + g2 d^2
+    const float4 *recB;     // [n] (s, w, g0, g2): radius (cells), weight (real part), d -> 0 series g0 + g2 d^2
+    const float *recWi;     // [n] imaginary part of the weight (complex weights: BOX mode only)
+    int cplx;               // complex weights: the box holds float2 cells
     const int *counts, *offs, *lists;  // the bins (SzBinArgs)
     int nbins;
     long long list_stride;
@@ -79,10 +81,10 @@ struct SpreadZArgs {
     const float2 *ctw;      // [c][L]
     float2 *out;            // T1 [b][L][L][K + 1]
     long long out_bstride;  // float2 elements
-    float *box;             // non-null: spread to this fp32 box [b][L][L][L] (stride box_bstride),
-    long long box_bstride;  // then a separate tile z transform (two kernels, see spread_z.cu)
+    float *box;             // non-null: spread to this fp32 box [b][L][L][L] (stride box_bstride, floats;
+    long long box_bstride;  // complex: float2 cells), then a separate z transform (spread_z.cu / passes.cu)
 };
-bool spread_z_supported(int L);
+bool spread_z_supported(int L, int complex_w);
 bool launch_spread_z(const SpreadZArgs &a, int batch, cudaStream_t s);  // false: unsupported plan/table
 
 // ----------------------------------------------------------------- coset-major band order
@@ -146,6 +148,16 @@ struct PassArgs {
     long long in_bstride, out_bstride;
     const void *in;
     float2 *out;
+    // contiguous rows of a box of L columns per x (row = x L + y): zskip = 1 treats the rows of
+    // the 4 x 4-column tiles that spread_z left unwritten (outside B's support cylinder, the
+    // spread's own test with centre (zcx, zcy) and zero_r2) as zero without reading them
+    int zskip;
+    float zcx, zcy, zero_r2;
+    // strided forward pass over such a box's T1 (O = x planes, rows = y): ylive = 1 loads only
+    // the rows within sqrt(live_r2) of the support axis (zcx, zcy) -- the rows zskip may leave
+    // unwritten lie beyond it -- and writes a zero plane without transforming it
+    int ylive;
+    float live_r2;
 };
 
 // fused x-pass of R B + spectral product with A + fold onto Np^3 (passes.cu)

@@ -67,12 +67,33 @@ __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TP
     if (IN_MODE == 2) {
         const int pin = a.pitch_in ? a.pitch_in : a.I;
         const float2 *in = (const float2 *)a.in + (long long)b * a.in_bstride + (long long)o * L * pin;
+        int ylo = 0, yhi = L - 1;
+        if (!INV && a.ylive) {  // live rows of this x plane (block-uniform)
+            const float dxl = (float)o - a.zcx;
+            const float h2 = a.live_r2 - dxl * dxl;
+            ylo = 0;
+            yhi = -1;
+            if (h2 > 0.f) {
+                const float hh = sqrtf(h2);
+                ylo = max(0, (int)ceilf(a.zcy - hh));
+                yhi = min(L - 1, (int)floorf(a.zcy + hh));
+            }
+            if (ylo > yhi) {  // plane outside the support cylinder: its band rows are zero
+                const int pout = a.pitch_out ? a.pitch_out : a.I;
+                float2 *out = a.out + (long long)b * a.out_bstride + (long long)o * a.nk * pout;
+                for (int e = threadIdx.x; e < a.nk * NL; e += NT) {
+                    const int q = e / NL, i = e % NL;
+                    if (i0 + i < a.I) out[(long long)q * pout + i0 + i] = make_float2(0.f, 0.f);
+                }
+                return;
+            }
+        }
         // all loads first (E independent loads in flight per thread), then the transpose
 #pragma unroll
         for (int m = 0; m < E; m++) {
             const int e = threadIdx.x + NT * m;
             const int n = e / NL, i = e % NL;
-            x[m] = (i0 + i < a.I) ? in[(long long)n * pin + i0 + i] : make_float2(0.f, 0.f);
+            x[m] = (i0 + i < a.I && n >= ylo && n <= yhi) ? in[(long long)n * pin + i0 + i] : make_float2(0.f, 0.f);
         }
 #pragma unroll
         for (int m = 0; m < E; m++) {
@@ -85,11 +106,32 @@ __global__ void __launch_bounds__(Plan<L>::TPL * Plan<L>::NL, 512 / (Plan<L>::TP
         __syncthreads();
     } else {
         const long long g = (long long)b * a.in_bstride + (row0 + line) * L;
+        bool live = valid;
+        if (IN_MODE != 2 && a.zskip) {
+            // the tile of this row (spread_z's zero-tile test): unwritten tiles read as zero
+            auto zero_tile = [&](long long row) {
+                const int X0 = (int)(row / L) & ~3, Y0 = (int)(row % L) & ~3;
+                const float dx = fmaxf(fmaxf((float)X0 - a.zcx, a.zcx - (float)(X0 + 3)), 0.f);
+                const float dy = fmaxf(fmaxf((float)Y0 - a.zcy, a.zcy - (float)(Y0 + 3)), 0.f);
+                return dx * dx + dy * dy > a.zero_r2;
+            };
+            live = valid && !zero_tile(row0 + line);
+            // whole block zero (NL consecutive rows of one x lie in NL / 4 tiles): zero rows out
+            if (zero_tile(row0) && zero_tile(row0 + NL - 1) && (NL <= 8 || __syncthreads_and(!live))) {
+                if (a.zskip == 2) return;  // the consumer (ylive) never reads these rows
+                float2 *outs = a.out + (long long)b * a.out_bstride;
+                for (int e = threadIdx.x; e < NL * a.nk; e += NT) {
+                    const long long r = row0 + e / a.nk;
+                    if (r < nrows) outs[r * a.nk + (e % a.nk)] = make_float2(0.f, 0.f);
+                }
+                return;
+            }
+        }
 #pragma unroll
         for (int m = 0; m < E; m++) {
             const int n = tl + TPL * m;
             x[m] = make_float2(0.f, 0.f);
-            if (valid) {
+            if (live) {
                 if (IN_MODE == 0)
                     x[m].x = ((const float *)a.in)[g + n];
                 else

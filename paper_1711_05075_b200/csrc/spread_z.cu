@@ -222,14 +222,17 @@ __device__ __forceinline__ void tile_z_transform(const SpreadZArgs &a, float *ac
 
 // BOX = false: spread + z transform of the tile (one kernel).  BOX = true: spread only, the
 // tile's 16 fp32 columns are written to the box (a.box) for pass_z_fast; without the FFT's
-// registers and buffers the spread runs at twice the occupancy.
-template <int L, bool BOX>
-__global__ void __launch_bounds__(128, BOX ? 8 : 4) spread_z_kernel(SpreadZArgs a)
+// registers and buffers the spread runs at twice the occupancy.  CPLX (BOX only): complex
+// weights w = (recB.y, recWi), two accumulators per cell, float2 box cells (the z transform
+// is then the complex-row pass of passes.cu, which skips the tiles left unwritten here).
+template <int L, bool BOX, bool CPLX = false>
+__global__ void __launch_bounds__(128, CPLX ? 4 : (BOX ? 8 : 4)) spread_z_kernel(SpreadZArgs a)
 {
+    static_assert(!CPLX || BOX, "complex weights: spread to the box only");
     constexpr int NT = 128;
     constexpr int TPL = Plan<L>::TPL, NG = NT / TPL;
     constexpr int LS = line_stride(L);
-    static_assert(NT % TPL == 0 && NG >= SZ_LINES && Plan<L>::n == 2 && warp_local<L>(), "spread_z plan");
+    static_assert(BOX || (NT % TPL == 0 && NG >= SZ_LINES && Plan<L>::n == 2 && warp_local<L>()), "spread_z plan");
     extern __shared__ float4 smz[];
     const int Kz = a.K + 1;
     // layout: phi table | tw | Abuf (NG lines) | region {acc  /  zb}   (BOX: phi table | acc)
@@ -239,6 +242,7 @@ __global__ void __launch_bounds__(128, BOX ? 8 : 4) spread_z_kernel(SpreadZArgs 
     constexpr int CS = L + 8;                         // column stride: the 4 lane groups of a warp
                                                       // (4 columns) sit 8 banks apart
     float *acc = BOX ? (float *)(phi + 2 * a.phi_n) : (float *)(Abuf + NG * LS);  // [16][CS]
+    float *acci = acc + SZ_COLS * CS;                 // CPLX: imaginary parts [16][CS]
 
     const int b = blockIdx.y;
     const int tpa = L / 4;
@@ -263,7 +267,8 @@ __global__ void __launch_bounds__(128, BOX ? 8 : 4) spread_z_kernel(SpreadZArgs 
 
     for (int e = threadIdx.x; e < 2 * a.phi_n; e += NT) phi[e] = a.phi[e];
     if (!BOX) load_twiddles<L>(tw, a.tw, threadIdx.x, NT);
-    for (int e = threadIdx.x; e < SZ_COLS * CS / 4; e += NT) reinterpret_cast<float4 *>(acc)[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int e = threadIdx.x; e < (CPLX ? 2 : 1) * SZ_COLS * CS / 4; e += NT)
+        reinterpret_cast<float4 *>(acc)[e] = make_float4(0.f, 0.f, 0.f, 0.f);
 
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int gi = lane >> 3, hl = lane & 7;
@@ -271,6 +276,7 @@ __global__ void __launch_bounds__(128, BOX ? 8 : 4) spread_z_kernel(SpreadZArgs 
     const float fx = (float)(X0 + wid), fy = (float)(Y0 + gi);
     const float fy0 = (float)Y0;
     float *accc = acc + col * CS;
+    float *acci_c = acci + col * CS;
     // the blob's profile table (pieces of W/48 over [-W, W], W = 4 cells: n = 96) as constants;
     // launch_spread_z refuses a table of another shape
     constexpr int nphi = SZ_PHI_N;
@@ -290,10 +296,12 @@ __global__ void __launch_bounds__(128, BOX ? 8 : 4) spread_z_kernel(SpreadZArgs 
         // lane k tests candidate base0 + k and keeps its two records for the broadcast below
         bool rel = false;
         float4 uc = make_float4(0.f, 0.f, 0.f, 0.f), wc = uc;
+        float wic = 0.f;
         if (base0 + lane < cnt) {
             const int jl = lst[base0 + lane];
             uc = recA[jl];
             wc = a.recB[jl];
+            if (CPLX) wic = a.recWi[jl];
             const float ddx = fx - uc.x;
             const float ddy = fmaxf(fmaxf(fy0 - uc.y, uc.y - (fy0 + 3.f)), 0.f);
             rel = fmaf(ddx, ddx, ddy * ddy) < uc.w;
@@ -320,6 +328,7 @@ __global__ void __launch_bounds__(128, BOX ? 8 : 4) spread_z_kernel(SpreadZArgs 
             const float4 we = make_float4(__shfl_sync(0xffffffffu, wc.x, src), __shfl_sync(0xffffffffu, wc.y, src),
                                           __shfl_sync(0xffffffffu, wc.z, src),
                                           __shfl_sync(0xffffffffu, wc.w, src));  // (s, w, g0, g2)
+            const float wie = CPLX ? __shfl_sync(0xffffffffu, wic, src) : 0.f;
             // two cells per lane per step (z and z + 8: independent evaluation chains)
             auto prof = [&](float d2) {
                 if (d2 < 0.01f) return fmaf(we.w, d2, we.z);
@@ -338,12 +347,23 @@ __global__ void __launch_bounds__(128, BOX ? 8 : 4) spread_z_kernel(SpreadZArgs 
                 const float g1 = ok1 ? prof(fmaf(dz1, dz1, dxy2)) : 0.f;
                 if (ok0) accc[z0] = fmaf(we.y, g0, accc[z0]);
                 if (ok1) accc[z1] = fmaf(we.y, g1, accc[z1]);
+                if (CPLX) {
+                    if (ok0) acci_c[z0] = fmaf(wie, g0, acci_c[z0]);
+                    if (ok1) acci_c[z1] = fmaf(wie, g1, acci_c[z1]);
+                }
             }
         }
     }
     __syncthreads();
 
-    if (BOX) {  // the tile's 16 columns (1 KB each) to the box
+    if (CPLX) {  // the tile's 16 complex columns to the box, two cells per 16-byte store
+        float2 *box = reinterpret_cast<float2 *>(a.box + (long long)b * a.box_bstride);
+        for (int e = threadIdx.x; e < SZ_COLS * L / 2; e += NT) {
+            const int cc = e / (L / 2), z2 = 2 * (e % (L / 2));
+            *reinterpret_cast<float4 *>(box + ((long long)(X0 + (cc >> 2)) * L + Y0 + (cc & 3)) * L + z2) =
+                make_float4(acc[cc * CS + z2], acci[cc * CS + z2], acc[cc * CS + z2 + 1], acci[cc * CS + z2 + 1]);
+        }
+    } else if (BOX) {  // the tile's 16 columns (1 KB each) to the box
         float *box = a.box + (long long)b * a.box_bstride;
         for (int e = threadIdx.x; e < SZ_COLS * L / 4; e += NT) {  // 16-byte rows (CS, L multiples of 4)
             const int cc = e / (L / 4), z4 = e % (L / 4);
@@ -396,7 +416,9 @@ __global__ void __launch_bounds__(128, 4) pass_z_fast_kernel(SpreadZArgs a)
     tile_z_transform<L, NT, B4>(a, acc, Abuf, tw, T1, X0, Y0);
 }
 
-bool spread_z_supported(int L) { return L == 128 || L == 256; }
+// real weights: the fused kernel or box + tile z transform (two-stage FFT plans); complex
+// weights: box only (the z transform is the generic complex-row pass)
+bool spread_z_supported(int L, int complex_w) { return complex_w ? (L == 128 || L == 256 || L == 384) : (L == 128 || L == 256); }
 
 template <int L>
 static void spread_z_launch(const SpreadZArgs &a, int batch, cudaStream_t s)
@@ -435,9 +457,27 @@ void launch_spread_z_bin(const SzBinArgs &a, int batch, cudaStream_t s)
     szb_fill_kernel<<<dim3(a.nbins, batch), 256, 0, s>>>(a);
 }
 
+template <int L>
+static void spread_z_launch_cplx(const SpreadZArgs &a, int batch, cudaStream_t s)
+{
+    const int tpa = L / 4;
+    const size_t sm = (size_t)a.phi_n * 32 + 2 * (size_t)SZ_COLS * (L + 8) * 4;
+    cudaFuncSetAttribute(spread_z_kernel<L, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    spread_z_kernel<L, true, true><<<dim3(tpa * tpa, batch), 128, sm, s>>>(a);
+}
+
 bool launch_spread_z(const SpreadZArgs &a, int batch, cudaStream_t s)
 {
     if (a.phi_n != SZ_PHI_N || a.phi_U != SZ_PHI_U) return false;  // the table shape is compiled in
+    if (a.cplx) {
+        if (!a.box) return false;
+        switch (a.L) {
+        case 128: spread_z_launch_cplx<128>(a, batch, s); return true;
+        case 256: spread_z_launch_cplx<256>(a, batch, s); return true;
+        case 384: spread_z_launch_cplx<384>(a, batch, s); return true;
+        default: return false;
+        }
+    }
     switch (a.L) {
     case 128: spread_z_launch<128>(a, batch, s); return true;
     case 256: spread_z_launch<256>(a, batch, s); return true;
