@@ -282,7 +282,7 @@ const char *bc_status_string(int status);
  * "cut_A", "cut_B", "band_modes", "batch", "bytes_workspace", "band_error" (the band-error
  * probe's estimate, -1 before it ran; see bc_params.tolerance), "query_modes" (m' the spectral
  * query's tables serve), "blob_B" (B smoothed with the
- * KB blob window), "fused_spread_z", "fused_fold_inv", "fold_fast" (which fused kernels the
+ * KB blob window), "fused_spread_z", "fused_fold_inv", "fold_fast", "dock_fast" (which fused kernels the
  * plan takes), "spread_cells_B" (sum of B's footprint volumes in fine cells), "live_tiles_B".
  * Unknown keys: BC_EINVAL.
  */

@@ -739,6 +739,15 @@ bc_status build_generic_bins_B(bc_ctx *ctx)
 
 bool use_spread_z(const bc_ctx *ctx) { return ctx->plan[1].ok && ctx->plan[1].blob; }
 
+// the docking plan shape on dock_fast.cu's kernels (blob spread to a complex box, then the
+// compile-time z / y passes and fold)
+bool use_dock_fast(const bc_ctx *ctx)
+{
+    const ShapePlan &pb = ctx->plan[1];
+    return use_spread_z(ctx) && !ctx->p.generic_only &&
+           dock_fast_supported(pb.L, pb.c, pb.G, ctx->K, ctx->p.Np, ctx->p.weights == BC_WEIGHTS_COMPLEX);
+}
+
 // Uniform grid of A's centres for bc_evaluate_points: cell size cs >= max r_A + max s_B, so
 // every A ball overlapping a B ball centred at c lies in the 27 cells around c.  CSR, ball
 // order within each cell (deterministic sums).  At most 128 cells per axis.
@@ -837,7 +846,9 @@ void spectral_ws_sizes(const bc_ctx *ctx, int which, size_t &s1, size_t &s2)
     const size_t L = pl.L, Kz = ctx->Kz, M = ctx->M, Np = ctx->p.Np, N = ctx->p.N, Fz = ctx->Fz;
     const bool cplx = ctx->p.weights == BC_WEIGHTS_COMPLEX;
     const size_t box = L * L * L * (cplx ? 8 : 4);
-    const size_t T1 = L * L * Kz * 8, T2 = L * M * Kz * 8;
+    // (the docking kernels keep T1 / T2 rows at pitch dock_t_pitch() >= Kz)
+    const size_t Pk = (which == 1 && use_dock_fast(ctx)) ? std::max(Kz, dock_t_pitch()) : Kz;
+    const size_t T1 = L * L * Pk * 8, T2 = L * M * Pk * 8;
     const size_t Fzp = (Fz + 7) & ~(size_t)7;  // padded row pitch of X1 / Y1 on the fast plan
     const size_t F = Np * Np * Fz * 8, X1 = N * Np * Fzp * 8, Y1 = N * N * Fzp * 8;
     s1 = std::max(std::max(box, T2), X1);
@@ -999,6 +1010,39 @@ bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, voi
     base.signed_k = 1;
     base.tw = tw;
     base.ctw = pl.d_ctw;
+    if (which == 1 && use_dock_fast(ctx)) {
+        DockPassArgs a{};
+        a.tw = tw;
+        a.ctw = pl.d_ctw;
+        a.cx = (float)(-pl.o[0]);
+        a.cy = (float)(-pl.o[1]);
+        a.live_r2 = (float)(ctx->live_r * ctx->live_r);
+        a.zero_r2 = (float)((ctx->live_r + 1) * (ctx->live_r + 1));
+        {
+            DockPassArgs z = a;
+            z.mult = pl.d_mult[2];
+            z.in = (const float2 *)ws1;
+            z.in_bstride = (long long)(s1_per / 8);
+            z.out = (float2 *)ws2;
+            z.out_bstride = (long long)(s2_per / 8);
+            StageScope sc(ctx, s, "pass_z_dk");
+            launch_pass_z_dk(z, nb, s);
+            ctx->launches++;
+        }
+        {
+            DockPassArgs y = a;
+            y.mult = pl.d_mult[1];
+            y.in = (const float2 *)ws2;
+            y.in_bstride = (long long)(s2_per / 8);
+            y.out = (float2 *)ws1;
+            y.out_bstride = (long long)(s1_per / 8);
+            StageScope sc(ctx, s, "pass_y_dk");
+            launch_pass_y_dk(y, nb, s);
+            ctx->launches++;
+        }
+        CU(ctx, cudaGetLastError());
+        return BC_OK;
+    }
     if (!(which == 1 && use_spread_z(ctx)) || (which == 1 && cplx)) {
         PassArgs a = base;
         a.klo = cplx ? -ctx->K : 0;
@@ -1619,7 +1663,8 @@ bc_status run_rotations(bc_ctx *ctx, int64_t n_rot, int out_kind, char *dout, si
         const int Np = ctx->p.Np;
         const ShapePlan &pB = ctx->plan[1];
         const bool fast_fold = !ctx->p.generic_only && fold_fast_supported(pB.L, pB.c, pB.G, ctx->K, Np, cplx);
-        const bool fused_inv = fast_fold || (!ctx->p.generic_only && fold_fuses_inverse(pB.L, Np));
+        const bool dock_fold = use_dock_fast(ctx);
+        const bool fused_inv = fast_fold || (!ctx->p.generic_only && !dock_fold && fold_fuses_inverse(pB.L, Np));
         // row pitch of X1 / Y1: padded to 8 modes on the fast plan (64-byte row pieces stay
         // 32-byte-sector aligned), the stored count elsewhere
         const int zpitch = fast_fold ? (ctx->Fz + 7) & ~7 : ctx->Fz;
@@ -1654,7 +1699,27 @@ bc_status run_rotations(bc_ctx *ctx, int64_t n_rot, int out_kind, char *dout, si
             TRY(shape_spectrum(ctx, 1, ctx->d_rot + 9 * r0, b, ws1, ws2, s1, s2, s, sl));
             const ShapePlan &pb = ctx->plan[1];
             // 4: x pass fused with the spectral product (A' conj(RB)) and the fold onto Np^3
-            if (fast_fold) {
+            if (dock_fold) {
+                DockFoldArgs a{};
+                a.tw = ctx->d_tw[pb.L];
+                a.ctw = pb.d_ctw;
+                a.T2 = (const float2 *)ws1;
+                a.t2_bstride = (long long)(s1 / 8);
+                a.Ahat = ctx->d_Ahat_cm;
+                a.MS = ctx->MS;
+                for (int p = 0; p < 2; p++) {
+                    const CmSeg sg = cm_segment(p, pb.L, pb.c, pb.G, ctx->K);
+                    a.pos_base[p] = sg.off - sg.qn;
+                }
+                a.F = (float2 *)ws2;
+                a.f_bstride = (long long)(s2 / 8);
+                a.cx = (float)(-pb.o[0]);
+                a.live_r2 = (float)(ctx->live_r * ctx->live_r);
+                StageScope sc(ctx, s, "fold_dk");
+                if (!launch_fold_dk(a, b, s))
+                    return fail(ctx, BC_EUNSUPPORTED, "fold_dk: A'' row stride MS = %d not the compiled plan's", a.MS);
+                ctx->launches++;
+            } else if (fast_fold) {
                 FoldFastArgs a{};
                 a.tw = ctx->d_tw[pb.L];
                 a.ctw = pb.d_ctw;
@@ -2628,6 +2693,7 @@ bc_status bc_query(const bc_ctx *ctx, const char *key, double *value)
     else if (k == "fold_fast")
         *value = (!ctx->p.generic_only && fold_fast_supported(B.L, B.c, B.G, ctx->K, ctx->p.Np,
                                                              ctx->p.weights == BC_WEIGHTS_COMPLEX)) ? 1 : 0;
+    else if (k == "dock_fast") *value = use_dock_fast(ctx) ? 1 : 0;
     else return BC_EINVAL;
     return BC_OK;
 }

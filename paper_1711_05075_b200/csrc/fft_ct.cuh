@@ -212,7 +212,7 @@ BC_PLAN(240, 3, 12, 5, 4, 20, 8)
 BC_PLAN(256, 2, 16, 16, 1, 16, 8)
 BC_PLAN(288, 3, 12, 2, 12, 24, 8)
 BC_PLAN(320, 3, 16, 5, 4, 20, 8)
-BC_PLAN(384, 3, 12, 8, 4, 32, 8)
+BC_PLAN(384, 3, 4, 8, 12, 32, 8)
 BC_PLAN(512, 3, 16, 2, 16, 32, 4)
 BC_PLAN(576, 3, 12, 4, 12, 48, 4)
 BC_PLAN(640, 3, 16, 5, 8, 40, 4)

@@ -199,6 +199,35 @@ struct FoldFastArgs {
 };
 bool fold_fast_supported(int L, int c, int G, int K, int Np, int complex_w);
 
+// dock_fast.cu: the docking plan shape (L = 384, c = 2, G = 768, K = 191, Np = 128, complex
+// weights) with compile-time constants: z and y passes of R B and the fold.  T1 / T2 rows
+// hold kz at index kz + 192 (pitch dock_t_pitch() = 384).
+struct DockPassArgs {
+    const float2 *tw, *ctw, *mult;  // twiddles, coset twiddles [2][384], the axis multipliers [2K + 1]
+    const float2 *in;               // z: box [b][L][L][L]; y: T1 [b][L][L][384]
+    long long in_bstride;
+    float2 *out;                    // z: T1; y: T2 [b][L][2K + 1][384]
+    long long out_bstride;
+    float cx, cy, live_r2, zero_r2; // B's support cylinder (spread_z's tile and row tests)
+};
+struct DockFoldArgs {
+    const float2 *tw, *ctw;
+    const float2 *T2;
+    long long t2_bstride;
+    const float2 *Ahat;             // A'' rows (coset-major, stride MS)
+    int MS;
+    int pos_base[2];
+    float2 *F;                      // [b][Np][Np][Np] (k'x, k'y, k'z)
+    long long f_bstride;
+    float cx, live_r2;              // live x planes of T2
+    int nb;                         // set by launch_fold_dk
+};
+bool dock_fast_supported(int L, int c, int G, int K, int Np, int complex_w);
+void launch_pass_z_dk(const DockPassArgs &a, int batch, cudaStream_t s);
+void launch_pass_y_dk(const DockPassArgs &a, int batch, cudaStream_t s);
+bool launch_fold_dk(const DockFoldArgs &a, int batch, cudaStream_t s);
+size_t dock_t_pitch();
+
 // fold_fast.cu: forward y pass of R B for the same plan shape (live-row input skipping)
 struct PassYFastArgs {
     const float2 *tw, *ctw, *mult;  // twiddles, coset twiddles [4][256], mult_y [2K + 1]
