@@ -234,12 +234,14 @@ __global__ void __launch_bounds__(DK_NT, 2) fold_dk_kernel(DockFoldArgs a)
         for (int j = 0; j < 2; j++)
 #pragma unroll
             for (int p = 0; p < DK_C; p++) acc[j][p] = make_float2(0.f, 0.f);
+        // aliases of k' in [0, 128) within the band [-191, 191]: k' - 256 (k' >= 65), k' - 128, k',
+        // k' + 128 (k' <= 63)
 #pragma unroll 1
-        for (int ny = -1; ny <= 1; ny++) {
+        for (int ny = -2; ny <= 1; ny++) {
             const int ky = kyp + DK_NP * ny;
             if (ky < -DK_K || ky > DK_K) continue;
 #pragma unroll 1
-            for (int nz = -1; nz <= 1; nz++) {
+            for (int nz = -2; nz <= 1; nz++) {
                 const int kzlo = z0 + DK_NP * nz, kzhi = kzlo + DK_NL - 1;
                 if (kzhi < -DK_K || kzlo > DK_K) continue;  // no line of the group in band
                 // T2 lines (-ky, -kz_i), transposed through A for coalescing

@@ -59,3 +59,39 @@ def test_sweep_plan_kernels_vs_bandlimited(bc, oracle_mod):
         check_extremum(mm[1]["val"], mm[1]["idx"], ref, "max", tol)
         check_extremum(mm[0]["val"], mm[0]["idx"], ref, "min", tol)
         c.close()
+
+
+# Docking plan (L = 384, c = 2, K = 191, Np = 128, complex weights): spread_z_kernel<384, BOX,
+# CPLX> + pass_z_dk / pass_y_dk / fold_dk (dock_fast.cu), then the generic inverse passes.  B:
+# the docking B's support edge (|b| = 26.6 A, the recipe's largest skin radius 3.2 A, weight 1)
+# around a core ball at the rotation centre (weight -15i); A: two core and two skin atoms of the
+# docking A.  Oracle ~1 min.
+EDGE_B_DK = np.array([[0.0, 0.0, 0.0, 1.7], [26.6, 0.0, 0.0, 3.2], [0.0, -26.6, 0.0, 2.6],
+                      [0.0, 0.0, 26.6, 1.2], [-15.3, 15.3, -15.3, 3.2]])
+EDGE_WB_DK = np.array([-15j, 1.0, 1.0, -15j, 1.0])
+
+
+def test_docking_plan_kernels_vs_bandlimited(bc, oracle_mod):
+    from paper_1711_05075_b200.presets import correlator_kwargs
+    from gpu_helpers import as_complex
+    w = make_config("docking", n_rot=2)
+    skin = np.flatnonzero(w.A_w == 1.0)[:2]
+    core = np.flatnonzero(w.A_w != 1.0)[:2]
+    sel = np.concatenate([core, skin])
+    A, wA = w.A_xyzr[sel], w.A_w[sel]
+    r = 1
+    P, K = 128 * w.h, 191
+    ref = oracle_mod.bandlimited_correlation(A, wA, EDGE_B_DK, EDGE_WB_DK, w.R[r], w.N, w.h, w.t0, P, K)
+    for generic in (False, True):
+        c = bc.Correlator(**correlator_kwargs("docking", w.N, w.h, w.t0, "complex", generic_only=generic))
+        c.shape_upload(0, A, wA)
+        c.shape_upload(1, EDGE_B_DK, EDGE_WB_DK)
+        c.spectrum_A()
+        if not generic:
+            assert c.query("dock_fast") == 1 and c.query("blob_B") == 1 and c.query("L_B") == 384
+        f = as_complex(c.correlate_rotations(w.R[r:r + 1], "full"))[0]
+        err = np.abs(f - ref).max() / np.abs(ref).max()
+        assert err <= IMPL_TOL, (generic, err)
+        best = c.correlate_rotations(w.R[r:r + 1], "max_real")[0]
+        check_extremum(best["val"], best["idx"], ref.real, "max", IMPL_TOL * np.abs(ref).max())
+        c.close()
