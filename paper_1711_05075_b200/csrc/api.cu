@@ -848,7 +848,7 @@ void spectral_ws_sizes(const bc_ctx *ctx, int which, size_t &s1, size_t &s2)
     const size_t box = L * L * L * (cplx ? 8 : 4);
     // (the docking kernels keep T1 / T2 rows at pitch dock_t_pitch() >= Kz)
     const size_t Pk = (which == 1 && use_dock_fast(ctx)) ? std::max(Kz, dock_t_pitch()) : Kz;
-    const size_t T1 = L * L * Pk * 8, T2 = L * M * Pk * 8;
+    const size_t T1 = L * L * Pk * 8, T2 = L * std::max(M, Pk) * Pk * 8;
     const size_t Fzp = (Fz + 7) & ~(size_t)7;  // padded row pitch of X1 / Y1 on the fast plan
     const size_t F = Np * Np * Fz * 8, X1 = N * Np * Fzp * 8, Y1 = N * N * Fzp * 8;
     s1 = std::max(std::max(box, T2), X1);

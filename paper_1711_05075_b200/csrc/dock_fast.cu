@@ -5,7 +5,7 @@
 // Same quantities as the generic passes (passes.cu; PAPER.md L398-L419 eq_ccghat, the band
 // spectrum of the relocated knots eq_rhoPhat, deconvolved by the blob window):
 //   pass_z_dk   box[x][y][n] (complex, spread_z CPLX)   -> T1[x][y][kz + 192]   (z transform)
-//   pass_y_dk   T1                                      -> T2[x][ky + 191][kz + 192]
+//   pass_y_dk   T1                                      -> T2[x][kz + 192][ky + 192]
 //   fold_dk     T2 -> x transform -> A''(k') B(-k') summed into F[k' mod 128]  (register-owned)
 // What the plan shape makes compile-time (FFT384 lines of 32 threads, radices 4 x 8 x 12):
 //  * thread tl of a line holds outputs q = tl + 32 m of coset p, k = 2 q + p (- 768 for the
@@ -123,9 +123,11 @@ __global__ void __launch_bounds__(DK_NT, 2) pass_z_dk_kernel(DockPassArgs a)
 }
 
 // ============================================================================ y pass
-// Block = one x plane, 8 consecutive T1 columns j0 .. j0 + 7 (kz = j - 192).  Rows outside
-// B's support cylinder at this x are not loaded; a plane outside it is not written (the fold
-// does not read it).
+// Block = one x plane, 8 consecutive T1 columns j0 .. j0 + 7 (kz = j - 192), one line each.
+// Rows outside B's support cylinder at this x are not loaded; a plane outside it is not
+// written (the fold does not read it).  T2 rows hold ky at index ky + 192, so, as in the z
+// pass, a thread stores the two cosets' outputs of one q with one 16-byte store: no output
+// staging (T2 = [x][j][ky + 192]).
 __global__ void __launch_bounds__(DK_NT, 2) pass_y_dk_kernel(DockPassArgs a)
 {
     extern __shared__ float2 smd[];
@@ -137,7 +139,7 @@ __global__ void __launch_bounds__(DK_NT, 2) pass_y_dk_kernel(DockPassArgs a)
     constexpr int JT = DK_P / DK_NL;  // 48 column tiles
     const int x = blockIdx.x / JT, j0 = (blockIdx.x % JT) * DK_NL;
     const float2 *T1 = a.in + (long long)b * a.in_bstride + (long long)x * DK_L * DK_P + j0;
-    float2 *T2 = a.out + (long long)b * a.out_bstride + (long long)x * DK_M * DK_P + j0;
+    float2 *T2 = a.out + (long long)b * a.out_bstride + ((long long)x * DK_P + j0) * DK_P;
     {   // planes the fold reads (dk_live_planes) but without a live row here are written as zero
         int xlo, xhi;
         dk_live_planes(a.cx, a.live_r2, xlo, xhi);
@@ -152,7 +154,7 @@ __global__ void __launch_bounds__(DK_NT, 2) pass_y_dk_kernel(DockPassArgs a)
         yhi = min(DK_L - 1, (int)floorf(a.cy + hh));
     }
     if (ylo > yhi) {
-        for (int e = threadIdx.x; e < DK_M * DK_NL; e += DK_NT) T2[(long long)(e / DK_NL) * DK_P + e % DK_NL] = make_float2(0.f, 0.f);
+        for (int e = threadIdx.x; e < DK_NL * DK_P; e += DK_NT) T2[e] = make_float2(0.f, 0.f);
         return;
     }
     load_twiddles<DK_L>(tw, a.tw, threadIdx.x, DK_NT);
@@ -174,42 +176,42 @@ __global__ void __launch_bounds__(DK_NT, 2) pass_y_dk_kernel(DockPassArgs a)
         for (int m = 0; m < DK_E; m++) xv[m] = A[line * DK_LS + pad(tl + DK_TPL * m)];
         __syncthreads();
     }
+    float2 keep[6];
 #pragma unroll 1
     for (int p = 0; p < DK_C; p++) {
         float2 yv[DK_E];
         dk_coset(yv, xv, a.ctw, p, tl);
         fft_regs<DK_L, -1, true>(yv, A + line * DK_LS, B + line * DK_LS, tw, tl);
         __syncwarp();
-        // the 6 in-band outputs x mult_y(ky) staged at u = q (q < 96) or q - 192 (q >= 288)
+        if (p == 0) {
 #pragma unroll
-        for (int u6 = 0; u6 < 6; u6++) {
-            const int m = u6 < 3 ? u6 : u6 + 6;
-            const int q = tl + DK_TPL * m;
-            const int k = dk_k(m, p, tl);
-            const float2 mu = k >= -DK_K ? __ldg(a.mult + k + DK_K) : make_float2(0.f, 0.f);
-            A[line * DK_LS + pad(m < 3 ? q : q - 192)] = cmul(yv[m], mu);
-        }
-        __syncthreads();
-        // rows ky of T2: 8 columns (64 bytes) each
+            for (int u = 0; u < 6; u++) {
+                const int m = u < 3 ? u : u + 6;
+                keep[u] = dk_in_band(m, 0, tl) ? yv[m] : make_float2(0.f, 0.f);
+            }
+        } else {
+            float2 *out = T2 + (long long)line * DK_P;
 #pragma unroll
-        for (int r = 0; r < 6; r++) {
-            const int e = threadIdx.x + DK_NT * r;
-            const int u = e / DK_NL, i = e % DK_NL;
-            const int q = u < 96 ? u : u + 192;
-            const int k = 2 * q + p - (q >= 288 ? DK_G : 0);
-            if (k >= -DK_K) T2[(long long)(k + DK_K) * DK_P + i] = A[i * DK_LS + pad(u)];
+            for (int u = 0; u < 6; u++) {
+                const int m = u < 3 ? u : u + 6;
+                const int k0 = dk_k(m, 0, tl);
+                const float2 m0 = k0 >= -DK_K ? __ldg(a.mult + k0 + DK_K) : make_float2(0.f, 0.f);
+                const float2 m1 = __ldg(a.mult + k0 + 1 + DK_K);
+                const float2 v0 = cmul(keep[u], m0), v1 = cmul(yv[m], m1);
+                *reinterpret_cast<float4 *>(out + k0 + DK_Z0) = make_float4(v0.x, v0.y, v1.x, v1.y);
+            }
         }
-        __syncthreads();  // A is the next coset's FFT buffer
     }
 }
 
 // ============================================================================ fold
 // Persistent blocks over (target block, rotation) items, rotation-fastest (the batch's items
-// share A'' rows through L2).  Item = target row k'y, 8 targets k'z in [z0, z0 + 8).  For each
-// alias ky = k'y + 128 ny and kz = k'z + 128 nz in the band, the x transform of B's T2 line at
-// (-ky, -kz) times A''(ky, kz) (= A'(k') mult_x(kx) at the coset-major position of the output
-// kx, reading C-3: weights not conjugated, f_hat_A'(k') f_hat_RB(-k')), summed into the target
-// k'x = -kx mod 128.
+// share A'' rows through L2).  Item = target plane k'z, 8 targets k'y with labels
+// 8 t + 1 .. 8 t + 8 (k'y = label mod 128: the lines' T2 rows -ky + 192 then start on a
+// 16-byte boundary).  For each alias ky = label + 128 ny and kz = k'z + 128 nz in the band,
+// the x transform of B's T2 line at (-ky, -kz) times A''(ky, kz) (= A'(k') mult_x(kx) at the
+// coset-major position of the output kx, reading C-3: weights not conjugated,
+// f_hat_A'(k') f_hat_RB(-k')), summed into the target k'x = -kx mod 128.
 __global__ void __launch_bounds__(DK_NT, 2) fold_dk_kernel(DockFoldArgs a)
 {
     extern __shared__ float2 smd[];
@@ -217,8 +219,8 @@ __global__ void __launch_bounds__(DK_NT, 2) fold_dk_kernel(DockFoldArgs a)
     float2 *A = tw + DK_L;
     float2 *B = A + DK_NL * DK_LS;
     const int line = threadIdx.x / DK_TPL, tl = threadIdx.x % DK_TPL;
-    constexpr int ZT = DK_NP / DK_NL;  // 16 target tiles per k'y row
-    const int n_items = DK_NP * ZT * a.nb;
+    constexpr int YT = DK_NP / DK_NL;  // 16 target tiles per k'z plane
+    const int n_items = DK_NP * YT * a.nb;
     load_twiddles<DK_L>(tw, a.tw, threadIdx.x, DK_NT);
     __syncthreads();
     int xlo, xhi;  // x planes of T2 the y pass writes
@@ -227,34 +229,34 @@ __global__ void __launch_bounds__(DK_NT, 2) fold_dk_kernel(DockFoldArgs a)
     for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
         const int b = w % a.nb;
         const int tb = w / a.nb;
-        const int kyp = tb / ZT, z0 = (tb % ZT) * DK_NL;
+        const int kzp = tb / YT, y1 = (tb % YT) * DK_NL + 1;  // labels y1 .. y1 + 7
         const float2 *T2 = a.T2 + (long long)b * a.t2_bstride;
         float2 acc[2][DK_C];
 #pragma unroll
         for (int j = 0; j < 2; j++)
 #pragma unroll
             for (int p = 0; p < DK_C; p++) acc[j][p] = make_float2(0.f, 0.f);
-        // aliases of k' in [0, 128) within the band [-191, 191]: k' - 256 (k' >= 65), k' - 128, k',
-        // k' + 128 (k' <= 63)
+        // aliases within the band [-191, 191] of a label in [1, 128]: label - 256, - 128, + 0,
+        // + 128; of k'z in [0, 128): k'z - 256 (k'z >= 65), - 128, + 0, + 128 (k'z <= 63)
 #pragma unroll 1
-        for (int ny = -2; ny <= 1; ny++) {
-            const int ky = kyp + DK_NP * ny;
-            if (ky < -DK_K || ky > DK_K) continue;
+        for (int nz = -2; nz <= 1; nz++) {
+            const int kz = kzp + DK_NP * nz;
+            if (kz < -DK_K || kz > DK_K) continue;
 #pragma unroll 1
-            for (int nz = -2; nz <= 1; nz++) {
-                const int kzlo = z0 + DK_NP * nz, kzhi = kzlo + DK_NL - 1;
-                if (kzhi < -DK_K || kzlo > DK_K) continue;  // no line of the group in band
-                // T2 lines (-ky, -kz_i), transposed through A for coalescing
+            for (int ny = -2; ny <= 1; ny++) {
+                const int kylo = y1 + DK_NP * ny, kyhi = kylo + DK_NL - 1;
+                if (kyhi < -DK_K || kylo > DK_K) continue;  // no line of the group in band
+                // T2 lines (-ky_i, -kz), transposed through A for coalescing
                 {
                     const int i = threadIdx.x % DK_NL, n0 = threadIdx.x / DK_NL;
-                    const int kzi = kzlo + i;
-                    const bool ok = kzi >= -DK_K && kzi <= DK_K;
-                    const float2 *src = T2 + (long long)(-ky + DK_K) * DK_P + (-kzi + DK_Z0);
+                    const int kyi = kylo + i;
+                    const bool ok = kyi >= -DK_K && kyi <= DK_K;
+                    const float2 *src = T2 + (long long)(-kz + DK_Z0) * DK_P + (-kyi + DK_Z0);
                     float2 xv[DK_E];
 #pragma unroll
                     for (int m = 0; m < DK_E; m++) {
                         const int n = n0 + (DK_NT / DK_NL) * m;
-                        xv[m] = (ok && n >= xlo && n <= xhi) ? src[(long long)n * DK_M * DK_P] : make_float2(0.f, 0.f);
+                        xv[m] = (ok && n >= xlo && n <= xhi) ? src[(long long)n * DK_P * DK_P] : make_float2(0.f, 0.f);
                     }
                     __syncthreads();  // previous group's FFTs are done with A
 #pragma unroll
@@ -265,9 +267,9 @@ __global__ void __launch_bounds__(DK_NT, 2) fold_dk_kernel(DockFoldArgs a)
 #pragma unroll
                 for (int m = 0; m < DK_E; m++) xv[m] = A[line * DK_LS + pad(tl + DK_TPL * m)];
                 __syncthreads();  // A is rewritten by the FFT below
-                const int kz = kzlo + line;
-                const bool my_ok = kz >= -DK_K && kz <= DK_K;
-                const float2 *arow = a.Ahat + ((long long)(ky + DK_K) * DK_M + (my_ok ? kz + DK_K : 0)) * DK_MS;
+                const int ky = kylo + line;
+                const bool my_ok = ky >= -DK_K && ky <= DK_K;
+                const float2 *arow = a.Ahat + ((long long)(my_ok ? ky + DK_K : 0) * DK_M + (kz + DK_K)) * DK_MS;
 #pragma unroll 1
                 for (int p = 0; p < DK_C; p++) {
                     const int pb = (p == 0 ? a.pos_base[0] : a.pos_base[1]) + tl;
@@ -295,7 +297,7 @@ __global__ void __launch_bounds__(DK_NT, 2) fold_dk_kernel(DockFoldArgs a)
                 }
             }
         }
-        // targets k'x = -(2 tl + 64 j + p) mod 128 -> F[k'x][k'y][k'z] (8 k'z per 64-byte row piece)
+        // targets k'x = -(2 tl + 64 j + p) mod 128 -> F[k'x][k'y][k'z]
         __syncthreads();
 #pragma unroll
         for (int j = 0; j < 2; j++)
@@ -305,7 +307,7 @@ __global__ void __launch_bounds__(DK_NT, 2) fold_dk_kernel(DockFoldArgs a)
         float2 *F = a.F + (long long)b * a.f_bstride;
         for (int e = threadIdx.x; e < DK_NL * DK_NP; e += DK_NT) {
             const int i = e % DK_NL, t = e / DK_NL;
-            F[((long long)t * DK_NP + kyp) * DK_NP + z0 + i] = A[i * DK_LS + t];
+            F[((long long)t * DK_NP + ((y1 + i) & (DK_NP - 1))) * DK_NP + kzp] = A[i * DK_LS + t];
         }
     }
 }

@@ -206,7 +206,7 @@ struct DockPassArgs {
     const float2 *tw, *ctw, *mult;  // twiddles, coset twiddles [2][384], the axis multipliers [2K + 1]
     const float2 *in;               // z: box [b][L][L][L]; y: T1 [b][L][L][384]
     long long in_bstride;
-    float2 *out;                    // z: T1; y: T2 [b][L][2K + 1][384]
+    float2 *out;                    // z: T1; y: T2 [b][L][kz + 192][ky + 192] (384 x 384 per x)
     long long out_bstride;
     float cx, cy, live_r2, zero_r2; // B's support cylinder (spread_z's tile and row tests)
 };
