@@ -99,6 +99,7 @@ struct bc_ctx {
     float2 *d_g02 = nullptr;
     float4 *d_recB = nullptr;      // (s, w, g0, g2) per ball of B (cells)
     float *d_recWi = nullptr;      // imaginary part of B's weights (complex weights)
+    float4 *d_recBim = nullptr;    // (s, Im w, g0, g2) per ball of B (planar complex spread)
     double rc_max_B = 0;           // max (s + W) / hf over B
 
     float4 *d_phi = nullptr;
@@ -698,6 +699,9 @@ bc_status build_spread_z_tables(bc_ctx *ctx)
     for (int64_t j = 0; j < nb; j++) wi[j] = (float)ctx->hw[1][2 * j + 1];
     TRY(dalloc(ctx, &ctx->d_recWi, sizeof(float) * cnt));
     CU(ctx, cudaMemcpy(ctx->d_recWi, wi.data(), sizeof(float) * cnt, cudaMemcpyHostToDevice));
+    for (int64_t j = 0; j < nb; j++) rb[j].y = wi[j];  // (s, Im w, g0, g2) for the planar spread
+    TRY(dalloc(ctx, &ctx->d_recBim, sizeof(float4) * cnt));
+    CU(ctx, cudaMemcpy(ctx->d_recBim, rb.data(), sizeof(float4) * cnt, cudaMemcpyHostToDevice));
     ctx->slot[0].sz_cap = ctx->slot[1].sz_cap = 0;  // binning workspace resized at the next correlate
     TRY(dalloc(ctx, &ctx->d_phi, sizeof(float4) * tab.size()));
     TRY(dalloc(ctx, &ctx->d_bcells, sizeof(float4) * cnt));
@@ -905,7 +909,9 @@ bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, voi
         a.recA = sl.recA;
         a.recB = ctx->d_recB;
         a.recWi = ctx->d_recWi;
+        a.recBim = ctx->d_recBim;
         a.cplx = cplx ? 1 : 0;
+        a.planar = (cplx && use_dock_fast(ctx)) ? 1 : 0;  // pass_z_dk reads the planar box
         a.counts = sl.szcnt;
         a.offs = sl.szoff;
         a.lists = sl.szlist;
@@ -936,7 +942,7 @@ bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, voi
         if (!launch_spread_z(a, nb, s))
             return fail(ctx, BC_EUNSUPPORTED, "spread_z: profile table (n = %d, U = %g) or box L = %d not compiled in",
                         a.phi_n, (double)a.phi_U, a.L);
-        ctx->launches += (a.box && !cplx) ? 2 : 1;
+        ctx->launches += ((a.box && !cplx) || a.planar) ? 2 : 1;
     } else {
         SpreadArgs a{};
         if (which == 1 && generic_bins_B(ctx)) {  // per-rotation column bins (spread_z.cu kernels)
@@ -2072,6 +2078,7 @@ bc_status bc_destroy(bc_ctx *ctx)
     dfree(ctx->d_dec);
     dfree(ctx->d_recB);
     dfree(ctx->d_recWi);
+    dfree(ctx->d_recBim);
     for (Slot &sl : ctx->slot) {
         if (sl.ws1) cudaFree(sl.ws1);
         if (sl.ws2) cudaFree(sl.ws2);

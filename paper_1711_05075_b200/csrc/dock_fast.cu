@@ -4,7 +4,7 @@
 //
 // Same quantities as the generic passes (passes.cu; PAPER.md L398-L419 eq_ccghat, the band
 // spectrum of the relocated knots eq_rhoPhat, deconvolved by the blob window):
-//   pass_z_dk   box[x][y][n] (complex, spread_z CPLX)   -> T1[x][y][kz + 192]   (z transform)
+//   pass_z_dk   box[re|im][x][y][n] (spread_z planar)  -> T1[x][y][kz + 192]   (z transform)
 //   pass_y_dk   T1                                      -> T2[x][kz + 192][ky + 192]
 //   fold_dk     T2 -> x transform -> A''(k') B(-k') summed into F[k' mod 128]  (register-owned)
 // What the plan shape makes compile-time (FFT384 lines of 32 threads, radices 4 x 8 x 12):
@@ -29,6 +29,7 @@ constexpr int DK_TPL = 32, DK_NL = 8, DK_NT = DK_TPL * DK_NL, DK_E = DK_L / DK_T
 constexpr int DK_P = 384;   // T1 / T2 row pitch: kz at index kz + 192
 constexpr int DK_Z0 = 192;  // index of kz = 0
 constexpr int DK_LS = line_stride(DK_L);
+constexpr int DK_TW = T3<DK_L>::SIZE;  // conflict-free twiddle tables (fft_regs_t3)
 constexpr int DK_MS = cm_row_stride(DK_L, DK_C, DK_G, DK_K);  // A'' row stride (coset-major)
 static_assert(Plan<DK_L>::TPL == DK_TPL && Plan<DK_L>::n == 3 && warp_local<DK_L>(), "dock plan");
 static_assert(DK_E == 12, "outputs per thread");
@@ -80,26 +81,28 @@ __global__ void __launch_bounds__(DK_NT, 2) pass_z_dk_kernel(DockPassArgs a)
 {
     extern __shared__ float2 smd[];
     float2 *tw = smd;
-    float2 *A = tw + DK_L;
+    float2 *A = tw + DK_TW;
     float2 *B = A + DK_NL * DK_LS;
     const int line = threadIdx.x / DK_TPL, tl = threadIdx.x % DK_TPL;
     const int b = blockIdx.y;
     const long long row0 = (long long)blockIdx.x * DK_NL;
     const int x = (int)(row0 / DK_L), y0 = (int)(row0 % DK_L);
     if (dk_zero_tile(x, y0, a.cx, a.cy, a.zero_r2) && dk_zero_tile(x, y0 + DK_NL - 1, a.cx, a.cy, a.zero_r2)) return;
-    load_twiddles<DK_L>(tw, a.tw, threadIdx.x, DK_NT);
+    load_twiddles_t3<DK_L>(tw, a.tw, threadIdx.x, DK_NT);
     const bool live = !dk_zero_tile(x, y0 + line, a.cx, a.cy, a.zero_r2);
-    const float2 *in = a.in + (long long)b * a.in_bstride + (row0 + line) * DK_L;
+    // planar box: real plane, then the imaginary plane L^3 floats further
+    const float *inr = reinterpret_cast<const float *>(a.in + (long long)b * a.in_bstride) + (row0 + line) * DK_L;
+    const float *ini = inr + (long long)DK_L * DK_L * DK_L;
     float2 xv[DK_E];
 #pragma unroll
-    for (int m = 0; m < DK_E; m++) xv[m] = live ? in[tl + DK_TPL * m] : make_float2(0.f, 0.f);
+    for (int m = 0; m < DK_E; m++) xv[m] = live ? make_float2(inr[tl + DK_TPL * m], ini[tl + DK_TPL * m]) : make_float2(0.f, 0.f);
     __syncthreads();  // twiddle table
     float2 keep[6];
 #pragma unroll 1
     for (int p = 0; p < DK_C; p++) {
         float2 yv[DK_E];
         dk_coset(yv, xv, a.ctw, p, tl);
-        fft_regs<DK_L, -1, true>(yv, A + line * DK_LS, B + line * DK_LS, tw, tl);
+        fft_regs_t3<DK_L, -1, true>(yv, A + line * DK_LS, B + line * DK_LS, tw, tl);
         __syncwarp();  // the next coset's FFT rewrites this line's buffers
         if (p == 0) {
 #pragma unroll
@@ -132,7 +135,7 @@ __global__ void __launch_bounds__(DK_NT, 2) pass_y_dk_kernel(DockPassArgs a)
 {
     extern __shared__ float2 smd[];
     float2 *tw = smd;
-    float2 *A = tw + DK_L;
+    float2 *A = tw + DK_TW;
     float2 *B = A + DK_NL * DK_LS;
     const int line = threadIdx.x / DK_TPL, tl = threadIdx.x % DK_TPL;
     const int b = blockIdx.y;
@@ -157,7 +160,7 @@ __global__ void __launch_bounds__(DK_NT, 2) pass_y_dk_kernel(DockPassArgs a)
         for (int e = threadIdx.x; e < DK_NL * DK_P; e += DK_NT) T2[e] = make_float2(0.f, 0.f);
         return;
     }
-    load_twiddles<DK_L>(tw, a.tw, threadIdx.x, DK_NT);
+    load_twiddles_t3<DK_L>(tw, a.tw, threadIdx.x, DK_NT);
     float2 xv[DK_E];
     {
 #pragma unroll
@@ -181,7 +184,7 @@ __global__ void __launch_bounds__(DK_NT, 2) pass_y_dk_kernel(DockPassArgs a)
     for (int p = 0; p < DK_C; p++) {
         float2 yv[DK_E];
         dk_coset(yv, xv, a.ctw, p, tl);
-        fft_regs<DK_L, -1, true>(yv, A + line * DK_LS, B + line * DK_LS, tw, tl);
+        fft_regs_t3<DK_L, -1, true>(yv, A + line * DK_LS, B + line * DK_LS, tw, tl);
         __syncwarp();
         if (p == 0) {
 #pragma unroll
@@ -216,12 +219,12 @@ __global__ void __launch_bounds__(DK_NT, 2) fold_dk_kernel(DockFoldArgs a)
 {
     extern __shared__ float2 smd[];
     float2 *tw = smd;
-    float2 *A = tw + DK_L;
+    float2 *A = tw + DK_TW;
     float2 *B = A + DK_NL * DK_LS;
     const int line = threadIdx.x / DK_TPL, tl = threadIdx.x % DK_TPL;
     constexpr int YT = DK_NP / DK_NL;  // 16 target tiles per k'z plane
     const int n_items = DK_NP * YT * a.nb;
-    load_twiddles<DK_L>(tw, a.tw, threadIdx.x, DK_NT);
+    load_twiddles_t3<DK_L>(tw, a.tw, threadIdx.x, DK_NT);
     __syncthreads();
     int xlo, xhi;  // x planes of T2 the y pass writes
     dk_live_planes(a.cx, a.live_r2, xlo, xhi);
@@ -282,7 +285,7 @@ __global__ void __launch_bounds__(DK_NT, 2) fold_dk_kernel(DockFoldArgs a)
                     }
                     float2 yv[DK_E];
                     dk_coset(yv, xv, a.ctw, p, tl);
-                    fft_regs<DK_L, -1, true>(yv, A + line * DK_LS, B + line * DK_LS, tw, tl);
+                    fft_regs_t3<DK_L, -1, true>(yv, A + line * DK_LS, B + line * DK_LS, tw, tl);
                     __syncwarp();
                     // outputs m and m' with the same m & 1 share a target: (0, 2, 10) -> j = 0, (1, 9, 11) -> j = 1
                     const float2 s0 = cfma(av[0], yv[0], cfma(av[2], yv[2], cmul(av[4], yv[10])));
@@ -318,7 +321,7 @@ bool dock_fast_supported(int L, int c, int G, int K, int Np, int complex_w)
     return L == DK_L && c == DK_C && G == DK_G && K == DK_K && Np == DK_NP && complex_w;
 }
 
-static size_t dk_smem() { return sizeof(float2) * ((size_t)DK_L + 2 * DK_NL * (size_t)DK_LS); }
+static size_t dk_smem() { return sizeof(float2) * ((size_t)DK_TW + 2 * DK_NL * (size_t)DK_LS); }
 
 void launch_pass_z_dk(const DockPassArgs &a, int batch, cudaStream_t s)
 {

@@ -407,6 +407,108 @@ BC_DEV void fft_regs_tab(float2 (&x)[L / Plan<L>::TPL], float2 *A, const float2 
     }
 }
 
+// ---------------------------------------------------------------- three-stage plans, conflict-free tables
+// The flat table read as tw[r * jm * TWS] (mid stage) and tw[r * j] (last stage) puts lanes at
+// stride r (or the Ns distinct jm rows at stride r TWS) and serialises up to 8-way (ncu on the
+// L = 384 docking passes: 27 % of all shared wavefronts excessive).  T3 tables instead:
+//   mid stage (S = 1, Ns = R0): twm[jm * (R1 + 1) + r] = w^{r jm L / (R0 R1)} -- a warp reads
+//     R0 distinct rows, padded by one entry so they fall in different banks;
+//   last stage (Ns = R0 R1): twl[(r - 1) Ns + j] = w^{r j} -- lanes read consecutive entries.
+template <int L>
+struct T3 {
+    static_assert(Plan<L>::n == 3, "three-stage plans only");
+    static constexpr int R0 = Plan<L>::r[0], R1 = Plan<L>::r[1], R2 = Plan<L>::r[2];
+    static constexpr int NS2 = R0 * R1, MROW = R1 + 1;
+    static constexpr int MSIZE = R0 * MROW, LSIZE = (R2 - 1) * NS2;
+    static constexpr int SIZE = (MSIZE + LSIZE + 1) & ~1;  // even: 16-byte aligned buffers after it
+};
+
+template <int L>
+BC_DEV void load_twiddles_t3(float2 *t, const float2 *tw_g, int tid, int nt)
+{
+    using P = T3<L>;
+    for (int e = tid; e < P::MSIZE + P::LSIZE; e += nt) {
+        int idx;
+        if (e < P::MSIZE) {
+            const int jm = e / P::MROW, r = e % P::MROW;
+            idx = r < P::R1 ? r * jm * (L / (P::R0 * P::R1)) : 0;
+        } else {
+            const int q = e - P::MSIZE;
+            idx = ((q / P::NS2 + 1) * (q % P::NS2)) % L;
+        }
+        t[e] = tw_g[idx];
+    }
+}
+
+// fft_regs for three-stage plans on the T3 tables (same data layout in and out).
+template <int L, int SIGN, bool WS = false>
+BC_DEV void fft_regs_t3(float2 (&x)[L / Plan<L>::TPL], float2 *A, float2 *B, const float2 *t3, int tl)
+{
+    static_assert(!WS || warp_local<L>(), "warp-synchronous FFT needs lines inside one warp");
+    static_assert(plan_ok<L>(), "bad FFT plan");
+    using P = T3<L>;
+    constexpr int TPL = Plan<L>::TPL;
+    {   // stage 0 (Ns = 1): registers -> A
+        constexpr int R = P::R0, U = (L / R) / TPL;
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int j = tl + TPL * u;
+            float2 v[R];
+#pragma unroll
+            for (int r = 0; r < R; r++) v[r] = x[u + U * r];
+            Dft<R, SIGN>::run(v);
+#pragma unroll
+            for (int r = 0; r < R; r++) A[pad(j * R + r)] = v[r];
+        }
+    }
+    line_sync<WS>();
+    {   // mid stage (Ns = R0): A -> B
+        constexpr int R = P::R1, Ns = P::R0, LR = L / R;
+#pragma unroll
+        for (int j0 = 0; j0 < LR; j0 += TPL) {
+            const int j = j0 + tl;
+            if ((LR % TPL) != 0 && j >= LR) break;
+            const int jm = j % Ns;
+            float2 v[R];
+#pragma unroll
+            for (int r = 0; r < R; r++) {
+                float2 y = A[pad(j + r * LR)];
+                if (r > 0) {
+                    const float2 w = t3[jm * P::MROW + r];
+                    y = SIGN < 0 ? cmul(y, w) : cmulc(y, w);
+                }
+                v[r] = y;
+            }
+            Dft<R, SIGN>::run(v);
+            const int idxD = (j / Ns) * Ns * R + jm;
+#pragma unroll
+            for (int r = 0; r < R; r++) B[pad(idxD + r * Ns)] = v[r];
+        }
+    }
+    line_sync<WS>();
+    {   // last stage (Ns = R0 R1): B -> registers
+        constexpr int R = P::R2, Ns = P::NS2, U = Ns / TPL;
+        const float2 *twl = t3 + P::MSIZE;
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int j = tl + TPL * u;
+            float2 v[R];
+#pragma unroll
+            for (int r = 0; r < R; r++) {
+                float2 y = B[pad(j + r * Ns)];
+                if (r > 0) {
+                    const float2 w = twl[(r - 1) * Ns + j];
+                    y = SIGN < 0 ? cmul(y, w) : cmulc(y, w);
+                }
+                v[r] = y;
+            }
+            Dft<R, SIGN>::run(v);
+#pragma unroll
+            for (int r = 0; r < R; r++) x[u + U * r] = v[r];
+        }
+    }
+}
+
 // FFT of the calling thread-group's line, registers in / registers out (see header).
 // A and B are this line's shared-memory buffers (B used only when n >= 3).
 // Contains barriers (block-wide, or warp-wide with WS = true, which requires

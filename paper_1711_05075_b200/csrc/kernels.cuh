@@ -66,7 +66,10 @@ struct SpreadZArgs {
     const float4 *recA;     // [b][n] rotated balls (SzBinArgs)
     const float4 *recB;     // [n] (s, w, g0, g2): radius (cells), weight (real part), d -> 0 series g0 + g2 d^2
     const float *recWi;     // [n] imaginary part of the weight (complex weights: BOX mode only)
+    const float4 *recBim;   // [n] (s, Im w, g0, g2) (complex weights, planar box)
     int cplx;               // complex weights: the box holds float2 cells
+    int planar;             // complex weights: two real spreads (Re w, then Im w) into the planes
+                            // box[b][0 .. L^3) (real parts) and box[b][L^3 .. 2 L^3) (imaginary)
     const int *counts, *offs, *lists;  // the bins (SzBinArgs)
     int nbins;
     long long list_stride;
@@ -204,7 +207,8 @@ bool fold_fast_supported(int L, int c, int G, int K, int Np, int complex_w);
 // hold kz at index kz + 192 (pitch dock_t_pitch() = 384).
 struct DockPassArgs {
     const float2 *tw, *ctw, *mult;  // twiddles, coset twiddles [2][384], the axis multipliers [2K + 1]
-    const float2 *in;               // z: box [b][L][L][L]; y: T1 [b][L][L][384]
+    const float2 *in;               // z: planar box [b][2][L][L][L] floats (real plane, then
+                                    // imaginary plane, spread_z planar); y: T1 [b][L][L][384]
     long long in_bstride;
     float2 *out;                    // z: T1; y: T2 [b][L][kz + 192][ky + 192] (384 x 384 per x)
     long long out_bstride;

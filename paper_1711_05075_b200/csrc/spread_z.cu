@@ -304,7 +304,9 @@ __global__ void __launch_bounds__(128, CPLX ? 4 : (BOX ? 8 : 4)) spread_z_kernel
             if (CPLX) wic = a.recWi[jl];
             const float ddx = fx - uc.x;
             const float ddy = fmaxf(fmaxf(fy0 - uc.y, uc.y - (fy0 + 3.f)), 0.f);
-            rel = fmaf(ddx, ddx, ddy * ddy) < uc.w;
+            // zero-weight balls add nothing (the planar complex spreads see each docking ball in
+            // one of their two passes only)
+            rel = fmaf(ddx, ddx, ddy * ddy) < uc.w && (wc.y != 0.f || (CPLX && wic != 0.f));
         }
         unsigned msk = __ballot_sync(0xffffffffu, rel);
         while (msk) {
@@ -345,9 +347,13 @@ __global__ void __launch_bounds__(128, CPLX ? 4 : (BOX ? 8 : 4)) spread_z_kernel
                 const float dz0 = (float)z0 - ue.z, dz1 = (float)z1 - ue.z;
                 const float g0 = ok0 ? prof(fmaf(dz0, dz0, dxy2)) : 0.f;
                 const float g1 = ok1 ? prof(fmaf(dz1, dz1, dxy2)) : 0.f;
-                if (ok0) accc[z0] = fmaf(we.y, g0, accc[z0]);
-                if (ok1) accc[z1] = fmaf(we.y, g1, accc[z1]);
-                if (CPLX) {
+                // complex weights: a ball whose weight is purely real or purely imaginary (the
+                // docking recipe's skin and core balls) updates one accumulator (warp-uniform test)
+                if (!CPLX || we.y != 0.f) {
+                    if (ok0) accc[z0] = fmaf(we.y, g0, accc[z0]);
+                    if (ok1) accc[z1] = fmaf(we.y, g1, accc[z1]);
+                }
+                if (CPLX && wie != 0.f) {
                     if (ok0) acci_c[z0] = fmaf(wie, g0, acci_c[z0]);
                     if (ok1) acci_c[z1] = fmaf(wie, g1, acci_c[z1]);
                 }
@@ -461,6 +467,16 @@ template <int L>
 static void spread_z_launch_cplx(const SpreadZArgs &a, int batch, cudaStream_t s)
 {
     const int tpa = L / 4;
+    if (a.planar) {  // two real spreads at the real kernel's occupancy (half the accumulator)
+        const size_t sm1 = (size_t)a.phi_n * 32 + (size_t)SZ_COLS * (L + 8) * 4;
+        cudaFuncSetAttribute(spread_z_kernel<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
+        SpreadZArgs im = a;
+        im.recB = a.recBim;
+        im.box = a.box + (long long)L * L * L;
+        spread_z_kernel<L, true><<<dim3(tpa * tpa, batch), 128, sm1, s>>>(a);
+        spread_z_kernel<L, true><<<dim3(tpa * tpa, batch), 128, sm1, s>>>(im);
+        return;
+    }
     const size_t sm = (size_t)a.phi_n * 32 + 2 * (size_t)SZ_COLS * (L + 8) * 4;
     cudaFuncSetAttribute(spread_z_kernel<L, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     spread_z_kernel<L, true, true><<<dim3(tpa * tpa, batch), 128, sm, s>>>(a);
