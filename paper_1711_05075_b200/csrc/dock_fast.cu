@@ -77,18 +77,20 @@ BC_DEV void dk_live_planes(float cx, float live_r2, int &xlo, int &xhi)
 // Block = 8 box rows (x, y0 .. y0 + 7).  Rows in tiles spread_z left unwritten read as zero; a
 // block of only such rows writes nothing (the y pass loads only rows within live_r, all of
 // them in written tiles).
-__global__ void __launch_bounds__(DK_NT, 2) pass_z_dk_kernel(DockPassArgs a)
+template <int NL>
+__global__ void __launch_bounds__(32 * NL, 20 / NL) pass_z_dk_kernel(DockPassArgs a)
 {
+    constexpr int NT = 32 * NL;
     extern __shared__ float2 smd[];
     float2 *tw = smd;
     float2 *A = tw + DK_TW;
-    float2 *B = A + DK_NL * DK_LS;
+    float2 *B = A + NL * DK_LS;
     const int line = threadIdx.x / DK_TPL, tl = threadIdx.x % DK_TPL;
     const int b = blockIdx.y;
-    const long long row0 = (long long)blockIdx.x * DK_NL;
+    const long long row0 = (long long)blockIdx.x * NL;
     const int x = (int)(row0 / DK_L), y0 = (int)(row0 % DK_L);
-    if (dk_zero_tile(x, y0, a.cx, a.cy, a.zero_r2) && dk_zero_tile(x, y0 + DK_NL - 1, a.cx, a.cy, a.zero_r2)) return;
-    load_twiddles_t3<DK_L>(tw, a.tw, threadIdx.x, DK_NT);
+    if (dk_zero_tile(x, y0, a.cx, a.cy, a.zero_r2) && dk_zero_tile(x, y0 + NL - 1, a.cx, a.cy, a.zero_r2)) return;
+    load_twiddles_t3<DK_L>(tw, a.tw, threadIdx.x, NT);
     const bool live = !dk_zero_tile(x, y0 + line, a.cx, a.cy, a.zero_r2);
     // planar box: real plane, then the imaginary plane L^3 floats further
     const float *inr = reinterpret_cast<const float *>(a.in + (long long)b * a.in_bstride) + (row0 + line) * DK_L;
@@ -131,16 +133,18 @@ __global__ void __launch_bounds__(DK_NT, 2) pass_z_dk_kernel(DockPassArgs a)
 // written (the fold does not read it).  T2 rows hold ky at index ky + 192, so, as in the z
 // pass, a thread stores the two cosets' outputs of one q with one 16-byte store: no output
 // staging (T2 = [x][j][ky + 192]).
-__global__ void __launch_bounds__(DK_NT, 2) pass_y_dk_kernel(DockPassArgs a)
+template <int NL>
+__global__ void __launch_bounds__(32 * NL, 20 / NL) pass_y_dk_kernel(DockPassArgs a)
 {
+    constexpr int NT = 32 * NL;
     extern __shared__ float2 smd[];
     float2 *tw = smd;
     float2 *A = tw + DK_TW;
-    float2 *B = A + DK_NL * DK_LS;
+    float2 *B = A + NL * DK_LS;
     const int line = threadIdx.x / DK_TPL, tl = threadIdx.x % DK_TPL;
     const int b = blockIdx.y;
-    constexpr int JT = DK_P / DK_NL;  // 48 column tiles
-    const int x = blockIdx.x / JT, j0 = (blockIdx.x % JT) * DK_NL;
+    constexpr int JT = DK_P / NL;  // 48 column tiles
+    const int x = blockIdx.x / JT, j0 = (blockIdx.x % JT) * NL;
     const float2 *T1 = a.in + (long long)b * a.in_bstride + (long long)x * DK_L * DK_P + j0;
     float2 *T2 = a.out + (long long)b * a.out_bstride + ((long long)x * DK_P + j0) * DK_P;
     {   // planes the fold reads (dk_live_planes) but without a live row here are written as zero
@@ -157,22 +161,22 @@ __global__ void __launch_bounds__(DK_NT, 2) pass_y_dk_kernel(DockPassArgs a)
         yhi = min(DK_L - 1, (int)floorf(a.cy + hh));
     }
     if (ylo > yhi) {
-        for (int e = threadIdx.x; e < DK_NL * DK_P; e += DK_NT) T2[e] = make_float2(0.f, 0.f);
+        for (int e = threadIdx.x; e < NL * DK_P; e += NT) T2[e] = make_float2(0.f, 0.f);
         return;
     }
-    load_twiddles_t3<DK_L>(tw, a.tw, threadIdx.x, DK_NT);
+    load_twiddles_t3<DK_L>(tw, a.tw, threadIdx.x, NT);
     float2 xv[DK_E];
     {
 #pragma unroll
         for (int m = 0; m < DK_E; m++) {
-            const int e = threadIdx.x + DK_NT * m;
-            const int n = e / DK_NL, i = e % DK_NL;
+            const int e = threadIdx.x + NT * m;
+            const int n = e / NL, i = e % NL;
             xv[m] = (n >= ylo && n <= yhi) ? T1[(long long)n * DK_P + i] : make_float2(0.f, 0.f);
         }
 #pragma unroll
         for (int m = 0; m < DK_E; m++) {
-            const int e = threadIdx.x + DK_NT * m;
-            A[(e % DK_NL) * DK_LS + pad(e / DK_NL)] = xv[m];
+            const int e = threadIdx.x + NT * m;
+            A[(e % NL) * DK_LS + pad(e / NL)] = xv[m];
         }
         __syncthreads();
 #pragma unroll
@@ -321,20 +325,24 @@ bool dock_fast_supported(int L, int c, int G, int K, int Np, int complex_w)
     return L == DK_L && c == DK_C && G == DK_G && K == DK_K && Np == DK_NP && complex_w;
 }
 
-static size_t dk_smem() { return sizeof(float2) * ((size_t)DK_TW + 2 * DK_NL * (size_t)DK_LS); }
+static size_t dk_smem(int nl = DK_NL) { return sizeof(float2) * ((size_t)DK_TW + 2 * nl * (size_t)DK_LS); }
+
+constexpr int DK_PASS_NL = 4;  // lines per block of the z / y passes (128 threads, 5 blocks per SM)
 
 void launch_pass_z_dk(const DockPassArgs &a, int batch, cudaStream_t s)
 {
-    const size_t sm = dk_smem();
-    cudaFuncSetAttribute(pass_z_dk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    pass_z_dk_kernel<<<dim3((unsigned)(DK_L * DK_L / DK_NL), batch), DK_NT, sm, s>>>(a);
+    constexpr int NL = DK_PASS_NL;
+    const size_t sm = dk_smem(NL);
+    cudaFuncSetAttribute(pass_z_dk_kernel<NL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    pass_z_dk_kernel<NL><<<dim3((unsigned)(DK_L * DK_L / NL), batch), 32 * NL, sm, s>>>(a);
 }
 
 void launch_pass_y_dk(const DockPassArgs &a, int batch, cudaStream_t s)
 {
-    const size_t sm = dk_smem();
-    cudaFuncSetAttribute(pass_y_dk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    pass_y_dk_kernel<<<dim3((unsigned)(DK_L * (DK_P / DK_NL)), batch), DK_NT, sm, s>>>(a);
+    constexpr int NL = DK_PASS_NL;
+    const size_t sm = dk_smem(NL);
+    cudaFuncSetAttribute(pass_y_dk_kernel<NL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    pass_y_dk_kernel<NL><<<dim3((unsigned)(DK_L * (DK_P / NL)), batch), 32 * NL, sm, s>>>(a);
 }
 
 bool launch_fold_dk(const DockFoldArgs &a_in, int batch, cudaStream_t s)
