@@ -158,6 +158,95 @@ __global__ void __launch_bounds__(256) exact_knot_kernel(ExactArgs a)
     }
 }
 
+// ---------------------------------------------------------------- fp32 lens, branch-free
+// The fp32 exact mode (tolerance 1e-4 of max|f|; the fp64 mode keeps lens_volume_dev<double>)
+// evaluates the lens volume division-free:
+//   V = pi/12 e^2 (d^2 + 2 d S - 3 D^2) / d = pi/12 e^2 (d + 2 S - 3 D^2 / d),  e = S - d,
+//   S = r + s, D = r - s;  V = 4/3 pi min(r, s)^3 when d <= |D|;  0 when d >= S (the chord test).
+// 1/d from one MUFU.RSQ (d = d^2 rsqrt(d^2), d^2 floored at 1e-30 so d = 0 gives 0, not NaN:
+// it is then inside the containment branch, or D = 0 and the 3 D^2 / d term is 0 x finite).
+// The weight w_i v_j (x h^3 x the fixed-point scale) is folded into two per-knot constants.
+struct LensF32 {
+    float cx, cy, cz;   // knot centre relative to its box's first point (grid units)
+    float rho2, S, aD, c1, c2;
+    float kr, ki;       // pi/12 x weight (re, im) x scale
+    float fr, fi;       // 4/3 pi min(r, s)^3 x weight x scale
+};
+
+__device__ __forceinline__ LensF32 lens_f32_setup(const ExactArgs &a, const KnotBox &kb, int i, int j, double scale)
+{
+    LensF32 L;
+    const double ih = a.inv_h;
+    L.cx = (float)((kb.cx - a.t0x) * ih - kb.lo[0]);
+    L.cy = (float)((kb.cy - a.t0y) * ih - kb.lo[1]);
+    L.cz = (float)((kb.cz - a.t0z) * ih - kb.lo[2]);
+    const double rr = a.A[i].w * ih, ss = a.B[j].w * ih;
+    L.rho2 = (float)((rr + ss) * (rr + ss));
+    L.S = (float)(rr + ss);
+    L.aD = (float)fabs(rr - ss);
+    L.c1 = 2.f * L.S;
+    L.c2 = (float)(3.0 * (rr - ss) * (rr - ss));
+    const double2 wa = a.wA[i], wb = a.wB[j];
+    const double h3q = a.h * a.h * a.h * scale;
+    const double wr = (wa.x * wb.x - wa.y * wb.y) * h3q, wi = (wa.x * wb.y + wa.y * wb.x) * h3q;
+    const double pi = 3.14159265358979323846, m = rr < ss ? rr : ss, vf = 4.0 / 3.0 * pi * m * m * m;
+    L.kr = (float)(pi / 12.0 * wr);
+    L.ki = (float)(pi / 12.0 * wi);
+    L.fr = (float)(vf * wr);
+    L.fi = (float)(vf * wi);
+    return L;
+}
+
+// visit the grid points inside the knot's ball (per (x, y) row its z range from the chord):
+// f(x, y, z, term_re, term_im) with box-relative indices
+template <bool CPLX, typename F>
+__device__ __forceinline__ void lens_f32_walk(const LensF32 &L, int nx, int ny, int nz, F &&f)
+{
+    for (int ix = 0; ix < nx; ix++) {
+        const float dx = L.cx - (float)ix;
+        for (int iy = 0; iy < ny; iy++) {
+            const float dy = L.cy - (float)iy;
+            const float dxy2 = fmaf(dx, dx, dy * dy);
+            if (dxy2 >= L.rho2) continue;
+            const float hz = sqrtf(L.rho2 - dxy2);
+            const int z0 = max(0, (int)ceilf(L.cz - hz)), z1 = min(nz - 1, (int)floorf(L.cz + hz));
+            for (int iz = z0; iz <= z1; iz++) {
+                const float dz = L.cz - (float)iz;
+                const float d2 = fmaf(dz, dz, dxy2);
+                if (d2 >= L.rho2) continue;
+                const float rd = rsqrtf(fmaxf(d2, 1e-30f));
+                const float d = d2 * rd;
+                const float e = L.S - d;
+                const float t = e * e * fmaf(-L.c2, rd, d + L.c1);
+                const bool inside = d <= L.aD;
+                f(ix, iy, iz, inside ? L.fr : L.kr * t, CPLX ? (inside ? L.fi : L.ki * t) : 0.f);
+            }
+        }
+    }
+}
+
+// fp32 thread-per-knot kernel (B by radius, as exact_knot_kernel; the same 64-bit integer
+// reductions)
+template <bool CPLX>
+__global__ void __launch_bounds__(256) exact_knot_f32_kernel(ExactArgs a)
+{
+    const int b = blockIdx.z;
+    const int i = a.i0 + blockIdx.y, jj = blockIdx.x * 256 + threadIdx.x;
+    if (jj >= a.nB) return;
+    const int j = a.permB[jj];
+    const KnotBox kb = knot_box(a, b, i, j);
+    const int nx = kb.hi[0] - kb.lo[0] + 1, ny = kb.hi[1] - kb.lo[1] + 1, nz = kb.hi[2] - kb.lo[2] + 1;
+    if (nx <= 0 || ny <= 0 || nz <= 0) return;
+    const LensF32 L = lens_f32_setup(a, kb, i, j, a.qscale);
+    const long long N = a.N, N3 = N * N * N;
+    unsigned long long *acc = (unsigned long long *)a.iacc + (long long)b * a.acc_bstride;
+    lens_f32_walk<CPLX>(L, nx, ny, nz, [&](int ix, int iy, int iz, float tr, float ti) {
+        const long long idx = ((long long)(kb.lo[0] + ix) * N + (kb.lo[1] + iy)) * N + kb.lo[2] + iz;
+        atomicAdd(acc + idx, (unsigned long long)__float2ll_rn(tr));
+        if (CPLX) atomicAdd(acc + N3 + idx, (unsigned long long)__float2ll_rn(ti));
+    });
+}
+
 void launch_exact_scatter(const ExactArgs &a_in, int batch, cudaStream_t s)
 {
     ExactArgs a = a_in;
@@ -170,8 +259,8 @@ void launch_exact_scatter(const ExactArgs &a_in, int batch, cudaStream_t s)
                 if (a.complex_w) exact_knot_kernel<double, true><<<grid, 256, 0, s>>>(a);
                 else exact_knot_kernel<double, false><<<grid, 256, 0, s>>>(a);
             } else {
-                if (a.complex_w) exact_knot_kernel<float, true><<<grid, 256, 0, s>>>(a);
-                else exact_knot_kernel<float, false><<<grid, 256, 0, s>>>(a);
+                if (a.complex_w) exact_knot_f32_kernel<true><<<grid, 256, 0, s>>>(a);
+                else exact_knot_f32_kernel<false><<<grid, 256, 0, s>>>(a);
             }
         } else {
             dim3 grid((unsigned)((a.nB + 7) / 8), ny, batch);
