@@ -130,6 +130,7 @@ struct bc_ctx {
     size_t acc_bytes = 0;
     bool ex_ready = false;          // exact_plan() for the current shapes
     double ex_qscale = 1.0;
+    bool ex_packed = false;         // fp32: packed 32-bit pair accumulators (exact.cu)
     bool ex_thread_per_knot = false;
     int *d_permB = nullptr;         // B's balls by radius (exact mode, thread-per-knot kernel)
     double *d_part = nullptr;
@@ -1314,6 +1315,33 @@ bc_status exact_plan(bc_ctx *ctx)
     ms /= std::max<int64_t>(ctx->n[1], 1);
     const double side = 2 * (mr + ms) / ctx->p.h + 1;
     ctx->ex_thread_per_knot = side * side * side <= 1000.0 && (double)ctx->n[0] * ctx->n[1] >= 262144.0;
+    // fp32 thread-per-knot with even N: packed pair accumulators, scale 2^30 / B' with the tight
+    // bound B' = min(inf'_A |B|_1, |A|_1 inf'_B) >= sum |terms| at any point, where
+    // inf'_S = max_i sum_{i' : |c_i - c_i'| < r_i + r_i'} |w_i'| >= |rho_S|_inf (a point of
+    // density is inside some ball i, and every ball containing it meets ball i); O(n^2), so only
+    // for n <= 16384
+    ctx->ex_packed = false;
+    if (ctx->p.precision == BC_FP32 && ctx->ex_thread_per_knot && ctx->p.N % 2 == 0 && ctx->n[0] <= 16384 &&
+        ctx->n[1] <= 16384) {
+        double inf[2] = {0, 0};
+        for (int w = 0; w < 2; w++) {
+            const std::vector<double> &x = ctx->hxyzr[w];
+            for (int64_t i = 0; i < ctx->n[w]; i++) {
+                double acc = 0;
+                for (int64_t k = 0; k < ctx->n[w]; k++) {
+                    const double dx = x[4 * i] - x[4 * k], dy = x[4 * i + 1] - x[4 * k + 1], dz = x[4 * i + 2] - x[4 * k + 2];
+                    const double rr = x[4 * i + 3] + x[4 * k + 3];
+                    if (dx * dx + dy * dy + dz * dz < rr * rr) acc += std::hypot(ctx->hw[w][2 * k], ctx->hw[w][2 * k + 1]);
+                }
+                inf[w] = std::max(inf[w], acc);
+            }
+        }
+        const double tight = std::min(inf[0] * sB1, sA1 * inf[1]);
+        if (tight > 0) {
+            ctx->ex_packed = true;
+            ctx->ex_qscale = std::ldexp(1.0, 30) / tight;
+        }
+    }
     std::vector<int> perm((size_t)std::max<int64_t>(ctx->n[1], 1), 0);
     for (int64_t j = 0; j < ctx->n[1]; j++) perm[j] = (int)j;
     std::stable_sort(perm.begin(), perm.begin() + ctx->n[1],
@@ -1616,6 +1644,7 @@ bc_status run_rotations(bc_ctx *ctx, int64_t n_rot, int out_kind, char *dout, si
             a.qscale = ctx->ex_qscale;
             a.thread_per_knot = ctx->ex_thread_per_knot ? 1 : 0;
             a.permB = ctx->d_permB;
+            a.packed = ctx->ex_packed ? 1 : 0;
             {
                 StageScope sc(ctx, s, "exact_pairs");
                 launch_exact_scatter(a, b, s);
@@ -1628,6 +1657,7 @@ bc_status run_rotations(bc_ctx *ctx, int64_t n_rot, int out_kind, char *dout, si
             o.iacc = a.iacc;
             o.acc_bstride = a.acc_bstride;
             o.inv_qscale = 1.0 / ctx->ex_qscale;
+            o.packed = a.packed;
             o.out_kind = out_kind;
             o.out = dout + out_per * r0;
             o.partials = ctx->d_part;

@@ -247,6 +247,65 @@ __global__ void __launch_bounds__(256) exact_knot_f32_kernel(ExactArgs a)
     });
 }
 
+// Packed pairs (fp32 mode, even N): the kernel above is bound by its global 64-bit reductions
+// (4.9e7 for Single; without the lens arithmetic it takes 90 % of the time).  Here each 64-bit
+// word holds the 32-bit fixed-point sums of two neighbouring grid points (flat index 2m in the
+// low half, 2m + 1 in the high half), so a chord adds two points with one reduction: the word
+// gets t0 + 2^32 t1 (signed 64-bit arithmetic), and as long as each point's sum fits int32 the
+// word decodes exactly (low = int32(word), high = (word - low) / 2^32).  The host's scale
+// (2^30 / a tight bound on sum |terms| at any point, exact_plan) guarantees the fit; integer
+// sums stay order-independent (deterministic).
+template <bool CPLX>
+__global__ void __launch_bounds__(256) exact_knot_pack_kernel(ExactArgs a)
+{
+    const int b = blockIdx.z;
+    const int i = a.i0 + blockIdx.y, jj = blockIdx.x * 256 + threadIdx.x;
+    if (jj >= a.nB) return;
+    const int j = a.permB[jj];
+    const KnotBox kb = knot_box(a, b, i, j);
+    const int nx = kb.hi[0] - kb.lo[0] + 1, ny = kb.hi[1] - kb.lo[1] + 1, nz = kb.hi[2] - kb.lo[2] + 1;
+    if (nx <= 0 || ny <= 0 || nz <= 0) return;
+    const LensF32 L = lens_f32_setup(a, kb, i, j, a.qscale);
+    const long long N = a.N, N3 = N * N * N;
+    unsigned long long *acc = (unsigned long long *)a.iacc + (long long)b * a.acc_bstride;
+    auto term = [&](float dxy2, int iz, int z0, int z1, long long &tr, long long &ti) {
+        tr = ti = 0;
+        if (iz < z0 || iz > z1) return;
+        const float dz = L.cz - (float)iz;
+        const float d2 = fmaf(dz, dz, dxy2);
+        if (d2 >= L.rho2) return;
+        const float rd = rsqrtf(fmaxf(d2, 1e-30f));
+        const float d = d2 * rd;
+        const float e = L.S - d;
+        const float t = e * e * fmaf(-L.c2, rd, d + L.c1);
+        const bool inside = d <= L.aD;
+        tr = __float2ll_rn(inside ? L.fr : L.kr * t);
+        if (CPLX) ti = __float2ll_rn(inside ? L.fi : L.ki * t);
+    };
+    const int pz = kb.lo[2] & 1;  // parity of the box's first z (N even: the flat index's parity)
+    for (int ix = 0; ix < nx; ix++) {
+        const float dx = L.cx - (float)ix;
+        for (int iy = 0; iy < ny; iy++) {
+            const float dy = L.cy - (float)iy;
+            const float dxy2 = fmaf(dx, dx, dy * dy);
+            if (dxy2 >= L.rho2) continue;
+            const float hz = sqrtf(L.rho2 - dxy2);
+            const int z0 = max(0, (int)ceilf(L.cz - hz)), z1 = min(nz - 1, (int)floorf(L.cz + hz));
+            if (z0 > z1) continue;
+            // word of box-relative z: (lo_z + z) >> 1; pairs start at the even flat index
+            const long long rowp = ((long long)(kb.lo[0] + ix) * N + (kb.lo[1] + iy)) * N + kb.lo[2] - pz;  // even
+            unsigned long long *w = acc + (rowp >> 1);
+            for (int q = (z0 + pz) & ~1; q <= z1 + pz; q += 2) {  // q = z + pz of the pair's even point
+                long long r0, i0, r1, i1;
+                term(dxy2, q - pz, z0, z1, r0, i0);
+                term(dxy2, q - pz + 1, z0, z1, r1, i1);
+                atomicAdd(w + (q >> 1), (unsigned long long)r0 + ((unsigned long long)r1 << 32));
+                if (CPLX) atomicAdd(w + (N3 >> 1) + (q >> 1), (unsigned long long)i0 + ((unsigned long long)i1 << 32));
+            }
+        }
+    }
+}
+
 void launch_exact_scatter(const ExactArgs &a_in, int batch, cudaStream_t s)
 {
     ExactArgs a = a_in;
@@ -259,8 +318,14 @@ void launch_exact_scatter(const ExactArgs &a_in, int batch, cudaStream_t s)
                 if (a.complex_w) exact_knot_kernel<double, true><<<grid, 256, 0, s>>>(a);
                 else exact_knot_kernel<double, false><<<grid, 256, 0, s>>>(a);
             } else {
-                if (a.complex_w) exact_knot_f32_kernel<true><<<grid, 256, 0, s>>>(a);
-                else exact_knot_f32_kernel<false><<<grid, 256, 0, s>>>(a);
+                if (a.packed) {
+                    if (a.complex_w) exact_knot_pack_kernel<true><<<grid, 256, 0, s>>>(a);
+                    else exact_knot_pack_kernel<false><<<grid, 256, 0, s>>>(a);
+                } else if (a.complex_w) {
+                    exact_knot_f32_kernel<true><<<grid, 256, 0, s>>>(a);
+                } else {
+                    exact_knot_f32_kernel<false><<<grid, 256, 0, s>>>(a);
+                }
             }
         } else {
             dim3 grid((unsigned)((a.nB + 7) / 8), ny, batch);
@@ -277,6 +342,15 @@ void launch_exact_scatter(const ExactArgs &a_in, int batch, cudaStream_t s)
 
 // ---------------------------------------------------------------- outputs of exact mode
 
+// accumulator value of point i (part offset applied by the caller): 64-bit, or packed pairs
+__device__ __forceinline__ long long acc_value(const long long *acc, long long i, int packed)
+{
+    if (!packed) return acc[i];
+    const long long w = acc[i >> 1];
+    const long long lo = (long long)(int)(unsigned)w;  // the even point's int32 sum
+    return (i & 1) ? (w - lo) >> 32 : lo;
+}
+
 __global__ void exact_full_kernel(ExactOutArgs a)
 {
     const int b = blockIdx.y;
@@ -284,7 +358,9 @@ __global__ void exact_full_kernel(ExactOutArgs a)
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N3) return;
     const long long *acc = a.iacc + (long long)b * a.acc_bstride;
-    const double re = (double)acc[i] * a.inv_qscale, im = a.complex_w ? (double)acc[N3 + i] * a.inv_qscale : 0.0;
+    const long long *acci = acc + (a.packed ? N3 / 2 : N3);
+    const double re = (double)acc_value(acc, i, a.packed) * a.inv_qscale,
+                 im = a.complex_w ? (double)acc_value(acci, i, a.packed) * a.inv_qscale : 0.0;
     if (a.fp64) {
         double *o = (double *)a.out;
         if (a.complex_w) {
@@ -326,7 +402,7 @@ __global__ void __launch_bounds__(256) exact_reduce1(ExactOutArgs a, int nblk)
     const long long *acc = a.iacc + (long long)b * a.acc_bstride;
     ValIdx mn = {1e300, 0x7fffffffffffffffll}, mx = {-1e300, 0x7fffffffffffffffll};
     for (long long i = (long long)blockIdx.x * 256 + threadIdx.x; i < N3; i += (long long)nblk * 256) {
-        const ValIdx c = {(double)acc[i] * a.inv_qscale + 0.0, i};
+        const ValIdx c = {(double)acc_value(acc, i, a.packed) * a.inv_qscale + 0.0, i};
         if (better_min(c, mn)) mn = c;
         if (better_max(c, mx)) mx = c;
     }

@@ -312,6 +312,7 @@ struct ExactArgs {
     int i0;              // first A ball of the launch (set by launch_exact_scatter)
     int thread_per_knot; // 1: thread per knot (small footprints), 0: warp per knot
     const int *permB;    // B's balls in order of radius (thread-per-knot kernel)
+    int packed;          // fp32: two 32-bit point sums per 64-bit word (exact_knot_pack_kernel)
 };
 void launch_exact_scatter(const ExactArgs &a, int batch, cudaStream_t s);
 
@@ -321,6 +322,7 @@ struct ExactOutArgs {
     const long long *iacc;
     long long acc_bstride;
     double inv_qscale;
+    int packed;          // accumulators as packed 32-bit pairs (ExactArgs::packed)
     int out_kind;
     void *out;           // full output or bc_extremum[]
     double *partials;    // scratch: [b][nblocks][2] vals
