@@ -11,7 +11,7 @@ for round in 1 2; do
     if [ "$v" = main ]; then unset BALLCORR_LIB; else export BALLCORR_LIB=$PWD/paper_1711_05075_b200/lib_$v/libballcorr.so; fi
     python bench.py --no-cpu-baseline 2>/dev/null | python -c "
 import json, sys
-d = json.loads(sys.stdin.read()); n = d['config']['rotations_per_rank_per_step']
+d = json.loads(sys.stdin.read()); n = d['config']['rotations_per_rank']
 print('$v', round(d['value'] / 1e10, 4), {k: round(v / n, 5) for k, v in d['stages_ms_per_step'].items()})"
   done
 done
