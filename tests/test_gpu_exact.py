@@ -151,3 +151,27 @@ def test_single_exact_reductions_and_large_knots(bc, oracle_mod):
     for r in range(2):
         rb = oracle_mod.correlate_grid(big.A_xyzr, big.A_w, big.B_xyzr, big.B_w, big.R[r], big.N, big.h, big.t0)
         assert rel_max_err(f[r], rb) <= 1e-9
+
+
+def test_packed_pairs_signed_complex_weights(bc, oracle_mod):
+    """fp32 thread-per-knot path with packed 32-bit pair accumulators (exact_knot_pack_kernel):
+    the Single shapes with complex weights of both signs (negative terms exercise the signed
+    low/high-half decoding) on the full grid against the oracle; and odd N (no packing) agrees."""
+    ws = make_config("single")
+    rng = np.random.default_rng(5)
+    wa = rng.uniform(-1, 1, ws.A_xyzr.shape[0]) + 1j * rng.uniform(-1, 1, ws.A_xyzr.shape[0])
+    wb = rng.uniform(-1, 1, ws.B_xyzr.shape[0]) + 1j * rng.uniform(-1, 1, ws.B_xyzr.shape[0])
+    c = bc.Correlator(N=ws.N, h=ws.h, t0=ws.t0, mode="exact", precision="f32", weights="complex")
+    c.shape_upload(0, ws.A_xyzr, wa)
+    c.shape_upload(1, ws.B_xyzr, wb)
+    f = as_complex(c.correlate_rotations(ws.R, "full"))[0]
+    ref = oracle_mod.correlate_grid(ws.A_xyzr, wa, ws.B_xyzr, wb, ws.R[0], ws.N, ws.h, ws.t0)
+    assert rel_max_err(f, ref) <= 1e-4
+    best = c.correlate_rotations(ws.R, "max_real")
+    check_extremum(best[0]["val"], best[0]["idx"], ref.real, "max", 1e-4 * np.abs(ref).max())
+    # odd N (63): the unpacked 64-bit kernel, same grid points as the first 63^3 of N = 64
+    co = bc.Correlator(N=ws.N - 1, h=ws.h, t0=ws.t0, mode="exact", precision="f32", weights="complex")
+    co.shape_upload(0, ws.A_xyzr, wa)
+    co.shape_upload(1, ws.B_xyzr, wb)
+    fo = as_complex(co.correlate_rotations(ws.R, "full"))[0]
+    assert rel_max_err(fo, ref[:-1, :-1, :-1]) <= 1e-4
