@@ -19,6 +19,7 @@
 // Transform: columns (2l, 2l+1) form one complex line z = a + i b; its c coset FFTs give
 // Z(k) on the band |k| <= K, and A(k) = (Z(k) + conj Z(-k)) / 2, B(k) = (Z(k) - conj Z(-k)) / 2i.
 #include <algorithm>
+#include <type_traits>
 
 #include "kernels.cuh"
 #include "fft_ct.cuh"
@@ -44,6 +45,16 @@ struct PhiVal {
 __device__ __forceinline__ PhiVal phi_lookup(const float4 *__restrict__ tab, int n, float tmax, float U, float invD, float u)
 {
     const float t = fminf(fmaxf((u + U) * invD, 0.f), tmax);
+    const int i = (int)t;
+    const float f = t - (float)i;
+    const float4 a = tab[i], b = tab[n + i];
+    return PhiVal{fmaf(f, fmaf(f, fmaf(f, a.w, a.z), a.y), a.x), fmaf(f, fmaf(f, fmaf(f, b.w, b.z), b.y), b.x)};
+}
+
+// the same at the table coordinate t = (u + U) / D, unclamped (callers form it with one FFMA)
+__device__ __forceinline__ PhiVal phi_lookup_t(const float4 *__restrict__ tab, int n, float tmax, float t)
+{
+    t = fminf(fmaxf(t, 0.f), tmax);
     const int i = (int)t;
     const float f = t - (float)i;
     const float4 a = tab[i], b = tab[n + i];
@@ -331,33 +342,45 @@ __global__ void __launch_bounds__(128, CPLX ? 4 : (BOX ? 8 : 4)) spread_z_kernel
                                           __shfl_sync(0xffffffffu, wc.z, src),
                                           __shfl_sync(0xffffffffu, wc.w, src));  // (s, w, g0, g2)
             const float wie = CPLX ? __shfl_sync(0xffffffffu, wic, src) : 0.f;
-            // two cells per lane per step (z and z + 8: independent evaluation chains)
-            auto prof = [&](float d2) {
-                if (d2 < 0.01f) return fmaf(we.w, d2, we.z);
-                const float rd = rsqrtf(d2);
-                const float d = d2 * rd;
-                const PhiVal p = phi_lookup(phi, nphi, tmax, U, invD, we.x - d);
-                PhiVal q = PhiVal{0.5f, 0.f};
-                if (we.x + d < U) q = phi_lookup(phi, nphi, tmax, U, invD, we.x + d);
-                return p.p1 + q.p1 - (p.p2 - q.p2) * rd;
+            // two cells per lane per step (z and z + 8: independent evaluation chains).  Table
+            // coordinates of s -+ d as one FFMA each from tS = (s + U) / D; rsqrt without the
+            // denormal fix-up (d^2 >= 0.01 on that path); the s + d lookup only for balls with
+            // s < U (warp-uniform: two copies of the loop), beyond it Phi1 = 1/2, Phi2 = 0.
+            const float tS = (we.x + U) * invD, tQ = 2.f * U * invD;
+            auto cells = [&](auto small_ball) {
+                auto prof = [&](float d2) {
+                    if (d2 < 0.01f) return fmaf(we.w, d2, we.z);
+                    float rd;
+                    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rd) : "f"(d2));
+                    const float d = d2 * rd;
+                    const PhiVal p = phi_lookup_t(phi, nphi, tmax, fmaf(-d, invD, tS));
+                    PhiVal q = PhiVal{0.5f, 0.f};
+                    if (decltype(small_ball)::value) {
+                        const float t = fmaf(d, invD, tS);
+                        if (t < tQ) q = phi_lookup_t(phi, nphi, tmax, t);
+                    }
+                    return p.p1 + q.p1 - (p.p2 - q.p2) * rd;
+                };
+                for (int it = 0; it < nmax; it += 2) {
+                    const int z0 = zlo + (it << 3) + hl, z1 = z0 + 8;
+                    const bool ok0 = z0 <= zhi, ok1 = z1 <= zhi;
+                    const float dz0 = (float)z0 - ue.z, dz1 = (float)z1 - ue.z;
+                    const float g0 = ok0 ? prof(fmaf(dz0, dz0, dxy2)) : 0.f;
+                    const float g1 = ok1 ? prof(fmaf(dz1, dz1, dxy2)) : 0.f;
+                    // complex weights: a ball whose weight is purely real or purely imaginary
+                    // (the docking recipe's skin and core balls) updates one accumulator
+                    if (!CPLX || we.y != 0.f) {
+                        if (ok0) accc[z0] = fmaf(we.y, g0, accc[z0]);
+                        if (ok1) accc[z1] = fmaf(we.y, g1, accc[z1]);
+                    }
+                    if (CPLX && wie != 0.f) {
+                        if (ok0) acci_c[z0] = fmaf(wie, g0, acci_c[z0]);
+                        if (ok1) acci_c[z1] = fmaf(wie, g1, acci_c[z1]);
+                    }
+                }
             };
-            for (int it = 0; it < nmax; it += 2) {
-                const int z0 = zlo + (it << 3) + hl, z1 = z0 + 8;
-                const bool ok0 = z0 <= zhi, ok1 = z1 <= zhi;
-                const float dz0 = (float)z0 - ue.z, dz1 = (float)z1 - ue.z;
-                const float g0 = ok0 ? prof(fmaf(dz0, dz0, dxy2)) : 0.f;
-                const float g1 = ok1 ? prof(fmaf(dz1, dz1, dxy2)) : 0.f;
-                // complex weights: a ball whose weight is purely real or purely imaginary (the
-                // docking recipe's skin and core balls) updates one accumulator (warp-uniform test)
-                if (!CPLX || we.y != 0.f) {
-                    if (ok0) accc[z0] = fmaf(we.y, g0, accc[z0]);
-                    if (ok1) accc[z1] = fmaf(we.y, g1, accc[z1]);
-                }
-                if (CPLX && wie != 0.f) {
-                    if (ok0) acci_c[z0] = fmaf(wie, g0, acci_c[z0]);
-                    if (ok1) acci_c[z1] = fmaf(wie, g1, acci_c[z1]);
-                }
-            }
+            if (we.x < U) cells(std::true_type());
+            else cells(std::false_type());
         }
     }
     __syncthreads();
