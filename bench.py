@@ -63,6 +63,8 @@ def parse():
                     help="strong scaling: nccl = NCCL broadcast of A's spectrum + all-gather of the records per "
                          "step; p2p = A's spectrum sharded by balls and reduced over peer memory inside the A'' "
                          "build, records stored into every rank's buffer by the reduction epilogue (no gather)")
+    ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
+                    help="replay each step's kernels from a CUDA graph (auto: one GPU, <= 16 rotations per step)")
     ap.add_argument("--dry-run", action="store_true",
                     help="CPU-only launcher/protocol check: gloo, stand-in correlator, no CUDA")
     args = ap.parse_args()
@@ -431,6 +433,28 @@ def run_ours(args, rank, world, local_rank):
     for _ in range(args.warmup):
         step()
     sync()
+    # small steps (one or a few rotations: Tiny, Single) are bound by the host-side cost of the
+    # launches, not by the GPU: replay the call's kernels from a CUDA graph (captured from the
+    # same library call on a side stream; the replay is bitwise the eager result)
+    graph, graph_launches = None, 0
+    if (not dry and world == 1 and not p2p and
+            (args.graph == "on" or (args.graph == "auto" and n_rot <= 16))):
+        gs = torch.cuda.Stream(dev)
+        gs.wait_stream(stream)
+        lc0 = ctx.launch_count()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=gs):
+            ctx.correlate_rotations(R_dev, kind, out=out, stream=gs)
+        graph_launches = ctx.launch_count() - lc0
+        stream.wait_stream(gs)
+        graph.replay()
+        sync()
+
+        def step():  # noqa: F811
+            graph.replay()
+            if reduced:
+                return gather_records(out[:out_bytes], n_rot, cap, 1, dev)
+            return out
 
     sampler = None if dry else ClockSampler(local_rank)
     if sampler:
@@ -456,7 +480,7 @@ def run_ours(args, rank, world, local_rank):
         ms = e0.elapsed_time(e1)
     if world > 1:
         dist.barrier()
-    launches = ctx.launch_count() - l0
+    launches = ctx.launch_count() - l0 + graph_launches * args.steps
     clocks = sampler.stop() if sampler else None
     t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -588,6 +612,7 @@ def run_ours(args, rank, world, local_rank):
                              "the per-rotation records (strong scaling, SURVEY.md §8(d)-(e))"
                              if args.scaling == "strong" else "per step: every rank its own full rotation set"),
                    "collectives": args.collectives,
+                   "cuda_graph": graph is not None,
                    "setup_s": setup_s,
                    "spectrum_A": ("sharded by balls, partials reduced over peer memory in the A'' build" if p2p
                                   else "rank 0, NCCL broadcast" if world > 1 else "computed")},
