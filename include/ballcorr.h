@@ -183,6 +183,11 @@ bc_status bc_spectrum_A_import(bc_ctx *ctx);
  * call stages them and returns after the result has reached `out`.  Calls on one context
  * must be ordered by the caller (same stream, or synchronised): they share workspaces.
  * Spectral mode needs bc_spectrum_A first (BC_ESTATE otherwise).
+ * CUDA graphs: with device R and out, a call made after a first (warm-up) call with the same
+ * n_rot and out_kind (workspaces then exist) may be captured into a CUDA graph on `stream`;
+ * replaying the graph recomputes from the current contents of R (and the uploaded shapes)
+ * into the same out, bitwise as an eager call.  Re-uploading a shape or changing n_rot
+ * invalidates the graph (workspaces may move).
  */
 bc_status bc_correlate_rotations(bc_ctx *ctx, const double *R, int64_t n_rot, int out_kind,
                                  void *out, void *stream);

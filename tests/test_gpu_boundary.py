@@ -13,7 +13,7 @@
 import numpy as np
 import pytest
 
-from synth import make_config, random_small_case
+from synth import make_config, random_small_case, random_rotations
 from gpu_helpers import rel_max_err, as_complex
 
 pytestmark = pytest.mark.gpu
@@ -213,3 +213,38 @@ def test_odd_N_on_the_np256_generic_plan(bc, oracle_mod):
     idx = np.unique(np.concatenate([rng.choice(255 ** 3, 60, replace=False), [int(mm255[1]["idx"]), 255 ** 3 - 1]]))
     ref = oracle_mod.correlate_points(w.A_xyzr, w.A_w, w.B_xyzr, w.B_w, w.R[0], 255, w.h, w.t0, idx)
     assert np.abs(f255.reshape(-1)[idx] - ref).max() <= TOL_F32 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("name", ["tiny", "single", "sweep"])
+def test_cuda_graph_capture_is_bitwise_eager(bc, name):
+    """ballcorr.h: after a warm-up call, a device-buffer bc_correlate_rotations can be captured
+    into a CUDA graph; replays recompute from the current R bitwise as eager calls."""
+    import torch
+    from paper_1711_05075_b200.presets import correlator_kwargs
+    w = make_config(name, n_rot=4 if name == "sweep" else None)
+    c = bc.Correlator(**correlator_kwargs(name, w.N, w.h, w.t0, w.weights))
+    c.shape_upload(0, w.A_xyzr, w.A_w)
+    c.shape_upload(1, w.B_xyzr, w.B_w)
+    c.spectrum_A()
+    kind = "minmax" if name == "sweep" else "full"
+    R = torch.tensor(w.R[:2] if name == "sweep" else w.R[:1], dtype=torch.float64, device="cuda")
+    _, shp, dt = c.out_shape(R.shape[0], kind)
+    out = torch.empty(int(np.prod(shp)) * np.dtype(dt).itemsize, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        c.correlate_rotations(R, kind, out=out, stream=s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        c.correlate_rotations(R, kind, out=out, stream=s)
+    # new rotations written into R after capture: the replay must use them
+    R2 = torch.tensor(random_rotations(np.random.default_rng(9), R.shape[0]), dtype=torch.float64, device="cuda")
+    R.copy_(R2)
+    out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    got = out.clone()
+    with torch.cuda.stream(s):
+        c.correlate_rotations(R, kind, out=out, stream=s)
+    torch.cuda.synchronize()
+    assert torch.equal(got, out)
