@@ -28,7 +28,12 @@ constexpr int DK_L = 384, DK_C = 2, DK_G = 768, DK_K = 191, DK_M = 2 * DK_K + 1,
 constexpr int DK_TPL = 32, DK_NL = 8, DK_NT = DK_TPL * DK_NL, DK_E = DK_L / DK_TPL;
 constexpr int DK_P = 384;   // T1 / T2 row pitch: kz at index kz + 192
 constexpr int DK_Z0 = 192;  // index of kz = 0
-constexpr int DK_LS = line_stride(DK_L);
+// line buffer strides: each line's A (stage-0 output, default pad) and B (mid-stage output,
+// T3 padB) buffers; = 8 mod 16 float2 for the passes' 4-line transposes (a warp stores 8
+// consecutive rows of 4 lines) and = 4 mod 16 for the fold's 8-line ones (4 rows of 8 lines):
+// the warp's stores fall on distinct bank pairs
+constexpr int DK_LSP = 440, DK_LSF = 436;
+static_assert(DK_LSF >= T3<384>::BLEN && DK_LSF >= fct::pad(383) + 1 && DK_LSP % 16 == 8 && DK_LSF % 16 == 4, "dock strides");
 constexpr int DK_TW = T3<DK_L>::SIZE;  // conflict-free twiddle tables (fft_regs_t3)
 constexpr int DK_MS = cm_row_stride(DK_L, DK_C, DK_G, DK_K);  // A'' row stride (coset-major)
 static_assert(Plan<DK_L>::TPL == DK_TPL && Plan<DK_L>::n == 3 && warp_local<DK_L>(), "dock plan");
@@ -84,7 +89,7 @@ __global__ void __launch_bounds__(32 * NL, 20 / NL) pass_z_dk_kernel(DockPassArg
     extern __shared__ float2 smd[];
     float2 *tw = smd;
     float2 *A = tw + DK_TW;
-    float2 *B = A + NL * DK_LS;
+    float2 *B = A + NL * DK_LSP;
     const int line = threadIdx.x / DK_TPL, tl = threadIdx.x % DK_TPL;
     const int b = blockIdx.y;
     const long long row0 = (long long)blockIdx.x * NL;
@@ -104,7 +109,7 @@ __global__ void __launch_bounds__(32 * NL, 20 / NL) pass_z_dk_kernel(DockPassArg
     for (int p = 0; p < DK_C; p++) {
         float2 yv[DK_E];
         dk_coset(yv, xv, a.ctw, p, tl);
-        fft_regs_t3<DK_L, -1, true>(yv, A + line * DK_LS, B + line * DK_LS, tw, tl);
+        fft_regs_t3<DK_L, -1, true>(yv, A + line * DK_LSP, B + line * DK_LSP, tw, tl);
         __syncwarp();  // the next coset's FFT rewrites this line's buffers
         if (p == 0) {
 #pragma unroll
@@ -140,7 +145,7 @@ __global__ void __launch_bounds__(32 * NL, 20 / NL) pass_y_dk_kernel(DockPassArg
     extern __shared__ float2 smd[];
     float2 *tw = smd;
     float2 *A = tw + DK_TW;
-    float2 *B = A + NL * DK_LS;
+    float2 *B = A + NL * DK_LSP;
     const int line = threadIdx.x / DK_TPL, tl = threadIdx.x % DK_TPL;
     const int b = blockIdx.y;
     constexpr int JT = DK_P / NL;  // 48 column tiles
@@ -176,11 +181,11 @@ __global__ void __launch_bounds__(32 * NL, 20 / NL) pass_y_dk_kernel(DockPassArg
 #pragma unroll
         for (int m = 0; m < DK_E; m++) {
             const int e = threadIdx.x + NT * m;
-            A[(e % NL) * DK_LS + pad(e / NL)] = xv[m];
+            A[(e % NL) * DK_LSP + pad(e / NL)] = xv[m];
         }
         __syncthreads();
 #pragma unroll
-        for (int m = 0; m < DK_E; m++) xv[m] = A[line * DK_LS + pad(tl + DK_TPL * m)];
+        for (int m = 0; m < DK_E; m++) xv[m] = A[line * DK_LSP + pad(tl + DK_TPL * m)];
         __syncthreads();
     }
     float2 keep[6];
@@ -188,7 +193,7 @@ __global__ void __launch_bounds__(32 * NL, 20 / NL) pass_y_dk_kernel(DockPassArg
     for (int p = 0; p < DK_C; p++) {
         float2 yv[DK_E];
         dk_coset(yv, xv, a.ctw, p, tl);
-        fft_regs_t3<DK_L, -1, true>(yv, A + line * DK_LS, B + line * DK_LS, tw, tl);
+        fft_regs_t3<DK_L, -1, true>(yv, A + line * DK_LSP, B + line * DK_LSP, tw, tl);
         __syncwarp();
         if (p == 0) {
 #pragma unroll
@@ -224,7 +229,7 @@ __global__ void __launch_bounds__(DK_NT, 2) fold_dk_kernel(DockFoldArgs a)
     extern __shared__ float2 smd[];
     float2 *tw = smd;
     float2 *A = tw + DK_TW;
-    float2 *B = A + DK_NL * DK_LS;
+    float2 *B = A + DK_NL * DK_LSF;
     const int line = threadIdx.x / DK_TPL, tl = threadIdx.x % DK_TPL;
     constexpr int YT = DK_NP / DK_NL;  // 16 target tiles per k'z plane
     const int n_items = DK_NP * YT * a.nb;
@@ -267,12 +272,12 @@ __global__ void __launch_bounds__(DK_NT, 2) fold_dk_kernel(DockFoldArgs a)
                     }
                     __syncthreads();  // previous group's FFTs are done with A
 #pragma unroll
-                    for (int m = 0; m < DK_E; m++) A[i * DK_LS + pad(n0 + (DK_NT / DK_NL) * m)] = xv[m];
+                    for (int m = 0; m < DK_E; m++) A[i * DK_LSF + pad(n0 + (DK_NT / DK_NL) * m)] = xv[m];
                 }
                 __syncthreads();
                 float2 xv[DK_E];
 #pragma unroll
-                for (int m = 0; m < DK_E; m++) xv[m] = A[line * DK_LS + pad(tl + DK_TPL * m)];
+                for (int m = 0; m < DK_E; m++) xv[m] = A[line * DK_LSF + pad(tl + DK_TPL * m)];
                 __syncthreads();  // A is rewritten by the FFT below
                 const int ky = kylo + line;
                 const bool my_ok = ky >= -DK_K && ky <= DK_K;
@@ -289,7 +294,7 @@ __global__ void __launch_bounds__(DK_NT, 2) fold_dk_kernel(DockFoldArgs a)
                     }
                     float2 yv[DK_E];
                     dk_coset(yv, xv, a.ctw, p, tl);
-                    fft_regs_t3<DK_L, -1, true>(yv, A + line * DK_LS, B + line * DK_LS, tw, tl);
+                    fft_regs_t3<DK_L, -1, true>(yv, A + line * DK_LSF, B + line * DK_LSF, tw, tl);
                     __syncwarp();
                     // outputs m and m' with the same m & 1 share a target: (0, 2, 10) -> j = 0, (1, 9, 11) -> j = 1
                     const float2 s0 = cfma(av[0], yv[0], cfma(av[2], yv[2], cmul(av[4], yv[10])));
@@ -309,12 +314,12 @@ __global__ void __launch_bounds__(DK_NT, 2) fold_dk_kernel(DockFoldArgs a)
 #pragma unroll
         for (int j = 0; j < 2; j++)
 #pragma unroll
-            for (int p = 0; p < DK_C; p++) A[line * DK_LS + ((DK_NP - (2 * tl + 64 * j + p)) & (DK_NP - 1))] = acc[j][p];
+            for (int p = 0; p < DK_C; p++) A[line * DK_LSF + ((DK_NP - (2 * tl + 64 * j + p)) & (DK_NP - 1))] = acc[j][p];
         __syncthreads();
         float2 *F = a.F + (long long)b * a.f_bstride;
         for (int e = threadIdx.x; e < DK_NL * DK_NP; e += DK_NT) {
             const int i = e % DK_NL, t = e / DK_NL;
-            F[((long long)t * DK_NP + ((y1 + i) & (DK_NP - 1))) * DK_NP + kzp] = A[i * DK_LS + t];
+            F[((long long)t * DK_NP + ((y1 + i) & (DK_NP - 1))) * DK_NP + kzp] = A[i * DK_LSF + t];
         }
     }
 }
@@ -325,14 +330,14 @@ bool dock_fast_supported(int L, int c, int G, int K, int Np, int complex_w)
     return L == DK_L && c == DK_C && G == DK_G && K == DK_K && Np == DK_NP && complex_w;
 }
 
-static size_t dk_smem(int nl = DK_NL) { return sizeof(float2) * ((size_t)DK_TW + 2 * nl * (size_t)DK_LS); }
+static size_t dk_smem(int nl, int ls) { return sizeof(float2) * ((size_t)DK_TW + 2 * nl * (size_t)ls); }
 
 constexpr int DK_PASS_NL = 4;  // lines per block of the z / y passes (128 threads, 5 blocks per SM)
 
 void launch_pass_z_dk(const DockPassArgs &a, int batch, cudaStream_t s)
 {
     constexpr int NL = DK_PASS_NL;
-    const size_t sm = dk_smem(NL);
+    const size_t sm = dk_smem(NL, DK_LSP);
     cudaFuncSetAttribute(pass_z_dk_kernel<NL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     pass_z_dk_kernel<NL><<<dim3((unsigned)(DK_L * DK_L / NL), batch), 32 * NL, sm, s>>>(a);
 }
@@ -340,7 +345,7 @@ void launch_pass_z_dk(const DockPassArgs &a, int batch, cudaStream_t s)
 void launch_pass_y_dk(const DockPassArgs &a, int batch, cudaStream_t s)
 {
     constexpr int NL = DK_PASS_NL;
-    const size_t sm = dk_smem(NL);
+    const size_t sm = dk_smem(NL, DK_LSP);
     cudaFuncSetAttribute(pass_y_dk_kernel<NL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     pass_y_dk_kernel<NL><<<dim3((unsigned)(DK_L * (DK_P / NL)), batch), 32 * NL, sm, s>>>(a);
 }
@@ -350,7 +355,7 @@ bool launch_fold_dk(const DockFoldArgs &a_in, int batch, cudaStream_t s)
     if (a_in.MS != DK_MS) return false;
     DockFoldArgs a = a_in;
     a.nb = batch;
-    const size_t sm = dk_smem();
+    const size_t sm = dk_smem(DK_NL, DK_LSF);
     cudaFuncSetAttribute(fold_dk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);

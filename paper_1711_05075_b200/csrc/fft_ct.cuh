@@ -421,6 +421,12 @@ struct T3 {
     static constexpr int NS2 = R0 * R1, MROW = R1 + 1;
     static constexpr int MSIZE = R0 * MROW, LSIZE = (R2 - 1) * NS2;
     static constexpr int SIZE = (MSIZE + LSIZE + 1) & ~1;  // even: 16-byte aligned buffers after it
+    // the mid stage writes rows of R0 R1 outputs with lane groups R1 elements apart; 4 pad
+    // slots per row put the warp's 32 stores on distinct bank pairs (the default pad, one slot
+    // per 16, left up to 4 lanes on one pair).  A line's B buffer needs BLEN elements.
+    static constexpr int ROW = R0 * R1;
+    __host__ __device__ static constexpr int padB(int idx) { return idx + (idx / ROW) * 4; }
+    static constexpr int BLEN = L + (L / ROW) * 4;
 };
 
 template <int L>
@@ -482,7 +488,7 @@ BC_DEV void fft_regs_t3(float2 (&x)[L / Plan<L>::TPL], float2 *A, float2 *B, con
             Dft<R, SIGN>::run(v);
             const int idxD = (j / Ns) * Ns * R + jm;
 #pragma unroll
-            for (int r = 0; r < R; r++) B[pad(idxD + r * Ns)] = v[r];
+            for (int r = 0; r < R; r++) B[P::padB(idxD + r * Ns)] = v[r];
         }
     }
     line_sync<WS>();
@@ -495,7 +501,7 @@ BC_DEV void fft_regs_t3(float2 (&x)[L / Plan<L>::TPL], float2 *A, float2 *B, con
             float2 v[R];
 #pragma unroll
             for (int r = 0; r < R; r++) {
-                float2 y = B[pad(j + r * Ns)];
+                float2 y = B[P::padB(j + r * Ns)];
                 if (r > 0) {
                     const float2 w = twl[(r - 1) * Ns + j];
                     y = SIGN < 0 ? cmul(y, w) : cmulc(y, w);
