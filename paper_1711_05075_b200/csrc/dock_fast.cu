@@ -29,11 +29,12 @@ constexpr int DK_TPL = 32, DK_NL = 8, DK_NT = DK_TPL * DK_NL, DK_E = DK_L / DK_T
 constexpr int DK_P = 384;   // T1 / T2 row pitch: kz at index kz + 192
 constexpr int DK_Z0 = 192;  // index of kz = 0
 // line buffer strides: each line's A (stage-0 output, default pad) and B (mid-stage output,
-// T3 padB) buffers; = 8 mod 16 float2 for the passes' 4-line transposes (a warp stores 8
-// consecutive rows of 4 lines) and = 4 mod 16 for the fold's 8-line ones (4 rows of 8 lines):
-// the warp's stores fall on distinct bank pairs
-constexpr int DK_LSP = 440, DK_LSF = 436;
-static_assert(DK_LSF >= T3<384>::BLEN && DK_LSF >= fct::pad(383) + 1 && DK_LSP % 16 == 8 && DK_LSF % 16 == 4, "dock strides");
+// T3 padB) buffers.  64-bit shared stores are served a half-warp (128 bytes) at a time, so the
+// transposes need each half-warp on 16 distinct 8-byte bank slots: = 4 mod 16 float2 for the
+// passes' 4-line transposes (a half-warp stores 4 rows of 4 lines), = 2 mod 16 for the fold's
+// 8-line ones (2 rows of 8 lines)
+constexpr int DK_LSP = 436, DK_LSF = 434;
+static_assert(DK_LSF >= T3<384>::BLEN && DK_LSF >= fct::pad(383) + 1 && DK_LSP % 16 == 4 && DK_LSF % 16 == 2, "dock strides");
 constexpr int DK_TW = T3<DK_L>::SIZE;  // conflict-free twiddle tables (fft_regs_t3)
 constexpr int DK_MS = cm_row_stride(DK_L, DK_C, DK_G, DK_K);  // A'' row stride (coset-major)
 static_assert(Plan<DK_L>::TPL == DK_TPL && Plan<DK_L>::n == 3 && warp_local<DK_L>(), "dock plan");
