@@ -96,7 +96,6 @@ __global__ void __launch_bounds__(32 * NL, 20 / NL) pass_z_dk_kernel(DockPassArg
     const long long row0 = (long long)blockIdx.x * NL;
     const int x = (int)(row0 / DK_L), y0 = (int)(row0 % DK_L);
     if (dk_zero_tile(x, y0, a.cx, a.cy, a.zero_r2) && dk_zero_tile(x, y0 + NL - 1, a.cx, a.cy, a.zero_r2)) return;
-    load_twiddles_t3<DK_L>(tw, a.tw, threadIdx.x, NT);
     const bool live = !dk_zero_tile(x, y0 + line, a.cx, a.cy, a.zero_r2);
     // planar box: real plane, then the imaginary plane L^3 floats further
     const float *inr = reinterpret_cast<const float *>(a.in + (long long)b * a.in_bstride) + (row0 + line) * DK_L;
@@ -104,6 +103,8 @@ __global__ void __launch_bounds__(32 * NL, 20 / NL) pass_z_dk_kernel(DockPassArg
     float2 xv[DK_E];
 #pragma unroll
     for (int m = 0; m < DK_E; m++) xv[m] = live ? make_float2(inr[tl + DK_TPL * m], ini[tl + DK_TPL * m]) : make_float2(0.f, 0.f);
+    // the twiddle tables after the row loads are issued: both latencies overlap
+    load_twiddles_t3<DK_L>(tw, a.tw, threadIdx.x, NT);
     __syncthreads();  // twiddle table
     float2 keep[6];
 #pragma unroll 1
@@ -170,7 +171,6 @@ __global__ void __launch_bounds__(32 * NL, 20 / NL) pass_y_dk_kernel(DockPassArg
         for (int e = threadIdx.x; e < NL * DK_P; e += NT) T2[e] = make_float2(0.f, 0.f);
         return;
     }
-    load_twiddles_t3<DK_L>(tw, a.tw, threadIdx.x, NT);
     float2 xv[DK_E];
     {
 #pragma unroll
@@ -179,6 +179,8 @@ __global__ void __launch_bounds__(32 * NL, 20 / NL) pass_y_dk_kernel(DockPassArg
             const int n = e / NL, i = e % NL;
             xv[m] = (n >= ylo && n <= yhi) ? T1[(long long)n * DK_P + i] : make_float2(0.f, 0.f);
         }
+        // the twiddle tables after the row loads are issued: both latencies overlap
+        load_twiddles_t3<DK_L>(tw, a.tw, threadIdx.x, NT);
 #pragma unroll
         for (int m = 0; m < DK_E; m++) {
             const int e = threadIdx.x + NT * m;

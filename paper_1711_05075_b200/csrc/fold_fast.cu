@@ -282,7 +282,6 @@ __global__ void __launch_bounds__(FF_NT, 5) pass_y_fast_kernel(PassYFastArgs a)
         for (int e = threadIdx.x; e < FF_M * FF_NL; e += FF_NT) T2[(e / FF_NL) * FF_KZ + kz0 + e % FF_NL] = make_float2(0.f, 0.f);
         return;
     }
-    load_twiddles<FF_L>(tw, a.tw, threadIdx.x, FF_NT);
     {
         float2 x[E];
 #pragma unroll
@@ -291,6 +290,8 @@ __global__ void __launch_bounds__(FF_NT, 5) pass_y_fast_kernel(PassYFastArgs a)
             const int n = e / FF_NL, i = e % FF_NL;
             x[m] = (n >= ylo && n <= yhi) ? T1[n * FF_KZ + kz0 + i] : make_float2(0.f, 0.f);
         }
+        // the twiddle table after the row loads are issued: both latencies overlap
+        load_twiddles<FF_L>(tw, a.tw, threadIdx.x, FF_NT);
 #pragma unroll
         for (int m = 0; m < E; m++) {
             const int e = threadIdx.x + FF_NT * m;

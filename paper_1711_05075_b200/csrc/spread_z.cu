@@ -434,12 +434,22 @@ __global__ void __launch_bounds__(128, 4) pass_z_fast_kernel(SpreadZArgs a)
             return;
         }
     }
-    load_twiddles<L>(tw, a.tw, threadIdx.x, NT);
     const float *box = a.box + (long long)b * a.box_bstride;
-    for (int e = threadIdx.x; e < SZ_COLS * L / 4; e += NT) {
-        const int cc = e / (L / 4), z4 = e % (L / 4);
-        *reinterpret_cast<float4 *>(acc + cc * CS + 4 * z4) =
-            *reinterpret_cast<const float4 *>(box + ((long long)(X0 + (cc >> 2)) * L + Y0 + (cc & 3)) * L + 4 * z4);
+    {   // the tile's columns: all loads issued before the stores, then the twiddle table
+        constexpr int PER = SZ_COLS * L / 4 / NT;  // float4 per thread
+        static_assert(SZ_COLS * L / 4 % NT == 0, "tile load");
+        float4 v[PER];
+#pragma unroll
+        for (int u = 0; u < PER; u++) {
+            const int e = threadIdx.x + NT * u, cc = e / (L / 4), z4 = e % (L / 4);
+            v[u] = *reinterpret_cast<const float4 *>(box + ((long long)(X0 + (cc >> 2)) * L + Y0 + (cc & 3)) * L + 4 * z4);
+        }
+        load_twiddles<L>(tw, a.tw, threadIdx.x, NT);
+#pragma unroll
+        for (int u = 0; u < PER; u++) {
+            const int e = threadIdx.x + NT * u, cc = e / (L / 4), z4 = e % (L / 4);
+            *reinterpret_cast<float4 *>(acc + cc * CS + 4 * z4) = v[u];
+        }
     }
     __syncthreads();
     tile_z_transform<L, NT, B4>(a, acc, Abuf, tw, T1, X0, Y0);
