@@ -32,6 +32,8 @@ constexpr int SZ_COLS = 16;    // columns per block (4 x 4)
 constexpr int SZ_LINES = 8;    // complex lines (column pairs)
 constexpr int SZ_BIN = 16;     // binning: 16 x 16 columns
 constexpr int SZ_PHI_N = 96;   // profile table pieces over [-W, W], W = 4 cells
+constexpr int ZB_RP = 132;     // coset row pitch of the band-4 z staging (= 4 mod 16 8-byte slots: the
+                               // unpack reads of 4 cosets x 4 slots per half-warp are distinct)
 constexpr float SZ_PHI_U = 4.f;
 
 struct PhiVal {
@@ -198,12 +200,15 @@ __device__ __forceinline__ void tile_z_transform(const SpreadZArgs &a, float *ac
         fft_regs<L, -1, true>(y, Abuf + g * LS, Abuf + g * LS, tw, tl);
         if (L == 256 && band4) {
             // plan L = 256, c = 4, K = 255: outputs m < 4 (k = 4q + p) and m >= 12
-            // (k = 4q + p - 1024) are the band, minus (p, q) = (0, 192)
+            // (k = 4q + p - 1024) are the band, minus (p, q) = (0, 192).  Stored coset-major,
+            // zb[line][p][s] (s = q, or q - 128 for q >= 192; rows of ZB_RP): a half-warp's
+            // consecutive q land in consecutive 8-byte slots (the k-ordered row put lanes 32
+            // bytes apart: 4-way bank conflicts)
 #pragma unroll
             for (int m = 0; m < E; m++) {
                 if (m >= 4 && m < 12) continue;
-                const int k = 4 * (tl + TPL * m) + p - (m >= 12 ? 1024 : 0);
-                if (m != 12 || p != 0 || tl != 0) zb[line * M + k + K] = y[m];
+                const int q = tl + TPL * m;
+                zb[line * (4 * ZB_RP) + p * ZB_RP + (m < 4 ? q : q - 128)] = y[m];
             }
         } else if (active) {
 #pragma unroll
@@ -216,6 +221,24 @@ __device__ __forceinline__ void tile_z_transform(const SpreadZArgs &a, float *ac
         __syncwarp();  // the next round's FFT rewrites this group's buffer
     }
     __syncthreads();  // zb complete
+    if (L == 256 && band4) {  // the coset-major zb above: Z(k) at (k & 3, k >> 2), Z(-k) at
+                              // ((-k) & 3, ((1024 - k) >> 2) - 128) for k >= 1
+#pragma unroll 1
+        for (int l = 0; l < SZ_LINES; l++) {
+            const int ca = 2 * l, cb = 2 * l + 1;
+            float2 *Ta = T1 + ((long long)(X0 + (ca >> 2)) * L + Y0 + (ca & 3)) * Kz;
+            float2 *Tb = T1 + ((long long)(X0 + (cb >> 2)) * L + Y0 + (cb & 3)) * Kz;
+            const float2 *zl = zb + l * (4 * ZB_RP);
+            for (int k = threadIdx.x; k < Kz; k += NT) {
+                const float2 Z = zl[(k & 3) * ZB_RP + (k >> 2)];
+                const float2 Zm = k ? zl[((-k) & 3) * ZB_RP + ((1024 - k) >> 2) - 128] : Z;
+                const float2 mu = a.mult_z[k];
+                Ta[k] = cmul(make_float2(0.5f * (Z.x + Zm.x), 0.5f * (Z.y - Zm.y)), mu);
+                Tb[k] = cmul(make_float2(0.5f * (Z.y + Zm.y), -0.5f * (Z.x - Zm.x)), mu);
+            }
+        }
+        return;
+    }
 #pragma unroll 1
     for (int l = 0; l < SZ_LINES; l++) {  // line l = columns 2l (real part) and 2l + 1 (imaginary)
         const int ca = 2 * l, cb = 2 * l + 1;
@@ -468,7 +491,7 @@ static void spread_z_launch(const SpreadZArgs &a, int batch, cudaStream_t s)
         const size_t sm1 = (size_t)a.phi_n * 32 + (size_t)SZ_COLS * (L + 8) * 4;
         cudaFuncSetAttribute(spread_z_kernel<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
         spread_z_kernel<L, true><<<dim3(tpa * tpa, batch), 128, sm1, s>>>(a);
-        const size_t region = std::max((size_t)SZ_COLS * (L + 8) * 4, (size_t)SZ_LINES * (2 * a.K + 1) * 8);
+        const size_t region = std::max({(size_t)SZ_COLS * (L + 8) * 4, (size_t)SZ_LINES * (2 * a.K + 1) * 8, L == 256 ? (size_t)SZ_LINES * 4 * ZB_RP * 8 : (size_t)0});
         const size_t sm2 = (size_t)L * 8 + (size_t)NG * line_stride(L) * 8 + region;
         if (L == 256 && a.c == 4 && a.G == 1024 && a.K == 255) {
             cudaFuncSetAttribute(pass_z_fast_kernel<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
@@ -479,7 +502,7 @@ static void spread_z_launch(const SpreadZArgs &a, int batch, cudaStream_t s)
         }
         return;
     }
-    const size_t region = std::max((size_t)SZ_COLS * (L + 8) * 4, (size_t)SZ_LINES * (2 * a.K + 1) * 8);
+    const size_t region = std::max({(size_t)SZ_COLS * (L + 8) * 4, (size_t)SZ_LINES * (2 * a.K + 1) * 8, L == 256 ? (size_t)SZ_LINES * 4 * ZB_RP * 8 : (size_t)0});
     const size_t sm = (size_t)a.phi_n * 32 + (size_t)L * 8 + (size_t)NG * line_stride(L) * 8 + region;
     cudaFuncSetAttribute(spread_z_kernel<L, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     spread_z_kernel<L, false><<<dim3(tpa * tpa, batch), 128, sm, s>>>(a);
