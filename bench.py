@@ -214,6 +214,26 @@ def ncu_traffic(stage, rotations, workload="sweep"):
         return None
 
 
+def smem_view(stage, rotations, avg_launch_s, sm_mhz, workload="sweep"):
+    """Shared-memory crossbar view of the dominant kernel: ncu's shared wavefronts per rotation
+    (profiles/r2/ncu_smem.json, from the committed --set full summary) x rotations per launch,
+    over the live launch time, against 148 SM x 1 wavefront (128 B) per cycle at the clock
+    sampled under load (B300_MICROARCH.md "LDS/STS": 128/N B/cyc/SM).  None off the sweep."""
+    path = os.path.join(ROOT, "profiles/r2/ncu_smem.json")
+    if workload != "sweep" or not os.path.exists(path) or not sm_mhz:
+        return None
+    try:
+        k = json.load(open(path))["per_kernel"][STAGE_KERNEL[stage]]
+    except Exception:
+        return None
+    wf = k["wavefronts_per_rotation"] * rotations
+    peak = 148 * sm_mhz * 1e6
+    return {"wavefronts_per_launch": wf, "Gwavefronts_per_s": wf / avg_launch_s / 1e9, "peak_Gwavefronts_per_s": peak / 1e9,
+            "frac": wf / avg_launch_s / peak, "bank_conflict_share": k["bank_conflicts_per_rotation"] / k["wavefronts_per_rotation"],
+            "source": "profiles/r2/ncu_smem.json (l1tex__data_pipe_lsu_wavefronts_mem_shared.sum); peak 148 SM x 1 "
+                      "wavefront/cycle x the sampled SM clock"}
+
+
 def path_roofline(N, Np, K, complex_w, rot_per_s, peak):
     """SURVEY §8(d)'s two whole-path numbers.  R2 (method efficiency): the method's
     algorithmic bytes per rotation B_alg = 8 M_b 3 (write + read B's band spectrum, read A's)
@@ -584,7 +604,8 @@ def run_ours(args, rank, world, local_rank):
                 "impl_view": {"bytes_per_launch": impl * batch, "GBps": st["impl_GBps"], "frac": st["hbm_frac_impl"],
                               "note": "compulsory read+write of the kernel's own input/output incl. FFT intermediates"},
                 "alu_view": {"fp32_TFLOPs": st["fp32_TFLOPs"], "peak_TFLOPs": alu_peak, "frac": st["alu_frac"],
-                             "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz"}}
+                             "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz"},
+                "smem_view": smem_view(name, batch, tot_ms / nl / 1e3, (clocks or {}).get("sm_mhz"), w.name)}
     cpu = None
     rel_err = None
     if world == 1 and not args.no_cpu_baseline:
