@@ -259,9 +259,21 @@ __device__ __forceinline__ void tile_z_transform(const SpreadZArgs &a, float *ac
 // registers and buffers the spread runs at twice the occupancy.  CPLX (BOX only): complex
 // weights w = (recB.y, recWi), two accumulators per cell, float2 box cells (the z transform
 // is then the complex-row pass of passes.cu, which skips the tiles left unwritten here).
+// Accumulator slot -> column of the 4 x 4 tile.  Slot 4 w + g belongs to warp w, lane group g.
+// QUAD: warp w owns the 2 x 2 quadrant (2 (w >> 1), 2 (w & 1)); else the 1 x 4 strip x = w.
+// The slots (not the columns) index acc, so the groups' rows stay 8 banks apart either way.
+template <bool QUAD>
+__device__ __forceinline__ int slot_x(int s) { return QUAD ? 2 * (s >> 3) + ((s >> 1) & 1) : s >> 2; }
+template <bool QUAD>
+__device__ __forceinline__ int slot_y(int s) { return QUAD ? 2 * ((s >> 2) & 1) + (s & 1) : s & 3; }
+
 template <int L, bool BOX, bool CPLX = false>
 __global__ void __launch_bounds__(128, CPLX ? 4 : (BOX ? 8 : 4)) spread_z_kernel(SpreadZArgs a)
 {
+    // 2 x 2 quadrants when spreading to the box (the fused z transform reads the slots as strip
+    // columns): fewer ball visits per warp and more even chords (sweep spread 0.1511 -> 0.1484,
+    // torus 0.0489 -> 0.0472 ms per rotation)
+    constexpr bool QUAD = BOX;
     static_assert(!CPLX || BOX, "complex weights: spread to the box only");
     constexpr int NT = 128;
     constexpr int TPL = Plan<L>::TPL, NG = NT / TPL;
@@ -306,9 +318,11 @@ __global__ void __launch_bounds__(128, CPLX ? 4 : (BOX ? 8 : 4)) spread_z_kernel
 
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int gi = lane >> 3, hl = lane & 7;
-    const int col = 4 * wid + gi;                     // = (cx << 2) | cy
-    const float fx = (float)(X0 + wid), fy = (float)(Y0 + gi);
-    const float fy0 = (float)Y0;
+    const int col = 4 * wid + gi;                     // accumulator slot (column slot_x(col), slot_y(col))
+    const float fx = (float)(X0 + slot_x<QUAD>(col)), fy = (float)(Y0 + slot_y<QUAD>(col));
+    // the warp's column footprint: [wx0, wx0 + wxn] x [wy0, wy0 + wyn]
+    const float wx0 = (float)(X0 + slot_x<QUAD>(4 * wid)), wy0 = (float)(Y0 + slot_y<QUAD>(4 * wid));
+    constexpr float wxn = QUAD ? 1.f : 0.f, wyn = QUAD ? 1.f : 3.f;
     float *accc = acc + col * CS;
     float *acci_c = acci + col * CS;
     // the blob's profile table (pieces of W/48 over [-W, W], W = 4 cells: n = 96) as constants;
@@ -336,8 +350,8 @@ __global__ void __launch_bounds__(128, CPLX ? 4 : (BOX ? 8 : 4)) spread_z_kernel
             uc = recA[jl];
             wc = a.recB[jl];
             if (CPLX) wic = a.recWi[jl];
-            const float ddx = fx - uc.x;
-            const float ddy = fmaxf(fmaxf(fy0 - uc.y, uc.y - (fy0 + 3.f)), 0.f);
+            const float ddx = fmaxf(fmaxf(wx0 - uc.x, uc.x - (wx0 + wxn)), 0.f);
+            const float ddy = fmaxf(fmaxf(wy0 - uc.y, uc.y - (wy0 + wyn)), 0.f);
             // zero-weight balls add nothing (the planar complex spreads see each docking ball in
             // one of their two passes only)
             rel = fmaf(ddx, ddx, ddy * ddy) < uc.w && (wc.y != 0.f || (CPLX && wic != 0.f));
@@ -412,14 +426,14 @@ __global__ void __launch_bounds__(128, CPLX ? 4 : (BOX ? 8 : 4)) spread_z_kernel
         float2 *box = reinterpret_cast<float2 *>(a.box + (long long)b * a.box_bstride);
         for (int e = threadIdx.x; e < SZ_COLS * L / 2; e += NT) {
             const int cc = e / (L / 2), z2 = 2 * (e % (L / 2));
-            *reinterpret_cast<float4 *>(box + ((long long)(X0 + (cc >> 2)) * L + Y0 + (cc & 3)) * L + z2) =
+            *reinterpret_cast<float4 *>(box + ((long long)(X0 + slot_x<QUAD>(cc)) * L + Y0 + slot_y<QUAD>(cc)) * L + z2) =
                 make_float4(acc[cc * CS + z2], acci[cc * CS + z2], acc[cc * CS + z2 + 1], acci[cc * CS + z2 + 1]);
         }
     } else if (BOX) {  // the tile's 16 columns (1 KB each) to the box
         float *box = a.box + (long long)b * a.box_bstride;
         for (int e = threadIdx.x; e < SZ_COLS * L / 4; e += NT) {  // 16-byte rows (CS, L multiples of 4)
             const int cc = e / (L / 4), z4 = e % (L / 4);
-            *reinterpret_cast<float4 *>(box + ((long long)(X0 + (cc >> 2)) * L + Y0 + (cc & 3)) * L + 4 * z4) =
+            *reinterpret_cast<float4 *>(box + ((long long)(X0 + slot_x<QUAD>(cc)) * L + Y0 + slot_y<QUAD>(cc)) * L + 4 * z4) =
                 *reinterpret_cast<const float4 *>(acc + cc * CS + 4 * z4);
         }
     } else {
