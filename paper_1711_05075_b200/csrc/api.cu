@@ -744,6 +744,20 @@ bc_status build_generic_bins_B(bc_ctx *ctx)
 
 bool use_spread_z(const bc_ctx *ctx) { return ctx->plan[1].ok && ctx->plan[1].blob; }
 
+// The fast plan (spread_z -> pass_z_fast -> pass_y_fast -> fold_fast, real weights): B's y and z
+// multipliers are folded into A'' with the x ones (the fold's product is per mode), so the
+// z unpack and the y pass store their outputs without them.
+bool yz_in_A(const bc_ctx *ctx)
+{
+#ifdef BC_NO_YZ_FOLD
+    return false;
+#endif
+    const ShapePlan &pB = ctx->plan[1];
+    return use_spread_z(ctx) && !ctx->p.generic_only && ctx->p.weights != BC_WEIGHTS_COMPLEX &&
+           fold_fast_supported(pB.L, pB.c, pB.G, ctx->K, ctx->p.Np, 0) &&
+           pass_y_fast_supported(pB.L, pB.c, pB.G, ctx->K, 0);
+}
+
 // the docking plan shape on dock_fast.cu's kernels (blob spread to a complex box, then the
 // compile-time z / y passes and fold)
 bool use_dock_fast(const bc_ctx *ctx)
@@ -935,7 +949,7 @@ bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, voi
             a.box = (float *)ws1;
             a.box_bstride = (long long)(s1_per / 4);
         }
-        a.mult_z = pl.d_mult[2];
+        a.mult_z = yz_in_A(ctx) ? nullptr : pl.d_mult[2];
         a.tw = tw;
         a.ctw = pl.d_ctw;
         a.out = (float2 *)ws2;
@@ -1076,7 +1090,7 @@ bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, voi
         PassYFastArgs a{};
         a.tw = tw;
         a.ctw = pl.d_ctw;
-        a.mult = pl.d_mult[1];
+        a.mult = yz_in_A(ctx) ? nullptr : pl.d_mult[1];
         a.T1 = (const float2 *)ws2;
         a.t1_bstride = (long long)(s2_per / 8);
         a.T2 = (float2 *)ws1;
@@ -1715,7 +1729,8 @@ bc_status run_rotations(bc_ctx *ctx, int64_t n_rot, int out_kind, char *dout, si
                 ctx->Ahat_cm_bytes = sizeof(float2) * nspec;
             }
             launch_permute_cm(ctx->d_Ahat, pb.d_mult[0], ctx->d_Ahat_cm, (long long)ctx->M * ctx->Kz, ctx->K, pb.L, pb.c,
-                              pb.G, cplx, ctx->MS, ctx->Kz, ctx->p.band_radius, pb.blob ? ctx->d_dec : nullptr, s);
+                              pb.G, cplx, ctx->MS, ctx->Kz, ctx->p.band_radius, pb.blob ? ctx->d_dec : nullptr, s,
+                              yz_in_A(ctx) ? pb.d_mult[1] : nullptr, yz_in_A(ctx) ? pb.d_mult[2] : nullptr);
             ctx->launches++;
             CU(ctx, cudaGetLastError());
             ctx->cm_ready = true;
@@ -2638,6 +2653,8 @@ bc_status bc_spectrum_A_reduce(bc_ctx *ctx, const void *const *partials, int n, 
     a.n_parts = n;
     a.Ahat = ctx->d_Ahat;
     a.mult = pb.d_mult[0];
+    a.mult_y = yz_in_A(ctx) ? pb.d_mult[1] : nullptr;
+    a.mult_z = yz_in_A(ctx) ? pb.d_mult[2] : nullptr;
     a.out = ctx->d_Ahat_cm;
     a.rows = (long long)ctx->M * ctx->Kz;
     a.K = ctx->K;

@@ -253,6 +253,8 @@ bool launch_fold_fast(const FoldFastArgs &a_in, int batch, cudaStream_t s)
 // Block = one ix, 8 consecutive kz.  Rows iy outside B's support cylinder at this ix are
 // zero (spread_z writes them so) and are not loaded.  Per coset only the 128 in-band
 // outputs (q < 64 or q >= 192) are staged and stored.
+// MULT = false: mult_y is folded into A'' (permute_cm_kernel) and the outputs are stored as they are
+template <bool MULT>
 __global__ void __launch_bounds__(FF_NT, 5) pass_y_fast_kernel(PassYFastArgs a)
 {
     constexpr int E = FF_L / FF_TPL;
@@ -327,8 +329,12 @@ __global__ void __launch_bounds__(FF_NT, 5) pass_y_fast_kernel(PassYFastArgs a)
             const int q = tl + FF_TPL * m;
             const int ky = FF_C * q + p - (m >= 12 ? FF_G : 0);
             const int u = m < 4 ? q : q - 128;
-            const float2 mu = (ky >= -FF_K) ? __ldg(a.mult + ky + FF_K) : make_float2(0.f, 0.f);
-            Ab[line * FF_LS + u] = cmul(y[m], mu);
+            if (MULT) {
+                const float2 mu = (ky >= -FF_K) ? __ldg(a.mult + ky + FF_K) : make_float2(0.f, 0.f);
+                Ab[line * FF_LS + u] = cmul(y[m], mu);
+            } else {
+                Ab[line * FF_LS + u] = y[m];  // (ky < -K: never stored below)
+            }
         }
         __syncthreads();
         const int io = threadIdx.x % FF_NL, u0 = threadIdx.x / FF_NL;  // e = tid + 128 r
@@ -351,6 +357,12 @@ bool pass_y_fast_supported(int L, int c, int G, int K, int complex_w)
 void launch_pass_y_fast(const PassYFastArgs &a, int batch, cudaStream_t s)
 {
     const size_t sm = sizeof(float2) * ((size_t)FF_L + FF_NL * FF_LS);
-    cudaFuncSetAttribute(pass_y_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    pass_y_fast_kernel<<<dim3((unsigned)(FF_L * (FF_KZ / FF_NL)), batch), FF_NT, sm, s>>>(a);
+    const dim3 grid((unsigned)(FF_L * (FF_KZ / FF_NL)), batch);
+    if (a.mult) {
+        cudaFuncSetAttribute(pass_y_fast_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        pass_y_fast_kernel<true><<<grid, FF_NT, sm, s>>>(a);
+    } else {
+        cudaFuncSetAttribute(pass_y_fast_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        pass_y_fast_kernel<false><<<grid, FF_NT, sm, s>>>(a);
+    }
 }

@@ -269,7 +269,7 @@ void launch_fold_x(const FoldXArgs &a, int batch, cudaStream_t s);
 bool fold_fuses_inverse(int L, int Np);
 void launch_last(const LastArgs &a, int batch, cudaStream_t s);
 void launch_permute_cm(const float2 *in, const float2 *mult, float2 *out, long long rows, int K, int L, int c, int G,
-                       int neg, int MS, int Kz, double band_radius, const float *dec, cudaStream_t s);
+                       int neg, int MS, int Kz, double band_radius, const float *dec, cudaStream_t s, const float2 *mult_y = nullptr, const float2 *mult_z = nullptr);
 void launch_keys_init(unsigned long long *keys, int n, cudaStream_t s);
 // peers: result buffers (bc_extremum[], device pointers, possibly mapped from other GPUs) that
 // receive the same records at global rotation index peer_base + r (nullptr / 0: none)
@@ -292,6 +292,7 @@ struct ReducePermuteArgs {
     int K, L, c, G, neg, MS, Kz;
     double R2;
     const float *dec;
+    const float2 *mult_y, *mult_z;      // B's y / z multipliers folded in too (fast plan), or nullptr
 };
 void launch_reduce_permute(const ReducePermuteArgs &a, cudaStream_t s);
 

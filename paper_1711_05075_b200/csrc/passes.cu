@@ -387,9 +387,12 @@ __global__ void __launch_bounds__(8 * Plan<L>::TPL, 512 / (8 * Plan<L>::TPL) > 0
 // B's x multipliers (natural order, index k + K) are folded in: real weights store
 // A'(k) conj(mult(k)) at cm(k); complex weights store A'(k) mult(-k) at cm(-k).
 // dec != nullptr: B's radial window deconvolution 1 / phi_hat(|k|) (indexed by |k|^2) is folded in.
+// mult_y != nullptr (real weights, the fast plan): B's y and z multipliers too, as conj(mult):
+// the fold's product A'' conj(B) is then the same mode by mode, and the y / z passes skip them.
 __global__ void permute_cm_kernel(const float2 *__restrict__ in, const float2 *__restrict__ mult,
                                   float2 *__restrict__ out, long long rows, int K, int L, int c, int G, int neg, int MS,
-                                  int Kz, double R2, const float *__restrict__ dec)
+                                  int Kz, double R2, const float *__restrict__ dec,
+                                  const float2 *__restrict__ mult_y, const float2 *__restrict__ mult_z)
 {
     const int M = 2 * K + 1;
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -400,17 +403,20 @@ __global__ void permute_cm_kernel(const float2 *__restrict__ in, const float2 *_
     const long long ky = row / Kz - K, kz = (row % Kz) - (Kz == M ? K : 0);
     const long long k2 = k * (long long)k + ky * ky + kz * kz;
     if (dec) v = cscale(v, dec[k2]);
+    if (mult_y) v = cmulc(cmulc(v, mult_y[ky + K]), mult_z[kz]);  // fast plan: the y / z passes skip theirs
     if (R2 > 0 && (double)k2 > R2) v = make_float2(0.f, 0.f);  // spherical band: |k| <= band_radius
     out[row * MS + cm_of_k(neg ? -k : k, L, c, G, K)] = v;
 }
 
 void launch_permute_cm(const float2 *in, const float2 *mult, float2 *out, long long rows, int K, int L, int c, int G,
-                       int neg, int MS, int Kz, double band_radius, const float *dec, cudaStream_t s)
+                       int neg, int MS, int Kz, double band_radius, const float *dec, cudaStream_t s,
+                       const float2 *mult_y, const float2 *mult_z)
 {
     const long long n = rows * (2LL * K + 1);
     cudaMemsetAsync(out, 0, sizeof(float2) * rows * MS, s);
     permute_cm_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(in, mult, out, rows, K, L, c, G, neg, MS, Kz,
-                                                                 band_radius > 0 ? band_radius * band_radius : 0.0, dec);
+                                                                 band_radius > 0 ? band_radius * band_radius : 0.0, dec,
+                                                                 mult_y, mult_z);
 }
 
 // ============================================================================ last inverse pass + epilogue

@@ -232,9 +232,16 @@ __device__ __forceinline__ void tile_z_transform(const SpreadZArgs &a, float *ac
             for (int k = threadIdx.x; k < Kz; k += NT) {
                 const float2 Z = zl[(k & 3) * ZB_RP + (k >> 2)];
                 const float2 Zm = k ? zl[((-k) & 3) * ZB_RP + ((1024 - k) >> 2) - 128] : Z;
-                const float2 mu = a.mult_z[k];
-                Ta[k] = cmul(make_float2(0.5f * (Z.x + Zm.x), 0.5f * (Z.y - Zm.y)), mu);
-                Tb[k] = cmul(make_float2(0.5f * (Z.y + Zm.y), -0.5f * (Z.x - Zm.x)), mu);
+                const float2 za = make_float2(0.5f * (Z.x + Zm.x), 0.5f * (Z.y - Zm.y));
+                const float2 zb2 = make_float2(0.5f * (Z.y + Zm.y), -0.5f * (Z.x - Zm.x));
+                if (a.mult_z) {  // (nullptr: mult_z folded into A'', permute_cm_kernel)
+                    const float2 mu = a.mult_z[k];
+                    Ta[k] = cmul(za, mu);
+                    Tb[k] = cmul(zb2, mu);
+                } else {
+                    Ta[k] = za;
+                    Tb[k] = zb2;
+                }
             }
         }
         return;
