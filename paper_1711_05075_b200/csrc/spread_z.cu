@@ -254,7 +254,7 @@ __device__ __forceinline__ void tile_z_transform(const SpreadZArgs &a, float *ac
         const float2 *zl = zb + l * M + K;
         for (int k = threadIdx.x; k < Kz; k += NT) {
             const float2 Z = zl[k], Zm = zl[-k];
-            const float2 mu = a.mult_z[k];
+            const float2 mu = a.mult_z ? a.mult_z[k] : make_float2(1.f, 0.f);  // (nullptr: folded into A'')
             Ta[k] = cmul(make_float2(0.5f * (Z.x + Zm.x), 0.5f * (Z.y - Zm.y)), mu);
             Tb[k] = cmul(make_float2(0.5f * (Z.y + Zm.y), -0.5f * (Z.x - Zm.x)), mu);
         }
