@@ -744,17 +744,6 @@ bc_status build_generic_bins_B(bc_ctx *ctx)
 
 bool use_spread_z(const bc_ctx *ctx) { return ctx->plan[1].ok && ctx->plan[1].blob; }
 
-// Real-weight blob plans (spread_z -> z unpack -> y pass -> fold, every fold variant reading A''
-// mode by mode): B's y and z multipliers are folded into A'' with the x ones, so the z unpack
-// and B's y pass store their outputs without them (sweep y pass 0.124 -> 0.099 ms per rotation).
-// generic_only keeps them in the passes (the reference path of the fused-vs-generic tests).
-bool yz_in_A(const bc_ctx *ctx)
-{
-#ifdef BC_NO_YZ_FOLD
-    return false;
-#endif
-    return use_spread_z(ctx) && !ctx->p.generic_only && ctx->p.weights != BC_WEIGHTS_COMPLEX;
-}
 
 // the docking plan shape on dock_fast.cu's kernels (blob spread to a complex box, then the
 // compile-time z / y passes and fold)
@@ -763,6 +752,19 @@ bool use_dock_fast(const bc_ctx *ctx)
     const ShapePlan &pb = ctx->plan[1];
     return use_spread_z(ctx) && !ctx->p.generic_only &&
            dock_fast_supported(pb.L, pb.c, pb.G, ctx->K, ctx->p.Np, ctx->p.weights == BC_WEIGHTS_COMPLEX);
+}
+
+// Real-weight blob plans (spread_z -> z unpack -> y pass -> fold, every fold variant reading A''
+// mode by mode) and the docking plan (dock_fast.cu): B's y and z multipliers are folded into A''
+// with the x ones, so the z unpack and B's y / z passes store their outputs without them (sweep
+// y pass 0.124 -> 0.099 ms per rotation).  generic_only keeps them in the passes (the reference
+// path of the fused-vs-generic tests).
+bool yz_in_A(const bc_ctx *ctx)
+{
+#ifdef BC_NO_YZ_FOLD
+    return false;
+#endif
+    return (use_spread_z(ctx) && !ctx->p.generic_only && ctx->p.weights != BC_WEIGHTS_COMPLEX) || use_dock_fast(ctx);
 }
 
 // Uniform grid of A's centres for bc_evaluate_points: cell size cs >= max r_A + max s_B, so
@@ -1040,7 +1042,7 @@ bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, voi
         a.zero_r2 = (float)((ctx->live_r + 1) * (ctx->live_r + 1));
         {
             DockPassArgs z = a;
-            z.mult = pl.d_mult[2];
+            z.mult = yz_in_A(ctx) ? nullptr : pl.d_mult[2];
             z.in = (const float2 *)ws1;
             z.in_bstride = (long long)(s1_per / 8);
             z.out = (float2 *)ws2;
@@ -1051,7 +1053,7 @@ bc_status shape_spectrum(bc_ctx *ctx, int which, const float *d_rot, int nb, voi
         }
         {
             DockPassArgs y = a;
-            y.mult = pl.d_mult[1];
+            y.mult = yz_in_A(ctx) ? nullptr : pl.d_mult[1];
             y.in = (const float2 *)ws2;
             y.in_bstride = (long long)(s2_per / 8);
             y.out = (float2 *)ws1;

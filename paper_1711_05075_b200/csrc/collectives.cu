@@ -31,7 +31,9 @@ __global__ void reduce_permute_kernel(ReducePermuteArgs a)
     const long long ky = row / a.Kz - a.K, kz = (row % a.Kz) - (a.Kz == M ? a.K : 0);
     const long long k2 = k * (long long)k + ky * ky + kz * kz;
     if (a.dec) u = cscale(u, a.dec[k2]);
-    if (a.mult_y) u = cmulc(cmulc(u, a.mult_y[ky + a.K]), a.mult_z[kz]);  // as permute_cm_kernel
+    if (a.mult_y)  // as permute_cm_kernel
+        u = a.neg ? cmul(cmul(u, a.mult_y[-ky + a.K]), a.mult_z[-kz + a.K])
+                  : cmulc(cmulc(u, a.mult_y[ky + a.K]), a.mult_z[kz]);
     if (a.R2 > 0 && (double)k2 > a.R2) u = make_float2(0.f, 0.f);
     a.out[row * a.MS + cm_of_k(a.neg ? -k : k, a.L, a.c, a.G, a.K)] = u;
 }

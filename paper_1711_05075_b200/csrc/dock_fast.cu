@@ -83,7 +83,7 @@ BC_DEV void dk_live_planes(float cx, float live_r2, int &xlo, int &xhi)
 // Block = 8 box rows (x, y0 .. y0 + 7).  Rows in tiles spread_z left unwritten read as zero; a
 // block of only such rows writes nothing (the y pass loads only rows within live_r, all of
 // them in written tiles).
-template <int NL>
+template <int NL, bool MULT>
 __global__ void __launch_bounds__(32 * NL, 20 / NL) pass_z_dk_kernel(DockPassArgs a)
 {
     constexpr int NT = 32 * NL;
@@ -125,9 +125,13 @@ __global__ void __launch_bounds__(32 * NL, 20 / NL) pass_z_dk_kernel(DockPassArg
             for (int u = 0; u < 6; u++) {
                 const int m = u < 3 ? u : u + 6;
                 const int k0 = dk_k(m, 0, tl);  // even: k0, k0 + 1 adjacent at index k + 192
-                const float2 m0 = k0 >= -DK_K ? __ldg(a.mult + k0 + DK_K) : make_float2(0.f, 0.f);
-                const float2 m1 = __ldg(a.mult + k0 + 1 + DK_K);
-                const float2 v0 = cmul(keep[u], m0), v1 = cmul(yv[m], m1);
+                float2 v0 = keep[u], v1 = yv[m];  // (keep: zero outside the band)
+                if (MULT) {  // else the multipliers are folded into A'' (permute_cm_kernel)
+                    const float2 m0 = k0 >= -DK_K ? __ldg(a.mult + k0 + DK_K) : make_float2(0.f, 0.f);
+                    const float2 m1 = __ldg(a.mult + k0 + 1 + DK_K);
+                    v0 = cmul(v0, m0);
+                    v1 = cmul(v1, m1);
+                }
                 *reinterpret_cast<float4 *>(out + k0 + DK_Z0) = make_float4(v0.x, v0.y, v1.x, v1.y);
             }
         }
@@ -140,7 +144,7 @@ __global__ void __launch_bounds__(32 * NL, 20 / NL) pass_z_dk_kernel(DockPassArg
 // written (the fold does not read it).  T2 rows hold ky at index ky + 192, so, as in the z
 // pass, a thread stores the two cosets' outputs of one q with one 16-byte store: no output
 // staging (T2 = [x][j][ky + 192]).
-template <int NL>
+template <int NL, bool MULT>
 __global__ void __launch_bounds__(32 * NL, 20 / NL) pass_y_dk_kernel(DockPassArgs a)
 {
     constexpr int NT = 32 * NL;
@@ -210,9 +214,13 @@ __global__ void __launch_bounds__(32 * NL, 20 / NL) pass_y_dk_kernel(DockPassArg
             for (int u = 0; u < 6; u++) {
                 const int m = u < 3 ? u : u + 6;
                 const int k0 = dk_k(m, 0, tl);
-                const float2 m0 = k0 >= -DK_K ? __ldg(a.mult + k0 + DK_K) : make_float2(0.f, 0.f);
-                const float2 m1 = __ldg(a.mult + k0 + 1 + DK_K);
-                const float2 v0 = cmul(keep[u], m0), v1 = cmul(yv[m], m1);
+                float2 v0 = keep[u], v1 = yv[m];  // (keep: zero outside the band)
+                if (MULT) {  // else the multipliers are folded into A'' (permute_cm_kernel)
+                    const float2 m0 = k0 >= -DK_K ? __ldg(a.mult + k0 + DK_K) : make_float2(0.f, 0.f);
+                    const float2 m1 = __ldg(a.mult + k0 + 1 + DK_K);
+                    v0 = cmul(v0, m0);
+                    v1 = cmul(v1, m1);
+                }
                 *reinterpret_cast<float4 *>(out + k0 + DK_Z0) = make_float4(v0.x, v0.y, v1.x, v1.y);
             }
         }
@@ -341,16 +349,28 @@ void launch_pass_z_dk(const DockPassArgs &a, int batch, cudaStream_t s)
 {
     constexpr int NL = DK_PASS_NL;
     const size_t sm = dk_smem(NL, DK_LSP);
-    cudaFuncSetAttribute(pass_z_dk_kernel<NL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    pass_z_dk_kernel<NL><<<dim3((unsigned)(DK_L * DK_L / NL), batch), 32 * NL, sm, s>>>(a);
+    const dim3 grid((unsigned)(DK_L * DK_L / NL), batch);
+    if (a.mult) {
+        cudaFuncSetAttribute(pass_z_dk_kernel<NL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        pass_z_dk_kernel<NL, true><<<grid, 32 * NL, sm, s>>>(a);
+    } else {
+        cudaFuncSetAttribute(pass_z_dk_kernel<NL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        pass_z_dk_kernel<NL, false><<<grid, 32 * NL, sm, s>>>(a);
+    }
 }
 
 void launch_pass_y_dk(const DockPassArgs &a, int batch, cudaStream_t s)
 {
     constexpr int NL = DK_PASS_NL;
     const size_t sm = dk_smem(NL, DK_LSP);
-    cudaFuncSetAttribute(pass_y_dk_kernel<NL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    pass_y_dk_kernel<NL><<<dim3((unsigned)(DK_L * (DK_P / NL)), batch), 32 * NL, sm, s>>>(a);
+    const dim3 grid((unsigned)(DK_L * (DK_P / NL)), batch);
+    if (a.mult) {
+        cudaFuncSetAttribute(pass_y_dk_kernel<NL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        pass_y_dk_kernel<NL, true><<<grid, 32 * NL, sm, s>>>(a);
+    } else {
+        cudaFuncSetAttribute(pass_y_dk_kernel<NL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        pass_y_dk_kernel<NL, false><<<grid, 32 * NL, sm, s>>>(a);
+    }
 }
 
 bool launch_fold_dk(const DockFoldArgs &a_in, int batch, cudaStream_t s)

@@ -387,8 +387,9 @@ __global__ void __launch_bounds__(8 * Plan<L>::TPL, 512 / (8 * Plan<L>::TPL) > 0
 // B's x multipliers (natural order, index k + K) are folded in: real weights store
 // A'(k) conj(mult(k)) at cm(k); complex weights store A'(k) mult(-k) at cm(-k).
 // dec != nullptr: B's radial window deconvolution 1 / phi_hat(|k|) (indexed by |k|^2) is folded in.
-// mult_y != nullptr (real weights, the fast plan): B's y and z multipliers too, as conj(mult):
-// the fold's product A'' conj(B) is then the same mode by mode, and the y / z passes skip them.
+// mult_y != nullptr: B's y and z multipliers too -- real weights as conj(mult(ky)) conj(mult(kz))
+// (the fold's product A'' conj(B) per mode); complex weights (docking plan, whose fold takes
+// A''(ky, kz) times B's line at (-ky, -kz)) as mult(-ky) mult(-kz) -- and the passes skip them.
 __global__ void permute_cm_kernel(const float2 *__restrict__ in, const float2 *__restrict__ mult,
                                   float2 *__restrict__ out, long long rows, int K, int L, int c, int G, int neg, int MS,
                                   int Kz, double R2, const float *__restrict__ dec,
@@ -403,7 +404,8 @@ __global__ void permute_cm_kernel(const float2 *__restrict__ in, const float2 *_
     const long long ky = row / Kz - K, kz = (row % Kz) - (Kz == M ? K : 0);
     const long long k2 = k * (long long)k + ky * ky + kz * kz;
     if (dec) v = cscale(v, dec[k2]);
-    if (mult_y) v = cmulc(cmulc(v, mult_y[ky + K]), mult_z[kz]);  // fast plan: the y / z passes skip theirs
+    if (mult_y)  // the y / z passes skip theirs (real: conj at k; complex, docking fold: at -k)
+        v = neg ? cmul(cmul(v, mult_y[-ky + K]), mult_z[-kz + K]) : cmulc(cmulc(v, mult_y[ky + K]), mult_z[kz]);
     if (R2 > 0 && (double)k2 > R2) v = make_float2(0.f, 0.f);  // spherical band: |k| <= band_radius
     out[row * MS + cm_of_k(neg ? -k : k, L, c, G, K)] = v;
 }
